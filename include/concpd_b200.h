@@ -1,0 +1,213 @@
+/*
+ * concpd_b200 — C ABI of the B200-native CoNCPD-APG / lraCoNCPD-APG hot path.
+ *
+ * Drop-in boundary for the reference package `concpd` (arXiv 2302.05119,
+ * /root/reference/pkg/src/concpd).  The reference is pure Python/numpy with no
+ * FFI of its own; these entry points are what a ctypes binding inside the
+ * reference would call.  Every function cites the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *   - Tensors: dense, first-index-fastest (Fortran) order, fp32 or fp64
+ *     (`cb_dtype`), device pointers owned by the caller
+ *     (tensor_ops.py:1-15 layout convention).
+ *   - Factor matrices: fp64, row-major I_n x R (numpy C order of an
+ *     (I_n, R) array).  Gram / step matrices: fp64 row-major R x R.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Operator
+ *     calls are asynchronous on that stream; engine calls synchronise only
+ *     where documented.
+ *   - Every call returns a cb_status; on failure cb_last_error() returns a
+ *     thread-local message.  No global mutable state: handles are re-entrant
+ *     per solve (the reference's bench runs solves from a thread pool,
+ *     cli.py:277-282).
+ *   - Nothing here falls back to the CPU.
+ */
+#ifndef CONCPD_B200_H
+#define CONCPD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CB_ABI_VERSION 1
+
+typedef enum {
+  CB_OK = 0,
+  CB_ERR_ARG = 1,          /* invalid argument -> ValueError in the Python host      */
+  CB_ERR_CUDA = 2,         /* CUDA runtime failure                                   */
+  CB_ERR_NONFINITE = 3,    /* non-finite objective -> FloatingPointError (solver.py:523-527) */
+  CB_ERR_UNSUPPORTED = 4,  /* shape outside the kernels' limits (rank > 64, order > 8)  */
+  CB_ERR_DIVERGED = 5,     /* ALS non-finite grams -> ValueError (cpd_als.py:107-108)  */
+  CB_ERR_STATE = 6         /* handle used out of order                               */
+} cb_status;
+
+typedef enum { CB_F32 = 0, CB_F64 = 1 } cb_dtype;
+
+const char* cb_last_error(void);
+int cb_abi_version(void);
+/* number of this library's kernels launched by the calling thread since the
+ * last reset (the bench's "gpu_launches" evidence). */
+long long cb_launch_count(void);
+void cb_launch_count_reset(void);
+
+/* ------------------------------------------------------------------------
+ * Operator level (device pointers in, device pointers out, async on stream)
+ * ---------------------------------------------------------------------- */
+
+/* out[I_mode x rank] = X_(mode) . KR_{-mode}; `factors` is a host array of
+ * `order` device pointers.  Replaces solver.py:243-245 factor_linear_term
+ * (and the matricize/factors_khatri_rao pair tensor_ops.py:45-54, 88-95). */
+int cb_mttkrp(int dtype, const void* X, int order, const int64_t* dims,
+              const double* const* factors, int rank, int mode, double* out,
+              void* stream);
+
+/* Khatri-Rao product of `nmats` row-major matrices (first slowest), out has
+ * prod(rows) x rank entries.  Replaces tensor_ops.py:66-85 khatri_rao. */
+int cb_khatri_rao(const double* const* mats, int nmats, const int64_t* rows, int rank,
+                  double* out, void* stream);
+
+/* out[ra x rb] = hadamard_{m != skip} mats[m]^T mats2[m] (mats2 NULL -> mats),
+ * product taken in mode order; skip < 0 means none.
+ * Replaces tensor_ops.py:98-124 hadamard_gram. */
+int cb_hadamard_gram(const double* const* mats, const double* const* mats2,
+                     const int64_t* rows, int nmodes, int skip, int ra, int rb,
+                     double* out, void* stream);
+
+/* out[b] = max(lambda_max(g_b), 0), 0 for an all-zero matrix; g is batch x r x r,
+ * r <= 64.  Replaces tensor_ops.py:127-140 spectral_norm (LAPACK syevd). */
+int cb_spectral_norm_batched(const double* g, int r, int batch, double* out, void* stream);
+
+/* out3 = {sum of squares, min value, count of non-finite values} of X[0:n] in
+ * fp64.  Feeds CoupledProblem.validate (solver.py:114-117) and ||M||^2
+ * (solver.py:327). */
+int cb_tensor_stats(int dtype, const void* X, int64_t n, double* out3, void* stream);
+
+/* *out = || X - [[weights; factors]] ||_F^2 by an explicit streaming residual.
+ * Replaces the residual of solver.py:194-202 objective(). */
+int cb_kruskal_residual(int dtype, const void* X, int order, const int64_t* dims,
+                        const double* const* factors, const double* weights, int rank,
+                        double* out, void* stream);
+
+/* out[r] = sum_i a[i,r] * b[i,r]  (einsum "ir,ir->r", solver.py:218, :507-511). */
+int cb_rowdot(const double* a, const double* b, int64_t rows, int r, double* out,
+              void* stream);
+
+/* C = alpha * op(A) op(B) + beta * C, fp64 row-major, small shapes.  Used by
+ * the operator-level lra linear terms and gradients (solver.py:205-251). */
+int cb_gemm(int trans_a, int trans_b, int m, int n, int k, double alpha, const double* a,
+            int lda, const double* b, int ldb, double beta, double* c, int ldc,
+            void* stream);
+
+/* out = u_hat (gram_skip o lam lam^T) - mtt o lam  (solver.py:232-240). */
+int cb_factor_gradient(const double* u_hat, int64_t rows, const double* gram_skip,
+                       const double* mtt, const double* lam, int r, double* out,
+                       void* stream);
+
+/* ------------------------------------------------------------------------
+ * CP-ALS compression engine (cpd_als.py:52-120), batched over blocks.
+ * Each block is an independent ALS fit with its own stop rule.
+ * ---------------------------------------------------------------------- */
+typedef struct cb_als cb_als;
+
+typedef struct {
+  int n_blocks;
+  int order;                      /* <= 8                                   */
+  const int64_t* dims;            /* host, n_blocks*order                   */
+  const int* ranks;               /* host, n_blocks (<= 64)                 */
+  int dtype;                      /* cb_dtype of the tensors                */
+  const void* const* tensors;     /* host array of device pointers          */
+  const double* const* init;      /* host array (n_blocks*order) of host
+                                     I_n x R row-major initial factors      */
+  double tol;                     /* AlsOptions.tol                         */
+  int max_iter;                   /* AlsOptions.max_iter                    */
+} cb_als_desc;
+
+int cb_als_create(const cb_als_desc* desc, void* stream, cb_als** out);
+/* runs every block to convergence or max_iter; synchronises the stream */
+int cb_als_run(cb_als* h);
+/* per block: rel_err, n_iter, converged flag, and the rel-err history
+ * (history capacity max_iter doubles); factors copied to host row-major. */
+int cb_als_block_result(cb_als* h, int block, double* rel_err, int* n_iter, int* converged,
+                        double* history, double* const* host_factors);
+/* device pointer of the fitted factor (block, mode), valid until destroy */
+const double* cb_als_factor_device(cb_als* h, int block, int mode);
+int cb_als_destroy(cb_als* h);
+
+/* ------------------------------------------------------------------------
+ * APG solver engine (solver.py:546-624 with the _Apg state machine
+ * solver.py:311-543), device-resident: sweep, evaluation, restart rule and
+ * stop rule all run on the GPU; the host only launches and polls a flag.
+ * ---------------------------------------------------------------------- */
+typedef struct cb_solver cb_solver;
+
+typedef struct {
+  int n_blocks;                   /* blocks owned by this process            */
+  int order;
+  const int64_t* dims;            /* host, n_blocks*order                    */
+  const int* ranks;               /* host, n_blocks                          */
+  const int* coupled;             /* host, order (L_n)                       */
+  int lra;                        /* 0 = CoNCPD-APG, 1 = lraCoNCPD-APG       */
+  int update_core;                /* 0 = fixed-core variant                  */
+  int dtype;                      /* tensor storage dtype                    */
+  const void* const* tensors;     /* host array of device pointers           */
+  const double* const* init_factors;  /* host (n_blocks*order) host arrays   */
+  const double* const* init_weights;  /* host (n_blocks) host arrays         */
+  const int* tilde_ranks;             /* lra: host, n_blocks                 */
+  const double* const* tilde_factors; /* lra: host array of DEVICE pointers  */
+  const double* const* tilde_weights; /* lra: host array of HOST arrays      */
+  int objective;                  /* 0 = explicit residual, 1 = gram expansion */
+  double delta_w;
+  double tol;
+  int max_iter;
+  /* multi-GPU block sharding (world_size 1: all NULL/0) */
+  int world_size;
+  int rank_id;
+  void* nccl_comm;                /* ncclComm_t created by cb_nccl_comm_init */
+  int total_blocks;               /* S over all ranks                        */
+  int block_offset;               /* global index of this rank's first block */
+} cb_solver_desc;
+
+typedef struct {
+  int n_iter;
+  int n_restarts;
+  int done;
+  int reason;                     /* 0 max_iterations, 1 tolerance           */
+  int error;                      /* 0 ok, CB_ERR_NONFINITE                  */
+  int error_block;
+  int error_iter;
+} cb_solver_summary;
+
+int cb_solver_create(const cb_solver_desc* desc, void* stream, cb_solver** out);
+/* run up to `iters` more iterations (device stops early at tolerance);
+ * synchronises and reports the summary. */
+int cb_solver_run(cb_solver* h, int iters, cb_solver_summary* summary);
+/* enqueue exactly one APG iteration (sweep, evaluation, restart rule, stop
+ * rule) without synchronising: the bench's timed step. */
+int cb_solver_step_async(cb_solver* h);
+int cb_solver_summary_get(cb_solver* h, cb_solver_summary* summary);
+/* per accepted iteration 0..n_iter: internal objective, original-tensor
+ * objective, RelErr, device timestamp (ns) */
+int cb_solver_history(cb_solver* h, double* obj_int, double* obj_orig, double* rel,
+                      double* t_ns, int cap);
+int cb_solver_block_factors(cb_solver* h, int block, double* const* host_factors,
+                            double* host_weights);
+/* CUDA-event timing of the dominant tensor-streaming kernel: on/off, and the
+ * accumulated (milliseconds, launches, algorithmic bytes). */
+int cb_solver_set_timing(cb_solver* h, int on);
+int cb_solver_timing(cb_solver* h, double* ms, long long* launches, double* bytes);
+int cb_solver_destroy(cb_solver* h);
+
+/* NCCL communicator for the block-sharded multi-GPU path. `unique_id` is the
+ * 128-byte ncclUniqueId produced on rank 0 (cb_nccl_unique_id) and broadcast
+ * by the caller (torch.distributed). */
+int cb_nccl_unique_id(void* out128);
+int cb_nccl_comm_init(const void* unique_id128, int world_size, int rank, void** comm);
+int cb_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CONCPD_B200_H */

@@ -1,0 +1,76 @@
+"""Device-memory plumbing: numpy <-> torch CUDA buffers for the C ABI.
+
+PyTorch is used only for device allocation, streams and copies; all
+arithmetic on the hot path happens in libconcpd_b200.so kernels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+def torch_mod():
+    return _lib.require_cuda()
+
+
+def device():
+    torch = torch_mod()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_dev_f64(a):
+    """Upload a numpy matrix (row-major) as a contiguous fp64 CUDA tensor."""
+    torch = torch_mod()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return torch.from_numpy(arr).to(device(), non_blocking=False)
+
+
+def tensor_to_dev(t, dtype="fp64"):
+    """Upload a tensor in first-index-fastest (Fortran) physical order.
+
+    numpy arrays of any layout are converted (a Fortran-contiguous array is
+    copied without reordering).  torch CUDA tensors are accepted as given if
+    their memory is already Fortran-ordered for their logical shape.
+    Returns (flat CUDA tensor, dims tuple).
+    """
+    torch = torch_mod()
+    want = torch.float64 if dtype == "fp64" else torch.float32
+    if isinstance(t, torch.Tensor):
+        dims = tuple(int(d) for d in t.shape)
+        if t.is_cuda and t.dtype == want and tuple(t.stride()) == fortran_strides(dims):
+            return t.as_strided((t.numel(),), (1,)), dims      # already first-index-fastest
+        perm = tuple(range(t.ndim - 1, -1, -1))
+        flat = t.permute(*perm).contiguous().reshape(-1)   # Fortran order of t
+        return flat.to(device=device(), dtype=want), dims
+    a = np.asarray(t)
+    dims = tuple(int(d) for d in a.shape)
+    np_dtype = np.float64 if dtype == "fp64" else np.float32
+    flat = np.ravel(np.asarray(a, dtype=np_dtype), order="F")
+    return torch.from_numpy(np.ascontiguousarray(flat)).to(device()), dims
+
+
+def fortran_strides(dims):
+    st, acc = [], 1
+    for d in dims:
+        st.append(acc)
+        acc *= int(d)
+    return tuple(st)
+
+
+def fortran_view(flat, dims):
+    """Logical-shape view of a flat first-index-fastest CUDA buffer."""
+    return flat.as_strided(tuple(int(d) for d in dims), fortran_strides(dims))
+
+
+def ptr(x):
+    return x.data_ptr()
+
+
+def stream():
+    return _lib.stream_handle()
+
+
+def to_host(x):
+    return x.detach().cpu().numpy()

@@ -1,0 +1,859 @@
+// APG solver engine: host orchestration + C ABI (cb_solver_*).
+//
+// Mirrors solve() (pkg/src/concpd/solver.py:546-624).  The whole iteration —
+// core update, N mode updates with common-column aggregation, evaluation,
+// restart branch and stop rule — is enqueued without host round trips; for
+// the 3-way fast path one iteration is captured once in a CUDA graph and
+// replayed.  The host polls the device `done` flag every few iterations.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "engine_kernels.cuh"
+#include "ops_internal.h"
+#include "status.h"
+#include "engine_host.h"
+
+namespace cb {
+
+template <typename TE, int RB>
+static void launch_fiber_t(int want_t, int want_b, int want_res, const XArgs& a,
+                           const FibUnit* u, int n, cudaStream_t st) {
+  if (want_t && want_b && want_res) fiber_kernel<TE, RB, true, true, true><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else if (want_t && want_b) fiber_kernel<TE, RB, true, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else if (want_t && want_res) fiber_kernel<TE, RB, true, false, true><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else if (want_t) fiber_kernel<TE, RB, true, false, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else fiber_kernel<TE, RB, false, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+}
+
+template <typename TE>
+static void launch_fiber_r(int rb, int want_t, int want_b, int want_res, const XArgs& a,
+                           const FibUnit* u, int n, cudaStream_t st) {
+  switch (rb) {
+    case 8: launch_fiber_t<TE, 8>(want_t, want_b, want_res, a, u, n, st); break;
+    case 16: launch_fiber_t<TE, 16>(want_t, want_b, want_res, a, u, n, st); break;
+    case 32: launch_fiber_t<TE, 32>(want_t, want_b, want_res, a, u, n, st); break;
+    case 40: launch_fiber_t<TE, 40>(want_t, want_b, want_res, a, u, n, st); break;
+    default: launch_fiber_t<TE, 64>(want_t, want_b, want_res, a, u, n, st); break;
+  }
+}
+
+void launch_fiber(int dtype, int rb, int want_t, int want_b, int want_res, const XArgs& a,
+                  const FibUnit* u, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  if (dtype == CB_F32) launch_fiber_r<float>(rb, want_t, want_b, want_res, a, u, n, st);
+  else launch_fiber_r<double>(rb, want_t, want_b, want_res, a, u, n, st);
+  count_launch(1);
+}
+
+template <typename TE, int RB, int SB>
+static void launch_slab_t(const XArgs& a, const SlabUnit* u, int n, size_t sm, cudaStream_t st) {
+  if (n < 0) {   // attribute setup call (outside any graph capture)
+    cudaFuncSetAttribute(slab_kernel<TE, RB, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    return;
+  }
+  slab_kernel<TE, RB, SB><<<n, SLAB_THREADS, sm, st>>>(a, u);
+}
+
+int slab_sb_for(int rb) { return rb <= 8 ? 8 : rb <= 16 ? 4 : rb <= 32 ? 2 : 1; }
+
+template <typename TE>
+static void launch_slab_r(int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
+                          cudaStream_t st) {
+  switch (rb) {
+    case 8: launch_slab_t<TE, 8, 8>(a, u, n, sm, st); break;
+    case 16: launch_slab_t<TE, 16, 4>(a, u, n, sm, st); break;
+    case 32: launch_slab_t<TE, 32, 2>(a, u, n, sm, st); break;
+    case 40: launch_slab_t<TE, 40, 1>(a, u, n, sm, st); break;
+    default: launch_slab_t<TE, 64, 1>(a, u, n, sm, st); break;
+  }
+}
+
+void prepare_slab(int dtype, int rb, size_t sm) {
+  XArgs a{};
+  if (dtype == CB_F32) launch_slab_r<float>(rb, a, nullptr, -1, sm, 0);
+  else launch_slab_r<double>(rb, a, nullptr, -1, sm, 0);
+}
+
+void launch_slab(int dtype, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
+                 cudaStream_t st) {
+  if (n <= 0) return;
+  if (dtype == CB_F32) launch_slab_r<float>(rb, a, u, n, sm, st);
+  else launch_slab_r<double>(rb, a, u, n, sm, st);
+  count_launch(1);
+}
+
+void launch_contract(int dtype, int mode, const XArgs& a, const RowUnit* u, int n,
+                     cudaStream_t st) {
+  if (n <= 0) return;
+  if (mode == 0) {
+    if (dtype == CB_F32) contract0_kernel<float><<<n, 256, 0, st>>>(a, u);
+    else contract0_kernel<double><<<n, 256, 0, st>>>(a, u);
+  } else {
+    if (dtype == CB_F32) contract1_kernel<float><<<n, 256, 0, st>>>(a, u);
+    else contract1_kernel<double><<<n, 256, 0, st>>>(a, u);
+  }
+  count_launch(1);
+}
+
+int rank_bucket(int r) { return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 40 ? 40 : 64; }
+
+void build_xtables(int S, const long long* dims, const int* R, int rb, int dtype, XTables& t) {
+  const int target = 148 * 4;
+  long long tiles = 0;
+  for (int s = 0; s < S; ++s) tiles += (dims[3 * s] * dims[3 * s + 1] + FIB_THREADS - 1) / FIB_THREADS;
+  t.fib.clear(); t.fib_first.assign(S + 1, 0); t.nsplit.assign(S, 1);
+  for (int s = 0; s < S; ++s) {
+    const long long J = dims[3 * s] * dims[3 * s + 1];
+    const long long I2 = dims[3 * s + 2];
+    int ns = 1;
+    while (tiles * ns < target && I2 / (ns * 2) >= 16) ns *= 2;
+    t.nsplit[s] = ns;
+    t.fib_first[s] = (int)t.fib.size();
+    for (int sp = 0; sp < ns; ++sp)
+      for (long long j0 = 0; j0 < J; j0 += FIB_THREADS) t.fib.push_back(FibUnit{s, sp, j0});
+  }
+  t.fib_first[S] = (int)t.fib.size();
+  t.sb = slab_sb_for(rb);
+  long long groups = 0;
+  for (int s = 0; s < S; ++s) groups += (dims[3 * s + 2] + t.sb - 1) / t.sb;
+  t.slab.clear(); t.slab_first.assign(S, 0); t.slab_nchunk.assign(S, 1);
+  long long maxI01 = 0;
+  for (int s = 0; s < S; ++s) {
+    const long long J = dims[3 * s] * dims[3 * s + 1];
+    const long long I2 = dims[3 * s + 2];
+    int nch = 1;
+    while (groups * nch < target && J / (nch * 2) >= 4 * SLAB_THREADS) nch *= 2;
+    t.slab_nchunk[s] = nch;
+    t.slab_first[s] = (int)t.slab.size();
+    const long long per = (J + nch - 1) / nch;
+    for (long long g0 = 0; g0 < I2; g0 += t.sb)
+      for (int ch = 0; ch < nch; ++ch) {
+        long long k0 = ch * per, k1 = std::min(J, k0 + per);
+        t.slab.push_back(SlabUnit{s, (int)g0, k0, k1});
+      }
+    maxI01 = std::max(maxI01, dims[3 * s] + dims[3 * s + 1]);
+  }
+  t.slab_smem = (size_t)maxI01 * rb * (dtype == CB_F32 ? 4 : 8);
+  t.c0.clear(); t.c1.clear();
+  for (int s = 0; s < S; ++s) {
+    const long long n0 = dims[3 * s] * R[s];
+    for (long long e = 0; e < n0; e += 256) t.c0.push_back(RowUnit{s, (int)e});
+    const long long n1 = dims[3 * s + 1] * R[s];
+    for (long long p = 0; p < n1; p += 8) t.c1.push_back(RowUnit{s, (int)p});
+  }
+}
+
+static thread_local cudaStream_t g_alloc_stream = nullptr;
+
+int dalloc(void** p, size_t bytes, std::vector<void*>& allocs) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 8;
+  CB_CUDA(cudaMalloc(p, bytes));
+  allocs.push_back(*p);
+  CB_CUDA(cudaMemsetAsync(*p, 0, bytes, g_alloc_stream));
+  return CB_OK;
+}
+
+void set_alloc_stream(cudaStream_t st) { g_alloc_stream = st; }
+
+}  // namespace cb
+
+using namespace cb;
+
+struct cb_solver {
+  cudaStream_t st = nullptr;
+  int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0;
+  int rmax = 1, rtmax = 0, rb = 8, max_iter = 0;
+  double delta_w = 0.9999, tol = 1e-8;
+  std::vector<long long> dims;
+  std::vector<int> R, Rt;
+  int counts[CB_MAX_ORDER] = {0};
+  std::vector<const void*> X;
+  std::vector<void*> allocs;
+  Ctx ctx{};
+  XArgs xa_main{}, xa_redo{};
+  XTables tab;
+  FibUnit* d_fib = nullptr;
+  SlabUnit* d_slab = nullptr;
+  RowUnit *d_c0 = nullptr, *d_c1 = nullptr;
+  std::vector<RowUnit*> d_rows;
+  std::vector<int> n_rows;
+  State* d_state = nullptr;
+  State* h_state = nullptr;     // pinned mirror
+  size_t blk_smem = 0, mu_smem = 0, qr_smem = 0;
+  std::vector<double*> h_U;     // device pointer tables mirrored on host
+  std::vector<double*> h_MTT;
+  std::vector<double*> h_LAM;
+  long long launches_per_iter = 0;
+  double* kr_scratch = nullptr; // generic path
+  double* res_part = nullptr;
+  int res_nparts = 0;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_ok = true;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  double t_ms = 0.0, t_bytes = 0.0;
+  long long t_launches = 0;
+  long long elem_total = 0;
+  int elem_bytes = 8;
+  int iters_enqueued = 0;
+  bool init_done = false;
+};
+
+namespace cb {
+
+static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b) {
+  while (h->ev_pool.size() < h->ev_used + 2) {
+    cudaEvent_t e;
+    CB_CUDA(cudaEventCreate(&e));
+    h->ev_pool.push_back(e);
+  }
+  *a = h->ev_pool[h->ev_used];
+  *b = h->ev_pool[h->ev_used + 1];
+  h->ev_used += 2;
+  return CB_OK;
+}
+
+// stream the blocks once through the fiber kernel (optionally timed)
+static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, int want_res) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) { int rc = ev_pair(h, &e0, &e1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+  launch_fiber(h->dtype, h->rb, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(), h->st);
+  CB_CHECK_LAUNCH();
+  if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
+  return CB_OK;
+}
+
+static int enqueue_slab(cb_solver* h, const XArgs& a) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) { int rc = ev_pair(h, &e0, &e1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+  launch_slab(h->dtype, h->rb, a, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, h->st);
+  CB_CHECK_LAUNCH();
+  if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
+  return CB_OK;
+}
+
+// generic-order helpers (per-block launches, host-driven restart)
+static int generic_mttkrp(cb_solver* h, int s, int n) {
+  std::vector<const double*> f(h->N);
+  for (int m = 0; m < h->N; ++m) f[m] = h->h_U[s * h->N + m];
+  return mttkrp_one(h->dtype, h->X[s], h->N, reinterpret_cast<const int64_t*>(&h->dims[s * h->N]), f.data(), h->R[s], n,
+                    h->h_MTT[s], h->kr_scratch, h->st);
+}
+
+static int generic_rowdot_into(cb_solver* h, int s, int n, double* out);
+static int generic_residuals(cb_solver* h);
+
+// one sweep (solver.py:459-463); redo = restart sweep with w_hat = 0
+static int enqueue_sweep(cb_solver* h, int redo) {
+  cudaStream_t st = h->st;
+  const XArgs& xa = redo ? h->xa_redo : h->xa_main;
+  k_sweep_begin<<<h->S, 256, h->blk_smem, st>>>(h->ctx, redo);
+  count_launch(1);
+  CB_CHECK_LAUNCH();
+  for (int n = 0; n < h->N; ++n) {
+    int src = 0;
+    if (h->lra) {
+      src = 2;
+    } else if (h->fast3) {
+      if (n < 2) {
+        launch_contract(h->dtype, n, xa, n == 0 ? h->d_c0 : h->d_c1,
+                        (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
+        CB_CHECK_LAUNCH();
+      } else {
+        int rc = enqueue_slab(h, xa);
+        if (rc) return rc;
+        src = 1;
+      }
+    } else {
+      for (int s = 0; s < h->S; ++s) {
+        int rc = generic_mttkrp(h, s, n);
+        if (rc) return rc;
+      }
+    }
+    k_mode_update<<<h->n_rows[n], 256, h->mu_smem, st>>>(h->ctx, n, redo, src, h->d_rows[n]);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+    k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
+  return CB_OK;
+}
+
+static int enqueue_qr(cb_solver* h, int redo) {
+  k_qr_factor<<<h->S * h->N, 256, h->qr_smem, h->st>>>(h->ctx, redo);
+  k_qr_core<<<h->S * h->ctx.qr_nchunks, 256, 0, h->st>>>(h->ctx, redo);
+  count_launch(2);
+  CB_CHECK_LAUNCH();
+  return CB_OK;
+}
+
+static int enqueue_control(cb_solver* h, int mode) {
+  k_control<<<1, 32, 0, h->st>>>(h->ctx, mode, h->fast3 ? 0 : 1);
+  count_launch(1);
+  CB_CHECK_LAUNCH();
+  return CB_OK;
+}
+
+// evaluation after a sweep (full mode): fiber pass (fast3) or generic terms
+static int enqueue_eval_full(cb_solver* h, int redo) {
+  if (h->fast3) {
+    XArgs a = redo ? h->xa_redo : h->xa_main;
+    a.t_other = 1;   // write the non-accepted T buffer
+    return enqueue_fiber(h, a, 1, 1, h->objective == 0 ? 1 : 0);
+  }
+  // generic: b from the last mode's MTTKRP (solver.py:506-509), residuals
+  for (int s = 0; s < h->S; ++s) {
+    int rc = generic_rowdot_into(h, s, h->N - 1, nullptr);
+    if (rc) return rc;
+  }
+  if (h->objective == 0) return generic_residuals(h);
+  return CB_OK;
+}
+
+static int enqueue_trace_lra(cb_solver* h) {
+  if (h->fast3) return enqueue_fiber(h, h->xa_main, 0, 1, 0);
+  for (int s = 0; s < h->S; ++s) {
+    int rc = generic_mttkrp(h, s, 0);
+    if (rc) return rc;
+    rc = generic_rowdot_into(h, s, 0, h->ctx.borig + (long long)s * RSTRIDE);
+    if (rc) return rc;
+  }
+  return CB_OK;
+}
+
+// one full APG iteration (solver.py:586-610), device-gated
+static int enqueue_iteration(cb_solver* h) {
+  int rc;
+  if (!h->lra) {
+    if ((rc = enqueue_sweep(h, 0))) return rc;
+    if ((rc = enqueue_eval_full(h, 0))) return rc;
+    if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
+    // restart branch (no-ops unless go_redo)
+    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+    if ((rc = enqueue_sweep(h, 1))) return rc;
+    if ((rc = enqueue_eval_full(h, 1))) return rc;
+    if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
+  } else {
+    if ((rc = enqueue_sweep(h, 0))) return rc;
+    if ((rc = enqueue_qr(h, 0))) return rc;
+    if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
+    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+    if ((rc = enqueue_sweep(h, 1))) return rc;
+    if ((rc = enqueue_qr(h, 1))) return rc;
+    if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
+    if ((rc = enqueue_trace_lra(h))) return rc;
+    if ((rc = enqueue_control(h, CTRL_FINISH))) return rc;
+  }
+  return CB_OK;
+}
+
+static int read_state(cb_solver* h) {
+  CB_CUDA(cudaMemcpyAsync(h->h_state, h->d_state, sizeof(State), cudaMemcpyDeviceToHost, h->st));
+  CB_CUDA(cudaStreamSynchronize(h->st));
+  return CB_OK;
+}
+
+// generic path: iteration with a host-side restart decision
+static int generic_iteration(cb_solver* h) {
+  int rc;
+  if ((rc = enqueue_sweep(h, 0))) return rc;
+  if (!h->lra) {
+    if ((rc = enqueue_eval_full(h, 0))) return rc;
+  } else if ((rc = enqueue_qr(h, 0))) return rc;
+  if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
+  if ((rc = read_state(h))) return rc;
+  if (h->h_state->go_redo) {
+    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+    if ((rc = enqueue_sweep(h, 1))) return rc;
+    if (!h->lra) {
+      if ((rc = enqueue_eval_full(h, 1))) return rc;
+    } else if ((rc = enqueue_qr(h, 1))) return rc;
+    if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
+  }
+  if (h->lra) {
+    if ((rc = enqueue_trace_lra(h))) return rc;
+    if ((rc = enqueue_control(h, CTRL_FINISH))) return rc;
+  }
+  return CB_OK;
+}
+
+static int generic_rowdot_into(cb_solver* h, int s, int n, double* out) {
+  // b[r] = sum_i U_n[i,r] MTT[i,r]; default target: staged b buffer 1 - bsel
+  // (bsel is read on the host: generic path syncs every iteration)
+  double* dst = out;
+  if (!dst) {
+    const int bsel = h->h_state->bsel;
+    dst = h->ctx.bbuf + ((long long)(1 - bsel) * h->S + s) * RSTRIDE;
+  }
+  return ::cb_rowdot(h->h_U[s * h->N + n], h->h_MTT[s], h->dims[s * h->N + n], h->R[s], dst,
+                   (void*)h->st);
+}
+
+static int generic_residuals(cb_solver* h) {
+  for (int s = 0; s < h->S; ++s) {
+    ResidArgs a{};
+    a.order = h->N; a.R = h->R[s]; a.n = 1;
+    a.w = h->h_LAM[s];
+    for (int m = 0; m < h->N; ++m) {
+      a.dims[m] = h->dims[s * h->N + m];
+      a.U[m] = h->h_U[s * h->N + m];
+      a.n *= a.dims[m];
+    }
+    int rc = kruskal_residual(h->dtype, a, h->X[s], h->ctx.res + s, h->res_part, h->res_nparts, h->st);
+    if (rc) return rc;
+  }
+  return CB_OK;
+}
+
+static int init_evaluation(cb_solver* h) {
+  int rc;
+  k_init_block<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+  count_launch(1);
+  CB_CHECK_LAUNCH();
+  if (!h->lra) {
+    if (h->fast3) {
+      XArgs a = h->xa_main;
+      a.t_other = 1;
+      if ((rc = enqueue_fiber(h, a, 1, 1, h->objective == 0 ? 1 : 0))) return rc;
+    } else {
+      // iteration 0 stages b from the mode-0 unfolding (solver.py:510-511)
+      for (int s = 0; s < h->S; ++s) {
+        if ((rc = generic_mttkrp(h, s, 0))) return rc;
+        if ((rc = generic_rowdot_into(h, s, 0, nullptr))) return rc;
+      }
+      if (h->objective == 0 && (rc = generic_residuals(h))) return rc;
+    }
+  } else {
+    if ((rc = enqueue_qr(h, 0))) return rc;
+    if ((rc = enqueue_trace_lra(h))) return rc;
+  }
+  return enqueue_control(h, CTRL_INIT);
+}
+
+}  // namespace cb
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
+  CB_ARG(d && out, "null descriptor");
+  *out = nullptr;
+  CB_ARG(d->n_blocks >= 1, "no tensors");
+  CB_ARG(d->order >= 1 && d->order <= CB_MAX_ORDER, "order %d outside [1, %d]", d->order, CB_MAX_ORDER);
+  CB_ARG(d->dtype == CB_F32 || d->dtype == CB_F64, "bad dtype");
+  CB_ARG(d->world_size <= 1, "multi-rank solves go through the sharded driver");
+  cb_solver* h = new cb_solver();
+  h->st = (cudaStream_t)stream;
+  h->S = d->n_blocks; h->N = d->order; h->lra = d->lra; h->update_core = d->update_core;
+  h->dtype = d->dtype; h->objective = d->objective; h->delta_w = d->delta_w; h->tol = d->tol;
+  h->max_iter = d->max_iter;
+  const int S = h->S, N = h->N;
+  h->dims.assign(d->dims, d->dims + S * N);
+  h->R.assign(d->ranks, d->ranks + S);
+  for (int n = 0; n < N; ++n) h->counts[n] = d->coupled[n];
+  h->X.assign(d->tensors, d->tensors + S);
+  for (int s = 0; s < S; ++s) {
+    if (h->R[s] < 1 || h->R[s] > CB_MAX_RANK) {
+      delete h;
+      set_error("rank %d outside [1, %d]", d->ranks[s], CB_MAX_RANK);
+      return CB_ERR_UNSUPPORTED;
+    }
+    h->rmax = std::max(h->rmax, h->R[s]);
+  }
+  if (h->lra) {
+    h->Rt.assign(d->tilde_ranks, d->tilde_ranks + S);
+    for (int s = 0; s < S; ++s) {
+      h->rtmax = std::max(h->rtmax, h->Rt[s]);
+      if (h->Rt[s] + h->R[s] > QR_MAXC || h->Rt[s] > CB_MAX_RANK) {
+        delete h;
+        set_error("compression rank %d + rank %d exceeds the QR route limit %d", d->tilde_ranks[s],
+                  d->ranks[s], QR_MAXC);
+        return CB_ERR_UNSUPPORTED;
+      }
+    }
+  } else {
+    h->Rt.assign(S, 0);
+  }
+  h->fast3 = (N == 3);
+  h->rb = rank_bucket(h->rmax);
+  h->elem_bytes = h->dtype == CB_F32 ? 4 : 8;
+  for (int s = 0; s < S; ++s) {
+    long long e = 1;
+    for (int n = 0; n < N; ++n) e *= h->dims[s * N + n];
+    h->elem_total += e;
+  }
+  std::vector<void*>& A = h->allocs;
+  cudaStream_t st = h->st;
+  set_alloc_stream(st);
+  int rc = CB_OK;
+#define TRY(x) do { rc = (x); if (rc) { cb_solver_destroy(h); return rc; } } while (0)
+  // ---- per-(s,n) factor buffers
+  std::vector<double*> U(S * N), Up(S * N), Un(S * N), G(S * N), C(S * N), Ut(S * N);
+  std::vector<double*> LAM(S), LAMP(S), TW(S), STEP(S), MTT(S);
+  long long maxIn = 0;
+  for (int s = 0; s < S; ++s) {
+    const int Rs = h->R[s];
+    long long mI = 0;
+    for (int n = 0; n < N; ++n) {
+      const long long In = h->dims[s * N + n];
+      mI = std::max(mI, In);
+      const size_t fb = sizeof(double) * In * Rs;
+      TRY(dalloc((void**)&U[s * N + n], fb, A));
+      TRY(dalloc((void**)&Up[s * N + n], fb, A));
+      TRY(dalloc((void**)&Un[s * N + n], fb, A));
+      TRY(dalloc((void**)&G[s * N + n], sizeof(double) * Rs * Rs, A));
+      CB_CUDA(cudaMemcpyAsync(U[s * N + n], d->init_factors[s * N + n], fb, cudaMemcpyHostToDevice, st));
+      CB_CUDA(cudaMemcpyAsync(Up[s * N + n], d->init_factors[s * N + n], fb, cudaMemcpyHostToDevice, st));
+      if (h->lra) {
+        const int Rts = h->Rt[s];
+        TRY(dalloc((void**)&C[s * N + n], sizeof(double) * Rts * Rs, A));
+        TRY(dalloc((void**)&Ut[s * N + n], sizeof(double) * In * Rts, A));
+        CB_CUDA(cudaMemcpyAsync(Ut[s * N + n], d->tilde_factors[s * N + n], sizeof(double) * In * Rts,
+                                cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    maxIn = std::max(maxIn, mI);
+    TRY(dalloc((void**)&LAM[s], sizeof(double) * Rs, A));
+    TRY(dalloc((void**)&LAMP[s], sizeof(double) * Rs, A));
+    CB_CUDA(cudaMemcpyAsync(LAM[s], d->init_weights[s], sizeof(double) * Rs, cudaMemcpyHostToDevice, st));
+    CB_CUDA(cudaMemcpyAsync(LAMP[s], d->init_weights[s], sizeof(double) * Rs, cudaMemcpyHostToDevice, st));
+    TRY(dalloc((void**)&STEP[s], sizeof(double) * Rs * Rs, A));
+    TRY(dalloc((void**)&MTT[s], sizeof(double) * mI * Rs, A));
+    if (h->lra) {
+      TRY(dalloc((void**)&TW[s], sizeof(double) * h->Rt[s], A));
+      CB_CUDA(cudaMemcpyAsync(TW[s], d->tilde_weights[s], sizeof(double) * h->Rt[s], cudaMemcpyHostToDevice, st));
+    }
+  }
+  h->h_U = U;
+  h->h_MTT = MTT;
+  h->h_LAM = LAM;
+  Ctx& c = h->ctx;
+  c.S = S; c.N = N; c.lra = h->lra; c.update_core = h->update_core; c.objective = h->objective;
+  c.fast3 = h->fast3; c.max_iter = h->max_iter; c.rmax = std::max(h->rmax, h->rtmax);
+  for (int n = 0; n < N; ++n) c.counts[n] = h->counts[n];
+  c.delta_w = h->delta_w; c.tol = h->tol;
+  long long* d_dims; int *d_R, *d_Rt;
+  TRY(upload(h->dims, &d_dims, A, st)); c.dims = d_dims;
+  TRY(upload(h->R, &d_R, A, st)); c.R = d_R;
+  TRY(upload(h->Rt, &d_Rt, A, st)); c.Rt = d_Rt;
+  double** p;
+  TRY(upload(U, &p, A, st)); c.U = p;
+  TRY(upload(Up, &p, A, st)); c.Up = p;
+  TRY(upload(Un, &p, A, st)); c.Un = p;
+  TRY(upload(G, &p, A, st)); c.G = p;
+  TRY(upload(LAM, &p, A, st)); c.LAM = p;
+  TRY(upload(LAMP, &p, A, st)); c.LAMP = p;
+  TRY(upload(STEP, &p, A, st)); c.STEP = p;
+  TRY(upload(MTT, &p, A, st)); c.MTT = p;
+  if (h->lra) {
+    TRY(upload(C, &p, A, st)); c.C = p;
+    TRY(upload(Ut, &p, A, st)); c.Ut = p;
+    TRY(upload(TW, &p, A, st)); c.TW = p;
+  }
+  TRY(dalloc((void**)&c.lipc_hist, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
+  TRY(dalloc((void**)&c.lu, sizeof(double) * N * S, A));
+  TRY(dalloc((void**)&c.lup, sizeof(double) * N * S, A));
+  TRY(dalloc((void**)&c.nsq, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.bbuf, sizeof(double) * 2 * S * RSTRIDE, A));
+  TRY(dalloc((void**)&c.model_sq, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.inner, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.res_t, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.tsq, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.res, sizeof(double) * S, A));
+  TRY(dalloc((void**)&c.borig, sizeof(double) * S * RSTRIDE, A));
+  int maxL = 0;
+  for (int n = 0; n < N; ++n) maxL = std::max(maxL, h->counts[n]);
+  c.gc_stride = maxIn * std::max(maxL, 1);
+  TRY(dalloc((void**)&c.gc_part, sizeof(double) * S * c.gc_stride, A));
+  TRY(dalloc((void**)&c.gc_valid, sizeof(int) * S, A));
+  TRY(dalloc((void**)&c.cnew, sizeof(double) * c.gc_stride, A));
+  TRY(dalloc((void**)&c.tile_cnt, sizeof(int) * (maxIn / MU_ROWS + 2), A));
+  if (h->lra) {
+    TRY(dalloc((void**)&c.qr_buf, sizeof(double) * (size_t)S * N * QR_MAXC * QR_MAXC, A));
+    c.qr_nchunks = 8;
+    TRY(dalloc((void**)&c.qr_part, sizeof(double) * S * c.qr_nchunks, A));
+  }
+  TRY(dalloc((void**)&c.h_obj, sizeof(double) * (h->max_iter + 1), A));
+  TRY(dalloc((void**)&c.h_orig, sizeof(double) * (h->max_iter + 1), A));
+  TRY(dalloc((void**)&c.h_rel, sizeof(double) * (h->max_iter + 1), A));
+  TRY(dalloc((void**)&c.h_tns, sizeof(double) * (h->max_iter + 1), A));
+  TRY(dalloc((void**)&h->d_state, sizeof(State), A));
+  c.st = h->d_state;
+  CB_CUDA(cudaMallocHost((void**)&h->h_state, sizeof(State)));
+  memset(h->h_state, 0, sizeof(State));
+  State s0{};
+  s0.k = 0; s0.go_main = 1; s0.go_redo = 0; s0.t_k = 1.0; s0.w_hat = 0.0;
+  s0.obj_prev = INFINITY; s0.rel_prev = 0.0;
+  CB_CUDA(cudaMemcpyAsync(h->d_state, &s0, sizeof(State), cudaMemcpyHostToDevice, st));
+  // ---- ||M_s||^2 (solver.py:327) with the validation statistics kernel
+  {
+    double* stats;
+    TRY(dalloc((void**)&stats, sizeof(double) * 3 * S, A));
+    double* part;
+    TRY(dalloc((void**)&part, sizeof(double) * 3 * 148 * 8, A));
+    for (int s = 0; s < S; ++s) {
+      long long n = 1;
+      for (int m = 0; m < N; ++m) n *= h->dims[s * N + m];
+      int np = (int)std::min<long long>(148 * 8, std::max<long long>(1, (n + 255) / 256));
+      TRY(tensor_stats(h->dtype, h->X[s], n, stats + 3 * s, part, np, st));
+    }
+    // nsq[s] = stats[3s]
+    std::vector<double> hs(3 * S);
+    CB_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(double) * 3 * S, cudaMemcpyDeviceToHost, st));
+    CB_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> ns(S);
+    for (int s = 0; s < S; ++s) ns[s] = hs[3 * s];
+    CB_CUDA(cudaMemcpyAsync(c.nsq, ns.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    CB_CUDA(cudaStreamSynchronize(st));
+  }
+  // ---- row-unit tables for the mode updates
+  h->d_rows.assign(N, nullptr);
+  h->n_rows.assign(N, 0);
+  for (int n = 0; n < N; ++n) {
+    std::vector<RowUnit> ru;
+    for (int s = 0; s < S; ++s)
+      for (long long r0 = 0; r0 < h->dims[s * N + n]; r0 += MU_ROWS) ru.push_back(RowUnit{s, (int)r0});
+    h->n_rows[n] = (int)ru.size();
+    TRY(upload(ru, &h->d_rows[n], A, st));
+  }
+  // ---- fast 3-way tables and T buffers
+  std::vector<void*> T0(S, nullptr), T1(S, nullptr);
+  if (h->fast3) {
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->dtype, h->tab);
+    TRY(upload(h->tab.fib, &h->d_fib, A, st));
+    TRY(upload(h->tab.slab, &h->d_slab, A, st));
+    TRY(upload(h->tab.c0, &h->d_c0, A, st));
+    TRY(upload(h->tab.c1, &h->d_c1, A, st));
+    int* di;
+    TRY(upload(h->tab.fib_first, &di, A, st)); c.fib_first = di;
+    TRY(upload(h->tab.slab_first, &di, A, st)); c.slab_first = di;
+    TRY(upload(h->tab.slab_nchunk, &di, A, st)); c.slab_nchunk = di;
+    int* d_ns;
+    TRY(upload(h->tab.nsplit, &d_ns, A, st));
+    c.slab_sb = h->tab.sb;
+    if (h->tab.slab_smem > 200 * 1024) {
+      set_error("slab staging (%zu bytes) exceeds shared memory", h->tab.slab_smem);
+      cb_solver_destroy(h);
+      return CB_ERR_UNSUPPORTED;
+    }
+    prepare_slab(h->dtype, h->rb, h->tab.slab_smem);
+    TRY(dalloc((void**)&c.fib_bpart, sizeof(double) * h->tab.fib.size() * RSTRIDE, A));
+    TRY(dalloc((void**)&c.fib_rpart, sizeof(double) * h->tab.fib.size(), A));
+    TRY(dalloc((void**)&c.slab_part, sizeof(double) * h->tab.slab.size() * h->tab.sb * RSTRIDE, A));
+    if (!h->lra) {
+      for (int s = 0; s < S; ++s) {
+        const size_t tb = (size_t)h->tab.nsplit[s] * h->R[s] * h->dims[3 * s] * h->dims[3 * s + 1] *
+                          h->elem_bytes;
+        TRY(dalloc(&T0[s], tb, A));
+        TRY(dalloc(&T1[s], tb, A));
+      }
+    }
+    void** pv;
+    TRY(upload(T0, &pv, A, st));
+    void** pv1;
+    TRY(upload(T1, &pv1, A, st));
+    const void** pX;
+    TRY(upload(h->X, &pX, A, st));
+    XArgs xa{};
+    xa.X = pX; xa.dims = c.dims; xa.R = c.R; xa.U = (const double* const*)c.U; xa.LAM = (const double* const*)c.LAM;
+    xa.T0 = pv; xa.T1 = pv1; xa.tsel = &h->d_state->tsel; xa.t_other = 0;
+    xa.nsplit = d_ns; xa.bpart = c.fib_bpart; xa.rpart = c.fib_rpart; xa.slab_part = c.slab_part;
+    xa.MTT = c.MTT; xa.active = nullptr;
+    xa.gate = &h->d_state->go_main;
+    h->xa_main = xa;
+    xa.gate = &h->d_state->go_redo;
+    h->xa_redo = xa;
+  } else {
+    size_t kr = 0;
+    for (int s = 0; s < S; ++s)
+      for (int n = 0; n < N; ++n) {
+        long long Lp = 1, Hp = 1;
+        for (int m = 0; m < n; ++m) Lp *= h->dims[s * N + m];
+        for (int m = n + 1; m < N; ++m) Hp *= h->dims[s * N + m];
+        kr = std::max(kr, (size_t)(Lp + Hp) * h->R[s]);
+      }
+    TRY(dalloc((void**)&h->kr_scratch, sizeof(double) * kr, A));
+    h->res_nparts = 148 * 4;
+    TRY(dalloc((void**)&h->res_part, sizeof(double) * h->res_nparts, A));
+  }
+  // ---- shared memory sizes
+  h->blk_smem = block_smem_bytes(c.rmax, c.rmax);
+  int maxRt = std::max(h->rtmax, 1);
+  h->mu_smem = sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)MU_ROWS * h->rmax +
+                                 (h->lra ? (size_t)maxRt * h->rmax : 0) + 16);
+  h->qr_smem = 0;
+  if (h->lra) {
+    int cmax = 0;
+    for (int s = 0; s < S; ++s) cmax = std::max(cmax, h->R[s] + h->Rt[s]);
+    h->qr_smem = sizeof(double) * ((size_t)(cmax + QR_CHUNK_ROWS) * (cmax + 1) + (cmax + QR_CHUNK_ROWS) + 40 + cmax + 8);
+  }
+  CB_CUDA(cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_mode_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->mu_smem));
+  if (h->lra)
+    CB_CUDA(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qr_smem));
+  // ---- iteration 0
+  TRY(init_evaluation(h));
+  TRY(read_state(h));
+  h->init_done = true;
+#undef TRY
+  *out = h;
+  return CB_OK;
+}
+
+int cb_solver_step_async(cb_solver* h) {
+  CB_ARG(h, "null handle");
+  if (!h->fast3) {
+    int rc = generic_iteration(h);
+    return rc;
+  }
+  if (h->timing) return enqueue_iteration(h);
+  if (!h->gexec && h->graph_ok) {
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      const long long before = cb_launch_count();
+      int rc = enqueue_iteration(h);
+      h->launches_per_iter = cb_launch_count() - before;
+      cudaError_t e2 = cudaStreamEndCapture(h->st, &g);
+      if (rc == CB_OK && e2 == cudaSuccess) {
+        if (cudaGraphInstantiate(&h->gexec, g, 0) != cudaSuccess) {
+          h->gexec = nullptr;
+          h->graph_ok = false;
+        }
+        cudaGraphDestroy(g);
+      } else {
+        h->graph_ok = false;
+      }
+      cudaGetLastError();
+    } else {
+      h->graph_ok = false;
+      cudaGetLastError();
+    }
+  }
+  if (h->gexec) {
+    CB_CUDA(cudaGraphLaunch(h->gexec, h->st));
+    count_launch(h->launches_per_iter);
+    return CB_OK;
+  }
+  return enqueue_iteration(h);
+}
+
+int cb_solver_summary_get(cb_solver* h, cb_solver_summary* sum) {
+  CB_ARG(h && sum, "null handle");
+  int rc = read_state(h);
+  if (rc) return rc;
+  const State& s = *h->h_state;
+  sum->n_iter = s.n_hist > 0 ? s.n_hist - 1 : 0;
+  sum->n_restarts = s.n_restarts;
+  sum->done = s.done;
+  sum->reason = s.reason;
+  sum->error = s.error;
+  sum->error_block = s.err_block;
+  sum->error_iter = s.err_iter;
+  return CB_OK;
+}
+
+int cb_solver_run(cb_solver* h, int iters, cb_solver_summary* sum) {
+  CB_ARG(h, "null handle");
+  int rc = read_state(h);
+  if (rc) return rc;
+  int left = iters;
+  while (left > 0 && !h->h_state->done) {
+    const int chunk = std::min(left, h->fast3 ? 16 : 1);
+    for (int i = 0; i < chunk; ++i) {
+      rc = cb_solver_step_async(h);
+      if (rc) return rc;
+    }
+    left -= chunk;
+    rc = read_state(h);
+    if (rc) return rc;
+  }
+  if (sum) return cb_solver_summary_get(h, sum);
+  return CB_OK;
+}
+
+int cb_solver_history(cb_solver* h, double* obj_int, double* obj_orig, double* rel, double* t_ns,
+                      int cap) {
+  CB_ARG(h, "null handle");
+  int rc = read_state(h);
+  if (rc) return rc;
+  const int n = std::min(cap, h->h_state->n_hist);
+  if (n <= 0) return CB_OK;
+  if (obj_int) CB_CUDA(cudaMemcpyAsync(obj_int, h->ctx.h_obj, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st));
+  if (obj_orig) CB_CUDA(cudaMemcpyAsync(obj_orig, h->ctx.h_orig, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st));
+  if (rel) CB_CUDA(cudaMemcpyAsync(rel, h->ctx.h_rel, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st));
+  if (t_ns) CB_CUDA(cudaMemcpyAsync(t_ns, h->ctx.h_tns, sizeof(double) * n, cudaMemcpyDeviceToHost, h->st));
+  CB_CUDA(cudaStreamSynchronize(h->st));
+  return CB_OK;
+}
+
+int cb_solver_block_factors(cb_solver* h, int block, double* const* host_factors,
+                            double* host_weights) {
+  CB_ARG(h && block >= 0 && block < h->S, "bad block %d", block);
+  for (int n = 0; n < h->N; ++n) {
+    if (!host_factors || !host_factors[n]) continue;
+    CB_CUDA(cudaMemcpyAsync(host_factors[n], h->h_U[block * h->N + n],
+                            sizeof(double) * h->dims[block * h->N + n] * h->R[block],
+                            cudaMemcpyDeviceToHost, h->st));
+  }
+  if (host_weights) {
+    CB_CUDA(cudaMemcpyAsync(host_weights, h->h_LAM[block], sizeof(double) * h->R[block], cudaMemcpyDeviceToHost, h->st));
+  }
+  CB_CUDA(cudaStreamSynchronize(h->st));
+  return CB_OK;
+}
+
+int cb_solver_set_timing(cb_solver* h, int on) {
+  CB_ARG(h, "null handle");
+  h->timing = on != 0;
+  h->ev_used = 0;
+  h->t_ms = 0.0; h->t_bytes = 0.0; h->t_launches = 0;
+  return CB_OK;
+}
+
+int cb_solver_timing(cb_solver* h, double* ms, long long* launches, double* bytes) {
+  CB_ARG(h, "null handle");
+  CB_CUDA(cudaStreamSynchronize(h->st));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+    float t = 0.f;
+    CB_CUDA(cudaEventElapsedTime(&t, h->ev_pool[i], h->ev_pool[i + 1]));
+    tot += t;
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = h->t_launches;
+  if (bytes) *bytes = h->t_bytes;
+  return CB_OK;
+}
+
+int cb_solver_destroy(cb_solver* h) {
+  if (!h) return CB_OK;
+  if (h->st) cudaStreamSynchronize(h->st);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (void* p : h->allocs) cudaFree(p);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  if (h->h_state) cudaFreeHost(h->h_state);
+  delete h;
+  return CB_OK;
+}
+
+}  // extern "C"

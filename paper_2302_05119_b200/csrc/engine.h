@@ -1,0 +1,87 @@
+// Device-side state and kernel argument structs of the APG solver engine.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "xpass.cuh"
+
+namespace cb {
+
+constexpr int MU_ROWS = 32;        // rows per mode-update CTA
+constexpr int QR_MAXC = 128;       // R~ + R limit of the QR route
+constexpr int QR_CHUNK_ROWS = 32;  // rows streamed per TSQR step
+
+// Iteration state living in device memory; only the control kernel writes it.
+struct State {
+  int k;              // iteration being computed (1-based); 0 during init
+  int go_main;        // 1 while not done (gates main-path kernels)
+  int go_redo;        // 1 iff the current iteration restarts (gates redo kernels)
+  int done;
+  int reason;         // 0 max_iterations, 1 tolerance
+  int n_restarts;
+  int error, err_block, err_iter;
+  int tsel, bsel;     // accepted T / b buffers
+  int n_hist;         // history entries written (n_iter + 1)
+  int pad;
+  double t_k;
+  double w_hat;       // extrapolation weight of the current (main) sweep
+  double rel_prev;    // RelErr of the last accepted iteration
+  double obj_prev;    // objective_history[-1]
+  double obj_pending; // lra: compressed objective of the accepted sweep
+  unsigned long long t0_ns;
+};
+
+struct Ctx {
+  int S, N, lra, update_core, objective, fast3, max_iter, rmax;
+  int counts[CB_MAX_ORDER];
+  double delta_w, tol;
+  const long long* dims;      // S*N
+  const int* R;               // S
+  const int* Rt;              // S (lra)
+  double* const* U;           // S*N current factors
+  double* const* Up;          // S*N previous factors
+  double* const* Un;          // S*N staging of the new individual columns
+  double* const* G;           // S*N grams R x R
+  double* const* C;           // S*N cross grams R~ x R (lra)
+  double* const* Ut;          // S*N compression factors I_n x R~ (lra)
+  double* const* LAM;         // S
+  double* const* LAMP;        // S
+  double* const* TW;          // S compression weights (lra)
+  double* const* STEP;        // S step matrices of the current mode
+  double* const* MTT;         // S MTTKRP outputs of the current mode (I_n x R)
+  double* lipc_hist;          // S (NaN = unset)
+  double* lipf_hist;          // N*S
+  double* lu;                 // N*S current factor Lipschitz constants
+  double* lup;                // N*S the "previous" constants used this sweep
+  double* nsq;                // S ||M_s||^2
+  double* bbuf;               // 2 * S * RSTRIDE staged core linear terms
+  double* model_sq;           // S lam^T (hadamard G) lam
+  double* inner;              // S (lra) lam^T (hadamard C)^T w~
+  double* res_t;              // S (lra) compressed residual by expansion
+  double* tsq;                // S (lra) ||M~||^2
+  double* res;                // S explicit residuals (generic path)
+  double* borig;              // S * RSTRIDE (generic lra trace / generic full b)
+  double* gc_part;            // S * gc_stride common-gradient partials
+  int* gc_valid;              // S
+  double* cnew;               // I_n x L_n new common columns
+  int* tile_cnt;              // per row tile arrival counters
+  long long gc_stride;
+  double* qr_buf;             // S*N*QR_MAXC*QR_MAXC R factors
+  double* qr_part;            // S*qr_nchunks partial core sums
+  int qr_nchunks;
+  int* qr_need;               // S flags: QR route taken this evaluation
+  double* fib_bpart;          // fiber partials
+  double* fib_rpart;
+  const int* fib_first;       // S+1 unit ranges
+  double* slab_part;
+  const int* slab_first;      // S
+  const int* slab_nchunk;     // S
+  int slab_sb;
+  State* st;
+  double* h_obj;              // max_iter+1 histories
+  double* h_orig;
+  double* h_rel;
+  double* h_tns;
+};
+
+}  // namespace cb

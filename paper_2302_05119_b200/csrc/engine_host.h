@@ -1,0 +1,44 @@
+// Host-side helpers shared by the solver (engine.cu) and ALS (als.cu) engines.
+#pragma once
+#include <vector>
+
+#include "status.h"
+#include "xpass.cuh"
+
+namespace cb {
+
+struct XTables {
+  std::vector<FibUnit> fib;
+  std::vector<int> fib_first;   // S+1
+  std::vector<int> nsplit;      // S
+  std::vector<SlabUnit> slab;
+  std::vector<int> slab_first;  // S
+  std::vector<int> slab_nchunk; // S
+  std::vector<RowUnit> c0, c1;
+  int sb = 1;
+  size_t slab_smem = 0;
+};
+
+void build_xtables(int S, const long long* dims, const int* R, int rb, int dtype, XTables& t);
+int rank_bucket(int r);
+void launch_fiber(int dtype, int rb, int want_t, int want_b, int want_res, const XArgs& a,
+                  const FibUnit* u, int n, cudaStream_t st);
+void prepare_slab(int dtype, int rb, size_t sm);
+void launch_slab(int dtype, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
+                 cudaStream_t st);
+void launch_contract(int dtype, int mode, const XArgs& a, const RowUnit* u, int n,
+                     cudaStream_t st);
+int dalloc(void** p, size_t bytes, std::vector<void*>& allocs);
+void set_alloc_stream(cudaStream_t st);
+
+template <typename T>
+int upload(const std::vector<T>& v, T** d, std::vector<void*>& allocs, cudaStream_t st) {
+  *d = nullptr;
+  if (v.empty()) return CB_OK;
+  CB_CUDA(cudaMalloc((void**)d, sizeof(T) * v.size()));
+  allocs.push_back(*d);
+  CB_CUDA(cudaMemcpyAsync(*d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+  return CB_OK;
+}
+
+}  // namespace cb

@@ -1,0 +1,775 @@
+// Small fused kernels of the APG iteration (per-block Gram/Hadamard, Lipschitz
+// constants, APG extrapolate/gradient/project, common-column aggregation,
+// restart, evaluation and the device-side control rule).
+//
+// Reference: pkg/src/concpd/solver.py:311-624 (the _Apg state machine and the
+// outer loop of solve()).  Every kernel is gated on device flags so that a
+// whole iteration (including the restart branch) can be enqueued or captured
+// in a CUDA graph without a host round trip.
+#pragma once
+#include "engine.h"
+#include "../../include/concpd_b200.h"
+
+namespace cb {
+
+__device__ __forceinline__ bool stopped(const Ctx& c, int redo) {
+  return redo ? (c.st->go_redo == 0) : (c.st->go_main == 0);
+}
+// np.maximum(0.0, x) semantics (NaN propagates)
+__device__ __forceinline__ double pos(double x) { return x < 0.0 ? 0.0 : x; }
+
+struct BlockSmem {
+  double* lmA;    // lam_max workspace: A, B, B2, vec, red
+  double* lmB;
+  double* lmB2;
+  double* vec;
+  double* red;
+  double* gr;     // gram staging 2 * 32 * gw
+  int gw;
+  double* misc;   // 4 * 64
+};
+
+__device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
+  BlockSmem b;
+  const int ld = lm_ld(rmax);
+  const int Rp = (rmax + 3) & ~3;
+  b.lmA = sm;
+  b.lmB = b.lmA + Rp * ld;
+  b.lmB2 = b.lmB + Rp * ld;
+  b.vec = b.lmB2 + Rp * ld;
+  b.red = b.vec + 128;
+  b.gr = b.red + 40;
+  b.gw = gw;
+  b.misc = b.gr + 2 * 32 * gw;
+  return b;
+}
+
+__host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
+  const int ld = ((rmax + 3) & ~3) + 1;
+  const int Rp = (rmax + 3) & ~3;
+  return sizeof(double) * (3 * (size_t)Rp * ld + 128 + 40 + 2 * 32 * (size_t)gw + 4 * 64 + 8);
+}
+
+// out[P x Q] = A^T B with A rows x P, B rows x Q (row-major), whole block,
+// fixed summation order over rows (deterministic).
+__device__ inline void block_gram(const double* __restrict__ A, int P, const double* __restrict__ B,
+                           int Q, long long rows, double* __restrict__ out, const BlockSmem& sm) {
+  double* As = sm.gr;
+  double* Bs = sm.gr + 32 * sm.gw;
+  const int nout = P * Q;
+  double acc[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+  for (long long c0 = 0; c0 < rows; c0 += 32) {
+    const int nr = (int)(rows - c0 < 32 ? rows - c0 : 32);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * P; e += blockDim.x) As[e] = A[c0 * P + e];
+    for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) Bs[e] = B[c0 * Q + e];
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int o = threadIdx.x + t * 256;
+      if (o < nout) {
+        const int p = o / Q, q = o - p * Q;
+        double s = acc[t];
+        for (int i = 0; i < nr; ++i) s = fma(As[i * P + p], Bs[i * Q + q], s);
+        acc[t] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int o = threadIdx.x + t * 256;
+    if (o < nout) out[o] = acc[t];
+  }
+  __syncthreads();
+}
+
+// Hadamard product of the block's grams over modes != skip (mode order,
+// starting from ones: solver.py:352-358) times optional lam lam^T, into the
+// lam_max matrix slot (leading dim lm_ld(R)).  Returns via smem.
+__device__ inline void build_gram_product(const Ctx& c, int s, int skip, bool times_lamlam,
+                                   const BlockSmem& sm) {
+  const int R = c.R[s];
+  const int ld = lm_ld(R);
+  const double* lam = c.LAM[s];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e - i * R;
+    double v = 1.0;
+    for (int m = 0; m < c.N; ++m)
+      if (m != skip) v *= c.G[s * c.N + m][e];
+    if (times_lamlam) v = v * (lam[i] * lam[j]);
+    sm.lmA[i * ld + j] = v;
+  }
+  __syncthreads();
+}
+
+// step(n) = (hadamard_{m != n} G) o lam lam^T, its lambda_max and the
+// Lipschitz history update (solver.py:402-406).
+__device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const BlockSmem& sm) {
+  const int R = c.R[s];
+  const int ld = lm_ld(R);
+  build_gram_product(c, s, n, true, sm);
+  double* step = c.STEP[s];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e - i * R;
+    step[e] = sm.lmA[i * ld + j];
+  }
+  const double lu = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+  if (threadIdx.x == 0) {
+    const int idx = n * c.S + s;
+    const double h = c.lipf_hist[idx];
+    c.lup[idx] = isnan(h) ? lu : h;
+    c.lipf_hist[idx] = lu;
+    c.lu[idx] = lu;
+  }
+  __syncthreads();
+}
+
+// Final per-block quantities of an evaluation: model_sq = lam^T (had G) lam and
+// for lra inner = lam^T (had C)^T w~, res_t (solver.py:513-515).
+__device__ inline void final_quantities(const Ctx& c, int s, const BlockSmem& sm) {
+  const int R = c.R[s];
+  const int ld = lm_ld(R);
+  const double* lam = c.LAM[s];
+  build_gram_product(c, s, -1, false, sm);
+  double* v = sm.misc;          // v = lam^T G
+  double* u = sm.misc + 64;     // u = C^T w~
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    double a = 0.0;
+    for (int i = 0; i < R; ++i) a = fma(lam[i], sm.lmA[i * ld + j], a);
+    v[j] = a;
+  }
+  if (c.lra) {
+    const int Rt = c.Rt[s];
+    const double* tw = c.TW[s];
+    for (int j = threadIdx.x; j < R; j += blockDim.x) {
+      double a = 0.0;
+      for (int q = 0; q < Rt; ++q) {
+        double cp = 0.0;
+        bool first = true;
+        for (int m = 0; m < c.N; ++m) {
+          const double g = c.C[s * c.N + m][q * R + j];
+          cp = first ? g : cp * g;
+          first = false;
+        }
+        a = fma(cp, tw[q], a);
+      }
+      u[j] = a;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double msq = 0.0;
+    for (int j = 0; j < R; ++j) msq = fma(v[j], lam[j], msq);
+    c.model_sq[s] = msq;
+    if (c.lra) {
+      double in = 0.0;
+      for (int j = 0; j < R; ++j) in = fma(lam[j], u[j], in);
+      c.inner[s] = in;
+      c.res_t[s] = c.tsq[s] - 2.0 * in + msq;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// init: grams, cross grams, ||M~||^2, Lipschitz histories unset
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_init_block(Ctx c) {
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const int s = blockIdx.x;
+  const int R = c.R[s];
+  for (int n = 0; n < c.N; ++n) {
+    const long long In = c.dims[s * c.N + n];
+    block_gram(c.U[s * c.N + n], R, c.U[s * c.N + n], R, In, c.G[s * c.N + n], sm);
+    if (c.lra) block_gram(c.Ut[s * c.N + n], c.Rt[s], c.U[s * c.N + n], R, In, c.C[s * c.N + n], sm);
+  }
+  if (threadIdx.x == 0) {
+    c.lipc_hist[s] = NAN;
+    for (int n = 0; n < c.N; ++n) c.lipf_hist[n * c.S + s] = NAN;
+  }
+  if (c.lra) {
+    // ||M~||^2 = 1^T (hadamard_n Ut_n^T Ut_n) 1 (solver.py:334-337): reuse the
+    // gram staging through the cross-gram slot of mode 0 as scratch
+    const int Rt = c.Rt[s];
+    double tot = 0.0;
+    double* H = sm.misc;  // column sums, Rt <= 64
+    for (int j = threadIdx.x; j < Rt; j += blockDim.x) H[j] = 0.0;
+    __syncthreads();
+    // build hadamard of tilde grams entry by entry (Rt^2 <= 4096)
+    for (int e = threadIdx.x; e < Rt * Rt; e += blockDim.x) {
+      const int p = e / Rt, q = e - p * Rt;
+      double v = 0.0;
+      bool first = true;
+      for (int n = 0; n < c.N; ++n) {
+        const double* A = c.Ut[s * c.N + n];
+        const long long In = c.dims[s * c.N + n];
+        double g = 0.0;
+        for (long long i = 0; i < In; ++i) g = fma(A[i * Rt + p], A[i * Rt + q], g);
+        v = first ? g : v * g;
+        first = false;
+      }
+      c.qr_buf[(long long)s * c.N * QR_MAXC * QR_MAXC + e] = v;   // scratch
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double* Hm = c.qr_buf + (long long)s * c.N * QR_MAXC * QR_MAXC;
+      // (1^T H) 1: column sums first, then their sum
+      for (int q = 0; q < Rt; ++q) {
+        double cs = 0.0;
+        for (int p = 0; p < Rt; ++p) cs += Hm[p * Rt + q];
+        tot += cs;
+      }
+      c.tsq[s] = tot;
+    }
+    __syncthreads();
+  }
+  final_quantities(c, s, sm);
+}
+
+// ---------------------------------------------------------------------------
+// sweep begin: core update (solver.py:375-395) and the mode-0 step matrix
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
+  if (stopped(c, redo)) return;
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const int s = blockIdx.x;
+  const int R = c.R[s];
+  const int ld = lm_ld(R);
+  const double w_hat = redo ? 0.0 : c.st->w_hat;
+  double* lam = c.LAM[s];
+  double* lamp = c.LAMP[s];
+  if (c.update_core) {
+    build_gram_product(c, s, -1, false, sm);
+    const double ldv = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+    double* sc = sm.misc + 192;
+    if (threadIdx.x == 0) {
+      const double h = c.lipc_hist[s];
+      sc[0] = isnan(h) ? ldv : h;
+      c.lipc_hist[s] = ldv;
+    }
+    __syncthreads();
+    const double ldp = sc[0];
+    if (ldv == 0.0) {
+      // all factor columns vanish, so does the gradient: keep lam
+      for (int r = threadIdx.x; r < R; r += blockDim.x) lamp[r] = lam[r];
+    } else {
+      const double w = extrap_weight(w_hat, ldp, ldv, c.delta_w);
+      double* lh = sm.misc;
+      double* lin = sm.misc + 64;
+      for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        lh[r] = lam[r] + w * (lam[r] - lamp[r]);
+        if (!c.lra) {
+          lin[r] = c.bbuf[((long long)c.st->bsel * c.S + s) * RSTRIDE + r];
+        } else {
+          const int Rt = c.Rt[s];
+          const double* tw = c.TW[s];
+          double a = 0.0;
+          for (int q = 0; q < Rt; ++q) {
+            double cp = 0.0;
+            bool first = true;
+            for (int m = 0; m < c.N; ++m) {
+              const double g = c.C[s * c.N + m][q * R + r];
+              cp = first ? g : cp * g;
+              first = false;
+            }
+            a = fma(cp, tw[q], a);
+          }
+          lin[r] = a;
+        }
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        double g = 0.0;
+        for (int j = 0; j < R; ++j) g = fma(sm.lmA[r * ld + j], lh[j], g);
+        g -= lin[r];
+        lamp[r] = lam[r];
+        lam[r] = pos(lh[r] - g / ldv);
+      }
+    }
+    __syncthreads();
+  }
+  step_and_lipschitz(c, s, 0, sm);
+}
+
+// ---------------------------------------------------------------------------
+// mode update: extrapolate, gradient, project individual columns, partial
+// common gradient; the last CTA of each row tile forms the new common columns
+// (solver.py:397-451).  src: 0 = MTT buffer, 1 = slab partials, 2 = lra.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int src,
+                                                      const RowUnit* __restrict__ units) {
+  if (stopped(c, redo)) return;
+  extern __shared__ double smd[];
+  const RowUnit u = units[blockIdx.x];
+  const int s = u.s;
+  const int R = c.R[s];
+  const int N = c.N;
+  const int L = c.counts[n];
+  const long long In = c.dims[s * N + n];
+  const int r0 = u.r0;
+  const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
+  const double w_hat = redo ? 0.0 : c.st->w_hat;
+  double* step = smd;                       // R*R
+  double* uh = step + R * R;                // MU_ROWS*R
+  double* mt = uh + MU_ROWS * R;            // MU_ROWS*R
+  double* P = mt + MU_ROWS * R;             // Rt*R (lra)
+  double* sc = P + (c.lra ? c.Rt[s] * R : 0);  // scalars
+  const double* lam = c.LAM[s];
+  if (threadIdx.x == 0) {
+    double sl = 0.0, slp = 0.0;
+    for (int q = 0; q < c.S; ++q) { sl += c.lu[n * c.S + q]; slp += c.lup[n * c.S + q]; }
+    sc[0] = sl;
+    sc[1] = extrap_weight(w_hat, slp, sl, c.delta_w);
+    sc[2] = extrap_weight(w_hat, c.lup[n * c.S + s], c.lu[n * c.S + s], c.delta_w);
+    sc[3] = c.lu[n * c.S + s];
+  }
+  const double* stp = c.STEP[s];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) step[e] = stp[e];
+  __syncthreads();
+  const double sumL = sc[0], wc = sc[1], ws = sc[2], lu = sc[3];
+  const double* Uc = c.U[s * N + n];
+  const double* Upr = c.Up[s * N + n];
+  const int R0 = c.R[0];
+  const double* U0c = c.U[n];
+  const double* U0p = c.Up[n];
+  for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+    const int il = e / R, r = e - il * R;
+    const long long i = r0 + il;
+    double v;
+    if (r < L) {
+      const double cc = U0c[i * R0 + r], cp = U0p[i * R0 + r];
+      v = cc + wc * (cc - cp);
+    } else {
+      const double cur = Uc[i * R + r], prv = Upr[i * R + r];
+      v = cur + ws * (cur - prv);
+    }
+    uh[e] = v;
+    if (src == 0) {
+      mt[e] = c.MTT[s][i * R + r];
+    } else if (src == 1) {
+      const int sb = c.slab_sb;
+      const long long g = i / sb;
+      const int m = (int)(i - g * sb);
+      const int nch = c.slab_nchunk[s];
+      const long long base = c.slab_first[s] + g * nch;
+      double a = 0.0;
+      for (int ch = 0; ch < nch; ++ch) a += c.slab_part[((base + ch) * sb + m) * RSTRIDE + r];
+      mt[e] = a;
+    }
+  }
+  if (src == 2) {
+    const int Rt = c.Rt[s];
+    for (int e = threadIdx.x; e < Rt * R; e += blockDim.x) {
+      double v = 0.0;
+      bool first = true;
+      for (int m = 0; m < N; ++m) {
+        if (m == n) continue;
+        const double g = c.C[s * N + m][e];
+        v = first ? g : v * g;
+        first = false;
+      }
+      P[e] = first ? 1.0 : v;
+    }
+    __syncthreads();
+    const double* Ut = c.Ut[s * N + n];
+    const double* tw = c.TW[s];
+    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+      const int il = e / R, r = e - il * R;
+      const long long i = r0 + il;
+      double a = 0.0;
+      for (int q = 0; q < Rt; ++q) a = fma(Ut[i * Rt + q] * tw[q], P[q * R + r], a);
+      mt[e] = a;
+    }
+  }
+  __syncthreads();
+  double* Un = c.Un[s * N + n];
+  double* gcp = c.gc_part + (long long)s * c.gc_stride;
+  for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+    const int il = e / R, r = e - il * R;
+    const long long i = r0 + il;
+    if (lu == 0.0) {
+      if (r >= L) Un[i * R + r] = Uc[i * R + r];
+      continue;
+    }
+    double g = 0.0;
+    for (int q = 0; q < R; ++q) g = fma(uh[il * R + q], step[q * R + r], g);
+    g -= mt[e] * lam[r];
+    if (r < L) gcp[i * L + r] = g;
+    else Un[i * R + r] = pos(uh[e] - g / lu);
+  }
+  if (L == 0) return;
+  if (threadIdx.x == 0 && r0 == 0) c.gc_valid[s] = lu > 0.0 ? 1 : 0;
+  __threadfence();
+  __syncthreads();
+  int* flag = reinterpret_cast<int*>(sc + 4);
+  if (threadIdx.x == 0) {
+    const int t = r0 / MU_ROWS;
+    const int old = atomicAdd(&c.tile_cnt[t], 1);
+    flag[0] = (old == c.S - 1);
+  }
+  __syncthreads();
+  if (!flag[0]) return;
+  __threadfence();
+  // last CTA of this row tile: sum the partials in block order (solver.py:444)
+  for (int e = threadIdx.x; e < rows * L; e += blockDim.x) {
+    const int il = e / L, l = e - il * L;
+    const long long i = r0 + il;
+    double acc = 0.0;
+    for (int q = 0; q < c.S; ++q) {
+      if (!__ldcg(&c.gc_valid[q])) continue;
+      acc += __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]);
+    }
+    const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
+    const double chat = cc + wc * (cc - cp);
+    c.cnew[i * L + l] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
+  }
+  if (threadIdx.x == 0) c.tile_cnt[r0 / MU_ROWS] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// finalize mode n: prev <- curr, curr <- [c_new | new individual], refresh the
+// gram / cross gram (solver.py:452-457, :367-371), then the next mode's step
+// matrix and Lipschitz constant, or the evaluation quantities after mode N-1.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo) {
+  if (stopped(c, redo)) return;
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const int s = blockIdx.x;
+  const int N = c.N;
+  const int R = c.R[s];
+  const int L = c.counts[n];
+  const long long In = c.dims[s * N + n];
+  double* Uc = c.U[s * N + n];
+  double* Upr = c.Up[s * N + n];
+  const double* Un = c.Un[s * N + n];
+  for (long long e = threadIdx.x; e < In * R; e += blockDim.x) {
+    const long long i = e / R;
+    const int r = (int)(e - i * R);
+    Upr[e] = Uc[e];
+    Uc[e] = r < L ? c.cnew[i * L + r] : Un[e];
+  }
+  __syncthreads();
+  block_gram(Uc, R, Uc, R, In, c.G[s * N + n], sm);
+  if (c.lra) block_gram(c.Ut[s * N + n], c.Rt[s], Uc, R, In, c.C[s * N + n], sm);
+  __syncthreads();
+  if (n + 1 < N) {
+    step_and_lipschitz(c, s, n + 1, sm);
+  } else {
+    final_quantities(c, s, sm);
+  }
+}
+
+// restore curr <- prev and refresh caches (solver.py:538-543)
+__global__ void __launch_bounds__(256) k_restore(Ctx c) {
+  if (c.st->go_redo == 0) return;
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const int s = blockIdx.x;
+  const int N = c.N;
+  const int R = c.R[s];
+  for (int r = threadIdx.x; r < R; r += blockDim.x) c.LAM[s][r] = c.LAMP[s][r];
+  for (int n = 0; n < N; ++n) {
+    const long long In = c.dims[s * N + n];
+    double* Uc = c.U[s * N + n];
+    const double* Upr = c.Up[s * N + n];
+    for (long long e = threadIdx.x; e < In * R; e += blockDim.x) Uc[e] = Upr[e];
+  }
+  __syncthreads();
+  for (int n = 0; n < N; ++n) {
+    const long long In = c.dims[s * N + n];
+    block_gram(c.U[s * N + n], R, c.U[s * N + n], R, In, c.G[s * N + n], sm);
+    if (c.lra) block_gram(c.Ut[s * N + n], c.Rt[s], c.U[s * N + n], R, In, c.C[s * N + n], sm);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// lra QR route (solver.py:467-482): R factors of [Ut_n, U_n] by streamed
+// Householder TSQR, then ||core||^2 of the (Rt+R)^N Kruskal core.
+// Only blocks with res_t < 1e-3 ||M~||^2 do work.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool qr_route_needed(const Ctx& c, int s) {
+  return c.res_t[s] < 1e-3 * c.tsq[s];
+}
+
+__global__ void __launch_bounds__(256) k_qr_factor(Ctx c, int redo) {
+  if (stopped(c, redo)) return;
+  const int s = blockIdx.x / c.N;
+  const int n = blockIdx.x - s * c.N;
+  if (!qr_route_needed(c, s)) return;
+  extern __shared__ double smd[];
+  const int R = c.R[s], Rt = c.Rt[s];
+  const int Cc = Rt + R;
+  const long long In = c.dims[s * c.N + n];
+  const int ldm = Cc + 1;
+  const int MR = Cc + QR_CHUNK_ROWS;      // stacked rows: current R (Cc) + chunk
+  double* M = smd;                        // MR x ldm
+  double* vv = M + MR * ldm;              // MR Householder vector
+  double* red = vv + MR;                  // 40
+  double* wv = red + 40;                  // Cc  (v^T M)
+  for (int e = threadIdx.x; e < MR * ldm; e += blockDim.x) M[e] = 0.0;
+  __syncthreads();
+  const double* A = c.Ut[s * c.N + n];
+  const double* B = c.U[s * c.N + n];
+  for (long long c0 = 0; c0 < In; c0 += QR_CHUNK_ROWS) {
+    const int nr = (int)(In - c0 < QR_CHUNK_ROWS ? In - c0 : QR_CHUNK_ROWS);
+    // rows Cc.. of M <- next chunk of [Ut, U]; zero the rest
+    for (int e = threadIdx.x; e < QR_CHUNK_ROWS * Cc; e += blockDim.x) {
+      const int il = e / Cc, j = e - il * Cc;
+      double v = 0.0;
+      if (il < nr) v = j < Rt ? A[(c0 + il) * Rt + j] : B[(c0 + il) * R + (j - Rt)];
+      M[(Cc + il) * ldm + j] = v;
+    }
+    __syncthreads();
+    // Householder on the stacked (Cc + nr) x Cc matrix
+    const int mrows = Cc + nr;
+    for (int k = 0; k < Cc; ++k) {
+      // norm of column k below the diagonal
+      double ss = 0.0;
+      for (int i = k + threadIdx.x; i < mrows; i += blockDim.x) ss = fma(M[i * ldm + k], M[i * ldm + k], ss);
+      ss = block_sum(ss, red);
+      const double x0 = M[k * ldm + k];
+      const double nrm = sqrt(ss);
+      if (nrm == 0.0) continue;
+      const double alpha = x0 >= 0.0 ? -nrm : nrm;
+      // v = x - alpha e_k ; v^T v = 2 (nrm^2 - alpha x0)
+      for (int i = k + threadIdx.x; i < mrows; i += blockDim.x)
+        vv[i] = (i == k) ? x0 - alpha : M[i * ldm + k];
+      __syncthreads();
+      const double vtv = 2.0 * (ss - alpha * x0);
+      if (vtv == 0.0) continue;
+      // w_j = v^T M[:, j] for j > k
+      for (int j = k + 1 + threadIdx.x; j < Cc; j += blockDim.x) {
+        double a = 0.0;
+        for (int i = k; i < mrows; ++i) a = fma(vv[i], M[i * ldm + j], a);
+        wv[j] = a;
+      }
+      __syncthreads();
+      const double beta = 2.0 / vtv;
+      for (int e = threadIdx.x; e < (mrows - k) * (Cc - k - 1); e += blockDim.x) {
+        const int i = k + e / (Cc - k - 1);
+        const int j = k + 1 + e % (Cc - k - 1);
+        M[i * ldm + j] -= beta * vv[i] * wv[j];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) M[k * ldm + k] = alpha;
+      for (int i = k + 1 + threadIdx.x; i < mrows; i += blockDim.x) M[i * ldm + k] = 0.0;
+      __syncthreads();
+    }
+    // rows >= Cc are now zero; the top Cc x Cc block is the running R
+  }
+  double* out = c.qr_buf + ((long long)s * c.N + n) * QR_MAXC * QR_MAXC;
+  for (int e = threadIdx.x; e < Cc * Cc; e += blockDim.x) {
+    const int i = e / Cc, j = e - i * Cc;
+    out[e] = j >= i ? M[i * ldm + j] : 0.0;
+  }
+}
+
+// ||core||^2 with core[a_0..a_{N-1}] = sum_q wts[q] prod_m Rm[a_m, q],
+// wts = [w~, -lam] (solver.py:476-482).  Grid: S * qr_nchunks.
+__global__ void __launch_bounds__(256) k_qr_core(Ctx c, int redo) {
+  if (stopped(c, redo)) return;
+  const int s = blockIdx.x / c.qr_nchunks;
+  const int ch = blockIdx.x - s * c.qr_nchunks;
+  if (!qr_route_needed(c, s)) return;
+  __shared__ double red[40];
+  __shared__ double wts[QR_MAXC];
+  const int R = c.R[s], Rt = c.Rt[s];
+  const int Cc = Rt + R;
+  for (int q = threadIdx.x; q < Cc; q += blockDim.x)
+    wts[q] = q < Rt ? c.TW[s][q] : -c.LAM[s][q - Rt];
+  __syncthreads();
+  long long K[CB_MAX_ORDER];
+  long long total = 1;
+  for (int m = 0; m < c.N; ++m) {
+    const long long Im = c.dims[s * c.N + m];
+    K[m] = Im < Cc ? Im : Cc;
+    total *= K[m];
+  }
+  const double* Rb = c.qr_buf + (long long)s * c.N * QR_MAXC * QR_MAXC;
+  double acc = 0.0;
+  for (long long e = (long long)ch * blockDim.x + threadIdx.x; e < total;
+       e += (long long)c.qr_nchunks * blockDim.x) {
+    long long rem = e;
+    int a[CB_MAX_ORDER];
+    for (int m = 0; m < c.N; ++m) { a[m] = (int)(rem % K[m]); rem /= K[m]; }
+    double v = 0.0;
+    for (int q = 0; q < Cc; ++q) {
+      double t = wts[q];
+      for (int m = 0; m < c.N; ++m) t *= Rb[(long long)m * QR_MAXC * QR_MAXC + a[m] * Cc + q];
+      v += t;
+    }
+    acc = fma(v, v, acc);
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) c.qr_part[(long long)s * c.qr_nchunks + ch] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// control: evaluation totals, restart rule, histories, stop rule, momentum
+// (solver.py:578-610).  One thread.
+// ---------------------------------------------------------------------------
+enum CtrlMode {
+  CTRL_INIT = 0,      // iteration-0 evaluation (accept unconditionally)
+  CTRL_DECIDE = 1,    // after the main sweep: restart or accept
+  CTRL_REDO = 2,      // after the restart sweep: accept (full) / stage (lra)
+  CTRL_FINISH = 3     // lra: after the original-tensor trace pass: accept
+};
+
+__device__ inline double block_res_full(const Ctx& c, int s, int bsrc) {
+  // bsrc: 0 = fiber partials (fast3), 1 = c.res / c.borig (generic)
+  if (c.objective == 0) {
+    if (bsrc == 0) {
+      double r = 0.0;
+      for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) r += c.fib_rpart[u];
+      return r;
+    }
+    return c.res[s];
+  }
+  // gram expansion ||M||^2 - 2 lam^T b + lam^T (had G) lam
+  const int R = c.R[s];
+  const double* lam = c.LAM[s];
+  const double* b = c.bbuf + ((long long)(1 - c.st->bsel) * c.S + s) * RSTRIDE;
+  double lb = 0.0;
+  for (int r = 0; r < R; ++r) lb = fma(lam[r], b[r], lb);
+  return c.nsq[s] - 2.0 * lb + c.model_sq[s];
+}
+
+// sum the staged core linear terms of the fiber units into bbuf[1 - bsel]
+__device__ inline void stage_b_from_fiber(const Ctx& c) {
+  for (int s = 0; s < c.S; ++s) {
+    double* b = c.bbuf + ((long long)(1 - c.st->bsel) * c.S + s) * RSTRIDE;
+    const int R = c.R[s];
+    for (int r = 0; r < R; ++r) {
+      double a = 0.0;
+      for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) a += c.fib_bpart[(long long)u * RSTRIDE + r];
+      b[r] = a;
+    }
+  }
+}
+
+__device__ inline double lra_compressed_obj(const Ctx& c) {
+  double oi = 0.0;
+  for (int s = 0; s < c.S; ++s) {
+    double rt = c.res_t[s];
+    if (qr_route_needed(c, s)) {
+      double a = 0.0;
+      for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
+      rt = a;
+    }
+    oi += 0.5 * (rt > 0.0 ? rt : 0.0);
+  }
+  return oi;
+}
+
+__device__ inline void accept_and_advance(const Ctx& c, double obj_int, double obj_orig, double rel,
+                                   int swap_t) {
+  State* st = c.st;
+  const int k = st->k;
+  c.h_obj[k] = obj_int;
+  c.h_orig[k] = obj_orig;
+  c.h_rel[k] = rel;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  if (k == 0) st->t0_ns = now;
+  c.h_tns[k] = (double)(now - st->t0_ns);
+  st->n_hist = k + 1;
+  st->bsel ^= 1;
+  if (swap_t) st->tsel ^= 1;
+  st->go_redo = 0;
+  st->obj_prev = obj_int;
+  bool stop = false;
+  if (k > 0) {
+    if (fabs(rel - st->rel_prev) < c.tol) { stop = true; st->reason = 1; }
+  }
+  st->rel_prev = rel;
+  if (!stop && k >= c.max_iter) { stop = true; st->reason = 0; }
+  if (stop) {
+    st->done = 1;
+    st->go_main = 0;
+    return;
+  }
+  // momentum for the next iteration (solver.py:588-590)
+  const double t_new = t_next(st->t_k);
+  st->w_hat = (st->t_k - 1.0) / t_new;
+  st->t_k = t_new;
+  st->k = k + 1;
+}
+
+__global__ void k_control(Ctx c, int mode, int bsrc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  State* st = c.st;
+  if (st->done) return;
+  if (mode == CTRL_REDO && !st->go_redo) return;
+  const int fast_t = (bsrc == 0);
+  if (!c.lra) {
+    if (mode == CTRL_FINISH) return;
+    if (fast_t) stage_b_from_fiber(c);
+    double oi = 0.0, rel = 0.0;
+    for (int s = 0; s < c.S; ++s) {
+      const double r = block_res_full(c, s, bsrc);
+      if (!isfinite(r)) {
+        st->error = CB_ERR_NONFINITE; st->err_block = s; st->err_iter = st->k;
+        st->done = 1; st->go_main = 0; st->go_redo = 0;
+        return;
+      }
+      oi += 0.5 * r;
+      const double nrm = sqrt(c.nsq[s]);
+      rel += nrm > 0.0 ? sqrt(r > 0.0 ? r : 0.0) / nrm : 0.0;
+    }
+    rel /= c.S;
+    if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
+      st->n_restarts += 1;
+      st->go_redo = 1;
+      return;
+    }
+    accept_and_advance(c, oi, oi, rel, fast_t);
+    return;
+  }
+  // ---- lra ----
+  if (mode == CTRL_DECIDE || mode == CTRL_REDO) {
+    const double oi = lra_compressed_obj(c);
+    st->obj_pending = oi;
+    if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
+      st->n_restarts += 1;
+      st->go_redo = 1;
+    }
+    return;
+  }
+  // CTRL_INIT or CTRL_FINISH: original-tensor trace quantities
+  const double oi = (mode == CTRL_INIT) ? lra_compressed_obj(c) : st->obj_pending;
+  double oo = 0.0, rel = 0.0;
+  for (int s = 0; s < c.S; ++s) {
+    const int R = c.R[s];
+    const double* lam = c.LAM[s];
+    double lb = 0.0;
+    for (int r = 0; r < R; ++r) {
+      double b;
+      if (fast_t) {
+        b = 0.0;
+        for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) b += c.fib_bpart[(long long)u * RSTRIDE + r];
+      } else {
+        b = c.borig[(long long)s * RSTRIDE + r];
+      }
+      lb = fma(lam[r], b, lb);
+    }
+    double r = c.nsq[s] - 2.0 * lb + c.model_sq[s];
+    r = r > 0.0 ? r : 0.0;
+    if (!isfinite(r)) {
+      st->error = CB_ERR_NONFINITE; st->err_block = s; st->err_iter = st->k;
+      st->done = 1; st->go_main = 0; st->go_redo = 0;
+      return;
+    }
+    oo += 0.5 * r;
+    const double nrm = sqrt(c.nsq[s]);
+    rel += nrm > 0.0 ? sqrt(r) / nrm : 0.0;
+  }
+  rel /= c.S;
+  accept_and_advance(c, oi, oo, rel, 0);
+}
+
+}  // namespace cb

@@ -1,0 +1,313 @@
+// Tensor-streaming kernels of the 3-way fast path (the only kernels that read
+// the dense blocks).  All batched over the S blocks of a solve, ragged shapes
+// handled through per-launch unit tables.
+//
+// Notation per block s: X is I0 x I1 x I2, first index fastest; J = I0*I1;
+// element (i0,i1,i2) lives at j + J*i2 with j = i0 + I0*i1.  Factors A0, A1,
+// A2 are fp64 row-major (I_n x R).  TE = storage/compute type of the tensor
+// (float in the fp32 throughput mode, double in the fp64 parity mode).
+//
+//  fiber  : T[j, r] = sum_{i2} X[j, i2] A2[i2, r]         ("X x_3 A2")
+//           + optional per-unit partials of
+//             b[r]  = sum_j A0[i0,r] A1[i1,r] T[j,r]       (core linear term,
+//                      solver.py:506-511, and the lra trace pass :519-522)
+//             res   = sum (X - [[lam; A0,A1,A2]])^2         (explicit residual,
+//                      solver.py:500-505)
+//  slab   : M2[i2, r] = sum_j X[j, i2] A0[i0,r] A1[i1,r]   (mode-2 MTTKRP,
+//                      solver.py:409-412 with n = N-1)
+//  contract0 : M0[i0, r] = sum_{i1} T[i0 + I0 i1, r] A1[i1, r]  (mode-0 MTTKRP)
+//  contract1 : M1[i1, r] = sum_{i0} T[i0 + I0 i1, r] A0[i0, r]  (mode-1 MTTKRP)
+//
+// Modes 0 and 1 of a Gauss-Seidel sweep both contract X with the SAME A2
+// (A2 only changes at mode 2), so one fiber pass serves both: a full-mode
+// iteration streams each block twice (fiber + slab) instead of N = 3 times,
+// and the explicit objective rides along the fiber pass for free.
+#pragma once
+#include "common.cuh"
+
+namespace cb {
+
+constexpr int FIB_THREADS = 256;
+constexpr int FIB_CHUNK = 32;     // i2 rows of A2 staged in smem per step
+constexpr int SLAB_THREADS = 256;
+constexpr int RSTRIDE = 64;       // per-unit partial stride (>= max rank)
+
+struct FibUnit { int s; int split; long long j0; };
+struct SlabUnit { int s; int g0; long long k0; long long k1; };
+struct RowUnit { int s; int r0; };
+
+struct XArgs {
+  const void* const* X;          // per block tensor
+  const long long* dims;         // S*3
+  const int* R;                  // per block rank
+  const double* const* U;        // S*3 current factors
+  const double* const* LAM;      // S weights (nullptr entries -> unit weights)
+  void* const* T0;               // per block T buffers [nsplit][R][J], double-buffered:
+  void* const* T1;               //   buffer index = (*tsel) ^ t_other
+  const int* tsel;
+  int t_other;
+  const int* nsplit;             // per block fiber splits
+  double* bpart;                 // [unit][RSTRIDE]
+  double* rpart;                 // [unit]
+  double* slab_part;             // [unit][SB][RSTRIDE]
+  double* const* MTT;            // per block I_n x R output (contract kernels)
+  const int* gate;               // if non-null and *gate == 0 -> skip (flag gating)
+  const int* active;             // per-block activity (ALS); nullptr -> all active
+};
+
+__device__ __forceinline__ bool gated(const XArgs& a) {
+  return a.gate != nullptr && *a.gate == 0;
+}
+__device__ __forceinline__ void* tbuf(const XArgs& a, int s) {
+  const int sel = (a.tsel ? *a.tsel : 0) ^ a.t_other;
+  return sel ? a.T1[s] : a.T0[s];
+}
+
+// ---------------------------------------------------------------------------
+// fiber pass
+// ---------------------------------------------------------------------------
+template <typename TE, int RB, bool STORE_T, bool WANT_B, bool WANT_RES>
+__global__ void __launch_bounds__(FIB_THREADS)
+fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
+  if (gated(a)) return;
+  const FibUnit u = units[blockIdx.x];
+  const int s = u.s;
+  if (a.active && !a.active[s]) return;
+  const int R = a.R[s];
+  const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1], I2 = a.dims[3 * s + 2];
+  const long long J = I0 * I1;
+  const int ns = a.nsplit[s];
+  const long long per = (I2 + ns - 1) / ns;
+  const long long i2b = (long long)u.split * per;
+  const long long i2e = i2b + per < I2 ? i2b + per : I2;
+  const TE* __restrict__ X = reinterpret_cast<const TE*>(a.X[s]);
+  const double* __restrict__ A0 = a.U[3 * s];
+  const double* __restrict__ A1 = a.U[3 * s + 1];
+  const double* __restrict__ A2 = a.U[3 * s + 2];
+
+  __shared__ TE a2s[FIB_CHUNK][RB];
+  __shared__ double red[FIB_THREADS / 32][RB + 1];
+
+  const long long j = u.j0 + threadIdx.x;
+  const bool valid = j < J;
+  long long i0 = 0, i1 = 0;
+  if (valid) { i1 = j / I0; i0 = j - i1 * I0; }
+
+  TE acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = TE(0);
+  TE w[WANT_RES ? RB : 1];
+  double res = 0.0;
+  if constexpr (WANT_RES) {
+    const double* lam = a.LAM[s];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      double v = 0.0;
+      if (r < R && valid) v = (lam ? lam[r] : 1.0) * A0[i0 * R + r] * A1[i1 * R + r];
+      w[r] = (TE)v;
+    }
+  }
+
+  for (long long c0 = i2b; c0 < i2e; c0 += FIB_CHUNK) {
+    const int nc = (int)((i2e - c0) < FIB_CHUNK ? (i2e - c0) : FIB_CHUNK);
+    __syncthreads();
+    for (int e = threadIdx.x; e < FIB_CHUNK * RB; e += FIB_THREADS) {
+      int q = e / RB, r = e - q * RB;
+      a2s[q][r] = (q < nc && r < R) ? (TE)A2[(c0 + q) * R + r] : TE(0);
+    }
+    __syncthreads();
+    if (valid) {
+      const TE* xp = X + j + J * c0;
+      int q = 0;
+      for (; q + 4 <= nc; q += 4) {
+        TE x[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) x[t] = __ldcs(xp + J * (q + t));
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          TE m = TE(0);
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            acc[r] = fma(x[t], a2s[q + t][r], acc[r]);
+            if constexpr (WANT_RES) m = fma(w[r], a2s[q + t][r], m);
+          }
+          if constexpr (WANT_RES) { double d = (double)x[t] - (double)m; res = fma(d, d, res); }
+        }
+      }
+      for (; q < nc; ++q) {
+        TE x = __ldcs(xp + J * q);
+        TE m = TE(0);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          acc[r] = fma(x, a2s[q][r], acc[r]);
+          if constexpr (WANT_RES) m = fma(w[r], a2s[q][r], m);
+        }
+        if constexpr (WANT_RES) { double d = (double)x - (double)m; res = fma(d, d, res); }
+      }
+    }
+  }
+
+  if constexpr (STORE_T) if (valid) {
+    TE* T = reinterpret_cast<TE*>(tbuf(a, s)) + (long long)u.split * R * J;
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (r < R) T[(long long)r * J + j] = acc[r];
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if constexpr (WANT_B) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      double v = 0.0;
+      if (valid && r < R) v = (double)acc[r] * (A0[i0 * R + r] * A1[i1 * R + r]);
+      v = warp_sum(v);
+      if (lane == 0) red[wid][r] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < R) {
+      double t = 0.0;
+      for (int q = 0; q < FIB_THREADS / 32; ++q) t += red[q][threadIdx.x];
+      a.bpart[(long long)blockIdx.x * RSTRIDE + threadIdx.x] = t;
+    }
+  }
+  if constexpr (WANT_RES) {
+    __syncthreads();
+    double v = warp_sum(res);
+    if (lane == 0) red[wid][0] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < FIB_THREADS / 32; ++q) t += red[q][0];
+      a.rpart[blockIdx.x] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// slab pass: each unit = (block, SB consecutive i2 slabs, j-range [k0, k1))
+// ---------------------------------------------------------------------------
+template <typename TE, int RB, int SB>
+__global__ void __launch_bounds__(SLAB_THREADS)
+slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
+  if (gated(a)) return;
+  const SlabUnit u = units[blockIdx.x];
+  const int s = u.s;
+  if (a.active && !a.active[s]) return;
+  const int R = a.R[s];
+  const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1], I2 = a.dims[3 * s + 2];
+  const long long J = I0 * I1;
+  const TE* __restrict__ X = reinterpret_cast<const TE*>(a.X[s]);
+  const double* __restrict__ A0 = a.U[3 * s];
+  const double* __restrict__ A1 = a.U[3 * s + 1];
+
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TE* a0s = reinterpret_cast<TE*>(smraw);          // I0 x RB
+  TE* a1s = a0s + I0 * RB;                         // I1 x RB
+  for (long long e = threadIdx.x; e < I0 * RB; e += SLAB_THREADS) {
+    long long i = e / RB; int r = (int)(e - i * RB);
+    a0s[e] = r < R ? (TE)A0[i * R + r] : TE(0);
+  }
+  for (long long e = threadIdx.x; e < I1 * RB; e += SLAB_THREADS) {
+    long long i = e / RB; int r = (int)(e - i * RB);
+    a1s[e] = r < R ? (TE)A1[i * R + r] : TE(0);
+  }
+  __syncthreads();
+
+  int nsl = (int)(I2 - u.g0 < SB ? I2 - u.g0 : SB);
+  TE acc[SB][RB];
+#pragma unroll
+  for (int m = 0; m < SB; ++m)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[m][r] = TE(0);
+
+  long long k = u.k0 + threadIdx.x;
+  long long i1 = k / I0, i0 = k - i1 * I0;
+  const long long st1 = SLAB_THREADS / I0, st0 = SLAB_THREADS - st1 * I0;
+  const TE* xb = X + J * u.g0;
+  for (; k < u.k1; k += SLAB_THREADS) {
+    TE x[SB];
+#pragma unroll
+    for (int m = 0; m < SB; ++m) x[m] = (m < nsl) ? __ldcs(xb + J * m + k) : TE(0);
+    const TE* p0 = a0s + i0 * RB;
+    const TE* p1 = a1s + i1 * RB;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      TE kr = p0[r] * p1[r];
+#pragma unroll
+      for (int m = 0; m < SB; ++m) acc[m][r] = fma(x[m], kr, acc[m][r]);
+    }
+    i0 += st0; i1 += st1;
+    if (i0 >= I0) { i0 -= I0; i1 += 1; }
+  }
+
+  __shared__ double red[SLAB_THREADS / 32][SB * RB + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < SB; ++m)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      double v = warp_sum((double)acc[m][r]);
+      if (lane == 0) red[wid][m * RB + r] = v;
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < SB * RB; e += SLAB_THREADS) {
+    double t = 0.0;
+    for (int q = 0; q < SLAB_THREADS / 32; ++q) t += red[q][e];
+    int m = e / RB, r = e - m * RB;
+    a.slab_part[((long long)blockIdx.x * SB + m) * RSTRIDE + r] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// contractions of T (mode 0 / mode 1 MTTKRP), fp64 outputs into MTT[s]
+// ---------------------------------------------------------------------------
+template <typename TE>
+__global__ void __launch_bounds__(256)
+contract0_kernel(XArgs a, const RowUnit* __restrict__ units) {
+  if (gated(a)) return;
+  const RowUnit u = units[blockIdx.x];
+  const int s = u.s;
+  if (a.active && !a.active[s]) return;
+  const int R = a.R[s];
+  const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1];
+  const long long J = I0 * I1;
+  const long long e = (long long)u.r0 + threadIdx.x;   // e = r * I0 + i0
+  if (e >= I0 * R) return;
+  const long long r = e / I0, i0 = e - r * I0;
+  const double* A1 = a.U[3 * s + 1];
+  const TE* T = reinterpret_cast<const TE*>(tbuf(a, s));
+  const int ns = a.nsplit[s];
+  double acc = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    const TE* Tr = T + ((long long)sp * R + r) * J + i0;
+    for (long long i1 = 0; i1 < I1; ++i1) acc = fma((double)Tr[I0 * i1], A1[i1 * R + r], acc);
+  }
+  a.MTT[s][i0 * R + r] = acc;
+}
+
+template <typename TE>
+__global__ void __launch_bounds__(256)
+contract1_kernel(XArgs a, const RowUnit* __restrict__ units) {
+  if (gated(a)) return;
+  const RowUnit u = units[blockIdx.x];
+  const int s = u.s;
+  if (a.active && !a.active[s]) return;
+  const int R = a.R[s];
+  const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1];
+  const long long J = I0 * I1;
+  const int lane = threadIdx.x & 31;
+  const long long p = (long long)u.r0 + (threadIdx.x >> 5);   // p = i1 * R + r
+  if (p >= I1 * R) return;
+  const long long i1 = p / R, r = p - i1 * R;
+  const double* A0 = a.U[3 * s];
+  const TE* T = reinterpret_cast<const TE*>(tbuf(a, s));
+  const int ns = a.nsplit[s];
+  double acc = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    const TE* Tr = T + ((long long)sp * R + r) * J + I0 * i1;
+    for (long long i0 = lane; i0 < I0; i0 += 32) acc = fma((double)Tr[i0], A0[i0 * R + r], acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) a.MTT[s][i1 * R + r] = acc;
+}
+
+}  // namespace cb

@@ -1,0 +1,544 @@
+"""Coupled nonnegative CP decomposition by APG — B200 drop-in for
+`pkg/src/concpd/solver.py`.
+
+The public surface is the reference's: ``CoupledProblem``, ``SolverOptions``,
+``SolveResult``, ``TraceRow``, ``solve`` and the operator-level building
+blocks (solver.py:34-52).  ``solve`` validates on the host, draws the
+reference's seeded start (bit-identical numpy PCG64 stream), uploads the
+blocks once, and hands the whole iteration to the device engine
+(`cb_solver_*`, csrc/engine.cu): sweep, objective, restart rule and stop
+rule all run on the GPU.  lra mode first compresses every block with the
+batched device ALS (`cb_als_*`).  No code path computes on the CPU.
+
+Additions over the reference (defaulted, so existing callers are unchanged):
+``SolverOptions.precision`` ("fp64" parity mode, "fp32" throughput mode that
+stores the tensors in fp32 while keeping factors and all small algebra in
+fp64) and ``SolverOptions.objective`` ("auto" = explicit residual in fp64
+like the reference, gram expansion in fp32; or force "explicit" /
+"expansion").
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _lib as L
+from .cpd_als import AlsOptions, _check_feasible, als_compress_blocks
+from .kruskal import CoupledFactorSet, KruskalTensor
+from .tensor_ops import hadamard_gram, spectral_norm
+
+__all__ = [
+    "CoupledProblem", "SolverOptions", "SolveResult", "TraceRow", "solve", "objective",
+    "core_gradient", "factor_gradient", "core_linear_term", "core_linear_term_lra",
+    "factor_linear_term", "factor_linear_term_lra", "lipschitz_core", "lipschitz_factor",
+    "extrapolation_weight", "t_next", "init_factors",
+]
+
+
+def _is_torch(t):
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(t, torch.Tensor)
+
+
+@dataclass
+class CoupledProblem:
+    """S nonnegative tensors decomposed jointly (solver.py:60-135).
+
+    ``tensors`` may be numpy arrays (cast to float64 like the reference) or
+    CUDA torch tensors already resident on the device (kept as given; an
+    fp32 tensor stored first-index-fastest is used without any copy).
+    """
+
+    tensors: list
+    ranks: list
+    coupled_counts: list
+    mode: str = "full"
+    update_core: bool = True
+    als_options: AlsOptions = None
+
+    def __post_init__(self):
+        self.tensors = [t if _is_torch(t) else np.asarray(t, dtype=float) for t in self.tensors]
+        if isinstance(self.ranks, (int, np.integer)):
+            self.ranks = [int(self.ranks)] * len(self.tensors)
+        self.ranks = [int(r) for r in self.ranks]
+        self.coupled_counts = [int(c) for c in self.coupled_counts]
+
+    @property
+    def n_blocks(self):
+        return len(self.tensors)
+
+    @property
+    def order(self):
+        return self.tensors[0].ndim
+
+    def validate(self):
+        if not self.tensors:
+            raise ValueError("no tensors")
+        if self.mode not in ("full", "lra"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        order = self.tensors[0].ndim
+        for s, t in enumerate(self.tensors):
+            if t.ndim != order:
+                raise ValueError(f"block {s} has order {t.ndim}, expected {order}")
+            finite, nonneg = _value_checks(t)
+            if not finite:
+                raise ValueError(f"block {s} contains non-finite values")
+            if not nonneg:
+                raise ValueError(f"block {s} contains negative entries")
+        if len(self.ranks) != len(self.tensors):
+            raise ValueError("one rank per block required")
+        if any(r < 1 for r in self.ranks):
+            raise ValueError("ranks must be >= 1")
+        if len(self.coupled_counts) != order:
+            raise ValueError("one coupled count per mode required")
+        lo = min(self.ranks)
+        for n, c in enumerate(self.coupled_counts):
+            if not 0 <= c <= lo:
+                raise ValueError(f"coupled count {c} in mode {n} exceeds minimum rank {lo}")
+            if c > 0:
+                sizes = sorted({int(t.shape[n]) for t in self.tensors})
+                if len(sizes) != 1:
+                    raise ValueError(f"mode {n} is coupled but block sizes differ: {sizes}")
+
+
+def _value_checks(t):
+    """(all finite, no negative entries).  Device tensors are checked by the
+    library's statistics kernel; host arrays with numpy (input validation,
+    not the hot path)."""
+    if _is_torch(t):
+        torch = D.torch_mod()
+        flat = t.reshape(-1) if t.is_contiguous() else t.contiguous().reshape(-1)
+        code = L.CB_F32 if flat.dtype == torch.float32 else L.CB_F64
+        if flat.dtype not in (torch.float32, torch.float64):
+            flat = flat.to(torch.float64)
+            code = L.CB_F64
+        out = torch.empty(3, dtype=torch.float64, device=flat.device)
+        L.check(L.lib.cb_tensor_stats(code, D.ptr(flat), flat.numel(), D.ptr(out), D.stream()))
+        ss, mn, bad = (float(v) for v in out.cpu())
+        return bad == 0.0, not (mn < 0.0)
+    return bool(np.isfinite(t).all()), not bool((t < 0).any())
+
+
+@dataclass
+class SolverOptions:
+    max_iter: int = 1000
+    tol: float = 1e-8
+    delta_w: float = 0.9999
+    seed: int = 0
+    trace_every: int = 1
+    precision: str = "fp64"        # "fp64" parity mode | "fp32" throughput mode
+    objective: str = "auto"        # "auto" | "explicit" | "expansion"
+
+    def __post_init__(self):
+        if self.max_iter < 0:
+            raise ValueError("max_iter must be >= 0")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        if not 0.0 < self.delta_w < 1.0:
+            raise ValueError("delta_w must lie in (0, 1)")
+        if self.trace_every < 1:
+            raise ValueError("trace_every must be >= 1")
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError(f"unknown precision {self.precision!r}")
+        if self.objective not in ("auto", "explicit", "expansion"):
+            raise ValueError(f"unknown objective evaluation {self.objective!r}")
+
+
+@dataclass(frozen=True)
+class TraceRow:
+    iteration: int
+    obj_fun: float
+    rel_err: float
+    elapsed_s: float
+
+
+@dataclass
+class SolveResult:
+    """Outcome of :func:`solve` (solver.py:165-186).  ``trace`` reports the
+    original-tensor objective and RelErr; ``objective_history`` is the
+    minimised objective (compressed in lra mode) kept non-increasing by the
+    restart rule."""
+
+    factors: CoupledFactorSet
+    trace: list
+    termination_reason: str
+    objective_history: list = field(repr=False, default_factory=list)
+    rel_err_history: list = field(repr=False, default_factory=list)
+    n_iter: int = 0
+    n_restarts: int = 0
+    solve_seconds: float = 0.0
+    compress_seconds: float = 0.0
+    compression: list = None
+
+
+# ---------------------------------------------------------------------------
+# scalar rules and the seeded start (host: they are not tensor arithmetic)
+# ---------------------------------------------------------------------------
+
+def t_next(t):
+    """t_k = (1 + sqrt(1 + 4 t_{k-1}^2)) / 2 (solver.py:265-267)."""
+    return 0.5 * (1.0 + np.sqrt(1.0 + 4.0 * t * t))
+
+
+def extrapolation_weight(w_hat, lip_prev, lip_curr, delta_w):
+    """min(w_hat, delta_w sqrt(L_prev/L_curr)); 0 on degenerate blocks (solver.py:270-274)."""
+    if lip_curr <= 0.0 or lip_prev <= 0.0:
+        return 0.0
+    return min(w_hat, delta_w * float(np.sqrt(lip_prev / lip_curr)))
+
+
+def init_factors(problem, seed):
+    """Uniform [0,1) start, common prefix drawn once; the draw order matches the
+    reference exactly (solver.py:277-303) so GPU runs start bit-identically."""
+    rng = np.random.default_rng(seed)
+    counts = problem.coupled_counts
+    shape0 = tuple(problem.tensors[0].shape)
+    shared = [rng.random((shape0[n], counts[n])) for n in range(problem.order)]
+    blocks = []
+    for s in range(problem.n_blocks):
+        r = problem.ranks[s]
+        shp = tuple(problem.tensors[s].shape)
+        facs = []
+        for n in range(problem.order):
+            own = rng.random((shp[n], r - counts[n]))
+            facs.append(np.hstack([shared[n], own]) if counts[n] else own)
+        lam = rng.random(r) if problem.update_core else np.ones(r)
+        blocks.append(KruskalTensor(facs, lam))
+    return CoupledFactorSet(blocks, list(counts))
+
+
+# ---------------------------------------------------------------------------
+# operator-level building blocks (GPU)
+# ---------------------------------------------------------------------------
+
+def _dev_tensor(t):
+    dtype = "fp64"
+    if _is_torch(t):
+        import torch
+        dtype = "fp32" if t.dtype == torch.float32 else "fp64"
+    flat, dims = D.tensor_to_dev(t, dtype)
+    return flat, dims, (L.CB_F32 if dtype == "fp32" else L.CB_F64)
+
+
+def factor_linear_term(tensor, factors, n):
+    """M_(n) U_kr^(-n) on the GPU (`cb_mttkrp`; solver.py:243-245)."""
+    torch = D.torch_mod()
+    flat, dims, code = _dev_tensor(tensor)
+    rank = int(np.asarray(factors[0]).shape[1])
+    dev = [D.to_dev_f64(f) for f in factors]
+    out = torch.empty((dims[n], rank), dtype=torch.float64, device=flat.device)
+    L.check(L.lib.cb_mttkrp(code, D.ptr(flat), len(dims), L.i64_array(dims),
+                            L.ptr_array([D.ptr(x) for x in dev]), rank, n, D.ptr(out),
+                            D.stream()))
+    return D.to_host(out)
+
+
+def core_linear_term(tensor, factors):
+    """(U_kr)^T vec(M) through the mode-0 MTTKRP (solver.py:215-218)."""
+    torch = D.torch_mod()
+    flat, dims, code = _dev_tensor(tensor)
+    rank = int(np.asarray(factors[0]).shape[1])
+    dev = [D.to_dev_f64(f) for f in factors]
+    mtt = torch.empty((dims[0], rank), dtype=torch.float64, device=flat.device)
+    L.check(L.lib.cb_mttkrp(code, D.ptr(flat), len(dims), L.i64_array(dims),
+                            L.ptr_array([D.ptr(x) for x in dev]), rank, 0, D.ptr(mtt),
+                            D.stream()))
+    out = torch.empty(rank, dtype=torch.float64, device=flat.device)
+    L.check(L.lib.cb_rowdot(D.ptr(dev[0]), D.ptr(mtt), dims[0], rank, D.ptr(out), D.stream()))
+    return D.to_host(out)
+
+
+def _gemm(a, b, ta=False, tb=False, alpha=1.0):
+    torch = D.torch_mod()
+    da, db = D.to_dev_f64(a), D.to_dev_f64(b)
+    m = a.shape[1] if ta else a.shape[0]
+    k = a.shape[0] if ta else a.shape[1]
+    n = b.shape[0] if tb else b.shape[1]
+    out = torch.empty((m, n), dtype=torch.float64, device=da.device)
+    L.check(L.lib.cb_gemm(int(ta), int(tb), m, n, k, float(alpha), D.ptr(da), a.shape[1],
+                          D.ptr(db), b.shape[1], 0.0, D.ptr(out), n, D.stream()))
+    return D.to_host(out)
+
+
+def core_linear_term_lra(tilde, factors):
+    """(hadamard U^T U~) w~ via cross grams (solver.py:221-229)."""
+    cross = hadamard_gram(factors, mats2=tilde.factors)
+    return _gemm(cross, tilde.weights.reshape(-1, 1))[:, 0]
+
+
+def factor_linear_term_lra(tilde, factors, n):
+    """(U~_n * w~) (hadamard_{m!=n} U~_m^T U_m) (solver.py:248-251)."""
+    cross = hadamard_gram(tilde.factors, skip=n, mats2=factors)
+    scaled = np.asarray(tilde.factors[n]) * tilde.weights
+    return _gemm(scaled, cross)
+
+
+def core_gradient(gram_all, lam_hat, linear):
+    """gram_all lam_hat - linear (solver.py:205-212)."""
+    g = _gemm(np.asarray(gram_all, dtype=float), np.asarray(lam_hat, dtype=float).reshape(-1, 1))
+    return g[:, 0] - np.asarray(linear, dtype=float)
+
+
+def factor_gradient(u_hat, gram_skip, mtt, lam):
+    """u_hat (gram_skip o lam lam^T) - mtt o lam (`cb_factor_gradient`; solver.py:232-240)."""
+    torch = D.torch_mod()
+    u_hat = np.asarray(u_hat, dtype=float)
+    du = D.to_dev_f64(u_hat)
+    dg = D.to_dev_f64(gram_skip)
+    dm = D.to_dev_f64(mtt)
+    dl = D.to_dev_f64(lam)
+    out = torch.empty(u_hat.shape, dtype=torch.float64, device=du.device)
+    L.check(L.lib.cb_factor_gradient(D.ptr(du), u_hat.shape[0], D.ptr(dg), D.ptr(dm), D.ptr(dl),
+                                     u_hat.shape[1], D.ptr(out), D.stream()))
+    return D.to_host(out)
+
+
+def lipschitz_core(factors):
+    """lambda_max of the all-modes Hadamard gram (solver.py:254-256)."""
+    return spectral_norm(hadamard_gram(factors))
+
+
+def lipschitz_factor(factors, lam, n):
+    """lambda_max of (hadamard_{m!=n} gram) o lam lam^T (solver.py:259-262)."""
+    g = hadamard_gram(factors, skip=n) * np.outer(lam, lam)
+    return spectral_norm(g)
+
+
+def objective(tensors, blocks):
+    """1/2 sum_s ||M_s - [[lam_s; U_s]]||^2 by explicit streaming residuals on
+    the GPU (`cb_kruskal_residual`; solver.py:194-202)."""
+    torch = D.torch_mod()
+    total = 0.0
+    for t, k in zip(tensors, blocks):
+        flat, dims, code = _dev_tensor(np.asarray(t, dtype=float) if not _is_torch(t) else t)
+        dev = [D.to_dev_f64(f) for f in k.factors]
+        dw = D.to_dev_f64(k.weights)
+        out = torch.empty(1, dtype=torch.float64, device=flat.device)
+        L.check(L.lib.cb_kruskal_residual(code, D.ptr(flat), len(dims), L.i64_array(dims),
+                                          L.ptr_array([D.ptr(x) for x in dev]), D.ptr(dw),
+                                          k.rank, D.ptr(out), D.stream()))
+        total += 0.5 * float(out.item())
+    return total
+
+
+# ---------------------------------------------------------------------------
+# solve
+# ---------------------------------------------------------------------------
+
+class _Engine:
+    """Owns one device solver handle (re-entrant: one per solve)."""
+
+    def __init__(self, desc, stream):
+        h = L.c_vp()
+        L.check(L.lib.cb_solver_create(ctypes.byref(desc), stream, ctypes.byref(h)))
+        self.h = h
+
+    def run(self, iters):
+        summ = L.SolverSummary()
+        L.check(L.lib.cb_solver_run(self.h, int(iters), ctypes.byref(summ)))
+        return summ
+
+    def summary(self):
+        summ = L.SolverSummary()
+        L.check(L.lib.cb_solver_summary_get(self.h, ctypes.byref(summ)))
+        return summ
+
+    def step_async(self):
+        L.check(L.lib.cb_solver_step_async(self.h))
+
+    def history(self, n):
+        oi, oo, rel, tns = (np.zeros(n) for _ in range(4))
+        L.check(L.lib.cb_solver_history(self.h, oi.ctypes.data_as(L.c_dp),
+                                        oo.ctypes.data_as(L.c_dp), rel.ctypes.data_as(L.c_dp),
+                                        tns.ctypes.data_as(L.c_dp), n))
+        return oi, oo, rel, tns
+
+    def block(self, s, dims, rank):
+        facs = [np.zeros((d, rank)) for d in dims]
+        w = np.zeros(rank)
+        L.check(L.lib.cb_solver_block_factors(self.h, s, L.dptr_array(facs),
+                                              w.ctypes.data_as(L.c_dp)))
+        return facs, w
+
+    def set_timing(self, on):
+        L.check(L.lib.cb_solver_set_timing(self.h, int(on)))
+
+    def timing(self):
+        ms = ctypes.c_double()
+        n = ctypes.c_longlong()
+        b = ctypes.c_double()
+        L.check(L.lib.cb_solver_timing(self.h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b)))
+        return ms.value, n.value, b.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib.cb_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+class PreparedSolve:
+    """A solve with its inputs resident on the device, split into
+    prepare / iterate / collect so the bench can time the iterations alone."""
+
+    def __init__(self, problem, opts=None, stream=None):
+        torch = D.torch_mod()
+        opts = opts if opts is not None else SolverOptions()
+        problem.validate()
+        self.problem, self.opts = problem, opts
+        self.stream = stream if stream is not None else torch.cuda.Stream()
+        self.stream.wait_stream(torch.cuda.current_stream())
+        prec = opts.precision
+        self.code = L.CB_F32 if prec == "fp32" else L.CB_F64
+        objective_mode = opts.objective
+        if objective_mode == "auto":
+            objective_mode = "explicit" if prec == "fp64" else "expansion"
+        S, N = problem.n_blocks, problem.order
+        with torch.cuda.stream(self.stream):
+            self.dev = []
+            self.dims = []
+            for t in problem.tensors:
+                flat, dims = D.tensor_to_dev(t, prec)
+                self.dev.append(flat)
+                self.dims.append(dims)
+        st = L.c_vp(self.stream.cuda_stream)
+        # lra stage 1: batched device ALS (solver.py:556-573)
+        self.compress_seconds = 0.0
+        self.als = None
+        tilde_ranks = None
+        if problem.mode == "lra":
+            base = problem.als_options if problem.als_options is not None else AlsOptions()
+            ranks = [base.rank if base.rank is not None else r for r in problem.ranks]
+            for s, (dims, r) in enumerate(zip(self.dims, ranks)):
+                try:
+                    _check_feasible(dims, r)
+                except ValueError as exc:
+                    raise ValueError(f"compression of block {s} failed: {exc}") from exc
+            tic = time.perf_counter()
+            with torch.cuda.stream(self.stream):
+                try:
+                    self.als = als_compress_blocks(self.dev, self.dims, ranks, base.tol,
+                                                   base.max_iter,
+                                                   [base.seed + s for s in range(S)],
+                                                   self.code, st)
+                except ValueError as exc:
+                    msg = str(exc)
+                    blk = 0
+                    if msg.startswith("block "):
+                        blk = int(msg.split()[1].rstrip(":"))
+                        msg = msg.split(": ", 1)[1]
+                    raise ValueError(f"compression of block {blk} failed: {msg}") from exc
+            self.stream.synchronize()
+            self.compress_seconds = time.perf_counter() - tic
+            tilde_ranks = ranks
+        start = init_factors(problem, opts.seed)
+        self.start = start
+        desc = L.SolverDesc()
+        desc.n_blocks = S
+        desc.order = N
+        self._keep = []
+        flat_dims = [d for dims in self.dims for d in dims]
+        self._keep.append(L.i64_array(flat_dims))
+        desc.dims = ctypes.cast(self._keep[-1], L.c_i64p)
+        self._keep.append(L.int_array(problem.ranks))
+        desc.ranks = ctypes.cast(self._keep[-1], L.c_ip)
+        self._keep.append(L.int_array(problem.coupled_counts))
+        desc.coupled = ctypes.cast(self._keep[-1], L.c_ip)
+        desc.lra = 1 if problem.mode == "lra" else 0
+        desc.update_core = 1 if problem.update_core else 0
+        desc.dtype = self.code
+        self._keep.append(L.ptr_array([D.ptr(x) for x in self.dev]))
+        desc.tensors = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_vp))
+        init_f = [np.ascontiguousarray(f) for b in start.blocks for f in b.factors]
+        init_w = [np.ascontiguousarray(b.weights) for b in start.blocks]
+        self._keep.extend([init_f, init_w])
+        self._keep.append(L.dptr_array(init_f))
+        desc.init_factors = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_dp))
+        self._keep.append(L.dptr_array(init_w))
+        desc.init_weights = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_dp))
+        if self.als is not None:
+            self._keep.append(L.int_array(tilde_ranks))
+            desc.tilde_ranks = ctypes.cast(self._keep[-1], L.c_ip)
+            tptrs = [self.als.factor_device_ptr(s, n) for s in range(S) for n in range(N)]
+            self._keep.append((L.c_vp * len(tptrs))(*tptrs))
+            desc.tilde_factors = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_dp))
+            tw = [np.ones(r) for r in tilde_ranks]
+            self._keep.append(tw)
+            self._keep.append(L.dptr_array(tw))
+            desc.tilde_weights = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_dp))
+        desc.objective = 0 if objective_mode == "explicit" else 1
+        desc.delta_w = float(opts.delta_w)
+        desc.tol = float(opts.tol)
+        desc.max_iter = int(opts.max_iter)
+        desc.world_size = 1
+        self.t0 = time.perf_counter()
+        self.engine = _Engine(desc, st)
+        self.tilde_ranks = tilde_ranks
+
+    def run(self, iters=None):
+        iters = self.opts.max_iter if iters is None else iters
+        return self.engine.run(iters)
+
+    def collect(self):
+        problem, opts = self.problem, self.opts
+        summ = self.engine.summary()
+        solve_seconds = time.perf_counter() - self.t0
+        if summ.error == L.CB_ERR_NONFINITE:
+            raise FloatingPointError(
+                f"block {summ.error_block} produced a non-finite objective "
+                f"at iteration {summ.error_iter}")
+        n_iter = summ.n_iter
+        oi, oo, rel, tns = self.engine.history(n_iter + 1)
+        trace = []
+        for k in range(n_iter + 1):
+            last = k == n_iter and k > 0
+            if k == 0 or k % opts.trace_every == 0 or last:
+                trace.append(TraceRow(k, float(oo[k]), float(rel[k]), float(tns[k]) * 1e-9))
+        blocks = []
+        for s in range(problem.n_blocks):
+            facs, w = self.engine.block(s, self.dims[s], problem.ranks[s])
+            blocks.append(KruskalTensor(facs, w))
+        compression = None
+        if self.als is not None:
+            compression = []
+            for s in range(problem.n_blocks):
+                facs, _, _, _, _ = self.als.block(s)
+                compression.append(KruskalTensor(facs, np.ones(self.tilde_ranks[s])))
+        reason = "tolerance" if summ.reason == 1 else "max_iterations"
+        return SolveResult(
+            factors=CoupledFactorSet(blocks, list(problem.coupled_counts)),
+            trace=trace, termination_reason=reason,
+            objective_history=[float(v) for v in oi],
+            rel_err_history=[float(v) for v in rel],
+            n_iter=n_iter, n_restarts=summ.n_restarts, solve_seconds=solve_seconds,
+            compress_seconds=self.compress_seconds, compression=compression)
+
+    def close(self):
+        self.engine.close()
+        if self.als is not None:
+            self.als.close()
+
+
+def solve(problem, opts=None):
+    """Run the coupled decomposition on the GPU (drop-in for solver.py:546-624).
+
+    Stops when the original-tensor relative error changes by less than
+    ``opts.tol`` ("tolerance") or after ``opts.max_iter`` iterations
+    ("max_iterations").
+    """
+    run = PreparedSolve(problem, opts)
+    try:
+        run.run()
+        return run.collect()
+    finally:
+        run.close()

@@ -1,0 +1,189 @@
+"""GPU parity of the full solver (CoNCPD-APG and lraCoNCPD-APG) against the
+REAL reference's outputs on the same seeded inputs (tests/golden/*.npz), plus
+the reference's solver invariants (pkg/tests/test_solver.py) re-run on the
+GPU path.
+
+Tolerances (north_star): fp64 mode — histories and factors within 1e-9
+relative; fp32 throughput mode — within 1e-4 relative (oracle = reference in
+fp64 on the fp32-rounded inputs)."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from conftest import GOLDEN
+from store import tensor_fingerprint, unpack_solve
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2302_05119_b200 as P
+    return P
+
+
+def _rel_close(got, want, rtol, what):
+    got = np.asarray(got, dtype=float)
+    want = np.asarray(want, dtype=float)
+    scale = max(float(np.max(np.abs(want))) if want.size else 0.0, 1e-300)
+    err = float(np.max(np.abs(got - want))) / scale if want.size else 0.0
+    assert err <= rtol, f"{what}: max rel err {err:.3e} > {rtol:.1e}"
+    return err
+
+
+def compare(res, want, rtol, prefix_only=False):
+    """Compare a SolveResult with an unpacked reference result."""
+    n = min(res.n_iter, want["n_iter"]) + 1
+    if not prefix_only:
+        assert res.n_iter == want["n_iter"]
+        assert res.n_restarts == want["n_restarts"]
+        assert res.termination_reason == want["termination_reason"]
+    _rel_close(res.objective_history[:n], want["objective_history"][:n], rtol, "objective_history")
+    _rel_close(res.rel_err_history[:n], want["rel_err_history"][:n], rtol, "rel_err_history")
+    if not prefix_only:
+        assert [r.iteration for r in res.trace] == [r[0] for r in want["trace"]]
+        _rel_close([r.obj_fun for r in res.trace], [r[1] for r in want["trace"]], rtol, "trace obj")
+        _rel_close([r.rel_err for r in res.trace], [r[2] for r in want["trace"]], rtol, "trace rel")
+        for s, (blk, (wf, ww)) in enumerate(zip(res.factors.blocks, want["factors"])):
+            _rel_close(blk.weights, ww, rtol, f"block {s} weights")
+            for m, (a, b) in enumerate(zip(blk.factors, wf)):
+                _rel_close(a, b, rtol, f"block {s} mode {m} factor")
+
+
+SOLVE_CASES = sorted(os.path.basename(p)[6:-4] for p in glob.glob(os.path.join(GOLDEN, "solve_*.npz")))
+
+
+@pytest.mark.parametrize("name", SOLVE_CASES)
+def test_solve_matches_reference_fp64(P, name):
+    from cases import recipes
+    tensors, pkw, skw = recipes()[name]
+    want = unpack_solve(np.load(os.path.join(GOLDEN, f"solve_{name}.npz")))
+    prob = P.CoupledProblem(tensors, pkw["ranks"], pkw["coupled_counts"],
+                            mode=pkw.get("mode", "full"), update_core=pkw.get("update_core", True))
+    res = P.solve(prob, P.SolverOptions(**skw))
+    compare(res, want, rtol=1e-9)
+
+
+def _config(P, name, precision):
+    from cases import TINY_TOL
+    from paper_2302_05119_b200.configs import generate_config
+    z = np.load(os.path.join(GOLDEN, f"config_{name}.npz"))
+    tensors, spec = generate_config(name)
+    fp = np.stack([tensor_fingerprint(np.asarray(t, dtype=float)) for t in tensors])
+    np.testing.assert_allclose(fp, z["fingerprints"], rtol=1e-13)
+    prob = P.CoupledProblem([np.asarray(t, dtype=float) for t in tensors], spec.rank,
+                            list(spec.coupled), mode=spec.mode)
+    res = P.solve(prob, P.SolverOptions(max_iter=spec.max_iter, tol=TINY_TOL, seed=0,
+                                        precision=precision))
+    return res, unpack_solve(z)
+
+
+def test_config_c1_fp64_matches_reference(P):
+    res, want = _config(P, "c1", "fp64")
+    compare(res, want, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_config_fp32_matches_reference(P, name):
+    res, want = _config(P, name, "fp32")
+    # exact-zero RelErr steps may end the run at a different iteration; compare
+    # the common prefix of the histories, then the final state
+    compare(res, want, rtol=1e-4, prefix_only=True)
+    for s, (blk, (wf, ww)) in enumerate(zip(res.factors.blocks, want["factors"])):
+        _rel_close(blk.weights, ww, 1e-4, f"block {s} weights")
+        for m, (a, b) in enumerate(zip(blk.factors, wf)):
+            _rel_close(a, b, 1e-4, f"block {s} mode {m}")
+    assert abs(res.rel_err_history[-1] - want["rel_err_history"][-1]) <= 1e-4 * want["rel_err_history"][-1]
+
+
+# ---- reference solver invariants (pkg/tests/test_solver.py) on the GPU ----
+
+def _problem(P, seed, **kw):
+    from cases import coupled
+    snr = kw.pop("snr_db", None)
+    counts = kw.pop("counts", (2, 2, 2))
+    tensors = coupled(seed, counts=counts, snr_db=snr)
+    return P.CoupledProblem(tensors, 4, list(counts), **kw)
+
+
+def _monotone(hist, rel_tol=1e-10):
+    arr = np.asarray(hist)
+    bound = rel_tol * np.maximum(np.abs(arr[:-1]), 1.0)
+    assert (np.diff(arr) <= bound).all()
+
+
+def test_monotone_nonnegative_and_shared_columns(P):
+    for mode in ("full", "lra"):
+        prob = _problem(P, 8, counts=(2, 1, 0), mode=mode, snr_db=20.0)
+        res = P.solve(prob, P.SolverOptions(max_iter=60, seed=2))
+        _monotone(res.objective_history)
+        for blk in res.factors.blocks:
+            assert blk.is_nonnegative()
+        for n, ln in enumerate(prob.coupled_counts):
+            for blk in res.factors.blocks[1:]:
+                np.testing.assert_array_equal(blk.factors[n][:, :ln],
+                                              res.factors.blocks[0].factors[n][:, :ln])
+
+
+def test_deterministic_reruns(P):
+    a = P.solve(_problem(P, 10, snr_db=20.0), P.SolverOptions(max_iter=50, seed=4))
+    b = P.solve(_problem(P, 10, snr_db=20.0), P.SolverOptions(max_iter=50, seed=4))
+    assert a.objective_history == b.objective_history
+    assert a.rel_err_history == b.rel_err_history
+    for ba, bb in zip(a.factors.blocks, b.factors.blocks):
+        np.testing.assert_array_equal(ba.weights, bb.weights)
+        for fa, fb in zip(ba.factors, bb.factors):
+            np.testing.assert_array_equal(fa, fb)
+
+
+def test_fixed_core_and_max_iter_zero(P):
+    res = P.solve(_problem(P, 9, update_core=False, snr_db=20.0), P.SolverOptions(max_iter=80, seed=3))
+    for blk in res.factors.blocks:
+        np.testing.assert_array_equal(blk.weights, np.ones(4))
+    prob = _problem(P, 12)
+    res = P.solve(prob, P.SolverOptions(max_iter=0, seed=6))
+    assert res.n_iter == 0 and res.termination_reason == "max_iterations"
+    assert len(res.objective_history) == 1 and len(res.trace) == 1
+    start = P.init_factors(prob, seed=6)
+    for got, want in zip(res.factors.blocks, start.blocks):
+        for f_got, f_want in zip(got.factors, want.factors):
+            np.testing.assert_array_equal(f_got, f_want)
+
+
+def test_zero_tensors(P):
+    prob = P.CoupledProblem([np.zeros((4, 5, 6)), np.zeros((4, 5, 6))], 3, [1, 1, 1])
+    res = P.solve(prob, P.SolverOptions(max_iter=50, seed=7))
+    assert res.rel_err_history[-1] == 0.0
+    assert np.isfinite(res.objective_history).all()
+
+
+def test_lra_trace_reports_original_tensor_quantities(P):
+    prob = _problem(P, 16, snr_db=20.0, mode="lra")
+    res = P.solve(prob, P.SolverOptions(max_iter=80, seed=11))
+    want_obj = P.objective(prob.tensors, res.factors.blocks)
+    assert res.trace[-1].obj_fun == pytest.approx(want_obj, rel=1e-8)
+    assert res.compress_seconds > 0.0
+    assert len(res.compression) == prob.n_blocks
+
+
+def test_device_resident_fp32_inputs(P):
+    """torch CUDA fp32 tensors in first-index-fastest layout are used in place."""
+    import torch
+    from cases import coupled
+    from paper_2302_05119_b200._device import fortran_view
+    tensors = coupled(6, snr_db=20.0)
+    dev = []
+    for t in tensors:
+        flat = torch.from_numpy(np.ravel(t.astype(np.float32), order="F")).cuda()
+        dev.append(fortran_view(flat, t.shape))
+    res_dev = P.solve(P.CoupledProblem(dev, 4, [2, 2, 2]),
+                      P.SolverOptions(max_iter=40, seed=1, precision="fp32"))
+    res_host = P.solve(P.CoupledProblem([t.astype(np.float32).astype(float) for t in tensors], 4, [2, 2, 2]),
+                       P.SolverOptions(max_iter=40, seed=1, precision="fp32"))
+    assert res_dev.objective_history == res_host.objective_history
