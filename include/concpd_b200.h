@@ -193,10 +193,11 @@ int cb_solver_history(cb_solver* h, double* obj_int, double* obj_orig, double* r
                       double* t_ns, int cap);
 int cb_solver_block_factors(cb_solver* h, int block, double* const* host_factors,
                             double* host_weights);
-/* CUDA-event timing of the dominant tensor-streaming kernel: on/off, and the
- * accumulated (milliseconds, launches, algorithmic bytes). */
+/* CUDA-event timing of the tensor-streaming kernels (events on the solve
+ * stream around every launch): on/off, and per kind (0 = all, 1 = fiber pass,
+ * 2 = slab pass) the accumulated milliseconds, launches and algorithmic bytes. */
 int cb_solver_set_timing(cb_solver* h, int on);
-int cb_solver_timing(cb_solver* h, double* ms, long long* launches, double* bytes);
+int cb_solver_timing(cb_solver* h, int kind, double* ms, long long* launches, double* bytes);
 int cb_solver_destroy(cb_solver* h);
 
 /* NCCL communicator for the block-sharded multi-GPU path. `unique_id` is the

@@ -97,7 +97,7 @@ _sig("cb_solver_summary_get", c_int, [c_vp, ctypes.POINTER(SolverSummary)])
 _sig("cb_solver_history", c_int, [c_vp, c_dp, c_dp, c_dp, c_dp, c_int])
 _sig("cb_solver_block_factors", c_int, [c_vp, c_int, ctypes.POINTER(c_dp), c_dp])
 _sig("cb_solver_set_timing", c_int, [c_vp, c_int])
-_sig("cb_solver_timing", c_int, [c_vp, c_dp, ctypes.POINTER(ctypes.c_longlong), c_dp])
+_sig("cb_solver_timing", c_int, [c_vp, c_int, c_dp, ctypes.POINTER(ctypes.c_longlong), c_dp])
 _sig("cb_solver_destroy", c_int, [c_vp])
 _sig("cb_nccl_unique_id", c_int, [c_vp])
 _sig("cb_nccl_comm_init", c_int, [c_vp, c_int, c_int, ctypes.POINTER(c_vp)])

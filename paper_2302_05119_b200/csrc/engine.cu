@@ -196,6 +196,7 @@ struct cb_solver {
   bool graph_ok = true;
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_kind;     // per event pair: 1 fiber, 2 slab
   size_t ev_used = 0;
   double t_ms = 0.0, t_bytes = 0.0;
   long long t_launches = 0;
@@ -207,7 +208,8 @@ struct cb_solver {
 
 namespace cb {
 
-static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b) {
+static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b, int kind) {
+  h->ev_kind.push_back(kind);
   while (h->ev_pool.size() < h->ev_used + 2) {
     cudaEvent_t e;
     CB_CUDA(cudaEventCreate(&e));
@@ -222,7 +224,7 @@ static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b) {
 // stream the blocks once through the fiber kernel (optionally timed)
 static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, int want_res) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing) { int rc = ev_pair(h, &e0, &e1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+  if (h->timing) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
   launch_fiber(h->dtype, h->rb, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(), h->st);
   CB_CHECK_LAUNCH();
   if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
@@ -231,7 +233,7 @@ static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, i
 
 static int enqueue_slab(cb_solver* h, const XArgs& a) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing) { int rc = ev_pair(h, &e0, &e1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+  if (h->timing) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
   launch_slab(h->dtype, h->rb, a, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, h->st);
   CB_CHECK_LAUNCH();
   if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
@@ -826,22 +828,26 @@ int cb_solver_set_timing(cb_solver* h, int on) {
   CB_ARG(h, "null handle");
   h->timing = on != 0;
   h->ev_used = 0;
+  h->ev_kind.clear();
   h->t_ms = 0.0; h->t_bytes = 0.0; h->t_launches = 0;
   return CB_OK;
 }
 
-int cb_solver_timing(cb_solver* h, double* ms, long long* launches, double* bytes) {
+int cb_solver_timing(cb_solver* h, int kind, double* ms, long long* launches, double* bytes) {
   CB_ARG(h, "null handle");
   CB_CUDA(cudaStreamSynchronize(h->st));
   double tot = 0.0;
+  long long n = 0;
   for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+    if (kind != 0 && h->ev_kind[i / 2] != kind) continue;
     float t = 0.f;
     CB_CUDA(cudaEventElapsedTime(&t, h->ev_pool[i], h->ev_pool[i + 1]));
     tot += t;
+    n += 1;
   }
   if (ms) *ms = tot;
-  if (launches) *launches = h->t_launches;
-  if (bytes) *bytes = h->t_bytes;
+  if (launches) *launches = n;
+  if (bytes) *bytes = (double)n * (double)h->elem_total * h->elem_bytes;
   return CB_OK;
 }
 

@@ -402,7 +402,9 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     else Un[i * R + r] = pos(uh[e] - g / lu);
   }
   if (L == 0) return;
-  if (threadIdx.x == 0 && r0 == 0) c.gc_valid[s] = lu > 0.0 ? 1 : 0;
+  // every CTA of block s publishes the flag before its arrival is counted, so
+  // the last CTA of any row tile sees all S flags of this mode update
+  if (threadIdx.x == 0) c.gc_valid[s] = lu > 0.0 ? 1 : 0;
   __threadfence();
   __syncthreads();
   int* flag = reinterpret_cast<int*>(sc + 4);

@@ -99,7 +99,7 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
   TE w[WANT_RES ? RB : 1];
   double res = 0.0;
   if constexpr (WANT_RES) {
-    const double* lam = a.LAM[s];
+    const double* lam = a.LAM ? a.LAM[s] : nullptr;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       double v = 0.0;

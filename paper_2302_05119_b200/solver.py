@@ -371,11 +371,12 @@ class _Engine:
     def set_timing(self, on):
         L.check(L.lib.cb_solver_set_timing(self.h, int(on)))
 
-    def timing(self):
+    def timing(self, kind=0):
         ms = ctypes.c_double()
         n = ctypes.c_longlong()
         b = ctypes.c_double()
-        L.check(L.lib.cb_solver_timing(self.h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b)))
+        L.check(L.lib.cb_solver_timing(self.h, int(kind), ctypes.byref(ms), ctypes.byref(n),
+                                       ctypes.byref(b)))
         return ms.value, n.value, b.value
 
     def close(self):
