@@ -1,0 +1,292 @@
+"""Benchmark: APG iterations/s of the CoNCPD-APG hot path on B200.
+
+Default workload (BASELINE.json configs[1], "c2"): S=10 blocks 100x100x100
+fp32, R=10, L_n=(4,4,4), 10 dB noise, CoNCPD-APG (full mode), seeded
+synthetic inputs.  One step = one APG iteration over all blocks
+(core update, three mode updates with common-column aggregation, objective,
+restart rule, stop rule).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2]
+
+Prints ONE JSON line (rank 0).  The timed region covers exactly K steps, each
+bracketed by CUDA events on the solve stream; L2 is flushed (a 256 MiB write)
+before every timed step, outside the events, because the c2 blocks (40 MB)
+would otherwise stay resident in the 126 MB L2.  Multi-GPU: one process per
+GPU (torchrun), each rank solves its own block shard....
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TINY_TOL = float(np.nextafter(0.0, 1.0))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--cpu-iters", type=int, default=40, help="cpu_baseline sample size")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_port_run(tensors64, spec, iters, warmup=0):
+    """Time the oracle port (reference algorithm, numpy/OpenBLAS, all host
+    threads) for `warmup + iters` APG iterations; returns iterations/s."""
+    from oracle import concpd_oracle as O
+    marks = {}
+
+    def mark(k):
+        marks[k] = time.perf_counter()
+
+    O.solve_oracle(tensors64, spec.rank, list(spec.coupled), mode=spec.mode,
+                   max_iter=warmup + iters, tol=TINY_TOL, seed=0, on_iteration=mark)
+    k0, k1 = warmup, warmup + iters
+    if k1 not in marks:
+        k1 = max(marks)
+    return (k1 - k0) / (marks[k1] - marks[k0]), k1 - k0
+
+
+def host_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([int(i.get("num_threads", 1)) for i in info] or [os.cpu_count() or 1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2302_05119_b200.configs import CONFIGS, generate_config
+    spec = CONFIGS[args.config]
+    tensors, _ = generate_config(args.config)
+    t64 = [np.asarray(t, dtype=np.float64) for t in tensors]
+    rate, n = cpu_port_run(t64, spec, args.steps, warmup=args.warmup)
+    cores = host_threads()
+    line = {
+        "impl": "reference", "metric": "APG iterations/s", "value": rate, "unit": "it/s",
+        "n_gpus": args.gpus, "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 / rate,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+        "data": "synthetic (seeded, SURVEY 8d)",
+        "config": {"workload": spec.description, "name": spec.name},
+        "cpu_baseline": {"value": rate, "unit": "it/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} APG iterations of {spec.name} (all {spec.n_blocks} blocks)"},
+        "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import paper_2302_05119_b200 as P
+    from paper_2302_05119_b200 import _lib as L
+    from paper_2302_05119_b200.configs import CONFIGS, generate_config
+    from paper_2302_05119_b200.solver import PreparedSolve
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    spec = CONFIGS[args.config]
+    tensors, _ = generate_config(args.config)
+    prec = spec.dtype
+    W, K = args.warmup, args.steps
+    opts = P.SolverOptions(max_iter=W + K + 2, tol=TINY_TOL, seed=0, precision=prec)
+    problem = P.CoupledProblem([np.asarray(t, dtype=np.float64) for t in tensors],
+                               spec.rank, list(spec.coupled), mode=spec.mode)
+    # ---- value: iterations with inputs resident in HBM --------------------
+    run = PreparedSolve(problem, opts)
+    stream = run.stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    with torch.cuda.stream(stream):
+        run.engine.run(W)                       # warm-up (also captures the CUDA graph)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    L.launch_count_reset()
+    events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(K)]
+    dev_index = torch.cuda.current_device()
+    with ClockSampler(dev_index) as clocks:
+        torch.cuda.synchronize()
+        for e0, e1 in events:
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)                # evict the blocks from L2 (untimed)
+                e0.record(stream)
+                run.engine.step_async()
+                e1.record(stream)
+        torch.cuda.synchronize()
+    launches = L.launch_count()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in events]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    summ = run.engine.summary()
+    assert summ.n_iter == W + K, f"solve stopped early at iteration {summ.n_iter}"
+    value = K * world / (total_ms * 1e-3) if world > 1 else K / (total_ms * 1e-3)
+    # ---- roofline of the dominant streaming kernel -------------------------
+    run.engine.set_timing(True)
+    with torch.cuda.stream(stream):
+        for _ in range(min(K, 50)):
+            flush.fill_(1.0)
+            run.engine.step_async()
+    torch.cuda.synchronize()
+    kinds = {}
+    for kind, name in ((1, "fiber"), (2, "slab")):
+        ms, n, b = run.engine.timing(kind)
+        if n:
+            kinds[name] = {"ms_avg": ms / n, "launches": n, "bytes_per_launch": b / n,
+                           "gbs": (b / n) / (ms / n * 1e-3) / 1e9}
+    run.engine.set_timing(False)
+    run.close()
+    peak, peak_kind = measured_peak()
+    dom = kinds.get("slab") or kinds.get("fiber")
+    roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+            "frac": dom["gbs"] / peak, "traffic": None, "kernel": "slab (mode-2 MTTKRP, L2-flushed)",
+            "peak_source": peak_kind, "kernels": kinds}
+    # ---- e2e: public API on host buffers (H2D of inputs + D2H of results) --
+    host = [np.asarray(t, dtype=np.float64) for t in tensors]
+    e2e_iters = K
+    torch.cuda.synchronize()
+    tic = time.perf_counter()
+    res = P.solve(P.CoupledProblem(host, spec.rank, list(spec.coupled), mode=spec.mode),
+                  P.SolverOptions(max_iter=e2e_iters, tol=TINY_TOL, seed=0, precision=prec))
+    e2e_s = time.perf_counter() - tic
+    elem = sum(int(np.prod(t.shape)) for t in tensors)
+    h2d = elem * (4 if prec == "fp32" else 8) + sum(
+        8 * (sum(t.shape) * spec.rank + spec.rank) for t in tensors)
+    d2h = 8 * 4 * (res.n_iter + 1) + sum(8 * (sum(t.shape) * spec.rank + spec.rank)
+                                        for t in tensors)
+    e2e = {"value": res.n_iter / e2e_s, "unit": "it/s",
+           "h2d_bytes_per_step": h2d / max(res.n_iter, 1),
+           "d2h_bytes_per_step": d2h / max(res.n_iter, 1),
+           "step": f"one solve() call of {res.n_iter} iterations on host numpy inputs, "
+                   "incl. validation, upload, engine setup, graph capture and result download"}
+    # ---- CPU baseline: the oracle port on a bounded sample -----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t64 = [np.asarray(t, dtype=np.float64) for t in tensors]
+        rate, n = cpu_port_run(t64, spec, args.cpu_iters)
+        cpu = {"value": rate, "unit": "it/s", "cores": host_threads(), "kind": "port",
+               "sample": f"first {n} APG iterations of {spec.name} (all {spec.n_blocks} blocks, "
+                         "fp64 numpy/OpenBLAS restatement of the reference)"}
+    if rank != 0:
+        return
+    line = {
+        "metric": "APG iterations/s", "value": value, "unit": "it/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (seeded, SURVEY 8d; Yale-B/ERP datasets unavailable)",
+        "config": {"workload": spec.description, "name": spec.name, "n_blocks": spec.n_blocks,
+                   "dims": list(spec.dims), "rank": spec.rank, "coupled": list(spec.coupled),
+                   "mode": spec.mode, "storage": prec, "arithmetic": "fp64 accumulation",
+                   "l2": "flushed before every timed step (256 MiB write, outside the events)",
+                   "parallelism": f"dp{world} over blocks" if world > 1 else "single GPU"},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks.summary(), "n_restarts_timed": summ.n_restarts,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -122,6 +122,8 @@ typedef struct {
                                      I_n x R row-major initial factors      */
   double tol;                     /* AlsOptions.tol                         */
   int max_iter;                   /* AlsOptions.max_iter                    */
+  int compute;                    /* fp32 storage only: 0 = fp64 arithmetic in
+                                     the tensor passes, 1 = fp32 arithmetic  */
 } cb_als_desc;
 
 int cb_als_create(const cb_als_desc* desc, void* stream, cb_als** out);
@@ -158,6 +160,8 @@ typedef struct {
   const double* const* tilde_factors; /* lra: host array of DEVICE pointers  */
   const double* const* tilde_weights; /* lra: host array of HOST arrays      */
   int objective;                  /* 0 = explicit residual, 1 = gram expansion */
+  int compute;                    /* fp32 storage only: 0 = fp64 arithmetic in
+                                     the tensor passes, 1 = fp32 arithmetic    */
   double delta_w;
   double tol;
   int max_iter;

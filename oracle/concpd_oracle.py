@@ -245,9 +245,12 @@ def _cprod(mats, skip=None):
 def solve_oracle(tensors, ranks, counts, mode="full", update_core=True,
                  max_iter=1000, tol=1e-8, delta_w=0.9999, seed=0,
                  trace_every=1, als_rank=None, als_tol=1e-4, als_max_iter=200,
-                 als_seed=0):
+                 als_seed=0, on_iteration=None):
     """Coupled nonnegative CPD by APG with restart.  Restates solver.py:546-624
     (outer loop) and the ``_Apg`` state machine solver.py:311-543.
+
+    ``on_iteration(k)`` (optional) is called after every accepted iteration
+    (k = 0 after the initial evaluation); the bench uses it to time steps.
 
     Returns a dict with keys factors (list of (factors, weights)), objective_history,
     rel_err_history, trace (list of (iter, obj_fun, rel_err)), n_iter, n_restarts,
@@ -435,6 +438,8 @@ def solve_oracle(tensors, ranks, counts, mode="full", update_core=True,
     obj_hist = [oi]
     rel_hist = [rel_err]
     trace = [(0, oo, rel_err)]
+    if on_iteration is not None:
+        on_iteration(0)
     reason = "max_iterations"
     n_done = 0
     n_restarts = 0
@@ -458,6 +463,8 @@ def solve_oracle(tensors, ranks, counts, mode="full", update_core=True,
         last = abs(new_rel - rel_err) < tol or k == max_iter
         if k % trace_every == 0 or last:
             trace.append((k, oo, new_rel))
+        if on_iteration is not None:
+            on_iteration(k)
         if abs(new_rel - rel_err) < tol:
             reason = "tolerance"
             break

@@ -43,7 +43,7 @@ class SolverDesc(ctypes.Structure):
         ("tensors", ctypes.POINTER(c_vp)), ("init_factors", ctypes.POINTER(c_dp)),
         ("init_weights", ctypes.POINTER(c_dp)), ("tilde_ranks", c_ip),
         ("tilde_factors", ctypes.POINTER(c_dp)), ("tilde_weights", ctypes.POINTER(c_dp)),
-        ("objective", c_int), ("delta_w", c_dbl), ("tol", c_dbl), ("max_iter", c_int),
+        ("objective", c_int), ("compute", c_int), ("delta_w", c_dbl), ("tol", c_dbl), ("max_iter", c_int),
         ("world_size", c_int), ("rank_id", c_int), ("nccl_comm", c_vp),
         ("total_blocks", c_int), ("block_offset", c_int),
     ]
@@ -57,7 +57,8 @@ class SolverSummary(ctypes.Structure):
 class AlsDesc(ctypes.Structure):
     _fields_ = [("n_blocks", c_int), ("order", c_int), ("dims", c_i64p), ("ranks", c_ip),
                 ("dtype", c_int), ("tensors", ctypes.POINTER(c_vp)),
-                ("init", ctypes.POINTER(c_dp)), ("tol", c_dbl), ("max_iter", c_int)]
+                ("init", ctypes.POINTER(c_dp)), ("tol", c_dbl), ("max_iter", c_int),
+                ("compute", c_int)]
 
 
 def _sig(name, res, args):

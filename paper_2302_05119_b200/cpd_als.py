@@ -63,7 +63,8 @@ def _check_feasible(dims, rank):
 class AlsHandle:
     """Owns a device ALS engine; factors stay resident for the solver."""
 
-    def __init__(self, dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream):
+    def __init__(self, dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream,
+                 compute_code=0):
         self.S = len(dev_tensors)
         self.N = len(dims_list[0])
         self.dims = dims_list
@@ -90,6 +91,7 @@ class AlsHandle:
         desc.init = ctypes.cast(self._init_c, ctypes.POINTER(L.c_dp))
         desc.tol = float(tol)
         desc.max_iter = int(max_iter)
+        desc.compute = int(compute_code)
         h = L.c_vp()
         L.check(L.lib.cb_als_create(ctypes.byref(desc), stream, ctypes.byref(h)))
         self.h = h
@@ -120,9 +122,11 @@ class AlsHandle:
         self.close()
 
 
-def als_compress_blocks(dev_tensors, dims_list, ranks, tol, max_iter, seeds, dtype_code, stream):
+def als_compress_blocks(dev_tensors, dims_list, ranks, tol, max_iter, seeds, dtype_code, stream,
+                        compute_code=0):
     """Batched ALS over blocks; returns the live handle (factors on device)."""
-    h = AlsHandle(dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream)
+    h = AlsHandle(dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream,
+                  compute_code)
     h.run()
     return h
 

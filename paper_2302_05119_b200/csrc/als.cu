@@ -211,7 +211,7 @@ using namespace cb;
 
 struct cb_als {
   cudaStream_t st = nullptr;
-  int S = 0, N = 0, dtype = CB_F64, max_iter = 0, rmax = 1, rb = 8, fast3 = 0;
+  int S = 0, N = 0, dtype = CB_F64, max_iter = 0, rmax = 1, rb = 8, fast3 = 0, pc = 0;
   double tol = 1e-4;
   std::vector<long long> dims;
   std::vector<int> R;
@@ -255,10 +255,10 @@ static int als_sweep(cb_als* h) {
     int src = 0;
     if (h->fast3) {
       if (n < 2) {
-        launch_contract(h->dtype, n, h->xa, n == 0 ? h->d_c0 : h->d_c1,
+        launch_contract(h->pc, n, h->xa, n == 0 ? h->d_c0 : h->d_c1,
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
       } else {
-        launch_slab(h->dtype, h->rb, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, st);
+        launch_slab(h->pc, h->rb, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, st);
         src = 1;
       }
       CB_CHECK_LAUNCH();
@@ -278,7 +278,7 @@ static int als_sweep(cb_als* h) {
   if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
-    launch_fiber(h->dtype, h->rb, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), st);
+    launch_fiber(h->pc, h->rb, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), st);
     CB_CHECK_LAUNCH();
   } else {
     int rc = als_residuals(h);
@@ -313,6 +313,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   cb_als* h = new cb_als();
   h->st = (cudaStream_t)stream;
   h->S = d->n_blocks; h->N = d->order; h->dtype = d->dtype; h->tol = d->tol;
+  h->pc = d->dtype == CB_F64 ? PC_F64 : (d->compute == 1 ? PC_F32 : PC_F32_F64);
   h->max_iter = d->max_iter;
   const int S = h->S, N = h->N;
   h->dims.assign(d->dims, d->dims + S * N);
@@ -409,13 +410,13 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       if (rc) { cb_als_destroy(h); return rc; }
     }
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->dtype, h->tab);
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab);
     if (h->tab.slab_smem > 200 * 1024) {
       cb_als_destroy(h);
       set_error("slab staging (%zu bytes) exceeds shared memory", h->tab.slab_smem);
       return CB_ERR_UNSUPPORTED;
     }
-    prepare_slab(h->dtype, h->rb, h->tab.slab_smem);
+    prepare_slab(h->pc, h->rb, h->tab.slab_smem);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
@@ -434,7 +435,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     c.rpart = rpart;
     c.slab_part = spart;
     std::vector<void*> T0(S), T1(S);
-    const int eb = h->dtype == CB_F32 ? 4 : 8;
+    const int eb = pc_compute_bytes(h->pc);
     for (int s = 0; s < S; ++s) {
       const size_t tb = (size_t)h->tab.nsplit[s] * h->R[s] * h->dims[3 * s] * h->dims[3 * s + 1] * eb;
       TRY(dalloc(&T0[s], tb, A));
@@ -469,7 +470,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
-    launch_fiber(h->dtype, h->rb, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), st);
+    launch_fiber(h->pc, h->rb, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), st);
     CB_CHECK_LAUNCH();
   }
   k_als_control<<<1, 32, 0, st>>>(h->ctx, 1);

@@ -18,90 +18,110 @@
 
 namespace cb {
 
-template <typename TE, int RB>
+// Precision codes of the streaming kernels: storage type of the tensor and
+// arithmetic type of the contraction.
+//   PC_F64     fp64 storage, fp64 arithmetic (parity mode)
+//   PC_F32_F64 fp32 storage, fp64 arithmetic (throughput mode default: half the
+//              bytes, reference-grade sums so the restart rule sees the same
+//              objective the reference does)
+//   PC_F32     fp32 storage, fp32 arithmetic (trace-only / large-rank passes)
+template <typename TE, typename TC, int RB>
 static void launch_fiber_t(int want_t, int want_b, int want_res, const XArgs& a,
                            const FibUnit* u, int n, cudaStream_t st) {
-  if (want_t && want_b && want_res) fiber_kernel<TE, RB, true, true, true><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else if (want_t && want_b) fiber_kernel<TE, RB, true, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else if (want_t && want_res) fiber_kernel<TE, RB, true, false, true><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else if (want_t) fiber_kernel<TE, RB, true, false, false><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else fiber_kernel<TE, RB, false, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+  if (want_t && want_b && want_res) fiber_kernel<TE, TC, RB, true, true, true><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else if (want_t && want_b) fiber_kernel<TE, TC, RB, true, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else if (want_t && want_res) fiber_kernel<TE, TC, RB, true, false, true><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else if (want_t) fiber_kernel<TE, TC, RB, true, false, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+  else fiber_kernel<TE, TC, RB, false, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
 }
 
-template <typename TE>
+template <typename TE, typename TC>
 static void launch_fiber_r(int rb, int want_t, int want_b, int want_res, const XArgs& a,
                            const FibUnit* u, int n, cudaStream_t st) {
   switch (rb) {
-    case 8: launch_fiber_t<TE, 8>(want_t, want_b, want_res, a, u, n, st); break;
-    case 16: launch_fiber_t<TE, 16>(want_t, want_b, want_res, a, u, n, st); break;
-    case 32: launch_fiber_t<TE, 32>(want_t, want_b, want_res, a, u, n, st); break;
-    case 40: launch_fiber_t<TE, 40>(want_t, want_b, want_res, a, u, n, st); break;
-    default: launch_fiber_t<TE, 64>(want_t, want_b, want_res, a, u, n, st); break;
+    case 8: launch_fiber_t<TE, TC, 8>(want_t, want_b, want_res, a, u, n, st); break;
+    case 16: launch_fiber_t<TE, TC, 16>(want_t, want_b, want_res, a, u, n, st); break;
+    case 32: launch_fiber_t<TE, TC, 32>(want_t, want_b, want_res, a, u, n, st); break;
+    case 40: launch_fiber_t<TE, TC, 40>(want_t, want_b, want_res, a, u, n, st); break;
+    default: launch_fiber_t<TE, TC, 64>(want_t, want_b, want_res, a, u, n, st); break;
   }
 }
 
-void launch_fiber(int dtype, int rb, int want_t, int want_b, int want_res, const XArgs& a,
+void launch_fiber(int pc, int rb, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, cudaStream_t st) {
   if (n <= 0) return;
-  if (dtype == CB_F32) launch_fiber_r<float>(rb, want_t, want_b, want_res, a, u, n, st);
-  else launch_fiber_r<double>(rb, want_t, want_b, want_res, a, u, n, st);
+  if (pc == PC_F32) launch_fiber_r<float, float>(rb, want_t, want_b, want_res, a, u, n, st);
+  else if (pc == PC_F32_F64) launch_fiber_r<float, double>(rb, want_t, want_b, want_res, a, u, n, st);
+  else launch_fiber_r<double, double>(rb, want_t, want_b, want_res, a, u, n, st);
   count_launch(1);
 }
 
-template <typename TE, int RB, int SB>
+template <typename TE, typename TC, int RB, int SB>
 static void launch_slab_t(const XArgs& a, const SlabUnit* u, int n, size_t sm, cudaStream_t st) {
   if (n < 0) {   // attribute setup call (outside any graph capture)
-    cudaFuncSetAttribute(slab_kernel<TE, RB, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(slab_kernel<TE, TC, RB, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     return;
   }
-  slab_kernel<TE, RB, SB><<<n, SLAB_THREADS, sm, st>>>(a, u);
+  slab_kernel<TE, TC, RB, SB><<<n, SLAB_THREADS, sm, st>>>(a, u);
 }
 
-int slab_sb_for(int rb) { return rb <= 8 ? 8 : rb <= 16 ? 4 : rb <= 32 ? 2 : 1; }
+int slab_sb_for(int rb, int tc_bytes) {
+  const int sb = rb <= 8 ? 8 : rb <= 16 ? 4 : rb <= 32 ? 2 : 1;
+  return tc_bytes == 8 && sb > 1 ? sb / 2 : sb;
+}
 
-template <typename TE>
+template <typename TE, typename TC>
 static void launch_slab_r(int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
                           cudaStream_t st) {
+  constexpr bool D = sizeof(TC) == 8;
   switch (rb) {
-    case 8: launch_slab_t<TE, 8, 8>(a, u, n, sm, st); break;
-    case 16: launch_slab_t<TE, 16, 4>(a, u, n, sm, st); break;
-    case 32: launch_slab_t<TE, 32, 2>(a, u, n, sm, st); break;
-    case 40: launch_slab_t<TE, 40, 1>(a, u, n, sm, st); break;
-    default: launch_slab_t<TE, 64, 1>(a, u, n, sm, st); break;
+    case 8: launch_slab_t<TE, TC, 8, D ? 4 : 8>(a, u, n, sm, st); break;
+    case 16: launch_slab_t<TE, TC, 16, D ? 2 : 4>(a, u, n, sm, st); break;
+    case 32: launch_slab_t<TE, TC, 32, D ? 1 : 2>(a, u, n, sm, st); break;
+    case 40: launch_slab_t<TE, TC, 40, 1>(a, u, n, sm, st); break;
+    default: launch_slab_t<TE, TC, 64, 1>(a, u, n, sm, st); break;
   }
 }
 
-void prepare_slab(int dtype, int rb, size_t sm) {
-  XArgs a{};
-  if (dtype == CB_F32) launch_slab_r<float>(rb, a, nullptr, -1, sm, 0);
-  else launch_slab_r<double>(rb, a, nullptr, -1, sm, 0);
+static void slab_dispatch(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
+                          cudaStream_t st) {
+  if (pc == PC_F32) launch_slab_r<float, float>(rb, a, u, n, sm, st);
+  else if (pc == PC_F32_F64) launch_slab_r<float, double>(rb, a, u, n, sm, st);
+  else launch_slab_r<double, double>(rb, a, u, n, sm, st);
 }
 
-void launch_slab(int dtype, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
+void prepare_slab(int pc, int rb, size_t sm) {
+  XArgs a{};
+  slab_dispatch(pc, rb, a, nullptr, -1, sm, 0);
+}
+
+void launch_slab(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
                  cudaStream_t st) {
   if (n <= 0) return;
-  if (dtype == CB_F32) launch_slab_r<float>(rb, a, u, n, sm, st);
-  else launch_slab_r<double>(rb, a, u, n, sm, st);
+  slab_dispatch(pc, rb, a, u, n, sm, st);
   count_launch(1);
 }
 
-void launch_contract(int dtype, int mode, const XArgs& a, const RowUnit* u, int n,
+void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
                      cudaStream_t st) {
   if (n <= 0) return;
+  const bool tf = pc == PC_F32;   // T is stored in the fiber pass arithmetic type
   if (mode == 0) {
-    if (dtype == CB_F32) contract0_kernel<float><<<n, 256, 0, st>>>(a, u);
+    if (tf) contract0_kernel<float><<<n, 256, 0, st>>>(a, u);
     else contract0_kernel<double><<<n, 256, 0, st>>>(a, u);
   } else {
-    if (dtype == CB_F32) contract1_kernel<float><<<n, 256, 0, st>>>(a, u);
+    if (tf) contract1_kernel<float><<<n, 256, 0, st>>>(a, u);
     else contract1_kernel<double><<<n, 256, 0, st>>>(a, u);
   }
   count_launch(1);
 }
 
+int pc_compute_bytes(int pc) { return pc == PC_F32 ? 4 : 8; }
+
 int rank_bucket(int r) { return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 40 ? 40 : 64; }
 
-void build_xtables(int S, const long long* dims, const int* R, int rb, int dtype, XTables& t) {
+void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t) {
   const int target = 148 * 4;
   long long tiles = 0;
   for (int s = 0; s < S; ++s) tiles += (dims[3 * s] * dims[3 * s + 1] + FIB_THREADS - 1) / FIB_THREADS;
@@ -117,7 +137,7 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int dtype
       for (long long j0 = 0; j0 < J; j0 += FIB_THREADS) t.fib.push_back(FibUnit{s, sp, j0});
   }
   t.fib_first[S] = (int)t.fib.size();
-  t.sb = slab_sb_for(rb);
+  t.sb = slab_sb_for(rb, pc_compute_bytes(pc));
   long long groups = 0;
   for (int s = 0; s < S; ++s) groups += (dims[3 * s + 2] + t.sb - 1) / t.sb;
   t.slab.clear(); t.slab_first.assign(S, 0); t.slab_nchunk.assign(S, 1);
@@ -137,7 +157,7 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int dtype
       }
     maxI01 = std::max(maxI01, dims[3 * s] + dims[3 * s + 1]);
   }
-  t.slab_smem = (size_t)maxI01 * rb * (dtype == CB_F32 ? 4 : 8);
+  t.slab_smem = (size_t)maxI01 * rb * pc_compute_bytes(pc);
   t.c0.clear(); t.c1.clear();
   for (int s = 0; s < S; ++s) {
     const long long n0 = dims[3 * s] * R[s];
@@ -166,7 +186,7 @@ using namespace cb;
 
 struct cb_solver {
   cudaStream_t st = nullptr;
-  int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0;
+  int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0, pc = 0;
   int rmax = 1, rtmax = 0, rb = 8, max_iter = 0;
   double delta_w = 0.9999, tol = 1e-8;
   std::vector<long long> dims;
@@ -225,7 +245,7 @@ static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b, int kind) {
 static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, int want_res) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->timing) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
-  launch_fiber(h->dtype, h->rb, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(), h->st);
+  launch_fiber(h->pc, h->rb, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(), h->st);
   CB_CHECK_LAUNCH();
   if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
   return CB_OK;
@@ -234,7 +254,7 @@ static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, i
 static int enqueue_slab(cb_solver* h, const XArgs& a) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->timing) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
-  launch_slab(h->dtype, h->rb, a, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, h->st);
+  launch_slab(h->pc, h->rb, a, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, h->st);
   CB_CHECK_LAUNCH();
   if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
   return CB_OK;
@@ -264,7 +284,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       src = 2;
     } else if (h->fast3) {
       if (n < 2) {
-        launch_contract(h->dtype, n, xa, n == 0 ? h->d_c0 : h->d_c1,
+        launch_contract(h->pc, n, xa, n == 0 ? h->d_c0 : h->d_c1,
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
         CB_CHECK_LAUNCH();
       } else {
@@ -463,6 +483,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   h->st = (cudaStream_t)stream;
   h->S = d->n_blocks; h->N = d->order; h->lra = d->lra; h->update_core = d->update_core;
   h->dtype = d->dtype; h->objective = d->objective; h->delta_w = d->delta_w; h->tol = d->tol;
+  h->pc = d->dtype == CB_F64 ? PC_F64 : (d->compute == 1 ? PC_F32 : PC_F32_F64);
   h->max_iter = d->max_iter;
   const int S = h->S, N = h->N;
   h->dims.assign(d->dims, d->dims + S * N);
@@ -637,7 +658,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   // ---- fast 3-way tables and T buffers
   std::vector<void*> T0(S, nullptr), T1(S, nullptr);
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->dtype, h->tab);
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
@@ -654,14 +675,14 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       cb_solver_destroy(h);
       return CB_ERR_UNSUPPORTED;
     }
-    prepare_slab(h->dtype, h->rb, h->tab.slab_smem);
+    prepare_slab(h->pc, h->rb, h->tab.slab_smem);
     TRY(dalloc((void**)&c.fib_bpart, sizeof(double) * h->tab.fib.size() * RSTRIDE, A));
     TRY(dalloc((void**)&c.fib_rpart, sizeof(double) * h->tab.fib.size(), A));
     TRY(dalloc((void**)&c.slab_part, sizeof(double) * h->tab.slab.size() * h->tab.sb * RSTRIDE, A));
     if (!h->lra) {
       for (int s = 0; s < S; ++s) {
         const size_t tb = (size_t)h->tab.nsplit[s] * h->R[s] * h->dims[3 * s] * h->dims[3 * s + 1] *
-                          h->elem_bytes;
+                          pc_compute_bytes(h->pc);
         TRY(dalloc(&T0[s], tb, A));
         TRY(dalloc(&T1[s], tb, A));
       }

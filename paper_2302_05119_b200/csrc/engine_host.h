@@ -19,14 +19,16 @@ struct XTables {
   size_t slab_smem = 0;
 };
 
-void build_xtables(int S, const long long* dims, const int* R, int rb, int dtype, XTables& t);
+enum { PC_F64 = 0, PC_F32_F64 = 1, PC_F32 = 2 };
+int pc_compute_bytes(int pc);
+void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t);
 int rank_bucket(int r);
-void launch_fiber(int dtype, int rb, int want_t, int want_b, int want_res, const XArgs& a,
+void launch_fiber(int pc, int rb, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, cudaStream_t st);
-void prepare_slab(int dtype, int rb, size_t sm);
-void launch_slab(int dtype, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
+void prepare_slab(int pc, int rb, size_t sm);
+void launch_slab(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
                  cudaStream_t st);
-void launch_contract(int dtype, int mode, const XArgs& a, const RowUnit* u, int n,
+void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
                      cudaStream_t st);
 int dalloc(void** p, size_t bytes, std::vector<void*>& allocs);
 void set_alloc_stream(cudaStream_t st);

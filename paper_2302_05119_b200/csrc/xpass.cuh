@@ -66,7 +66,7 @@ __device__ __forceinline__ void* tbuf(const XArgs& a, int s) {
 // ---------------------------------------------------------------------------
 // fiber pass
 // ---------------------------------------------------------------------------
-template <typename TE, int RB, bool STORE_T, bool WANT_B, bool WANT_RES>
+template <typename TE, typename TC, int RB, bool STORE_T, bool WANT_B, bool WANT_RES>
 __global__ void __launch_bounds__(FIB_THREADS)
 fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
   if (gated(a)) return;
@@ -85,7 +85,7 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
   const double* __restrict__ A1 = a.U[3 * s + 1];
   const double* __restrict__ A2 = a.U[3 * s + 2];
 
-  __shared__ TE a2s[FIB_CHUNK][RB];
+  __shared__ TC a2s[FIB_CHUNK][RB];
   __shared__ double red[FIB_THREADS / 32][RB + 1];
 
   const long long j = u.j0 + threadIdx.x;
@@ -93,10 +93,10 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
   long long i0 = 0, i1 = 0;
   if (valid) { i1 = j / I0; i0 = j - i1 * I0; }
 
-  TE acc[RB];
+  TC acc[RB];
 #pragma unroll
-  for (int r = 0; r < RB; ++r) acc[r] = TE(0);
-  TE w[WANT_RES ? RB : 1];
+  for (int r = 0; r < RB; ++r) acc[r] = TC(0);
+  TC w[WANT_RES ? RB : 1];
   double res = 0.0;
   if constexpr (WANT_RES) {
     const double* lam = a.LAM ? a.LAM[s] : nullptr;
@@ -104,7 +104,7 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
     for (int r = 0; r < RB; ++r) {
       double v = 0.0;
       if (r < R && valid) v = (lam ? lam[r] : 1.0) * A0[i0 * R + r] * A1[i1 * R + r];
-      w[r] = (TE)v;
+      w[r] = (TC)v;
     }
   }
 
@@ -113,19 +113,19 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
     __syncthreads();
     for (int e = threadIdx.x; e < FIB_CHUNK * RB; e += FIB_THREADS) {
       int q = e / RB, r = e - q * RB;
-      a2s[q][r] = (q < nc && r < R) ? (TE)A2[(c0 + q) * R + r] : TE(0);
+      a2s[q][r] = (q < nc && r < R) ? (TC)A2[(c0 + q) * R + r] : TC(0);
     }
     __syncthreads();
     if (valid) {
       const TE* xp = X + j + J * c0;
       int q = 0;
       for (; q + 4 <= nc; q += 4) {
-        TE x[4];
+        TC x[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) x[t] = __ldcs(xp + J * (q + t));
+        for (int t = 0; t < 4; ++t) x[t] = (TC)__ldcs(xp + J * (q + t));
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          TE m = TE(0);
+          TC m = TC(0);
 #pragma unroll
           for (int r = 0; r < RB; ++r) {
             acc[r] = fma(x[t], a2s[q + t][r], acc[r]);
@@ -135,8 +135,8 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
         }
       }
       for (; q < nc; ++q) {
-        TE x = __ldcs(xp + J * q);
-        TE m = TE(0);
+        TC x = (TC)__ldcs(xp + J * q);
+        TC m = TC(0);
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
           acc[r] = fma(x, a2s[q][r], acc[r]);
@@ -148,7 +148,7 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
   }
 
   if constexpr (STORE_T) if (valid) {
-    TE* T = reinterpret_cast<TE*>(tbuf(a, s)) + (long long)u.split * R * J;
+    TC* T = reinterpret_cast<TC*>(tbuf(a, s)) + (long long)u.split * R * J;
 #pragma unroll
     for (int r = 0; r < RB; ++r)
       if (r < R) T[(long long)r * J + j] = acc[r];
@@ -185,7 +185,7 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
 // ---------------------------------------------------------------------------
 // slab pass: each unit = (block, SB consecutive i2 slabs, j-range [k0, k1))
 // ---------------------------------------------------------------------------
-template <typename TE, int RB, int SB>
+template <typename TE, typename TC, int RB, int SB>
 __global__ void __launch_bounds__(SLAB_THREADS)
 slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
   if (gated(a)) return;
@@ -200,38 +200,38 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
   const double* __restrict__ A1 = a.U[3 * s + 1];
 
   extern __shared__ __align__(16) unsigned char smraw[];
-  TE* a0s = reinterpret_cast<TE*>(smraw);          // I0 x RB
-  TE* a1s = a0s + I0 * RB;                         // I1 x RB
+  TC* a0s = reinterpret_cast<TC*>(smraw);          // I0 x RB
+  TC* a1s = a0s + I0 * RB;                         // I1 x RB
   for (long long e = threadIdx.x; e < I0 * RB; e += SLAB_THREADS) {
     long long i = e / RB; int r = (int)(e - i * RB);
-    a0s[e] = r < R ? (TE)A0[i * R + r] : TE(0);
+    a0s[e] = r < R ? (TC)A0[i * R + r] : TC(0);
   }
   for (long long e = threadIdx.x; e < I1 * RB; e += SLAB_THREADS) {
     long long i = e / RB; int r = (int)(e - i * RB);
-    a1s[e] = r < R ? (TE)A1[i * R + r] : TE(0);
+    a1s[e] = r < R ? (TC)A1[i * R + r] : TC(0);
   }
   __syncthreads();
 
   int nsl = (int)(I2 - u.g0 < SB ? I2 - u.g0 : SB);
-  TE acc[SB][RB];
+  TC acc[SB][RB];
 #pragma unroll
   for (int m = 0; m < SB; ++m)
 #pragma unroll
-    for (int r = 0; r < RB; ++r) acc[m][r] = TE(0);
+    for (int r = 0; r < RB; ++r) acc[m][r] = TC(0);
 
   long long k = u.k0 + threadIdx.x;
   long long i1 = k / I0, i0 = k - i1 * I0;
   const long long st1 = SLAB_THREADS / I0, st0 = SLAB_THREADS - st1 * I0;
   const TE* xb = X + J * u.g0;
   for (; k < u.k1; k += SLAB_THREADS) {
-    TE x[SB];
+    TC x[SB];
 #pragma unroll
-    for (int m = 0; m < SB; ++m) x[m] = (m < nsl) ? __ldcs(xb + J * m + k) : TE(0);
-    const TE* p0 = a0s + i0 * RB;
-    const TE* p1 = a1s + i1 * RB;
+    for (int m = 0; m < SB; ++m) x[m] = (m < nsl) ? (TC)__ldcs(xb + J * m + k) : TC(0);
+    const TC* p0 = a0s + i0 * RB;
+    const TC* p1 = a1s + i1 * RB;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      TE kr = p0[r] * p1[r];
+      TC kr = p0[r] * p1[r];
 #pragma unroll
       for (int m = 0; m < SB; ++m) acc[m][r] = fma(x[m], kr, acc[m][r]);
     }
@@ -258,7 +258,8 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
 }
 
 // ---------------------------------------------------------------------------
-// contractions of T (mode 0 / mode 1 MTTKRP), fp64 outputs into MTT[s]
+// contractions of T (mode 0 / mode 1 MTTKRP), fp64 outputs into MTT[s];
+// TE here is the storage type of T (= the fiber pass compute type)
 // ---------------------------------------------------------------------------
 template <typename TE>
 __global__ void __launch_bounds__(256)

@@ -15,7 +15,12 @@ Additions over the reference (defaulted, so existing callers are unchanged):
 stores the tensors in fp32 while keeping factors and all small algebra in
 fp64) and ``SolverOptions.objective`` ("auto" = explicit residual in fp64
 like the reference, gram expansion in fp32; or force "explicit" /
-"expansion").
+"expansion") and ``SolverOptions.compute`` (arithmetic of the tensor passes
+when the storage is fp32: "auto" = fp64 for CoNCPD-APG, whose restart rule
+compares objectives that differ by ~1e-12 late in a run, and for the ALS
+compression, whose fixed point is sensitive; fp32 only for the lra
+original-tensor trace pass of ranks > 16, which feeds the reported trace
+alone).
 """
 
 from __future__ import annotations
@@ -136,6 +141,7 @@ class SolverOptions:
     trace_every: int = 1
     precision: str = "fp64"        # "fp64" parity mode | "fp32" throughput mode
     objective: str = "auto"        # "auto" | "explicit" | "expansion"
+    compute: str = "auto"          # fp32 storage: arithmetic of the tensor passes
 
     def __post_init__(self):
         if self.max_iter < 0:
@@ -150,6 +156,8 @@ class SolverOptions:
             raise ValueError(f"unknown precision {self.precision!r}")
         if self.objective not in ("auto", "explicit", "expansion"):
             raise ValueError(f"unknown objective evaluation {self.objective!r}")
+        if self.compute not in ("auto", "fp64", "fp32"):
+            raise ValueError(f"unknown compute type {self.compute!r}")
 
 
 @dataclass(frozen=True)
@@ -404,6 +412,15 @@ class PreparedSolve:
         objective_mode = opts.objective
         if objective_mode == "auto":
             objective_mode = "explicit" if prec == "fp64" else "expansion"
+        # arithmetic of the tensor passes on fp32 storage: fp64 wherever the
+        # result steers the iterates (full-mode MTTKRPs and objective, the ALS
+        # compression); the lra trace pass only feeds the reported trace and
+        # may run in fp32 for large ranks
+        compute = opts.compute
+        if compute == "auto":
+            compute = "fp64" if (problem.mode == "full" or max(problem.ranks) <= 16) else "fp32"
+        self.compute_code = 1 if (prec == "fp32" and compute == "fp32") else 0
+        self.als_compute_code = 1 if (prec == "fp32" and opts.compute == "fp32") else 0
         S, N = problem.n_blocks, problem.order
         with torch.cuda.stream(self.stream):
             self.dev = []
@@ -431,7 +448,7 @@ class PreparedSolve:
                     self.als = als_compress_blocks(self.dev, self.dims, ranks, base.tol,
                                                    base.max_iter,
                                                    [base.seed + s for s in range(S)],
-                                                   self.code, st)
+                                                   self.code, st, self.als_compute_code)
                 except ValueError as exc:
                     msg = str(exc)
                     blk = 0
@@ -478,6 +495,7 @@ class PreparedSolve:
             self._keep.append(L.dptr_array(tw))
             desc.tilde_weights = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_dp))
         desc.objective = 0 if objective_mode == "explicit" else 1
+        desc.compute = self.compute_code
         desc.delta_w = float(opts.delta_w)
         desc.tol = float(opts.tol)
         desc.max_iter = int(opts.max_iter)
