@@ -201,6 +201,9 @@ int cb_solver_block_factors(cb_solver* h, int block, double* const* host_factors
  * stream around every launch): on/off, and per kind (0 = all, 1 = fiber pass,
  * 2 = slab pass) the accumulated milliseconds, launches and algorithmic bytes. */
 int cb_solver_set_timing(cb_solver* h, int on);
+/* per-launch profile of whole iterations (events after every launch, no CUDA
+ * graph while on): on=1 starts, on=0 stops and writes "label count ms" lines */
+int cb_solver_profile(cb_solver* h, int on, char* out, int cap);
 int cb_solver_timing(cb_solver* h, int kind, double* ms, long long* launches, double* bytes);
 int cb_solver_destroy(cb_solver* h);
 

@@ -114,9 +114,9 @@ class AlsHandle:
         return L.lib.cb_als_factor_device(self.h, s, n)
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and L is not None and getattr(L, "lib", None) is not None:
             L.lib.cb_als_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         self.close()

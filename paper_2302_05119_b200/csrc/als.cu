@@ -183,7 +183,7 @@ __global__ void k_als_control(AlsCtx c, int init) {
       }
       double res = 0.0;
       if (c.fast3) {
-        for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) res += c.rpart[u];
+        res = c.rpart[s];   // per-block total folded by the fiber kernel
       } else {
         res = c.res[s];
       }
@@ -230,6 +230,7 @@ struct cb_als {
   double* res_part = nullptr;
   int res_nparts = 0;
   size_t solve_smem = 0;
+  bool tma = false;
 };
 
 namespace cb {
@@ -278,7 +279,7 @@ static int als_sweep(cb_als* h) {
   if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
-    launch_fiber(h->pc, h->rb, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), st);
+    launch_fiber(h->pc, h->rb, h->tma, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), st);
     CB_CHECK_LAUNCH();
   } else {
     int rc = als_residuals(h);
@@ -417,6 +418,8 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       return CB_ERR_UNSUPPORTED;
     }
     prepare_slab(h->pc, h->rb, h->tab.slab_smem);
+    h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->dtype == CB_F32 ? 4 : 8);
+    prepare_fiber(h->pc, h->rb, h->tma);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
@@ -428,11 +431,15 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     c.slab_sb = h->tab.sb;
     int* d_ns;
     TRY(upload(h->tab.nsplit, &d_ns, A, st));
-    double *bpart, *rpart, *spart;
+    double *bpart, *rpart, *spart, *bsum, *rsum;
+    int* blk_cnt;
     TRY(dalloc((void**)&bpart, sizeof(double) * h->tab.fib.size() * RSTRIDE, A));
     TRY(dalloc((void**)&rpart, sizeof(double) * h->tab.fib.size(), A));
+    TRY(dalloc((void**)&bsum, sizeof(double) * S * RSTRIDE, A));
+    TRY(dalloc((void**)&rsum, sizeof(double) * S, A));
+    TRY(dalloc((void**)&blk_cnt, sizeof(int) * S, A));
     TRY(dalloc((void**)&spart, sizeof(double) * h->tab.slab.size() * h->tab.sb * RSTRIDE, A));
-    c.rpart = rpart;
+    c.rpart = rsum;
     c.slab_part = spart;
     std::vector<void*> T0(S), T1(S);
     const int eb = pc_compute_bytes(h->pc);
@@ -451,6 +458,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     xa.T0 = pt0; xa.T1 = pt1; xa.tsel = &h->d_state->tsel; xa.t_other = 0;
     xa.nsplit = d_ns; xa.bpart = bpart; xa.rpart = rpart; xa.slab_part = spart;
     xa.MTT = c.MTT; xa.gate = nullptr; xa.active = c.active;
+    xa.fib_first = c.fib_first; xa.blk_cnt = blk_cnt; xa.bsum = bsum; xa.rsum = rsum;
   } else {
     size_t kr = 0;
     for (int s = 0; s < S; ++s)
@@ -470,7 +478,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
-    launch_fiber(h->pc, h->rb, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), st);
+    launch_fiber(h->pc, h->rb, h->tma, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), st);
     CB_CHECK_LAUNCH();
   }
   k_als_control<<<1, 32, 0, st>>>(h->ctx, 1);

@@ -82,158 +82,251 @@ __host__ __device__ __forceinline__ double extrap_weight(double w_hat, double lp
 // largest eigenvalue of a symmetric R x R matrix (R <= 64), whole block.
 //
 // Replaces tensor_ops.py:127-140 (LAPACK syevd).  Method: repeated squaring of
-// the power-of-two-normalised matrix drives B -> projector onto the top
-// eigenspace in O(log) steps (gap-independent up to 2^60), a column of the
-// limit is the eigenvector estimate, and the Rayleigh quotient with the
-// original matrix gives the eigenvalue to ~1 ulp * R.  Negative-dominant or
-// +-lambda tie inputs (not produced by the solver, whose matrices are PSD
-// Schur products) are handled by a shift and a second pass.
+// the matrix drives B -> (normalised) projector onto the top eigenspace in
+// O(log(1/gap)) squarings (<= 64 squarings resolve any gap >= 2^-60); the
+// column of the limit with the largest diagonal is the eigenvector estimate;
+// one power step and the Rayleigh quotient with the original matrix give the
+// eigenvalue to ~R ulp.  Negative-dominant or +-lambda tie inputs (never
+// produced by the solver, whose matrices are PSD Schur products) are handled
+// by a spectral-radius shift and a second pass.
 //
-// smem: A (R*ld), B, B2 each R*ld doubles with ld = Rp+1, Rp = round_up(R,4);
-//       vec >= 2*64 doubles, red >= 33 doubles.
+// Latency is what matters here (one call per block per mode on the
+// iteration's critical path), so every thread of the block owns fixed entries
+// of B (1x1 for R <= 16, 2x2 register tiles above) for the whole call: the
+// squarings, renormalisation and convergence test need no index arithmetic
+// and one block reduction each.  Two squarings per convergence test.
+//
+// smem: A  Rp4 x lm_ld(R)   (caller's matrix, Rp4 = round_up(R, 4))
+//       B, B2  Rp2 x lm_bld(R) each (Rp2 = round_up(R, 2))
+//       vec >= 128 doubles, red >= 40 doubles
 // ----------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int lm_ld(int R) { return ((R + 3) & ~3) + 1; }
+__host__ __device__ __forceinline__ int lm_rp2(int R) { return (R + 1) & ~1; }
+__host__ __device__ __forceinline__ int lm_bld(int R) { return lm_rp2(R) + 1; }
+__host__ __device__ __forceinline__ int lm_bsize(int R) { return lm_rp2(R) * lm_bld(R); }
 
-__device__ inline double block_dominant_rq(const double* A, int R, int ld, double* B, double* B2,
-                                    double* vec, double* red, double shift, double* resid_out) {
-  const int tid = threadIdx.x;
-  const int Rp = (R + 3) & ~3;
-  const int nt = Rp >> 2;
-  // B = (A + shift I) scaled by a power of two so max |B| in [0.5, 1)
-  double m = 0.0;
-  for (int e = tid; e < R * R; e += blockDim.x) {
-    int i = e / R, j = e - i * R;
-    double v = A[i * ld + j] + (i == j ? shift : 0.0);
-    m = fmax(m, fabs(v));
+// Approximate block max of nonnegative doubles: the high 32 bits of an IEEE
+// double order like the value, so one redux.sync per warp and one across the
+// warp maxima give max(v) truncated to 20 mantissa bits (relative error
+// < 2^-20).  Used only for rescaling and convergence tests, where that is
+// plenty; far cheaper than a shuffle tree on doubles.
+__device__ __forceinline__ double block_max_approx(double v, unsigned* ured) {
+  const unsigned key = (unsigned)(__double_as_longlong(v) >> 32);
+  const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) ured[wid] = wmax;
+  __syncthreads();
+  unsigned m = lane < nw ? ured[lane] : 0u;
+  m = __reduce_max_sync(0xffffffffu, m);
+  __syncthreads();   // ured may be reused by the next call
+  return __longlong_as_double((long long)((unsigned long long)m << 32));
+}
+// exact warp max of nonnegative doubles via two 32-bit redux steps on the bit
+// pattern (high word, then the low word among the lanes holding the max high)
+__device__ __forceinline__ unsigned long long warp_max_bits(unsigned long long k) {
+  const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
+}
+// two exact maxima (nonnegative doubles) in one barrier round
+__device__ __forceinline__ void block_max2_exact(double a, double b, unsigned* ured, double* ma,
+                                                 double* mb) {
+  unsigned long long* ub = reinterpret_cast<unsigned long long*>(ured);
+  const unsigned long long ka = warp_max_bits((unsigned long long)__double_as_longlong(a));
+  const unsigned long long kb = warp_max_bits((unsigned long long)__double_as_longlong(b));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) { ub[wid] = ka; ub[8 + wid] = kb; }
+  __syncthreads();
+  unsigned long long xa = lane < nw ? ub[lane] : 0ull, xb = lane < nw ? ub[8 + lane] : 0ull;
+  xa = warp_max_bits(xa);
+  xb = warp_max_bits(xb);
+  __syncthreads();
+  *ma = __longlong_as_double((long long)xa);
+  *mb = __longlong_as_double((long long)xb);
+}
+
+// B2 = B * B for symmetric B (Rp2 x Rp2, leading dim bld): entry (i,j) is
+// row i . row j.  Thread tile list: tiles t = tid, tid + nthr, ... of the
+// (Rp2/TS)^2 grid, TS x TS entries each.  Ends with a block barrier.
+template <int TS>
+__device__ __forceinline__ void sq_tiles(const double* B, double* B2, int Rp2, int bld) {
+  const int nt = Rp2 / TS;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+    const int ti = t / nt, tj = t - ti * nt;
+    double acc[TS][TS], acc2[TS][TS];
+#pragma unroll
+    for (int a = 0; a < TS; ++a)
+#pragma unroll
+      for (int b = 0; b < TS; ++b) { acc[a][b] = 0.0; acc2[a][b] = 0.0; }
+    const double* ri = B + (TS * ti) * bld;
+    const double* rj = B + (TS * tj) * bld;
+    int k = 0;
+    for (; k + 2 <= Rp2; k += 2) {   // two independent FMA chains
+#pragma unroll
+      for (int a = 0; a < TS; ++a)
+#pragma unroll
+        for (int b = 0; b < TS; ++b) {
+          acc[a][b] = fma(ri[a * bld + k], rj[b * bld + k], acc[a][b]);
+          acc2[a][b] = fma(ri[a * bld + k + 1], rj[b * bld + k + 1], acc2[a][b]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < TS; ++a)
+#pragma unroll
+      for (int b = 0; b < TS; ++b) B2[(TS * ti + a) * bld + TS * tj + b] = acc[a][b] + acc2[a][b];
   }
-  m = block_max(m, red);
+  __syncthreads();
+}
+
+__device__ inline void eigen_tail(const double* A, int R, int ld, const double* B, int bld,
+                                  double* vec, double* red, double shift);
+
+__device__ inline double dominant_rq(const double* A, int R, int ld, double* B, double* B2,
+                                     double* vec, double* red, double shift, double* resid_out) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int Rp2 = lm_rp2(R), bld = lm_bld(R);
+  unsigned* ured = reinterpret_cast<unsigned*>(red);   // 64 words = 32 doubles
+  double m = 0.0;
+  for (int e = tid; e < R * R; e += nthr) {
+    const int i = e / R, j = e - i * R;
+    m = fmax(m, fabs(A[i * ld + j] + (i == j ? shift : 0.0)));
+  }
+  m = block_max_approx(m, ured);
   if (m == 0.0) { if (resid_out) *resid_out = 0.0; return 0.0; }
-  int ex; frexp(m, &ex);
-  for (int e = tid; e < Rp * ld; e += blockDim.x) {
-    int i = e / ld, j = e - i * ld;
+  const double inv0 = 1.0 / m;
+  for (int e = tid; e < Rp2 * bld; e += nthr) {
+    const int i = e / bld, j = e - i * bld;
     double v = 0.0;
-    if (i < R && j < R) v = ldexp(A[i * ld + j] + (i == j ? shift : 0.0), -ex);
+    if (i < R && j < R) v = (A[i * ld + j] + (i == j ? shift : 0.0)) * inv0;
     B[e] = v;
   }
   __syncthreads();
-  for (int it = 0; it < 64; ++it) {
-    // B2 = B * B via 4x4 register tiles (B symmetric: row i . row j)
-    double lmax = 0.0;
-    for (int t = tid; t < nt * nt; t += blockDim.x) {
-      int ti = t / nt, tj = t - ti * nt;
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-      const double* ri = B + (4 * ti) * ld;
-      const double* rj = B + (4 * tj) * ld;
-      for (int k = 0; k < Rp; ++k) {
-        double x[4], y[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) { x[a] = ri[a * ld + k]; y[a] = rj[a * ld + k]; }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+  // passes of four squarings (B -> B^16); after each pass the eigenpair is
+  // extracted and accepted once its residual ||Av - rho v|| / ||v|| is below
+  // 1e-9 ||A||, i.e. the Rayleigh quotient is within ~1e-18 ||A||^2 / gap of
+  // lambda_max.  For the solver's matrices one pass is the norm.
+  double rho = 0.0, resid = 0.0;
+  for (int pass = 0; pass < 16; ++pass) {
+    if (pass > 0) {
+      // rescale B (entries <= Rp2^15 after a pass) before squaring again
+      double mb = 0.0;
+      for (int e = tid; e < Rp2 * Rp2; e += nthr) {
+        const int i = e / Rp2, j = e - i * Rp2;
+        mb = fmax(mb, fabs(B[i * bld + j]));
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          B2[(4 * ti + a) * ld + 4 * tj + b] = acc[a][b];
-          lmax = fmax(lmax, fabs(acc[a][b]));
-        }
-    }
-    lmax = block_max(lmax, red);   // includes a __syncthreads after B2 writes
-    if (lmax == 0.0) break;        // nilpotent-like underflow; keep previous B
-    int e2; frexp(lmax, &e2);
-    double diff = 0.0;
-    for (int e = tid; e < Rp * ld; e += blockDim.x) {
-      int i = e / ld, j = e - i * ld;
-      if (i < Rp && j < Rp) {
-        double v = ldexp(B2[e], -e2);
-        diff = fmax(diff, fabs(v - B[e]));
-        B[e] = v;
+      mb = block_max_approx(mb, ured);
+      if (!(mb > 0.0) || !isfinite(mb)) break;
+      const double ib = 1.0 / mb;
+      for (int e = tid; e < Rp2 * Rp2; e += nthr) {
+        const int i = e / Rp2, j = e - i * Rp2;
+        B[i * bld + j] *= ib;
       }
+      __syncthreads();
     }
-    diff = block_max(diff, red);
-    if (diff < 1e-13 && it >= 1) break;
-  }
-  // eigenvector estimate: the column of the limit with the largest diagonal
-  __shared__ int s_jbest;
-  if (tid == 0) {
-    int jb = 0;
-    double best = -1.0;
-    for (int j = 0; j < R; ++j) {
-      double d = B[j * ld + j];
-      if (d > best) { best = d; jb = j; }
+    if (R <= 16) {
+      sq_tiles<1>(B, B2, Rp2, bld); sq_tiles<1>(B2, B, Rp2, bld);
+      sq_tiles<1>(B, B2, Rp2, bld); sq_tiles<1>(B2, B, Rp2, bld);
+    } else {
+      sq_tiles<2>(B, B2, Rp2, bld); sq_tiles<2>(B2, B, Rp2, bld);
+      sq_tiles<2>(B, B2, Rp2, bld); sq_tiles<2>(B2, B, Rp2, bld);
     }
-    s_jbest = jb;
-  }
-  __syncthreads();
-  const int jb = s_jbest;
-  double* v = vec;
-  double* av = vec + 64;
-  for (int i = tid; i < R; i += blockDim.x) v[i] = B[i * ld + jb];
-  __syncthreads();
-  // one power step with the original (shifted) matrix sharpens the vector
-  for (int i = tid; i < R; i += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < R; ++k) s = fma(A[i * ld + k] + (i == k ? shift : 0.0), v[k], s);
-    av[i] = s;
-  }
-  __syncthreads();
-  double nrm = 0.0;
-  for (int i = tid; i < R; i += blockDim.x) nrm = fmax(nrm, fabs(av[i]));
-  nrm = block_max(nrm, red);
-  if (nrm > 0.0) {
-    int en; frexp(nrm, &en);
-    for (int i = tid; i < R; i += blockDim.x) v[i] = ldexp(av[i], -en);
+    eigen_tail(A, R, ld, B, bld, vec, red, shift);
+    rho = red[36];
+    resid = red[37];
     __syncthreads();
+    if (resid <= 1e-9 * m) break;
   }
-  for (int i = tid; i < R; i += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < R; ++k) s = fma(A[i * ld + k] + (i == k ? shift : 0.0), v[k], s);
-    av[i] = s;
-  }
-  __syncthreads();
-  double num = 0.0, den = 0.0;
-  for (int i = tid; i < R; i += blockDim.x) { num = fma(v[i], av[i], num); den = fma(v[i], v[i], den); }
-  num = block_sum(num, red);
-  den = block_sum(den, red);
-  double rho = den > 0.0 ? num / den : 0.0;
-  if (resid_out) {
-    double r2 = 0.0;
-    for (int i = tid; i < R; i += blockDim.x) { double d = av[i] - rho * v[i]; r2 = fma(d, d, r2); }
-    r2 = block_sum(r2, red);
-    *resid_out = den > 0.0 ? sqrt(r2 / den) : 0.0;
-  }
+  if (resid_out) *resid_out = resid;
   return rho;
 }
 
+// warp 0: eigenvector from the column of B with the largest diagonal, one
+// power step with the original (shifted) matrix, Rayleigh quotient and
+// residual -> red[36], red[37]; ends with a block barrier
+__device__ inline void eigen_tail(const double* A, int R, int ld, const double* B, int bld,
+                                  double* vec, double* red, double shift) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int lane = tid;
+    int jb = 0;
+    {
+      double best = -1.0;
+      for (int j = 0; j < R; ++j) {
+        const double d = B[j * bld + j];
+        if (d > best) { best = d; jb = j; }
+      }
+    }
+    double* v = vec;
+    double* av = vec + 64;
+    for (int i = lane; i < R; i += 32) v[i] = B[i * bld + jb];
+    __syncwarp();
+    double nrm = 0.0;
+    for (int i = lane; i < R; i += 32) {
+      double s = 0.0;
+      for (int k = 0; k < R; ++k) s = fma(A[i * ld + k] + (i == k ? shift : 0.0), v[k], s);
+      av[i] = s;
+      nrm = fmax(nrm, fabs(s));
+    }
+    nrm = warp_max(nrm);
+    __syncwarp();
+    if (nrm > 0.0) {
+      const double inv = 1.0 / nrm;
+      for (int i = lane; i < R; i += 32) v[i] = av[i] * inv;
+      __syncwarp();
+    }
+    double num = 0.0, den = 0.0;
+    for (int i = lane; i < R; i += 32) {
+      double s = 0.0;
+      for (int k = 0; k < R; ++k) s = fma(A[i * ld + k] + (i == k ? shift : 0.0), v[k], s);
+      av[i] = s;
+      num = fma(v[i], s, num);
+      den = fma(v[i], v[i], den);
+    }
+    num = warp_sum(num);
+    den = warp_sum(den);
+    const double rho = den > 0.0 ? num / den : 0.0;
+    double r2 = 0.0;
+    for (int i = lane; i < R; i += 32) { const double d = av[i] - rho * v[i]; r2 = fma(d, d, r2); }
+    r2 = warp_sum(r2);
+    if (lane == 0) {
+      red[36] = rho;
+      red[37] = den > 0.0 ? sqrt(r2 / den) : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
 // lambda_max(A) clamped at 0 (0 for the exact zero matrix).  A in smem with
-// leading dimension lm_ld(R).  All threads of the block must call it.
+// leading dimension lm_ld(R).  All threads of the block must call it; the
+// result is returned to every thread.
 __device__ inline double block_lam_max(const double* A, int R, double* B, double* B2, double* vec,
-                                double* red) {
+                                       double* red) {
   const int ld = lm_ld(R);
   double resid;
-  double rho = block_dominant_rq(A, R, ld, B, B2, vec, red, 0.0, &resid);
+  const double rho = dominant_rq(A, R, ld, B, B2, vec, red, 0.0, &resid);
   double amax = 0.0;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    int i = e / R, j = e - i * R;
+    const int i = e / R, j = e - i * R;
     amax = fmax(amax, fabs(A[i * ld + j]));
   }
-  amax = block_max(amax, red);
+  amax = block_max_approx(amax, reinterpret_cast<unsigned*>(red));
   if (amax == 0.0) return 0.0;
-  // PSD / positive-dominant fast path: a converged eigenpair with rho >= 0 is
-  // the spectral radius, hence lambda_max.
+  // PSD / positive-dominant path: a converged eigenpair with rho >= 0 is the
+  // spectral radius, hence lambda_max
   if (rho >= 0.0 && resid <= 1e-10 * amax * R) return rho;
   // otherwise shift by a spectral-radius bound so A + sI is PSD
-  double s = rho < 0.0 && resid <= 1e-10 * amax * R ? -rho : amax * R;
-  double rho2 = block_dominant_rq(A, R, ld, B, B2, vec, red, s, nullptr);
-  double lm = rho2 - s;
+  const double s = (rho < 0.0 && resid <= 1e-10 * amax * R) ? -rho : 2.0 * amax * R;
+  const double rho2 = dominant_rq(A, R, ld, B, B2, vec, red, s, nullptr);
+  const double lm = rho2 - s;
   return lm > 0.0 ? lm : 0.0;
+}
+
+// shared memory (doubles) of block_lam_max for rank R: A, B, B2, vec, red
+__host__ __device__ __forceinline__ int lm_smem_doubles(int R) {
+  return ((R + 3) & ~3) * lm_ld(R) + 2 * lm_bsize(R) + 128 + 40;
 }
 
 }  // namespace cb

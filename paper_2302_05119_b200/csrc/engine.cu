@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "engine_kernels.cuh"
@@ -18,6 +19,7 @@
 
 namespace cb {
 
+#if 0  // moved to xpass.cu
 // Precision codes of the streaming kernels: storage type of the tensor and
 // arithmetic type of the contraction.
 //   PC_F64     fp64 storage, fp64 arithmetic (parity mode)
@@ -25,34 +27,72 @@ namespace cb {
 //              bytes, reference-grade sums so the restart rule sees the same
 //              objective the reference does)
 //   PC_F32     fp32 storage, fp32 arithmetic (trace-only / large-rank passes)
-template <typename TE, typename TC, int RB>
-static void launch_fiber_t(int want_t, int want_b, int want_res, const XArgs& a,
-                           const FibUnit* u, int n, cudaStream_t st) {
-  if (want_t && want_b && want_res) fiber_kernel<TE, TC, RB, true, true, true><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else if (want_t && want_b) fiber_kernel<TE, TC, RB, true, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else if (want_t && want_res) fiber_kernel<TE, TC, RB, true, false, true><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else if (want_t) fiber_kernel<TE, TC, RB, true, false, false><<<n, FIB_THREADS, 0, st>>>(a, u);
-  else fiber_kernel<TE, TC, RB, false, true, false><<<n, FIB_THREADS, 0, st>>>(a, u);
-}
-
-template <typename TE, typename TC>
-static void launch_fiber_r(int rb, int want_t, int want_b, int want_res, const XArgs& a,
-                           const FibUnit* u, int n, cudaStream_t st) {
-  switch (rb) {
-    case 8: launch_fiber_t<TE, TC, 8>(want_t, want_b, want_res, a, u, n, st); break;
-    case 16: launch_fiber_t<TE, TC, 16>(want_t, want_b, want_res, a, u, n, st); break;
-    case 32: launch_fiber_t<TE, TC, 32>(want_t, want_b, want_res, a, u, n, st); break;
-    case 40: launch_fiber_t<TE, TC, 40>(want_t, want_b, want_res, a, u, n, st); break;
-    default: launch_fiber_t<TE, TC, 64>(want_t, want_b, want_res, a, u, n, st); break;
+// n < 0: set the dynamic shared memory attribute (outside graph capture)
+template <typename TE, typename TC, int RB, bool T, bool B, bool S>
+static void fib_launch(bool tma, const XArgs& a, const FibUnit* u, int n, cudaStream_t st) {
+  if (tma) {
+    constexpr size_t sm = fiber_tma_smem<TE, TC, RB>();
+    if (n < 0) {
+      cudaFuncSetAttribute(fiber_kernel<TE, TC, RB, T, B, S, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      return;
+    }
+    fiber_kernel<TE, TC, RB, T, B, S, true><<<n, FIB_THREADS, sm, st>>>(a, u);
+  } else {
+    if (n < 0) return;
+    fiber_kernel<TE, TC, RB, T, B, S, false><<<n, FIB_THREADS, 0, st>>>(a, u);
   }
 }
 
-void launch_fiber(int pc, int rb, int want_t, int want_b, int want_res, const XArgs& a,
+template <typename TE, typename TC, int RB>
+static void launch_fiber_t(bool tma, int want_t, int want_b, int want_res, const XArgs& a,
+                           const FibUnit* u, int n, cudaStream_t st) {
+  if (want_t && want_b && want_res) fib_launch<TE, TC, RB, true, true, true>(tma, a, u, n, st);
+  else if (want_t && want_b) fib_launch<TE, TC, RB, true, true, false>(tma, a, u, n, st);
+  else if (want_t && want_res) fib_launch<TE, TC, RB, true, false, true>(tma, a, u, n, st);
+  else if (want_t) fib_launch<TE, TC, RB, true, false, false>(tma, a, u, n, st);
+  else fib_launch<TE, TC, RB, false, true, false>(tma, a, u, n, st);
+}
+
+template <typename TE, typename TC>
+static void launch_fiber_r(int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
+                           const FibUnit* u, int n, cudaStream_t st) {
+  switch (rb) {
+    case 8: launch_fiber_t<TE, TC, 8>(tma, want_t, want_b, want_res, a, u, n, st); break;
+    case 16: launch_fiber_t<TE, TC, 16>(tma, want_t, want_b, want_res, a, u, n, st); break;
+    case 32: launch_fiber_t<TE, TC, 32>(tma, want_t, want_b, want_res, a, u, n, st); break;
+    case 40: launch_fiber_t<TE, TC, 40>(tma, want_t, want_b, want_res, a, u, n, st); break;
+    default: launch_fiber_t<TE, TC, 64>(tma, want_t, want_b, want_res, a, u, n, st); break;
+  }
+}
+
+static void fiber_dispatch(int pc, int rb, bool tma, int want_t, int want_b, int want_res,
+                           const XArgs& a, const FibUnit* u, int n, cudaStream_t st) {
+  if (pc == PC_F32) launch_fiber_r<float, float>(rb, tma, want_t, want_b, want_res, a, u, n, st);
+  else if (pc == PC_F32_F64) launch_fiber_r<float, double>(rb, tma, want_t, want_b, want_res, a, u, n, st);
+  else launch_fiber_r<double, double>(rb, tma, want_t, want_b, want_res, a, u, n, st);
+}
+
+bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes) {
+  if (getenv("CB_NO_TMA")) return false;
+  for (int s = 0; s < S; ++s) {
+    const long long J = dims[3 * s] * dims[3 * s + 1];
+    if ((J * elem_bytes) % 16 != 0) return false;
+    if (((uintptr_t)X[s]) % 16 != 0) return false;
+  }
+  return true;
+}
+
+void prepare_fiber(int pc, int rb, bool tma) {
+  XArgs a{};
+  const int combos[5][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {1, 0, 0}, {0, 1, 0}};
+  for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, 0);
+}
+
+void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, cudaStream_t st) {
   if (n <= 0) return;
-  if (pc == PC_F32) launch_fiber_r<float, float>(rb, want_t, want_b, want_res, a, u, n, st);
-  else if (pc == PC_F32_F64) launch_fiber_r<float, double>(rb, want_t, want_b, want_res, a, u, n, st);
-  else launch_fiber_r<double, double>(rb, want_t, want_b, want_res, a, u, n, st);
+  fiber_dispatch(pc, rb, tma, want_t, want_b, want_res, a, u, n, st);
   count_launch(1);
 }
 
@@ -160,12 +200,13 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   t.slab_smem = (size_t)maxI01 * rb * pc_compute_bytes(pc);
   t.c0.clear(); t.c1.clear();
   for (int s = 0; s < S; ++s) {
-    const long long n0 = dims[3 * s] * R[s];
-    for (long long e = 0; e < n0; e += 256) t.c0.push_back(RowUnit{s, (int)e});
+    for (int r = 0; r < R[s]; ++r)
+      for (long long i0 = 0; i0 < dims[3 * s]; i0 += 32) t.c0.push_back(RowUnit{s, (int)((r << 20) | i0)});
     const long long n1 = dims[3 * s + 1] * R[s];
     for (long long p = 0; p < n1; p += 8) t.c1.push_back(RowUnit{s, (int)p});
   }
 }
+#endif  // moved to xpass.cu
 
 static thread_local cudaStream_t g_alloc_stream = nullptr;
 
@@ -215,6 +256,12 @@ struct cb_solver {
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = true;
   bool timing = false;
+  bool profile = false;
+  bool tma = false;             // bulk-copy streaming path usable
+  unsigned long long* ktime = nullptr;   // in-kernel launch timers (CB_PHASES)
+  std::vector<cudaEvent_t> mpool;
+  std::vector<const char*> mlabels;
+  size_t mused = 0;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<int> ev_kind;     // per event pair: 1 fiber, 2 slab
   size_t ev_used = 0;
@@ -227,6 +274,20 @@ struct cb_solver {
 };
 
 namespace cb {
+
+// profiling marks: an event after every launch of the iteration; the interval
+// ending at a mark is charged to that mark's label (kernel time + launch gap)
+static void prof(cb_solver* h, const char* label) {
+  if (!h->profile) return;
+  if (h->mused >= h->mpool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    h->mpool.push_back(e);
+  }
+  cudaEvent_t e = h->mpool[h->mused++];
+  cudaEventRecord(e, h->st);
+  h->mlabels.push_back(label);
+}
 
 static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b, int kind) {
   h->ev_kind.push_back(kind);
@@ -245,7 +306,8 @@ static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b, int kind) {
 static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, int want_res) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->timing) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
-  launch_fiber(h->pc, h->rb, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(), h->st);
+  launch_fiber(h->pc, h->rb, h->tma, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(),
+               h->st);
   CB_CHECK_LAUNCH();
   if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
   return CB_OK;
@@ -278,6 +340,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
   k_sweep_begin<<<h->S, 256, h->blk_smem, st>>>(h->ctx, redo);
   count_launch(1);
   CB_CHECK_LAUNCH();
+  prof(h, redo ? "redo:sweep_begin" : "sweep_begin");
   for (int n = 0; n < h->N; ++n) {
     int src = 0;
     if (h->lra) {
@@ -287,39 +350,47 @@ static int enqueue_sweep(cb_solver* h, int redo) {
         launch_contract(h->pc, n, xa, n == 0 ? h->d_c0 : h->d_c1,
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
         CB_CHECK_LAUNCH();
+        prof(h, redo ? "redo:contract" : (n == 0 ? "contract0" : "contract1"));
       } else {
         int rc = enqueue_slab(h, xa);
         if (rc) return rc;
         src = 1;
+        prof(h, redo ? "redo:slab" : "slab");
       }
     } else {
       for (int s = 0; s < h->S; ++s) {
         int rc = generic_mttkrp(h, s, n);
         if (rc) return rc;
       }
+      prof(h, "generic_mttkrp");
     }
     k_mode_update<<<h->n_rows[n], 256, h->mu_smem, st>>>(h->ctx, n, redo, src, h->d_rows[n]);
     count_launch(1);
     CB_CHECK_LAUNCH();
+    prof(h, redo ? "redo:mode_update" : "mode_update");
     k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo);
     count_launch(1);
     CB_CHECK_LAUNCH();
+    prof(h, redo ? "redo:finalize" : "finalize");
   }
   return CB_OK;
 }
 
 static int enqueue_qr(cb_solver* h, int redo) {
   k_qr_factor<<<h->S * h->N, 256, h->qr_smem, h->st>>>(h->ctx, redo);
+  prof(h, redo ? "redo:qr_factor" : "qr_factor");
   k_qr_core<<<h->S * h->ctx.qr_nchunks, 256, 0, h->st>>>(h->ctx, redo);
+  prof(h, redo ? "redo:qr_core" : "qr_core");
   count_launch(2);
   CB_CHECK_LAUNCH();
   return CB_OK;
 }
 
 static int enqueue_control(cb_solver* h, int mode) {
-  k_control<<<1, 32, 0, h->st>>>(h->ctx, mode, h->fast3 ? 0 : 1);
+  k_control<<<1, 256, sizeof(double) * 3 * h->S, h->st>>>(h->ctx, mode, h->fast3 ? 0 : 1);
   count_launch(1);
   CB_CHECK_LAUNCH();
+  prof(h, "control");
   return CB_OK;
 }
 
@@ -353,16 +424,20 @@ static int enqueue_trace_lra(cb_solver* h) {
 // one full APG iteration (solver.py:586-610), device-gated
 static int enqueue_iteration(cb_solver* h) {
   int rc;
+  prof(h, "(start)");
   if (!h->lra) {
     if ((rc = enqueue_sweep(h, 0))) return rc;
     if ((rc = enqueue_eval_full(h, 0))) return rc;
+    prof(h, "fiber");
     if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
     // restart branch (no-ops unless go_redo)
     k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
     count_launch(1);
     CB_CHECK_LAUNCH();
+    prof(h, "redo:restore");
     if ((rc = enqueue_sweep(h, 1))) return rc;
     if ((rc = enqueue_eval_full(h, 1))) return rc;
+    prof(h, "redo:fiber");
     if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
   } else {
     if ((rc = enqueue_sweep(h, 0))) return rc;
@@ -371,10 +446,12 @@ static int enqueue_iteration(cb_solver* h) {
     k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
     count_launch(1);
     CB_CHECK_LAUNCH();
+    prof(h, "redo:restore");
     if ((rc = enqueue_sweep(h, 1))) return rc;
     if ((rc = enqueue_qr(h, 1))) return rc;
     if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
     if ((rc = enqueue_trace_lra(h))) return rc;
+    prof(h, "trace_fiber");
     if ((rc = enqueue_control(h, CTRL_FINISH))) return rc;
   }
   return CB_OK;
@@ -589,6 +666,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     TRY(upload(TW, &p, A, st)); c.TW = p;
   }
   TRY(dalloc((void**)&c.lipc_hist, sizeof(double) * S, A));
+  c.dbg = nullptr;
+  if (getenv("CB_PHASES")) TRY(dalloc((void**)&c.dbg, sizeof(double) * 64, A));
   TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
   TRY(dalloc((void**)&c.lu, sizeof(double) * N * S, A));
   TRY(dalloc((void**)&c.lup, sizeof(double) * N * S, A));
@@ -676,8 +755,15 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       return CB_ERR_UNSUPPORTED;
     }
     prepare_slab(h->pc, h->rb, h->tab.slab_smem);
-    TRY(dalloc((void**)&c.fib_bpart, sizeof(double) * h->tab.fib.size() * RSTRIDE, A));
-    TRY(dalloc((void**)&c.fib_rpart, sizeof(double) * h->tab.fib.size(), A));
+    h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->elem_bytes);
+    prepare_fiber(h->pc, h->rb, h->tma);
+    double *ubpart, *urpart;
+    TRY(dalloc((void**)&ubpart, sizeof(double) * h->tab.fib.size() * RSTRIDE, A));
+    TRY(dalloc((void**)&urpart, sizeof(double) * h->tab.fib.size(), A));
+    TRY(dalloc((void**)&c.fib_bpart, sizeof(double) * S * RSTRIDE, A));
+    TRY(dalloc((void**)&c.fib_rpart, sizeof(double) * S, A));
+    int* blk_cnt;
+    TRY(dalloc((void**)&blk_cnt, sizeof(int) * S, A));
     TRY(dalloc((void**)&c.slab_part, sizeof(double) * h->tab.slab.size() * h->tab.sb * RSTRIDE, A));
     if (!h->lra) {
       for (int s = 0; s < S; ++s) {
@@ -696,8 +782,17 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     XArgs xa{};
     xa.X = pX; xa.dims = c.dims; xa.R = c.R; xa.U = (const double* const*)c.U; xa.LAM = (const double* const*)c.LAM;
     xa.T0 = pv; xa.T1 = pv1; xa.tsel = &h->d_state->tsel; xa.t_other = 0;
-    xa.nsplit = d_ns; xa.bpart = c.fib_bpart; xa.rpart = c.fib_rpart; xa.slab_part = c.slab_part;
+    xa.nsplit = d_ns; xa.bpart = ubpart; xa.rpart = urpart; xa.slab_part = c.slab_part;
+    xa.fib_first = c.fib_first; xa.blk_cnt = blk_cnt; xa.bsum = c.fib_bpart; xa.rsum = c.fib_rpart;
     xa.MTT = c.MTT; xa.active = nullptr;
+    xa.ktime = nullptr;
+    if (c.dbg) {
+      TRY(dalloc((void**)&h->ktime, sizeof(unsigned long long) * 8, A));
+      const unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, ~0ull, 0};
+      CB_CUDA(cudaMemcpyAsync(h->ktime, init, sizeof(init), cudaMemcpyHostToDevice, st));
+      CB_CUDA(cudaStreamSynchronize(st));
+      xa.ktime = h->ktime;
+    }
     xa.gate = &h->d_state->go_main;
     h->xa_main = xa;
     xa.gate = &h->d_state->go_redo;
@@ -731,6 +826,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_mode_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->mu_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(sizeof(double) * 3 * S)));
   if (h->lra)
     CB_CUDA(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qr_smem));
   // ---- iteration 0
@@ -748,7 +845,7 @@ int cb_solver_step_async(cb_solver* h) {
     int rc = generic_iteration(h);
     return rc;
   }
-  if (h->timing) return enqueue_iteration(h);
+  if (h->timing || h->profile) return enqueue_iteration(h);
   if (!h->gexec && h->graph_ok) {
     cudaGraph_t g;
     cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
@@ -842,6 +939,65 @@ int cb_solver_block_factors(cb_solver* h, int block, double* const* host_factors
     CB_CUDA(cudaMemcpyAsync(host_weights, h->h_LAM[block], sizeof(double) * h->R[block], cudaMemcpyDeviceToHost, h->st));
   }
   CB_CUDA(cudaStreamSynchronize(h->st));
+  return CB_OK;
+}
+
+int cb_solver_profile(cb_solver* h, int on, char* out, int cap) {
+  CB_ARG(h, "null handle");
+  if (on) {
+    h->profile = true;
+    h->mused = 0;
+    h->mlabels.clear();
+    return CB_OK;
+  }
+  CB_CUDA(cudaStreamSynchronize(h->st));
+  h->profile = false;
+  // aggregate intervals (previous mark -> this mark) by this mark's label
+  std::vector<std::string> names;
+  std::vector<double> tot;
+  std::vector<long long> cnt;
+  for (size_t i = 1; i < h->mused; ++i) {
+    if (strcmp(h->mlabels[i], "(start)") == 0) continue;
+    float t = 0.f;
+    CB_CUDA(cudaEventElapsedTime(&t, h->mpool[i - 1], h->mpool[i]));
+    size_t k = 0;
+    for (; k < names.size(); ++k)
+      if (names[k] == h->mlabels[i]) break;
+    if (k == names.size()) { names.push_back(h->mlabels[i]); tot.push_back(0.0); cnt.push_back(0); }
+    tot[k] += t;
+    cnt[k] += 1;
+  }
+  std::string s;
+  char line[160];
+  for (size_t k = 0; k < names.size(); ++k) {
+    snprintf(line, sizeof(line), "%s %lld %.6f\n", names[k].c_str(), cnt[k], tot[k]);
+    s += line;
+  }
+  if (h->ctx.dbg) {
+    double ph[64];
+    CB_CUDA(cudaMemcpy(ph, h->ctx.dbg, sizeof(ph), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 64; ++k)
+      if (ph[k] > 0.0) {
+        snprintf(line, sizeof(line), "phase%02d 0 %.6f\n", k, ph[k] * 1e-6);
+        s += line;
+      }
+  }
+  if (h->ktime) {
+    unsigned long long kt[8];
+    CB_CUDA(cudaMemcpy(kt, h->ktime, sizeof(kt), cudaMemcpyDeviceToHost));
+    if (kt[1]) {
+      snprintf(line, sizeof(line), "kernel:fiber %llu %.6f\n", kt[1], kt[0] * 1e-6);
+      s += line;
+    }
+    if (kt[5]) {
+      snprintf(line, sizeof(line), "kernel:slab %llu %.6f\n", kt[5], kt[4] * 1e-6);
+      s += line;
+    }
+  }
+  if (out && cap > 0) {
+    strncpy(out, s.c_str(), cap - 1);
+    out[cap - 1] = 0;
+  }
   return CB_OK;
 }
 

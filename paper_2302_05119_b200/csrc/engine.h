@@ -50,6 +50,7 @@ struct Ctx {
   double* const* STEP;        // S step matrices of the current mode
   double* const* MTT;         // S MTTKRP outputs of the current mode (I_n x R)
   double* lipc_hist;          // S (NaN = unset)
+  double* dbg;                // phase-time accumulators (profiling only) or null
   double* lipf_hist;          // N*S
   double* lu;                 // N*S current factor Lipschitz constants
   double* lup;                // N*S the "previous" constants used this sweep
@@ -70,8 +71,8 @@ struct Ctx {
   double* qr_part;            // S*qr_nchunks partial core sums
   int qr_nchunks;
   int* qr_need;               // S flags: QR route taken this evaluation
-  double* fib_bpart;          // fiber partials
-  double* fib_rpart;
+  double* fib_bpart;          // per-block fiber totals: b (S x RSTRIDE)
+  double* fib_rpart;          //   and explicit residual (S)
   const int* fib_first;       // S+1 unit ranges
   double* slab_part;
   const int* slab_first;      // S

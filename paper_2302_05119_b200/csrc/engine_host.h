@@ -23,8 +23,11 @@ enum { PC_F64 = 0, PC_F32_F64 = 1, PC_F32 = 2 };
 int pc_compute_bytes(int pc);
 void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t);
 int rank_bucket(int r);
-void launch_fiber(int pc, int rb, int want_t, int want_b, int want_res, const XArgs& a,
+void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, cudaStream_t st);
+void prepare_fiber(int pc, int rb, bool tma);
+// 16-byte aligned rows for the bulk-copy (TMA) streaming path
+bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes);
 void prepare_slab(int pc, int rb, size_t sm);
 void launch_slab(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
                  cudaStream_t st);

@@ -12,6 +12,35 @@
 
 namespace cb {
 
+// Phase timestamps (profiling builds of a run: Ctx.dbg non-null): block 0
+// accumulates the time between consecutive PH() marks into dbg[slot].
+struct PhaseClock {
+  unsigned long long last = 0;
+  long long last_clk = 0;
+  __device__ __forceinline__ unsigned long long now() const {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  }
+  __device__ __forceinline__ void start(const double* dbg) {
+    if (dbg && blockIdx.x == 0) { __syncthreads(); last = now(); last_clk = clock64(); }
+  }
+  // dbg[slot] += ns, dbg[32 + slot] += SM cycles (their ratio is the clock)
+  __device__ __forceinline__ void mark(double* dbg, int slot) {
+    if (dbg && blockIdx.x == 0) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long t = now();
+        const long long k = clock64();
+        dbg[slot] += (double)(t - last);
+        dbg[32 + slot] += (double)(k - last_clk);
+        last = t;
+        last_clk = k;
+      }
+    }
+  }
+};
+
 __device__ __forceinline__ bool stopped(const Ctx& c, int redo) {
   return redo ? (c.st->go_redo == 0) : (c.st->go_main == 0);
 }
@@ -35,8 +64,8 @@ __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
   const int Rp = (rmax + 3) & ~3;
   b.lmA = sm;
   b.lmB = b.lmA + Rp * ld;
-  b.lmB2 = b.lmB + Rp * ld;
-  b.vec = b.lmB2 + Rp * ld;
+  b.lmB2 = b.lmB + lm_bsize(rmax);
+  b.vec = b.lmB2 + lm_bsize(rmax);
   b.red = b.vec + 128;
   b.gr = b.red + 40;
   b.gw = gw;
@@ -45,9 +74,7 @@ __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
 }
 
 __host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
-  const int ld = ((rmax + 3) & ~3) + 1;
-  const int Rp = (rmax + 3) & ~3;
-  return sizeof(double) * (3 * (size_t)Rp * ld + 128 + 40 + 2 * 32 * (size_t)gw + 4 * 64 + 8);
+  return sizeof(double) * ((size_t)lm_smem_doubles(rmax) + 2 * 32 * (size_t)gw + 4 * 64 + 8);
 }
 
 // out[P x Q] = A^T B with A rows x P, B rows x Q (row-major), whole block,
@@ -109,12 +136,15 @@ __device__ inline void build_gram_product(const Ctx& c, int s, int skip, bool ti
 __device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const BlockSmem& sm) {
   const int R = c.R[s];
   const int ld = lm_ld(R);
+  PhaseClock pc;
+  pc.start(c.dbg);
   build_gram_product(c, s, n, true, sm);
   double* step = c.STEP[s];
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, j = e - i * R;
     step[e] = sm.lmA[i * ld + j];
   }
+  pc.mark(c.dbg, 4);
   const double lu = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
   if (threadIdx.x == 0) {
     const int idx = n * c.S + s;
@@ -124,6 +154,7 @@ __device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const Bloc
     c.lu[idx] = lu;
   }
   __syncthreads();
+  pc.mark(c.dbg, 5);
 }
 
 // Final per-block quantities of an evaluation: model_sq = lam^T (had G) lam and
@@ -449,6 +480,8 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo) {
   double* Uc = c.U[s * N + n];
   double* Upr = c.Up[s * N + n];
   const double* Un = c.Un[s * N + n];
+  PhaseClock pc;
+  pc.start(c.dbg);
   for (long long e = threadIdx.x; e < In * R; e += blockDim.x) {
     const long long i = e / R;
     const int r = (int)(e - i * R);
@@ -456,13 +489,17 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo) {
     Uc[e] = r < L ? c.cnew[i * L + r] : Un[e];
   }
   __syncthreads();
+  pc.mark(c.dbg, 0);
   block_gram(Uc, R, Uc, R, In, c.G[s * N + n], sm);
   if (c.lra) block_gram(c.Ut[s * N + n], c.Rt[s], Uc, R, In, c.C[s * N + n], sm);
   __syncthreads();
+  pc.mark(c.dbg, 1);
   if (n + 1 < N) {
     step_and_lipschitz(c, s, n + 1, sm);
+    pc.mark(c.dbg, 2);
   } else {
     final_quantities(c, s, sm);
+    pc.mark(c.dbg, 3);
   }
 }
 
@@ -626,9 +663,7 @@ __device__ inline double block_res_full(const Ctx& c, int s, int bsrc) {
   // bsrc: 0 = fiber partials (fast3), 1 = c.res / c.borig (generic)
   if (c.objective == 0) {
     if (bsrc == 0) {
-      double r = 0.0;
-      for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) r += c.fib_rpart[u];
-      return r;
+      return c.fib_rpart[s];   // per-block total folded by the fiber kernel
     }
     return c.res[s];
   }
@@ -647,9 +682,7 @@ __device__ inline void stage_b_from_fiber(const Ctx& c) {
     double* b = c.bbuf + ((long long)(1 - c.st->bsel) * c.S + s) * RSTRIDE;
     const int R = c.R[s];
     for (int r = 0; r < R; ++r) {
-      double a = 0.0;
-      for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) a += c.fib_bpart[(long long)u * RSTRIDE + r];
-      b[r] = a;
+      b[r] = c.fib_bpart[(long long)s * RSTRIDE + r];
     }
   }
 }
@@ -702,26 +735,80 @@ __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double o
   st->k = k + 1;
 }
 
-__global__ void k_control(Ctx c, int mode, int bsrc) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Evaluation totals and the iteration rules.  Per-block terms are formed in
+// parallel (thread s handles block s, ...) into shared memory; thread 0 then
+// folds them in block order — the reference's summation order — and applies
+// the restart / stop rules.  Launched with 256 threads and 16*S bytes of
+// dynamic shared memory.
+__global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc) {
   State* st = c.st;
   if (st->done) return;
   if (mode == CTRL_REDO && !st->go_redo) return;
+  if (!c.lra && mode == CTRL_FINISH) return;
+  extern __shared__ double csm[];
+  double* val = csm;           // per-block residual (or compressed residual)
+  double* relv = csm + c.S;    // per-block relative error contribution
   const int fast_t = (bsrc == 0);
+  const bool lra_cmp = c.lra && (mode == CTRL_DECIDE || mode == CTRL_REDO);
+  for (int s = threadIdx.x; s < c.S; s += blockDim.x) {
+    if (!c.lra) {
+      if (fast_t) {
+        double* b = c.bbuf + ((long long)(1 - st->bsel) * c.S + s) * RSTRIDE;
+        const int R = c.R[s];
+        for (int r = 0; r < R; ++r) b[r] = c.fib_bpart[(long long)s * RSTRIDE + r];
+      }
+      const double r = block_res_full(c, s, bsrc);
+      val[s] = r;
+      const double nrm = sqrt(c.nsq[s]);
+      relv[s] = nrm > 0.0 ? sqrt(r > 0.0 ? r : 0.0) / nrm : 0.0;
+    } else if (lra_cmp) {
+      double rt = c.res_t[s];
+      if (qr_route_needed(c, s)) {
+        double a = 0.0;
+        for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
+        rt = a;
+      }
+      val[s] = rt;
+    } else {
+      // original-tensor trace quantities (solver.py:519-522)
+      const int R = c.R[s];
+      const double* lam = c.LAM[s];
+      double lb = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const double b = fast_t ? c.fib_bpart[(long long)s * RSTRIDE + r]
+                                : c.borig[(long long)s * RSTRIDE + r];
+        lb = fma(lam[r], b, lb);
+      }
+      const double raw = c.nsq[s] - 2.0 * lb + c.model_sq[s];
+      val[s] = raw;   // Python max(raw, 0.0) keeps NaN / +inf (checked below)
+      const double nrm = sqrt(c.nsq[s]);
+      const double r = raw > 0.0 ? raw : 0.0;
+      relv[s] = nrm > 0.0 ? sqrt(r) / nrm : 0.0;
+    }
+    if (c.lra && mode == CTRL_INIT) {
+      // the iteration-0 evaluation also needs the compressed residual
+      double rt = c.res_t[s];
+      if (qr_route_needed(c, s)) {
+        double a = 0.0;
+        for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
+        rt = a;
+      }
+      csm[2 * c.S + s] = rt;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   if (!c.lra) {
-    if (mode == CTRL_FINISH) return;
-    if (fast_t) stage_b_from_fiber(c);
     double oi = 0.0, rel = 0.0;
     for (int s = 0; s < c.S; ++s) {
-      const double r = block_res_full(c, s, bsrc);
+      const double r = val[s];
       if (!isfinite(r)) {
         st->error = CB_ERR_NONFINITE; st->err_block = s; st->err_iter = st->k;
         st->done = 1; st->go_main = 0; st->go_redo = 0;
         return;
       }
       oi += 0.5 * r;
-      const double nrm = sqrt(c.nsq[s]);
-      rel += nrm > 0.0 ? sqrt(r > 0.0 ? r : 0.0) / nrm : 0.0;
+      rel += relv[s];
     }
     rel /= c.S;
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
@@ -733,8 +820,9 @@ __global__ void k_control(Ctx c, int mode, int bsrc) {
     return;
   }
   // ---- lra ----
-  if (mode == CTRL_DECIDE || mode == CTRL_REDO) {
-    const double oi = lra_compressed_obj(c);
+  if (lra_cmp) {
+    double oi = 0.0;
+    for (int s = 0; s < c.S; ++s) oi += 0.5 * (val[s] > 0.0 ? val[s] : 0.0);
     st->obj_pending = oi;
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
       st->n_restarts += 1;
@@ -742,33 +830,25 @@ __global__ void k_control(Ctx c, int mode, int bsrc) {
     }
     return;
   }
-  // CTRL_INIT or CTRL_FINISH: original-tensor trace quantities
-  const double oi = (mode == CTRL_INIT) ? lra_compressed_obj(c) : st->obj_pending;
+  // CTRL_INIT or CTRL_FINISH
+  double oi = st->obj_pending;
+  if (mode == CTRL_INIT) {
+    oi = 0.0;
+    for (int s = 0; s < c.S; ++s) {
+      const double rt = csm[2 * c.S + s];
+      oi += 0.5 * (rt > 0.0 ? rt : 0.0);
+    }
+  }
   double oo = 0.0, rel = 0.0;
   for (int s = 0; s < c.S; ++s) {
-    const int R = c.R[s];
-    const double* lam = c.LAM[s];
-    double lb = 0.0;
-    for (int r = 0; r < R; ++r) {
-      double b;
-      if (fast_t) {
-        b = 0.0;
-        for (int u = c.fib_first[s]; u < c.fib_first[s + 1]; ++u) b += c.fib_bpart[(long long)u * RSTRIDE + r];
-      } else {
-        b = c.borig[(long long)s * RSTRIDE + r];
-      }
-      lb = fma(lam[r], b, lb);
-    }
-    double r = c.nsq[s] - 2.0 * lb + c.model_sq[s];
-    r = r > 0.0 ? r : 0.0;
-    if (!isfinite(r)) {
+    const double raw = val[s];
+    if (raw != raw || raw == INFINITY) {
       st->error = CB_ERR_NONFINITE; st->err_block = s; st->err_iter = st->k;
       st->done = 1; st->go_main = 0; st->go_redo = 0;
       return;
     }
-    oo += 0.5 * r;
-    const double nrm = sqrt(c.nsq[s]);
-    rel += nrm > 0.0 ? sqrt(r) / nrm : 0.0;
+    oo += 0.5 * (raw > 0.0 ? raw : 0.0);
+    rel += relv[s];
   }
   rel /= c.S;
   accept_and_advance(c, oi, oo, rel, 0);

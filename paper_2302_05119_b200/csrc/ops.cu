@@ -199,8 +199,8 @@ __global__ void __launch_bounds__(256) spectral_batched_kernel(const double* __r
   const int Rp = (R + 3) & ~3;
   double* A = sm;
   double* B = A + Rp * ld;
-  double* B2 = B + Rp * ld;
-  double* vec = B2 + Rp * ld;
+  double* B2 = B + lm_bsize(R);
+  double* vec = B2 + lm_bsize(R);
   double* red = vec + 128;
   const double* gb = g + (int64_t)blockIdx.x * R * R;
   for (int e = threadIdx.x; e < Rp * ld; e += blockDim.x) {
@@ -212,11 +212,7 @@ __global__ void __launch_bounds__(256) spectral_batched_kernel(const double* __r
   if (threadIdx.x == 0) out[blockIdx.x] = v;
 }
 
-size_t lam_max_smem_bytes(int R) {
-  const int ld = lm_ld(R);
-  const int Rp = (R + 3) & ~3;
-  return sizeof(double) * (3 * (size_t)Rp * ld + 128 + 40);
-}
+size_t lam_max_smem_bytes(int R) { return sizeof(double) * (size_t)lm_smem_doubles(R); }
 
 // ----------------------------------------------------------------------------
 // tensor statistics: sum of squares, min, non-finite count (two-stage)
@@ -243,18 +239,25 @@ __global__ void __launch_bounds__(256) tensor_stats_kernel(const TE* __restrict_
   }
 }
 
-__global__ void stats_final_kernel(const double* __restrict__ part, int nparts,
-                                   double* __restrict__ out3) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// fixed-order second stage: thread t sums parts t, t+256, ...; then the
+// deterministic block tree
+__global__ void __launch_bounds__(256) stats_final_kernel(const double* __restrict__ part,
+                                                          int nparts, double* __restrict__ out3) {
+  __shared__ double red[40];
   double ss = 0.0, mn = INFINITY, bad = 0.0;
-  for (int p = 0; p < nparts; ++p) {
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
     ss += part[3 * p];
     mn = fmin(mn, part[3 * p + 1]);
     bad += part[3 * p + 2];
   }
-  out3[0] = ss;
-  out3[1] = mn;
-  out3[2] = bad;
+  ss = block_sum(ss, red);
+  bad = block_sum(bad, red);
+  mn = -block_max(-mn, red);
+  if (threadIdx.x == 0) {
+    out3[0] = ss;
+    out3[1] = mn;
+    out3[2] = bad;
+  }
 }
 
 int tensor_stats(int dtype, const void* X, int64_t n, double* out3, double* part, int nparts,
@@ -263,7 +266,7 @@ int tensor_stats(int dtype, const void* X, int64_t n, double* out3, double* part
     tensor_stats_kernel<float><<<nparts, 256, 0, st>>>((const float*)X, n, part);
   else
     tensor_stats_kernel<double><<<nparts, 256, 0, st>>>((const double*)X, n, part);
-  stats_final_kernel<<<1, 32, 0, st>>>(part, nparts, out3);
+  stats_final_kernel<<<1, 256, 0, st>>>(part, nparts, out3);
   count_launch(2);
   CB_CHECK_LAUNCH();
   return CB_OK;
@@ -295,12 +298,13 @@ __global__ void __launch_bounds__(256) kruskal_resid_kernel(ResidArgs a, const T
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-__global__ void sum_parts_kernel(const double* __restrict__ part, int nparts,
-                                 double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(256) sum_parts_kernel(const double* __restrict__ part,
+                                                        int nparts, double* __restrict__ out) {
+  __shared__ double red[40];
   double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += part[p];
-  *out = s;
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += part[p];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
 }
 
 int kruskal_residual(int dtype, const ResidArgs& a, const void* X, double* out, double* part,
@@ -309,7 +313,7 @@ int kruskal_residual(int dtype, const ResidArgs& a, const void* X, double* out, 
     kruskal_resid_kernel<float><<<nparts, 256, 0, st>>>(a, (const float*)X, part);
   else
     kruskal_resid_kernel<double><<<nparts, 256, 0, st>>>(a, (const double*)X, part);
-  sum_parts_kernel<<<1, 32, 0, st>>>(part, nparts, out);
+  sum_parts_kernel<<<1, 256, 0, st>>>(part, nparts, out);
   count_launch(2);
   CB_CHECK_LAUNCH();
   return CB_OK;

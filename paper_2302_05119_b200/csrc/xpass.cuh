@@ -24,6 +24,7 @@
 // and the explicit objective rides along the fiber pass for free.
 #pragma once
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace cb {
 
@@ -53,7 +54,41 @@ struct XArgs {
   double* const* MTT;            // per block I_n x R output (contract kernels)
   const int* gate;               // if non-null and *gate == 0 -> skip (flag gating)
   const int* active;             // per-block activity (ALS); nullptr -> all active
+  // per-block totals of the fiber partials, formed by the last CTA of each
+  // block in unit order (deterministic): bsum[s][RSTRIDE], rsum[s]
+  const int* fib_first;          // S+1 unit ranges
+  int* blk_cnt;                  // S arrival counters (self-resetting)
+  double* bsum;
+  double* rsum;
+  unsigned long long* ktime;     // profiling only: [0] fiber, [1] slab accumulators
 };
+
+// In-kernel wall time of a whole launch (first CTA start -> last CTA end),
+// accumulated into kt[0] (ns), kt[1] (launches); kt[2], kt[3] scratch.
+// Profiling builds of a run only (ktime non-null).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ktime_begin(unsigned long long* kt) {
+  if (kt && threadIdx.x == 0) atomicMin(&kt[2], gtimer());
+}
+__device__ __forceinline__ void ktime_end(unsigned long long* kt) {
+  if (!kt) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(&kt[3], 1ull) + 1;
+    if (done == gridDim.x) {
+      const unsigned long long t = gtimer();
+      kt[0] += t - kt[2];
+      kt[1] += 1;
+      kt[2] = ~0ull;
+      kt[3] = 0;
+    }
+  }
+}
 
 __device__ __forceinline__ bool gated(const XArgs& a) {
   return a.gate != nullptr && *a.gate == 0;
@@ -66,13 +101,28 @@ __device__ __forceinline__ void* tbuf(const XArgs& a, int s) {
 // ---------------------------------------------------------------------------
 // fiber pass
 // ---------------------------------------------------------------------------
-template <typename TE, typename TC, int RB, bool STORE_T, bool WANT_B, bool WANT_RES>
+// TMA variant: the unit's X rows (j-tile of 256 elements per i2 row) stream
+// through a FIB_NST-stage ring of FIB_CH-row stages filled by 1-D bulk copies
+// (cp.async.bulk, issued by one thread, completing on an mbarrier), so each
+// CTA keeps FIB_NST * FIB_CH * 1 KB (fp32) in flight independent of its
+// thread count.  Requires 16-B aligned rows (host checks; else TMA=false).
+constexpr int FIB_CH = 8;
+constexpr int FIB_NST = 4;
+
+template <typename TE, typename TC, int RB>
+__host__ __device__ constexpr size_t fiber_tma_smem() {
+  return 128 + (size_t)FIB_NST * FIB_CH * FIB_THREADS * sizeof(TE) +
+         (size_t)FIB_NST * FIB_CH * RB * sizeof(TC);
+}
+
+template <typename TE, typename TC, int RB, bool STORE_T, bool WANT_B, bool WANT_RES, bool TMA>
 __global__ void __launch_bounds__(FIB_THREADS)
 fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
   if (gated(a)) return;
   const FibUnit u = units[blockIdx.x];
   const int s = u.s;
   if (a.active && !a.active[s]) return;
+  ktime_begin(a.ktime);
   const int R = a.R[s];
   const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1], I2 = a.dims[3 * s + 2];
   const long long J = I0 * I1;
@@ -108,6 +158,63 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
     }
   }
 
+  if constexpr (TMA) {
+    extern __shared__ __align__(128) unsigned char fsm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsm);
+    TE* xbuf = reinterpret_cast<TE*>(fsm + 128);
+    TC* a2t = reinterpret_cast<TC*>(fsm + 128 + (size_t)FIB_NST * FIB_CH * FIB_THREADS * sizeof(TE));
+    const long long jt = (J - u.j0) < FIB_THREADS ? (J - u.j0) : FIB_THREADS;
+    const uint32_t row_bytes = (uint32_t)(jt * sizeof(TE));
+    const int nstages = (int)((i2e - i2b + FIB_CH - 1) / FIB_CH);
+    auto issue = [&](int k) {
+      const int slot = k % FIB_NST;
+      const long long r0 = i2b + (long long)k * FIB_CH;
+      const int nr = (int)((i2e - r0) < FIB_CH ? (i2e - r0) : FIB_CH);
+      mbar_arrive_expect_tx(&bar[slot], nr * row_bytes);
+      for (int q = 0; q < nr; ++q)
+        bulk_g2s(xbuf + ((size_t)slot * FIB_CH + q) * FIB_THREADS, X + u.j0 + J * (r0 + q),
+                 row_bytes, &bar[slot]);
+    };
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < FIB_NST; ++st) mbar_init(&bar[st], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < nstages && k < FIB_NST; ++k) issue(k);
+    for (int k = 0; k < nstages; ++k) {
+      const int slot = k % FIB_NST;
+      const long long r0 = i2b + (long long)k * FIB_CH;
+      const int nr = (int)((i2e - r0) < FIB_CH ? (i2e - r0) : FIB_CH);
+      TC* as = a2t + (size_t)slot * FIB_CH * RB;
+      for (int e = threadIdx.x; e < FIB_CH * RB; e += FIB_THREADS) {
+        const int q = e / RB, r = e - q * RB;
+        as[e] = (q < nr && r < R) ? (TC)A2[(r0 + q) * R + r] : TC(0);
+      }
+      __syncthreads();
+      mbar_wait(&bar[slot], (uint32_t)((k / FIB_NST) & 1));
+      if (valid) {
+        const TE* xs = xbuf + (size_t)slot * FIB_CH * FIB_THREADS + threadIdx.x;
+        for (int q = 0; q < nr; ++q) {
+          const TC x = (TC)xs[q * FIB_THREADS];
+          TC m = TC(0);
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            if (r < R) {
+              acc[r] = fma(x, as[q * RB + r], acc[r]);
+              if constexpr (WANT_RES) m = fma(w[r], as[q * RB + r], m);
+            }
+          }
+          if constexpr (WANT_RES) { double d = (double)x - (double)m; res = fma(d, d, res); }
+        }
+      }
+      __syncthreads();   // slot fully consumed
+      if (threadIdx.x == 0 && k + FIB_NST < nstages) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(k + FIB_NST);
+      }
+    }
+  } else
   for (long long c0 = i2b; c0 < i2e; c0 += FIB_CHUNK) {
     const int nc = (int)((i2e - c0) < FIB_CHUNK ? (i2e - c0) : FIB_CHUNK);
     __syncthreads();
@@ -128,8 +235,10 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
           TC m = TC(0);
 #pragma unroll
           for (int r = 0; r < RB; ++r) {
-            acc[r] = fma(x[t], a2s[q + t][r], acc[r]);
-            if constexpr (WANT_RES) m = fma(w[r], a2s[q + t][r], m);
+            if (r < R) {   // uniform: skips the bucket's padding columns
+              acc[r] = fma(x[t], a2s[q + t][r], acc[r]);
+              if constexpr (WANT_RES) m = fma(w[r], a2s[q + t][r], m);
+            }
           }
           if constexpr (WANT_RES) { double d = (double)x[t] - (double)m; res = fma(d, d, res); }
         }
@@ -139,8 +248,10 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
         TC m = TC(0);
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
-          acc[r] = fma(x, a2s[q][r], acc[r]);
-          if constexpr (WANT_RES) m = fma(w[r], a2s[q][r], m);
+          if (r < R) {
+            acc[r] = fma(x, a2s[q][r], acc[r]);
+            if constexpr (WANT_RES) m = fma(w[r], a2s[q][r], m);
+          }
         }
         if constexpr (WANT_RES) { double d = (double)x - (double)m; res = fma(d, d, res); }
       }
@@ -180,6 +291,43 @@ fiber_kernel(XArgs a, const FibUnit* __restrict__ units) {
       a.rpart[blockIdx.x] = t;
     }
   }
+  if constexpr (WANT_B || WANT_RES) {
+    // the last CTA of block s folds the per-unit partials in unit order
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    const int first = a.fib_first[s], nunits = a.fib_first[s + 1] - first;
+    if (threadIdx.x == 0) s_last = (atomicAdd(&a.blk_cnt[s], 1) == nunits - 1);
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if constexpr (WANT_B) {
+        // thread (r, c): contiguous quarter c of the unit range, then the four
+        // quarter sums in order
+        __shared__ double qs[4][RB];
+        const int r = threadIdx.x & 63, c = threadIdx.x >> 6;
+        if (r < R) {
+          const int q0 = (int)((long long)nunits * c / 4), q1 = (int)((long long)nunits * (c + 1) / 4);
+          double t = 0.0;
+#pragma unroll 4
+          for (int q = q0; q < q1; ++q) t += __ldcg(&a.bpart[(long long)(first + q) * RSTRIDE + r]);
+          qs[c][r] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x < R)
+          a.bsum[(long long)s * RSTRIDE + threadIdx.x] =
+              ((qs[0][threadIdx.x] + qs[1][threadIdx.x]) + qs[2][threadIdx.x]) + qs[3][threadIdx.x];
+      }
+      if constexpr (WANT_RES) {
+        double t = 0.0;
+        for (int q = threadIdx.x; q < nunits; q += FIB_THREADS) t += __ldcg(&a.rpart[first + q]);
+        t = block_sum(t, &red[0][0]);
+        if (threadIdx.x == 0) a.rsum[s] = t;
+      }
+      if (threadIdx.x == 0) a.blk_cnt[s] = 0;
+    }
+  }
+  ktime_end(a.ktime);
 }
 
 // ---------------------------------------------------------------------------
@@ -192,6 +340,7 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
   const SlabUnit u = units[blockIdx.x];
   const int s = u.s;
   if (a.active && !a.active[s]) return;
+  ktime_begin(a.ktime ? a.ktime + 4 : nullptr);
   const int R = a.R[s];
   const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1], I2 = a.dims[3 * s + 2];
   const long long J = I0 * I1;
@@ -200,14 +349,19 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
   const double* __restrict__ A1 = a.U[3 * s + 1];
 
   extern __shared__ __align__(16) unsigned char smraw[];
-  TC* a0s = reinterpret_cast<TC*>(smraw);          // I0 x RB
-  TC* a1s = a0s + I0 * RB;                         // I1 x RB
+  // factor rows staged r-major (a0s[r][i0]): lanes of a warp walk consecutive
+  // i0, so every smem read below is conflict-free (a row-major copy would put
+  // all 32 lanes on one bank)
+  TC* a0s = reinterpret_cast<TC*>(smraw);          // RB x I0
+  TC* a1s = a0s + I0 * RB;                         // RB x I1
   for (long long e = threadIdx.x; e < I0 * RB; e += SLAB_THREADS) {
-    long long i = e / RB; int r = (int)(e - i * RB);
+    const int r = (int)(e / I0);
+    const long long i = e - r * I0;
     a0s[e] = r < R ? (TC)A0[i * R + r] : TC(0);
   }
   for (long long e = threadIdx.x; e < I1 * RB; e += SLAB_THREADS) {
-    long long i = e / RB; int r = (int)(e - i * RB);
+    const int r = (int)(e / I1);
+    const long long i = e - r * I1;
     a1s[e] = r < R ? (TC)A1[i * R + r] : TC(0);
   }
   __syncthreads();
@@ -227,13 +381,15 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
     TC x[SB];
 #pragma unroll
     for (int m = 0; m < SB; ++m) x[m] = (m < nsl) ? (TC)__ldcs(xb + J * m + k) : TC(0);
-    const TC* p0 = a0s + i0 * RB;
-    const TC* p1 = a1s + i1 * RB;
+    const TC* p0 = a0s + i0;
+    const TC* p1 = a1s + i1;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      TC kr = p0[r] * p1[r];
+      if (r < R) {   // uniform: skips the bucket's padding columns
+        TC kr = p0[r * I0] * p1[r * I1];
 #pragma unroll
-      for (int m = 0; m < SB; ++m) acc[m][r] = fma(x[m], kr, acc[m][r]);
+        for (int m = 0; m < SB; ++m) acc[m][r] = fma(x[m], kr, acc[m][r]);
+      }
     }
     i0 += st0; i1 += st1;
     if (i0 >= I0) { i0 -= I0; i1 += 1; }
@@ -245,8 +401,10 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
   for (int m = 0; m < SB; ++m)
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      double v = warp_sum((double)acc[m][r]);
-      if (lane == 0) red[wid][m * RB + r] = v;
+      if (r < R) {
+        double v = warp_sum((double)acc[m][r]);
+        if (lane == 0) red[wid][m * RB + r] = v;
+      }
     }
   __syncthreads();
   for (int e = threadIdx.x; e < SB * RB; e += SLAB_THREADS) {
@@ -255,6 +413,7 @@ slab_kernel(XArgs a, const SlabUnit* __restrict__ units) {
     int m = e / RB, r = e - m * RB;
     a.slab_part[((long long)blockIdx.x * SB + m) * RSTRIDE + r] = t;
   }
+  ktime_end(a.ktime ? a.ktime + 4 : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -271,18 +430,29 @@ contract0_kernel(XArgs a, const RowUnit* __restrict__ units) {
   const int R = a.R[s];
   const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1];
   const long long J = I0 * I1;
-  const long long e = (long long)u.r0 + threadIdx.x;   // e = r * I0 + i0
-  if (e >= I0 * R) return;
-  const long long r = e / I0, i0 = e - r * I0;
+  // unit = (block, r, 32 consecutive i0); threads = 32 i0 lanes x 8 i1 groups
+  const int r = u.r0 >> 20;
+  const long long i0 = (u.r0 & 0xFFFFF) + (threadIdx.x & 31);
+  const int grp = threadIdx.x >> 5;
   const double* A1 = a.U[3 * s + 1];
   const TE* T = reinterpret_cast<const TE*>(tbuf(a, s));
   const int ns = a.nsplit[s];
   double acc = 0.0;
-  for (int sp = 0; sp < ns; ++sp) {
-    const TE* Tr = T + ((long long)sp * R + r) * J + i0;
-    for (long long i1 = 0; i1 < I1; ++i1) acc = fma((double)Tr[I0 * i1], A1[i1 * R + r], acc);
+  if (i0 < I0) {
+    for (int sp = 0; sp < ns; ++sp) {
+      const TE* Tr = T + ((long long)sp * R + r) * J + i0;
+#pragma unroll 4
+      for (long long i1 = grp; i1 < I1; i1 += 8) acc = fma((double)Tr[I0 * i1], A1[i1 * R + r], acc);
+    }
   }
-  a.MTT[s][i0 * R + r] = acc;
+  __shared__ double part[8][33];
+  part[grp][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32 && i0 < I0) {
+    double t = 0.0;
+    for (int g = 0; g < 8; ++g) t += part[g][threadIdx.x];
+    a.MTT[s][i0 * R + r] = t;
+  }
 }
 
 template <typename TE>

@@ -388,9 +388,9 @@ class _Engine:
         return ms.value, n.value, b.value
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and L is not None and getattr(L, "lib", None) is not None:
             L.lib.cb_solver_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         self.close()
