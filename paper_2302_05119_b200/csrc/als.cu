@@ -259,7 +259,7 @@ static int als_sweep(cb_als* h) {
         launch_contract(h->pc, n, h->xa, n == 0 ? h->d_c0 : h->d_c1,
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
       } else {
-        launch_slab(h->pc, h->rb, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, st);
+        launch_slab(h->pc, h->rb, h->tma, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab, st);
         src = 1;
       }
       CB_CHECK_LAUNCH();
@@ -279,7 +279,7 @@ static int als_sweep(cb_als* h) {
   if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
-    launch_fiber(h->pc, h->rb, h->tma, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), st);
+    launch_fiber(h->pc, h->rb, h->tma, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), h->tab, st);
     CB_CHECK_LAUNCH();
   } else {
     int rc = als_residuals(h);
@@ -411,15 +411,10 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       if (rc) { cb_als_destroy(h); return rc; }
     }
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab);
-    if (h->tab.slab_smem > 200 * 1024) {
-      cb_als_destroy(h);
-      set_error("slab staging (%zu bytes) exceeds shared memory", h->tab.slab_smem);
-      return CB_ERR_UNSUPPORTED;
-    }
-    prepare_slab(h->pc, h->rb, h->tab.slab_smem);
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab, S);
     h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->dtype == CB_F32 ? 4 : 8);
-    prepare_fiber(h->pc, h->rb, h->tma);
+    prepare_slab(h->pc, h->rb, h->tma, h->tab);
+    prepare_fiber(h->pc, h->rb, h->tma, h->tab);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
@@ -458,6 +453,8 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     xa.T0 = pt0; xa.T1 = pt1; xa.tsel = &h->d_state->tsel; xa.t_other = 0;
     xa.nsplit = d_ns; xa.bpart = bpart; xa.rpart = rpart; xa.slab_part = spart;
     xa.MTT = c.MTT; xa.gate = nullptr; xa.active = c.active;
+    xa.ktime = nullptr;
+    xa.slab_stage_rows = h->tab.slab_rows;
     xa.fib_first = c.fib_first; xa.blk_cnt = blk_cnt; xa.bsum = bsum; xa.rsum = rsum;
   } else {
     size_t kr = 0;
@@ -478,7 +475,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
-    launch_fiber(h->pc, h->rb, h->tma, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), st);
+    launch_fiber(h->pc, h->rb, h->tma, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), h->tab, st);
     CB_CHECK_LAUNCH();
   }
   k_als_control<<<1, 32, 0, st>>>(h->ctx, 1);

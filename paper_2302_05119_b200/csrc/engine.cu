@@ -303,22 +303,26 @@ static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b, int kind) {
 }
 
 // stream the blocks once through the fiber kernel (optionally timed)
+// timing mode brackets main-path launches only: the restart-branch copies are
+// gated no-ops unless a restart happens and would dilute the average
 static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, int want_res) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+  const bool timed = h->timing && a.gate != &h->d_state->go_redo;
+  if (timed) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
   launch_fiber(h->pc, h->rb, h->tma, want_t, want_b, want_res, a, h->d_fib, (int)h->tab.fib.size(),
-               h->st);
+               h->tab, h->st);
   CB_CHECK_LAUNCH();
-  if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
+  if (timed) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
   return CB_OK;
 }
 
 static int enqueue_slab(cb_solver* h, const XArgs& a) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
-  launch_slab(h->pc, h->rb, a, h->d_slab, (int)h->tab.slab.size(), h->tab.slab_smem, h->st);
+  const bool timed = h->timing && a.gate != &h->d_state->go_redo;
+  if (timed) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+  launch_slab(h->pc, h->rb, h->tma, a, h->d_slab, (int)h->tab.slab.size(), h->tab, h->st);
   CB_CHECK_LAUNCH();
-  if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
+  if (timed) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
   return CB_OK;
 }
 
@@ -737,7 +741,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   // ---- fast 3-way tables and T buffers
   std::vector<void*> T0(S, nullptr), T1(S, nullptr);
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab);
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab, S);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
@@ -749,14 +753,9 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     int* d_ns;
     TRY(upload(h->tab.nsplit, &d_ns, A, st));
     c.slab_sb = h->tab.sb;
-    if (h->tab.slab_smem > 200 * 1024) {
-      set_error("slab staging (%zu bytes) exceeds shared memory", h->tab.slab_smem);
-      cb_solver_destroy(h);
-      return CB_ERR_UNSUPPORTED;
-    }
-    prepare_slab(h->pc, h->rb, h->tab.slab_smem);
     h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->elem_bytes);
-    prepare_fiber(h->pc, h->rb, h->tma);
+    prepare_slab(h->pc, h->rb, h->tma, h->tab);
+    prepare_fiber(h->pc, h->rb, h->tma, h->tab);
     double *ubpart, *urpart;
     TRY(dalloc((void**)&ubpart, sizeof(double) * h->tab.fib.size() * RSTRIDE, A));
     TRY(dalloc((void**)&urpart, sizeof(double) * h->tab.fib.size(), A));
@@ -786,6 +785,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     xa.fib_first = c.fib_first; xa.blk_cnt = blk_cnt; xa.bsum = c.fib_bpart; xa.rsum = c.fib_rpart;
     xa.MTT = c.MTT; xa.active = nullptr;
     xa.ktime = nullptr;
+    xa.slab_stage_rows = h->tab.slab_rows;
     if (c.dbg) {
       TRY(dalloc((void**)&h->ktime, sizeof(unsigned long long) * 8, A));
       const unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, ~0ull, 0};

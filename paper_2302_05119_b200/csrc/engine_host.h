@@ -16,21 +16,25 @@ struct XTables {
   std::vector<int> slab_nchunk; // S
   std::vector<RowUnit> c0, c1;
   int sb = 1;
-  size_t slab_smem = 0;
+  long long fib_rows = 0;    // max i2 rows of a fiber unit (A2 rows staged per CTA)
+  long long slab_rows = 0;   // A0+A1 rows the slab kernel stages (0: read through L1)
 };
 
 enum { PC_F64 = 0, PC_F32_F64 = 1, PC_F32 = 2 };
 int pc_compute_bytes(int pc);
-void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t);
+void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t,
+                   int s_total);
 int rank_bucket(int r);
+// Streaming kernel launches: `t` supplies the unit shapes; n < 0 (prepare_*)
+// only sets the kernels' shared-memory attributes (outside graph capture).
 void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                  const FibUnit* u, int n, cudaStream_t st);
-void prepare_fiber(int pc, int rb, bool tma);
+                  const FibUnit* u, int n, const XTables& t, cudaStream_t st);
+void prepare_fiber(int pc, int rb, bool tma, const XTables& t);
 // 16-byte aligned rows for the bulk-copy (TMA) streaming path
 bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes);
-void prepare_slab(int pc, int rb, size_t sm);
-void launch_slab(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                 cudaStream_t st);
+void prepare_slab(int pc, int rb, bool tma, const XTables& t);
+void launch_slab(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, int n,
+                 const XTables& t, cudaStream_t st);
 void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
                      cudaStream_t st);
 int dalloc(void** p, size_t bytes, std::vector<void*>& allocs);

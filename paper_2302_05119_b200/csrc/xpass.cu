@@ -1,7 +1,14 @@
-// Launchers and unit tables of the tensor-streaming kernels (xpass.cuh),
-// shared by the solver (engine.cu) and ALS (als.cu) engines.  Kept in their
-// own translation unit: they hold every template instantiation of the
-// streaming kernels.
+// Launchers and unit tables of the tensor-streaming kernels (xpass2.cuh,
+// xpass.cuh), shared by the solver (engine.cu) and ALS (als.cu) engines.
+// Kept in their own translation unit: they hold every template instantiation
+// of the streaming kernels.
+//
+// Precision codes (storage type of the tensor, arithmetic of the pass):
+//   PC_F64     fp64 storage, fp64 arithmetic (parity mode)
+//   PC_F32_F64 fp32 storage, fp64 arithmetic (throughput mode default: half the
+//              bytes, reference-grade sums so the restart rule sees the same
+//              objective the reference does)
+//   PC_F32     fp32 storage, fp32 arithmetic (trace-only / large-rank passes)
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -11,129 +18,108 @@
 #include "engine_host.h"
 #include "ops_internal.h"
 #include "status.h"
+#include "xpass2.cuh"
 
 namespace cb {
 
-// Precision codes of the streaming kernels: storage type of the tensor and
-// arithmetic type of the contraction.
-//   PC_F64     fp64 storage, fp64 arithmetic (parity mode)
-//   PC_F32_F64 fp32 storage, fp64 arithmetic (throughput mode default: half the
-//              bytes, reference-grade sums so the restart rule sees the same
-//              objective the reference does)
-//   PC_F32     fp32 storage, fp32 arithmetic (trace-only / large-rank passes)
-// n < 0: set the dynamic shared memory attribute (outside graph capture)
-template <typename TE, typename TC, int RB, bool T, bool B, bool S>
-static void fib_launch(bool tma, const XArgs& a, const FibUnit* u, int n, cudaStream_t st) {
-  if (tma) {
-    constexpr size_t sm = fiber_tma_smem<TE, TC, RB>();
-    if (n < 0) {
-      cudaFuncSetAttribute(fiber_kernel<TE, TC, RB, T, B, S, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      return;
-    }
-    fiber_kernel<TE, TC, RB, T, B, S, true><<<n, FIB_THREADS, sm, st>>>(a, u);
-  } else {
-    if (n < 0) return;
-    fiber_kernel<TE, TC, RB, T, B, S, false><<<n, FIB_THREADS, 0, st>>>(a, u);
+int rank_bucket(int r) {
+  return r <= 8 ? 8 : r <= 12 ? 12 : r <= 16 ? 16 : r <= 24 ? 24 : r <= 32 ? 32 : r <= 40 ? 40 : 64;
+}
+int pc_compute_bytes(int pc) { return pc == PC_F32 ? 4 : 8; }
+static int pc_storage_bytes(int pc) { return pc == PC_F64 ? 8 : 4; }
+
+// ---- dispatch helpers: F(TE, TC, RB) over the precision code and bucket ----
+#define CB_RB_SWITCH(RBV, CALL)                     \
+  switch (RBV) {                                    \
+    case 8: { constexpr int RB = 8; CALL; } break;  \
+    case 12: { constexpr int RB = 12; CALL; } break; \
+    case 16: { constexpr int RB = 16; CALL; } break; \
+    case 24: { constexpr int RB = 24; CALL; } break; \
+    case 32: { constexpr int RB = 32; CALL; } break; \
+    case 40: { constexpr int RB = 40; CALL; } break; \
+    default: { constexpr int RB = 64; CALL; } break; \
   }
+
+// n < 0: set the dynamic shared-memory attribute (call outside graph capture)
+template <typename TE, typename TC, int RB, bool T, bool B, bool S>
+static void fib2_go(bool tma, const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                    cudaStream_t st) {
+  const size_t sm = fiber2_smem<TE, TC, RB>(t.fib_rows);
+  if (n < 0) {
+    cudaFuncSetAttribute(fiber2_kernel<TE, TC, RB, T, B, S>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return;
+  }
+  fiber2_kernel<TE, TC, RB, T, B, S><<<n, X2_THREADS, sm, st>>>(a, u, tma ? 1 : 0);
 }
 
 template <typename TE, typename TC, int RB>
-static void launch_fiber_t(bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                           const FibUnit* u, int n, cudaStream_t st) {
-  if (want_t && want_b && want_res) fib_launch<TE, TC, RB, true, true, true>(tma, a, u, n, st);
-  else if (want_t && want_b) fib_launch<TE, TC, RB, true, true, false>(tma, a, u, n, st);
-  else if (want_t && want_res) fib_launch<TE, TC, RB, true, false, true>(tma, a, u, n, st);
-  else if (want_t) fib_launch<TE, TC, RB, true, false, false>(tma, a, u, n, st);
-  else fib_launch<TE, TC, RB, false, true, false>(tma, a, u, n, st);
-}
-
-template <typename TE, typename TC>
-static void launch_fiber_r(int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                           const FibUnit* u, int n, cudaStream_t st) {
-  switch (rb) {
-    case 8: launch_fiber_t<TE, TC, 8>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    case 16: launch_fiber_t<TE, TC, 16>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    case 32: launch_fiber_t<TE, TC, 32>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    case 40: launch_fiber_t<TE, TC, 40>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    default: launch_fiber_t<TE, TC, 64>(tma, want_t, want_b, want_res, a, u, n, st); break;
-  }
+static void fib2_combo(bool tma, int want_t, int want_b, int want_res, const XArgs& a,
+                       const FibUnit* u, int n, const XTables& t, cudaStream_t st) {
+  // (T, B, RES) combinations used by the engines; T-only runs the RES variant
+  if (want_t && want_b && want_res) fib2_go<TE, TC, RB, true, true, true>(tma, a, u, n, t, st);
+  else if (want_t && want_b) fib2_go<TE, TC, RB, true, true, false>(tma, a, u, n, t, st);
+  else if (want_t) fib2_go<TE, TC, RB, true, false, true>(tma, a, u, n, t, st);
+  else fib2_go<TE, TC, RB, false, true, false>(tma, a, u, n, t, st);
 }
 
 static void fiber_dispatch(int pc, int rb, bool tma, int want_t, int want_b, int want_res,
-                           const XArgs& a, const FibUnit* u, int n, cudaStream_t st) {
-  if (pc == PC_F32) launch_fiber_r<float, float>(rb, tma, want_t, want_b, want_res, a, u, n, st);
-  else if (pc == PC_F32_F64) launch_fiber_r<float, double>(rb, tma, want_t, want_b, want_res, a, u, n, st);
-  else launch_fiber_r<double, double>(rb, tma, want_t, want_b, want_res, a, u, n, st);
-}
-
-bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes) {
-  if (getenv("CB_NO_TMA")) return false;
-  for (int s = 0; s < S; ++s) {
-    const long long J = dims[3 * s] * dims[3 * s + 1];
-    if ((J * elem_bytes) % 16 != 0) return false;
-    if (((uintptr_t)X[s]) % 16 != 0) return false;
+                           const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                           cudaStream_t st) {
+  if (pc == PC_F32) {
+    CB_RB_SWITCH(rb, (fib2_combo<float, float, RB>(tma, want_t, want_b, want_res, a, u, n, t, st)));
+  } else if (pc == PC_F32_F64) {
+    CB_RB_SWITCH(rb, (fib2_combo<float, double, RB>(tma, want_t, want_b, want_res, a, u, n, t, st)));
+  } else {
+    CB_RB_SWITCH(rb, (fib2_combo<double, double, RB>(tma, want_t, want_b, want_res, a, u, n, t, st)));
   }
-  return true;
 }
 
-void prepare_fiber(int pc, int rb, bool tma) {
+void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
-  const int combos[5][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {1, 0, 0}, {0, 1, 0}};
-  for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, 0);
+  const int combos[4][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {0, 1, 0}};
+  for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, t, 0);
 }
 
 void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                  const FibUnit* u, int n, cudaStream_t st) {
+                  const FibUnit* u, int n, const XTables& t, cudaStream_t st) {
   if (n <= 0) return;
-  fiber_dispatch(pc, rb, tma, want_t, want_b, want_res, a, u, n, st);
+  fiber_dispatch(pc, rb, tma, want_t, want_b, want_res, a, u, n, t, st);
   count_launch(1);
 }
 
-template <typename TE, typename TC, int RB, int SB>
-static void launch_slab_t(const XArgs& a, const SlabUnit* u, int n, size_t sm, cudaStream_t st) {
-  if (n < 0) {   // attribute setup call (outside any graph capture)
-    cudaFuncSetAttribute(slab_kernel<TE, TC, RB, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <typename TE, typename TC, int RB>
+static void slab2_go(bool tma, const XArgs& a, const SlabUnit* u, int n, const XTables& t,
+                     cudaStream_t st) {
+  const size_t sm = slab2_smem<TE, TC, RB>(t.slab_rows);
+  if (n < 0) {
+    cudaFuncSetAttribute(slab2_kernel<TE, TC, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     return;
   }
-  slab_kernel<TE, TC, RB, SB><<<n, SLAB_THREADS, sm, st>>>(a, u);
+  slab2_kernel<TE, TC, RB><<<n, X2_THREADS, sm, st>>>(a, u, tma ? 1 : 0);
 }
 
-int slab_sb_for(int rb, int tc_bytes) {
-  const int sb = rb <= 8 ? 8 : rb <= 16 ? 4 : rb <= 32 ? 2 : 1;
-  return tc_bytes == 8 && sb > 1 ? sb / 2 : sb;
-}
-
-template <typename TE, typename TC>
-static void launch_slab_r(int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                          cudaStream_t st) {
-  constexpr bool D = sizeof(TC) == 8;
-  switch (rb) {
-    case 8: launch_slab_t<TE, TC, 8, D ? 4 : 8>(a, u, n, sm, st); break;
-    case 16: launch_slab_t<TE, TC, 16, D ? 2 : 4>(a, u, n, sm, st); break;
-    case 32: launch_slab_t<TE, TC, 32, D ? 1 : 2>(a, u, n, sm, st); break;
-    case 40: launch_slab_t<TE, TC, 40, 1>(a, u, n, sm, st); break;
-    default: launch_slab_t<TE, TC, 64, 1>(a, u, n, sm, st); break;
+static void slab_dispatch(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, int n,
+                          const XTables& t, cudaStream_t st) {
+  if (pc == PC_F32) {
+    CB_RB_SWITCH(rb, (slab2_go<float, float, RB>(tma, a, u, n, t, st)));
+  } else if (pc == PC_F32_F64) {
+    CB_RB_SWITCH(rb, (slab2_go<float, double, RB>(tma, a, u, n, t, st)));
+  } else {
+    CB_RB_SWITCH(rb, (slab2_go<double, double, RB>(tma, a, u, n, t, st)));
   }
 }
 
-static void slab_dispatch(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                          cudaStream_t st) {
-  if (pc == PC_F32) launch_slab_r<float, float>(rb, a, u, n, sm, st);
-  else if (pc == PC_F32_F64) launch_slab_r<float, double>(rb, a, u, n, sm, st);
-  else launch_slab_r<double, double>(rb, a, u, n, sm, st);
-}
-
-void prepare_slab(int pc, int rb, size_t sm) {
+void prepare_slab(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
-  slab_dispatch(pc, rb, a, nullptr, -1, sm, 0);
+  slab_dispatch(pc, rb, tma, a, nullptr, -1, t, 0);
 }
 
-void launch_slab(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                 cudaStream_t st) {
+void launch_slab(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, int n,
+                 const XTables& t, cudaStream_t st) {
   if (n <= 0) return;
-  slab_dispatch(pc, rb, a, u, n, sm, st);
+  slab_dispatch(pc, rb, tma, a, u, n, t, st);
   count_launch(1);
 }
 
@@ -151,47 +137,58 @@ void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
   count_launch(1);
 }
 
-int pc_compute_bytes(int pc) { return pc == PC_F32 ? 4 : 8; }
+bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes) {
+  if (getenv("CB_NO_TMA")) return false;
+  for (int s = 0; s < S; ++s) {
+    const long long J = dims[3 * s] * dims[3 * s + 1];
+    if ((J * elem_bytes) % 16 != 0) return false;
+    if (((uintptr_t)X[s]) % 16 != 0) return false;
+  }
+  return true;
+}
 
-int rank_bucket(int r) { return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 40 ? 40 : 64; }
-
-void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t) {
-  const int target = 148 * 4;
-  long long tiles = 0;
-  for (int s = 0; s < S; ++s) tiles += (dims[3 * s] * dims[3 * s + 1] + FIB_THREADS - 1) / FIB_THREADS;
+// Work units.  The decomposition of a block depends only on that block's
+// shape and on `s_total` (the number of blocks of the whole solve), so every
+// block is reduced in the same order whether it runs alone or in a shard.
+void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t,
+                   int s_total) {
+  const int tcb = pc_compute_bytes(pc);
+  const int tile = x2_tile(rb, tcb);
+  const long long target_per_block = (148LL * 2 + s_total - 1) / std::max(s_total, 1);
   t.fib.clear(); t.fib_first.assign(S + 1, 0); t.nsplit.assign(S, 1);
+  const long long JT = (long long)X2_THREADS * tile;
   for (int s = 0; s < S; ++s) {
     const long long J = dims[3 * s] * dims[3 * s + 1];
     const long long I2 = dims[3 * s + 2];
+    const long long tiles = (J + JT - 1) / JT;
     int ns = 1;
-    while (tiles * ns < target && I2 / (ns * 2) >= 16) ns *= 2;
+    while (tiles * ns < target_per_block && I2 / (ns * 2) >= 2 * F2_CH) ns *= 2;
     t.nsplit[s] = ns;
     t.fib_first[s] = (int)t.fib.size();
     for (int sp = 0; sp < ns; ++sp)
-      for (long long j0 = 0; j0 < J; j0 += FIB_THREADS) t.fib.push_back(FibUnit{s, sp, j0});
+      for (long long j0 = 0; j0 < J; j0 += JT) t.fib.push_back(FibUnit{s, sp, j0});
   }
   t.fib_first[S] = (int)t.fib.size();
-  t.sb = slab_sb_for(rb, pc_compute_bytes(pc));
-  long long groups = 0;
-  for (int s = 0; s < S; ++s) groups += (dims[3 * s + 2] + t.sb - 1) / t.sb;
+  t.sb = tile;
+  const int kc = s2_kc(rb, tcb);
   t.slab.clear(); t.slab_first.assign(S, 0); t.slab_nchunk.assign(S, 1);
-  long long maxI01 = 0;
   for (int s = 0; s < S; ++s) {
     const long long J = dims[3 * s] * dims[3 * s + 1];
     const long long I2 = dims[3 * s + 2];
+    const long long groups = (I2 + tile - 1) / tile;
     int nch = 1;
-    while (groups * nch < target && J / (nch * 2) >= 4 * SLAB_THREADS) nch *= 2;
+    while (groups * nch < target_per_block && J / (nch * 2) >= 2 * kc) nch *= 2;
     t.slab_nchunk[s] = nch;
     t.slab_first[s] = (int)t.slab.size();
-    const long long per = (J + nch - 1) / nch;
-    for (long long g0 = 0; g0 < I2; g0 += t.sb)
+    // chunk boundaries on multiples of the stage width keep bulk copies aligned
+    long long per = (J + nch - 1) / nch;
+    per = (per + kc - 1) / kc * kc;
+    for (long long g0 = 0; g0 < I2; g0 += tile)
       for (int ch = 0; ch < nch; ++ch) {
-        long long k0 = ch * per, k1 = std::min(J, k0 + per);
+        const long long k0 = std::min(J, ch * per), k1 = std::min(J, k0 + per);
         t.slab.push_back(SlabUnit{s, (int)g0, k0, k1});
       }
-    maxI01 = std::max(maxI01, dims[3 * s] + dims[3 * s + 1]);
   }
-  t.slab_smem = (size_t)maxI01 * rb * pc_compute_bytes(pc);
   t.c0.clear(); t.c1.clear();
   for (int s = 0; s < S; ++s) {
     for (int r = 0; r < R[s]; ++r)
@@ -199,6 +196,17 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
     const long long n1 = dims[3 * s + 1] * R[s];
     for (long long p = 0; p < n1; p += 8) t.c1.push_back(RowUnit{s, (int)p});
   }
+  // shared-memory staging of factor rows: A2 rows of a fiber unit always; the
+  // A0/A1 rows of the slab kernel when they fit beside its X ring
+  t.fib_rows = 0;
+  long long ab = 0;
+  for (int s = 0; s < S; ++s) {
+    const long long I2 = dims[3 * s + 2];
+    t.fib_rows = std::max(t.fib_rows, (I2 + t.nsplit[s] - 1) / t.nsplit[s]);
+    ab = std::max(ab, dims[3 * s] + dims[3 * s + 1]);
+  }
+  const long long ring = 128 + (long long)S2_NST * tile * kc * pc_storage_bytes(pc);
+  t.slab_rows = (ring + ab * rb * tcb <= 200 * 1024) ? ab : 0;
 }
 
 }  // namespace cb

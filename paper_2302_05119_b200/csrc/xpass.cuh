@@ -61,6 +61,7 @@ struct XArgs {
   double* bsum;
   double* rsum;
   unsigned long long* ktime;     // profiling only: [0] fiber, [1] slab accumulators
+  long long slab_stage_rows;     // factor rows the slab kernel may stage in smem (0: none)
 };
 
 // In-kernel wall time of a whole launch (first CTA start -> last CTA end),
