@@ -124,6 +124,10 @@ typedef struct {
   int max_iter;                   /* AlsOptions.max_iter                    */
   int compute;                    /* fp32 storage only: 0 = fp64 arithmetic in
                                      the tensor passes, 1 = fp32 arithmetic  */
+  int total_blocks;               /* blocks of the whole (sharded) problem;
+                                     fixes each block's work decomposition so
+                                     a shard reproduces the unsharded bits
+                                     (0 = n_blocks)                          */
 } cb_als_desc;
 
 int cb_als_create(const cb_als_desc* desc, void* stream, cb_als** out);
@@ -165,7 +169,12 @@ typedef struct {
   double delta_w;
   double tol;
   int max_iter;
-  /* multi-GPU block sharding (world_size 1: all NULL/0) */
+  /* multi-GPU block sharding (world_size 1: all NULL/0).  Each rank owns the
+   * contiguous blocks [block_offset, block_offset + n_blocks) of
+   * total_blocks; the per-mode Lipschitz sums, common-column gradient
+   * partials and per-block evaluation terms are all-reduced (solver.py:422-451,
+   * :593-610).  nccl_comm NULL with world_size > 1: one rank of an emulated
+   * group on one GPU, driven by cb_group_step / cb_group_run. */
   int world_size;
   int rank_id;
   void* nccl_comm;                /* ncclComm_t created by cb_nccl_comm_init */
@@ -206,6 +215,15 @@ int cb_solver_set_timing(cb_solver* h, int on);
 int cb_solver_profile(cb_solver* h, int on, char* out, int cap);
 int cb_solver_timing(cb_solver* h, int kind, double* ms, long long* launches, double* bytes);
 int cb_solver_destroy(cb_solver* h);
+
+/* Emulated shard group: the handles of ranks 0..n-1 (created with
+ * world_size n, nccl_comm NULL, on ONE stream) run the sharded program one
+ * segment at a time with the exchanges done by a summing kernel between
+ * segments — the multi-GPU code path verified on a single GPU.
+ * program 0 = iteration-0 evaluation, 1 = one APG iteration. */
+#define CB_MAX_GROUP 16
+int cb_group_step(cb_solver* const* handles, int n, int program);
+int cb_group_run(cb_solver* const* handles, int n, int iters, cb_solver_summary* summary);
 
 /* NCCL communicator for the block-sharded multi-GPU path. `unique_id` is the
  * 128-byte ncclUniqueId produced on rank 0 (cb_nccl_unique_id) and broadcast

@@ -58,7 +58,7 @@ class AlsDesc(ctypes.Structure):
     _fields_ = [("n_blocks", c_int), ("order", c_int), ("dims", c_i64p), ("ranks", c_ip),
                 ("dtype", c_int), ("tensors", ctypes.POINTER(c_vp)),
                 ("init", ctypes.POINTER(c_dp)), ("tol", c_dbl), ("max_iter", c_int),
-                ("compute", c_int)]
+                ("compute", c_int), ("total_blocks", c_int)]
 
 
 def _sig(name, res, args):
@@ -101,6 +101,8 @@ _sig("cb_solver_set_timing", c_int, [c_vp, c_int])
 _sig("cb_solver_profile", c_int, [c_vp, c_int, ctypes.c_char_p, c_int])
 _sig("cb_solver_timing", c_int, [c_vp, c_int, c_dp, ctypes.POINTER(ctypes.c_longlong), c_dp])
 _sig("cb_solver_destroy", c_int, [c_vp])
+_sig("cb_group_step", c_int, [ctypes.POINTER(c_vp), c_int, c_int])
+_sig("cb_group_run", c_int, [ctypes.POINTER(c_vp), c_int, c_int, ctypes.POINTER(SolverSummary)])
 _sig("cb_nccl_unique_id", c_int, [c_vp])
 _sig("cb_nccl_comm_init", c_int, [c_vp, c_int, c_int, ctypes.POINTER(c_vp)])
 _sig("cb_nccl_comm_destroy", c_int, [c_vp])
@@ -114,7 +116,7 @@ EXPORTED = [
     "cb_als_destroy", "cb_solver_create", "cb_solver_run", "cb_solver_step_async",
     "cb_solver_summary_get", "cb_solver_history", "cb_solver_block_factors",
     "cb_solver_set_timing", "cb_solver_timing", "cb_solver_profile", "cb_solver_destroy",
-    "cb_nccl_unique_id",
+    "cb_group_step", "cb_group_run", "cb_nccl_unique_id",
     "cb_nccl_comm_init", "cb_nccl_comm_destroy",
 ]
 

@@ -64,7 +64,7 @@ class AlsHandle:
     """Owns a device ALS engine; factors stay resident for the solver."""
 
     def __init__(self, dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream,
-                 compute_code=0):
+                 compute_code=0, total_blocks=0):
         self.S = len(dev_tensors)
         self.N = len(dims_list[0])
         self.dims = dims_list
@@ -92,6 +92,7 @@ class AlsHandle:
         desc.tol = float(tol)
         desc.max_iter = int(max_iter)
         desc.compute = int(compute_code)
+        desc.total_blocks = int(total_blocks or 0)
         h = L.c_vp()
         L.check(L.lib.cb_als_create(ctypes.byref(desc), stream, ctypes.byref(h)))
         self.h = h
@@ -123,10 +124,11 @@ class AlsHandle:
 
 
 def als_compress_blocks(dev_tensors, dims_list, ranks, tol, max_iter, seeds, dtype_code, stream,
-                        compute_code=0):
-    """Batched ALS over blocks; returns the live handle (factors on device)."""
+                        compute_code=0, total_blocks=0):
+    """Batched ALS over blocks; returns the live handle (factors on device).
+    ``total_blocks``: blocks of the whole problem when this is one shard."""
     h = AlsHandle(dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream,
-                  compute_code)
+                  compute_code, total_blocks)
     h.run()
     return h
 

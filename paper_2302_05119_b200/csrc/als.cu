@@ -411,7 +411,8 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       if (rc) { cb_als_destroy(h); return rc; }
     }
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab, S);
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab,
+                  d->total_blocks > S ? d->total_blocks : S);
     h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->dtype == CB_F32 ? 4 : 8);
     prepare_slab(h->pc, h->rb, h->tma, h->tab);
     prepare_fiber(h->pc, h->rb, h->tma, h->tab);

@@ -16,197 +16,10 @@
 #include "ops_internal.h"
 #include "status.h"
 #include "engine_host.h"
+#include "nccl_shim.h"
 
 namespace cb {
 
-#if 0  // moved to xpass.cu
-// Precision codes of the streaming kernels: storage type of the tensor and
-// arithmetic type of the contraction.
-//   PC_F64     fp64 storage, fp64 arithmetic (parity mode)
-//   PC_F32_F64 fp32 storage, fp64 arithmetic (throughput mode default: half the
-//              bytes, reference-grade sums so the restart rule sees the same
-//              objective the reference does)
-//   PC_F32     fp32 storage, fp32 arithmetic (trace-only / large-rank passes)
-// n < 0: set the dynamic shared memory attribute (outside graph capture)
-template <typename TE, typename TC, int RB, bool T, bool B, bool S>
-static void fib_launch(bool tma, const XArgs& a, const FibUnit* u, int n, cudaStream_t st) {
-  if (tma) {
-    constexpr size_t sm = fiber_tma_smem<TE, TC, RB>();
-    if (n < 0) {
-      cudaFuncSetAttribute(fiber_kernel<TE, TC, RB, T, B, S, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      return;
-    }
-    fiber_kernel<TE, TC, RB, T, B, S, true><<<n, FIB_THREADS, sm, st>>>(a, u);
-  } else {
-    if (n < 0) return;
-    fiber_kernel<TE, TC, RB, T, B, S, false><<<n, FIB_THREADS, 0, st>>>(a, u);
-  }
-}
-
-template <typename TE, typename TC, int RB>
-static void launch_fiber_t(bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                           const FibUnit* u, int n, cudaStream_t st) {
-  if (want_t && want_b && want_res) fib_launch<TE, TC, RB, true, true, true>(tma, a, u, n, st);
-  else if (want_t && want_b) fib_launch<TE, TC, RB, true, true, false>(tma, a, u, n, st);
-  else if (want_t && want_res) fib_launch<TE, TC, RB, true, false, true>(tma, a, u, n, st);
-  else if (want_t) fib_launch<TE, TC, RB, true, false, false>(tma, a, u, n, st);
-  else fib_launch<TE, TC, RB, false, true, false>(tma, a, u, n, st);
-}
-
-template <typename TE, typename TC>
-static void launch_fiber_r(int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                           const FibUnit* u, int n, cudaStream_t st) {
-  switch (rb) {
-    case 8: launch_fiber_t<TE, TC, 8>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    case 16: launch_fiber_t<TE, TC, 16>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    case 32: launch_fiber_t<TE, TC, 32>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    case 40: launch_fiber_t<TE, TC, 40>(tma, want_t, want_b, want_res, a, u, n, st); break;
-    default: launch_fiber_t<TE, TC, 64>(tma, want_t, want_b, want_res, a, u, n, st); break;
-  }
-}
-
-static void fiber_dispatch(int pc, int rb, bool tma, int want_t, int want_b, int want_res,
-                           const XArgs& a, const FibUnit* u, int n, cudaStream_t st) {
-  if (pc == PC_F32) launch_fiber_r<float, float>(rb, tma, want_t, want_b, want_res, a, u, n, st);
-  else if (pc == PC_F32_F64) launch_fiber_r<float, double>(rb, tma, want_t, want_b, want_res, a, u, n, st);
-  else launch_fiber_r<double, double>(rb, tma, want_t, want_b, want_res, a, u, n, st);
-}
-
-bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes) {
-  if (getenv("CB_NO_TMA")) return false;
-  for (int s = 0; s < S; ++s) {
-    const long long J = dims[3 * s] * dims[3 * s + 1];
-    if ((J * elem_bytes) % 16 != 0) return false;
-    if (((uintptr_t)X[s]) % 16 != 0) return false;
-  }
-  return true;
-}
-
-void prepare_fiber(int pc, int rb, bool tma) {
-  XArgs a{};
-  const int combos[5][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {1, 0, 0}, {0, 1, 0}};
-  for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, 0);
-}
-
-void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
-                  const FibUnit* u, int n, cudaStream_t st) {
-  if (n <= 0) return;
-  fiber_dispatch(pc, rb, tma, want_t, want_b, want_res, a, u, n, st);
-  count_launch(1);
-}
-
-template <typename TE, typename TC, int RB, int SB>
-static void launch_slab_t(const XArgs& a, const SlabUnit* u, int n, size_t sm, cudaStream_t st) {
-  if (n < 0) {   // attribute setup call (outside any graph capture)
-    cudaFuncSetAttribute(slab_kernel<TE, TC, RB, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    return;
-  }
-  slab_kernel<TE, TC, RB, SB><<<n, SLAB_THREADS, sm, st>>>(a, u);
-}
-
-int slab_sb_for(int rb, int tc_bytes) {
-  const int sb = rb <= 8 ? 8 : rb <= 16 ? 4 : rb <= 32 ? 2 : 1;
-  return tc_bytes == 8 && sb > 1 ? sb / 2 : sb;
-}
-
-template <typename TE, typename TC>
-static void launch_slab_r(int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                          cudaStream_t st) {
-  constexpr bool D = sizeof(TC) == 8;
-  switch (rb) {
-    case 8: launch_slab_t<TE, TC, 8, D ? 4 : 8>(a, u, n, sm, st); break;
-    case 16: launch_slab_t<TE, TC, 16, D ? 2 : 4>(a, u, n, sm, st); break;
-    case 32: launch_slab_t<TE, TC, 32, D ? 1 : 2>(a, u, n, sm, st); break;
-    case 40: launch_slab_t<TE, TC, 40, 1>(a, u, n, sm, st); break;
-    default: launch_slab_t<TE, TC, 64, 1>(a, u, n, sm, st); break;
-  }
-}
-
-static void slab_dispatch(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                          cudaStream_t st) {
-  if (pc == PC_F32) launch_slab_r<float, float>(rb, a, u, n, sm, st);
-  else if (pc == PC_F32_F64) launch_slab_r<float, double>(rb, a, u, n, sm, st);
-  else launch_slab_r<double, double>(rb, a, u, n, sm, st);
-}
-
-void prepare_slab(int pc, int rb, size_t sm) {
-  XArgs a{};
-  slab_dispatch(pc, rb, a, nullptr, -1, sm, 0);
-}
-
-void launch_slab(int pc, int rb, const XArgs& a, const SlabUnit* u, int n, size_t sm,
-                 cudaStream_t st) {
-  if (n <= 0) return;
-  slab_dispatch(pc, rb, a, u, n, sm, st);
-  count_launch(1);
-}
-
-void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
-                     cudaStream_t st) {
-  if (n <= 0) return;
-  const bool tf = pc == PC_F32;   // T is stored in the fiber pass arithmetic type
-  if (mode == 0) {
-    if (tf) contract0_kernel<float><<<n, 256, 0, st>>>(a, u);
-    else contract0_kernel<double><<<n, 256, 0, st>>>(a, u);
-  } else {
-    if (tf) contract1_kernel<float><<<n, 256, 0, st>>>(a, u);
-    else contract1_kernel<double><<<n, 256, 0, st>>>(a, u);
-  }
-  count_launch(1);
-}
-
-int pc_compute_bytes(int pc) { return pc == PC_F32 ? 4 : 8; }
-
-int rank_bucket(int r) { return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 40 ? 40 : 64; }
-
-void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, XTables& t) {
-  const int target = 148 * 4;
-  long long tiles = 0;
-  for (int s = 0; s < S; ++s) tiles += (dims[3 * s] * dims[3 * s + 1] + FIB_THREADS - 1) / FIB_THREADS;
-  t.fib.clear(); t.fib_first.assign(S + 1, 0); t.nsplit.assign(S, 1);
-  for (int s = 0; s < S; ++s) {
-    const long long J = dims[3 * s] * dims[3 * s + 1];
-    const long long I2 = dims[3 * s + 2];
-    int ns = 1;
-    while (tiles * ns < target && I2 / (ns * 2) >= 16) ns *= 2;
-    t.nsplit[s] = ns;
-    t.fib_first[s] = (int)t.fib.size();
-    for (int sp = 0; sp < ns; ++sp)
-      for (long long j0 = 0; j0 < J; j0 += FIB_THREADS) t.fib.push_back(FibUnit{s, sp, j0});
-  }
-  t.fib_first[S] = (int)t.fib.size();
-  t.sb = slab_sb_for(rb, pc_compute_bytes(pc));
-  long long groups = 0;
-  for (int s = 0; s < S; ++s) groups += (dims[3 * s + 2] + t.sb - 1) / t.sb;
-  t.slab.clear(); t.slab_first.assign(S, 0); t.slab_nchunk.assign(S, 1);
-  long long maxI01 = 0;
-  for (int s = 0; s < S; ++s) {
-    const long long J = dims[3 * s] * dims[3 * s + 1];
-    const long long I2 = dims[3 * s + 2];
-    int nch = 1;
-    while (groups * nch < target && J / (nch * 2) >= 4 * SLAB_THREADS) nch *= 2;
-    t.slab_nchunk[s] = nch;
-    t.slab_first[s] = (int)t.slab.size();
-    const long long per = (J + nch - 1) / nch;
-    for (long long g0 = 0; g0 < I2; g0 += t.sb)
-      for (int ch = 0; ch < nch; ++ch) {
-        long long k0 = ch * per, k1 = std::min(J, k0 + per);
-        t.slab.push_back(SlabUnit{s, (int)g0, k0, k1});
-      }
-    maxI01 = std::max(maxI01, dims[3 * s] + dims[3 * s + 1]);
-  }
-  t.slab_smem = (size_t)maxI01 * rb * pc_compute_bytes(pc);
-  t.c0.clear(); t.c1.clear();
-  for (int s = 0; s < S; ++s) {
-    for (int r = 0; r < R[s]; ++r)
-      for (long long i0 = 0; i0 < dims[3 * s]; i0 += 32) t.c0.push_back(RowUnit{s, (int)((r << 20) | i0)});
-    const long long n1 = dims[3 * s + 1] * R[s];
-    for (long long p = 0; p < n1; p += 8) t.c1.push_back(RowUnit{s, (int)p});
-  }
-}
-#endif  // moved to xpass.cu
 
 static thread_local cudaStream_t g_alloc_stream = nullptr;
 
@@ -271,14 +84,60 @@ struct cb_solver {
   int elem_bytes = 8;
   int iters_enqueued = 0;
   bool init_done = false;
+  // ---- block sharding (see Ctx::S_tot).  With an NCCL communicator the
+  // exchanges are all-reduces enqueued in stream order (and captured in the
+  // iteration graph).  Without one (world > 1, comm null) the handle is one
+  // rank of an EMULATED group driven by cb_group_step: every handle of the
+  // group enqueues the program one segment at a time on the same stream and
+  // the exchanges between segments are done by k_xsum.
+  int world = 1, rank = 0, S_tot = 0, off = 0;
+  void* comm = nullptr;
+  int seg_cur = 0, seg_want = -1;   // -1: emit everything; -2: count segments
+  struct Xchg { double* send; double* recv; long long count; };
+  std::vector<Xchg> pending;
 };
 
 namespace cb {
 
+// does the current program position belong to the segment being enqueued?
+static inline bool emit(const cb_solver* h) {
+  return h->seg_want == -1 || h->seg_cur == h->seg_want;
+}
+
+// exchange point: recv <- sum over ranks of send (count doubles); closes the
+// current segment
+static int xchg(cb_solver* h, double* send, double* recv, long long count) {
+  if (h->world <= 1) return CB_OK;
+  if (h->comm) {
+    if (emit(h)) {
+      NcclApi& api = nccl_api();
+      ncclResult_t r = api.ncclAllReduce(send, recv, (size_t)count, ncclFloat64, ncclSum,
+                                         (ncclComm_t)h->comm, h->st);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    }
+  } else if (h->seg_cur == h->seg_want) {
+    h->pending.push_back(cb_solver::Xchg{send, recv, count});
+  }
+  h->seg_cur += 1;
+  return CB_OK;
+}
+
+// the Lipschitz constants of mode n (before its mode update), the common
+// gradient partials of mode n (after it), the per-block evaluation terms
+static int xchg_lip(cb_solver* h, int n) {
+  if (h->world <= 1 || h->counts[n] == 0) return CB_OK;
+  const long long o = lu_idx(h->ctx, n, 0);
+  return xchg(h, h->ctx.lip_w + o, h->ctx.lip + o, 2LL * h->S_tot);
+}
+static int xchg_gc(cb_solver* h, int n) {
+  if (h->world <= 1 || h->counts[n] == 0) return CB_OK;
+  return xchg(h, h->ctx.gc_w, h->ctx.gc_part, (long long)h->S_tot * h->ctx.gc_stride);
+}
+
 // profiling marks: an event after every launch of the iteration; the interval
 // ending at a mark is charged to that mark's label (kernel time + launch gap)
 static void prof(cb_solver* h, const char* label) {
-  if (!h->profile) return;
+  if (!h->profile || !emit(h)) return;
   if (h->mused >= h->mpool.size()) {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
@@ -306,6 +165,7 @@ static int ev_pair(cb_solver* h, cudaEvent_t* a, cudaEvent_t* b, int kind) {
 // timing mode brackets main-path launches only: the restart-branch copies are
 // gated no-ops unless a restart happens and would dilute the average
 static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, int want_res) {
+  if (!emit(h)) return CB_OK;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool timed = h->timing && a.gate != &h->d_state->go_redo;
   if (timed) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
@@ -317,6 +177,7 @@ static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, i
 }
 
 static int enqueue_slab(cb_solver* h, const XArgs& a) {
+  if (!emit(h)) return CB_OK;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool timed = h->timing && a.gate != &h->d_state->go_redo;
   if (timed) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
@@ -341,46 +202,66 @@ static int generic_residuals(cb_solver* h);
 static int enqueue_sweep(cb_solver* h, int redo) {
   cudaStream_t st = h->st;
   const XArgs& xa = redo ? h->xa_redo : h->xa_main;
-  k_sweep_begin<<<h->S, 256, h->blk_smem, st>>>(h->ctx, redo);
-  count_launch(1);
-  CB_CHECK_LAUNCH();
+  int rc;
+  if (emit(h)) {
+    k_sweep_begin<<<h->S, 256, h->blk_smem, st>>>(h->ctx, redo);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
   prof(h, redo ? "redo:sweep_begin" : "sweep_begin");
+  if ((rc = xchg_lip(h, 0))) return rc;
   for (int n = 0; n < h->N; ++n) {
     int src = 0;
     if (h->lra) {
       src = 2;
     } else if (h->fast3) {
       if (n < 2) {
-        launch_contract(h->pc, n, xa, n == 0 ? h->d_c0 : h->d_c1,
-                        (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
-        CB_CHECK_LAUNCH();
+        if (emit(h)) {
+          launch_contract(h->pc, n, xa, n == 0 ? h->d_c0 : h->d_c1,
+                          (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
+          CB_CHECK_LAUNCH();
+        }
         prof(h, redo ? "redo:contract" : (n == 0 ? "contract0" : "contract1"));
       } else {
-        int rc = enqueue_slab(h, xa);
-        if (rc) return rc;
+        if ((rc = enqueue_slab(h, xa))) return rc;
         src = 1;
         prof(h, redo ? "redo:slab" : "slab");
       }
     } else {
       for (int s = 0; s < h->S; ++s) {
-        int rc = generic_mttkrp(h, s, n);
-        if (rc) return rc;
+        if ((rc = generic_mttkrp(h, s, n))) return rc;
       }
       prof(h, "generic_mttkrp");
     }
-    k_mode_update<<<h->n_rows[n], 256, h->mu_smem, st>>>(h->ctx, n, redo, src, h->d_rows[n]);
-    count_launch(1);
-    CB_CHECK_LAUNCH();
+    if (emit(h)) {
+      k_mode_update<<<h->n_rows[n], 256, h->mu_smem, st>>>(h->ctx, n, redo, src, h->d_rows[n]);
+      count_launch(1);
+      CB_CHECK_LAUNCH();
+    }
     prof(h, redo ? "redo:mode_update" : "mode_update");
-    k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo);
-    count_launch(1);
-    CB_CHECK_LAUNCH();
+    if (h->world > 1 && h->counts[n] > 0) {
+      if ((rc = xchg_gc(h, n))) return rc;
+      if (emit(h)) {
+        const int tiles = (int)((h->dims[n] + MU_ROWS - 1) / MU_ROWS);
+        k_common<<<tiles, 256, 0, st>>>(h->ctx, n, redo);
+        count_launch(1);
+        CB_CHECK_LAUNCH();
+      }
+      prof(h, redo ? "redo:common" : "common");
+    }
+    if (emit(h)) {
+      k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo);
+      count_launch(1);
+      CB_CHECK_LAUNCH();
+    }
     prof(h, redo ? "redo:finalize" : "finalize");
+    if (n + 1 < h->N && (rc = xchg_lip(h, n + 1))) return rc;
   }
   return CB_OK;
 }
 
 static int enqueue_qr(cb_solver* h, int redo) {
+  if (!emit(h)) return CB_OK;
   k_qr_factor<<<h->S * h->N, 256, h->qr_smem, h->st>>>(h->ctx, redo);
   prof(h, redo ? "redo:qr_factor" : "qr_factor");
   k_qr_core<<<h->S * h->ctx.qr_nchunks, 256, 0, h->st>>>(h->ctx, redo);
@@ -391,10 +272,39 @@ static int enqueue_qr(cb_solver* h, int redo) {
 }
 
 static int enqueue_control(cb_solver* h, int mode) {
-  k_control<<<1, 256, sizeof(double) * 3 * h->S, h->st>>>(h->ctx, mode, h->fast3 ? 0 : 1);
-  count_launch(1);
-  CB_CHECK_LAUNCH();
+  const int bsrc = h->fast3 ? 0 : 1;
+  if (h->world <= 1) {
+    if (emit(h)) {
+      k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 3);
+      count_launch(1);
+      CB_CHECK_LAUNCH();
+    }
+    prof(h, "control");
+    return CB_OK;
+  }
+  if (emit(h)) {
+    k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 1);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
+  int rc = xchg(h, h->ctx.ctl_w, h->ctx.ctl, 3LL * h->S_tot);
+  if (rc) return rc;
+  if (emit(h)) {
+    k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 2);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
   prof(h, "control");
+  return CB_OK;
+}
+
+static int enqueue_restore(cb_solver* h) {
+  if (emit(h)) {
+    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
+  prof(h, "redo:restore");
   return CB_OK;
 }
 
@@ -435,10 +345,7 @@ static int enqueue_iteration(cb_solver* h) {
     prof(h, "fiber");
     if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
     // restart branch (no-ops unless go_redo)
-    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
-    count_launch(1);
-    CB_CHECK_LAUNCH();
-    prof(h, "redo:restore");
+    if ((rc = enqueue_restore(h))) return rc;
     if ((rc = enqueue_sweep(h, 1))) return rc;
     if ((rc = enqueue_eval_full(h, 1))) return rc;
     prof(h, "redo:fiber");
@@ -447,10 +354,7 @@ static int enqueue_iteration(cb_solver* h) {
     if ((rc = enqueue_sweep(h, 0))) return rc;
     if ((rc = enqueue_qr(h, 0))) return rc;
     if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
-    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
-    count_launch(1);
-    CB_CHECK_LAUNCH();
-    prof(h, "redo:restore");
+    if ((rc = enqueue_restore(h))) return rc;
     if ((rc = enqueue_sweep(h, 1))) return rc;
     if ((rc = enqueue_qr(h, 1))) return rc;
     if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
@@ -523,9 +427,11 @@ static int generic_residuals(cb_solver* h) {
 
 static int init_evaluation(cb_solver* h) {
   int rc;
-  k_init_block<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
-  count_launch(1);
-  CB_CHECK_LAUNCH();
+  if (emit(h)) {
+    k_init_block<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
   if (!h->lra) {
     if (h->fast3) {
       XArgs a = h->xa_main;
@@ -559,8 +465,24 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_ARG(d->n_blocks >= 1, "no tensors");
   CB_ARG(d->order >= 1 && d->order <= CB_MAX_ORDER, "order %d outside [1, %d]", d->order, CB_MAX_ORDER);
   CB_ARG(d->dtype == CB_F32 || d->dtype == CB_F64, "bad dtype");
-  CB_ARG(d->world_size <= 1, "multi-rank solves go through the sharded driver");
+  const int world = d->world_size > 1 ? d->world_size : 1;
+  if (world > 1) {
+    CB_ARG(d->order == 3, "block-sharded solves need 3-way blocks (order %d)", d->order);
+    CB_ARG(d->rank_id >= 0 && d->rank_id < world, "rank %d outside [0, %d)", d->rank_id, world);
+    CB_ARG(d->block_offset >= 0 && d->block_offset + d->n_blocks <= d->total_blocks,
+           "block range [%d, %d) outside the %d blocks", d->block_offset,
+           d->block_offset + d->n_blocks, d->total_blocks);
+    if (d->nccl_comm) {
+      int rc0 = nccl_load();
+      if (rc0) return rc0;
+    }
+  }
   cb_solver* h = new cb_solver();
+  h->world = world;
+  h->rank = world > 1 ? d->rank_id : 0;
+  h->comm = world > 1 ? d->nccl_comm : nullptr;
+  h->S_tot = world > 1 ? d->total_blocks : d->n_blocks;
+  h->off = world > 1 ? d->block_offset : 0;
   h->st = (cudaStream_t)stream;
   h->S = d->n_blocks; h->N = d->order; h->lra = d->lra; h->update_core = d->update_core;
   h->dtype = d->dtype; h->objective = d->objective; h->delta_w = d->delta_w; h->tol = d->tol;
@@ -647,7 +569,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   h->h_MTT = MTT;
   h->h_LAM = LAM;
   Ctx& c = h->ctx;
-  c.S = S; c.N = N; c.lra = h->lra; c.update_core = h->update_core; c.objective = h->objective;
+  c.S = S; c.S_tot = h->S_tot; c.off = h->off; c.shard = world > 1 ? 1 : 0;
+  c.N = N; c.lra = h->lra; c.update_core = h->update_core; c.objective = h->objective;
   c.fast3 = h->fast3; c.max_iter = h->max_iter; c.rmax = std::max(h->rmax, h->rtmax);
   for (int n = 0; n < N; ++n) c.counts[n] = h->counts[n];
   c.delta_w = h->delta_w; c.tol = h->tol;
@@ -673,8 +596,16 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   c.dbg = nullptr;
   if (getenv("CB_PHASES")) TRY(dalloc((void**)&c.dbg, sizeof(double) * 64, A));
   TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
-  TRY(dalloc((void**)&c.lu, sizeof(double) * N * S, A));
-  TRY(dalloc((void**)&c.lup, sizeof(double) * N * S, A));
+  // coupling arrays in global block slots; separate send copies when sharded
+  // (their foreign slots stay zero: the all-reduce is an exact all-gather)
+  const int ST = h->S_tot;
+  TRY(dalloc((void**)&c.lip, sizeof(double) * 2 * N * ST, A));
+  TRY(dalloc((void**)&c.ctl, sizeof(double) * 3 * ST, A));
+  c.lip_w = c.lip; c.ctl_w = c.ctl;
+  if (world > 1) {
+    TRY(dalloc((void**)&c.lip_w, sizeof(double) * 2 * N * ST, A));
+    TRY(dalloc((void**)&c.ctl_w, sizeof(double) * 3 * ST, A));
+  }
   TRY(dalloc((void**)&c.nsq, sizeof(double) * S, A));
   TRY(dalloc((void**)&c.bbuf, sizeof(double) * 2 * S * RSTRIDE, A));
   TRY(dalloc((void**)&c.model_sq, sizeof(double) * S, A));
@@ -686,8 +617,9 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   int maxL = 0;
   for (int n = 0; n < N; ++n) maxL = std::max(maxL, h->counts[n]);
   c.gc_stride = maxIn * std::max(maxL, 1);
-  TRY(dalloc((void**)&c.gc_part, sizeof(double) * S * c.gc_stride, A));
-  TRY(dalloc((void**)&c.gc_valid, sizeof(int) * S, A));
+  TRY(dalloc((void**)&c.gc_part, sizeof(double) * ST * c.gc_stride, A));
+  c.gc_w = c.gc_part;
+  if (world > 1) TRY(dalloc((void**)&c.gc_w, sizeof(double) * ST * c.gc_stride, A));
   TRY(dalloc((void**)&c.cnew, sizeof(double) * c.gc_stride, A));
   TRY(dalloc((void**)&c.tile_cnt, sizeof(int) * (maxIn / MU_ROWS + 2), A));
   if (h->lra) {
@@ -741,7 +673,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   // ---- fast 3-way tables and T buffers
   std::vector<void*> T0(S, nullptr), T1(S, nullptr);
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab, S);
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab, h->S_tot);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
@@ -826,14 +758,16 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_mode_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->mu_smem));
-  CB_CUDA(cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(sizeof(double) * 3 * S)));
   if (h->lra)
     CB_CUDA(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qr_smem));
-  // ---- iteration 0
-  TRY(init_evaluation(h));
-  TRY(read_state(h));
-  h->init_done = true;
+  // ---- iteration 0 (an emulated group runs it through cb_group_step)
+  if (world == 1 || h->comm) {
+    TRY(init_evaluation(h));
+    TRY(read_state(h));
+    h->init_done = true;
+  } else {
+    CB_CUDA(cudaStreamSynchronize(st));
+  }
 #undef TRY
   *out = h;
   return CB_OK;
@@ -841,6 +775,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
 
 int cb_solver_step_async(cb_solver* h) {
   CB_ARG(h, "null handle");
+  CB_ARG(h->world == 1 || h->comm, "emulated shard groups are stepped with cb_group_step");
   if (!h->fast3) {
     int rc = generic_iteration(h);
     return rc;
@@ -894,6 +829,7 @@ int cb_solver_summary_get(cb_solver* h, cb_solver_summary* sum) {
 
 int cb_solver_run(cb_solver* h, int iters, cb_solver_summary* sum) {
   CB_ARG(h, "null handle");
+  CB_ARG(h->world == 1 || h->comm, "emulated shard groups run through cb_group_run");
   int rc = read_state(h);
   if (rc) return rc;
   int left = iters;
@@ -1025,6 +961,72 @@ int cb_solver_timing(cb_solver* h, int kind, double* ms, long long* launches, do
   if (ms) *ms = tot;
   if (launches) *launches = n;
   if (bytes) *bytes = (double)n * (double)h->elem_total * h->elem_bytes;
+  return CB_OK;
+}
+
+// ---- emulated shard groups (verification of the sharded program on one GPU)
+int cb_group_step(cb_solver* const* hs, int n, int program) {
+  CB_ARG(hs && n >= 1 && n <= CB_MAX_GROUP, "group of %d handles outside [1, %d]", n, CB_MAX_GROUP);
+  CB_ARG(program == 0 || program == 1, "program %d", program);
+  for (int k = 0; k < n; ++k) {
+    CB_ARG(hs[k] && hs[k]->world == n && !hs[k]->comm && hs[k]->rank == k,
+           "handle %d is not rank %d of an emulated group of %d", k, k, n);
+    CB_ARG(hs[k]->st == hs[0]->st, "group handles must share one stream");
+    CB_ARG(program == 1 || !hs[k]->init_done, "iteration 0 already evaluated");
+    CB_ARG(program == 0 || hs[k]->init_done, "iteration 0 not evaluated yet");
+  }
+  auto run = [&](cb_solver* h, int want) -> int {
+    h->seg_cur = 0;
+    h->seg_want = want;
+    h->pending.clear();
+    int rc = program == 0 ? init_evaluation(h) : enqueue_iteration(h);
+    h->seg_want = -1;
+    return rc;
+  };
+  int rc = run(hs[0], -2);
+  if (rc) return rc;
+  const int nseg = hs[0]->seg_cur + 1;
+  for (int seg = 0; seg < nseg; ++seg) {
+    for (int k = 0; k < n; ++k) {
+      if ((rc = run(hs[k], seg))) return rc;
+    }
+    for (size_t x = 0; x < hs[0]->pending.size(); ++x) {
+      XsumArgs a{};
+      a.n = n;
+      a.count = hs[0]->pending[x].count;
+      for (int k = 0; k < n; ++k) {
+        CB_ARG(hs[k]->pending.size() == hs[0]->pending.size() && hs[k]->pending[x].count == a.count,
+               "group handles disagree on the exchange program");
+        a.send[k] = hs[k]->pending[x].send;
+        a.recv[k] = hs[k]->pending[x].recv;
+      }
+      const int blocks = (int)std::min<long long>(148 * 4, (a.count + 255) / 256);
+      k_xsum<<<std::max(blocks, 1), 256, 0, hs[0]->st>>>(a);
+      count_launch(1);
+      CB_CHECK_LAUNCH();
+    }
+  }
+  for (int k = 0; k < n; ++k) {
+    hs[k]->pending.clear();
+    if (program == 0) hs[k]->init_done = true;
+  }
+  return CB_OK;
+}
+
+int cb_group_run(cb_solver* const* hs, int n, int iters, cb_solver_summary* sum) {
+  CB_ARG(hs && n >= 1, "empty group");
+  int rc;
+  if (!hs[0]->init_done && (rc = cb_group_step(hs, n, 0))) return rc;
+  if ((rc = read_state(hs[0]))) return rc;
+  int left = iters;
+  while (left > 0 && !hs[0]->h_state->done) {
+    const int chunk = std::min(left, 8);
+    for (int i = 0; i < chunk; ++i)
+      if ((rc = cb_group_step(hs, n, 1))) return rc;
+    left -= chunk;
+    if ((rc = read_state(hs[0]))) return rc;
+  }
+  if (sum) return cb_solver_summary_get(hs[0], sum);
   return CB_OK;
 }
 

@@ -52,8 +52,18 @@ struct Ctx {
   double* lipc_hist;          // S (NaN = unset)
   double* dbg;                // phase-time accumulators (profiling only) or null
   double* lipf_hist;          // N*S
-  double* lu;                 // N*S current factor Lipschitz constants
-  double* lup;                // N*S the "previous" constants used this sweep
+  // Block sharding (one process per GPU, blocks [off, off+S) of S_tot).  Every
+  // quantity that couples blocks lives in a GLOBAL-slot array indexed by the
+  // global block number; a rank writes only its own slots into the *_w copy,
+  // whose other slots stay zero, and an all-reduce (sum) of the *_w copy into
+  // the read copy is then an exact all-gather.  Single GPU: *_w == read copy.
+  int S_tot, off, shard;
+  // Lipschitz constants, per mode n: lu at [n*2*S_tot + g], lup at
+  // [n*2*S_tot + S_tot + g]  (lup = the "previous" constant used this sweep)
+  double* lip;
+  double* lip_w;
+  double* ctl;                // 3*S_tot per-block evaluation terms
+  double* ctl_w;
   double* nsq;                // S ||M_s||^2
   double* bbuf;               // 2 * S * RSTRIDE staged core linear terms
   double* model_sq;           // S lam^T (hadamard G) lam
@@ -62,9 +72,9 @@ struct Ctx {
   double* tsq;                // S (lra) ||M~||^2
   double* res;                // S explicit residuals (generic path)
   double* borig;              // S * RSTRIDE (generic lra trace / generic full b)
-  double* gc_part;            // S * gc_stride common-gradient partials
-  int* gc_valid;              // S
-  double* cnew;               // I_n x L_n new common columns
+  double* gc_part;            // S_tot * gc_stride common-gradient partials (global slots)
+  double* gc_w;
+  double* cnew;             // I_n x L_n new common columns
   int* tile_cnt;              // per row tile arrival counters
   long long gc_stride;
   double* qr_buf;             // S*N*QR_MAXC*QR_MAXC R factors
@@ -84,5 +94,12 @@ struct Ctx {
   double* h_rel;
   double* h_tns;
 };
+
+__host__ __device__ inline long long lu_idx(const Ctx& c, int n, int g) {
+  return (long long)n * 2 * c.S_tot + g;
+}
+__host__ __device__ inline long long lup_idx(const Ctx& c, int n, int g) {
+  return (long long)n * 2 * c.S_tot + c.S_tot + g;
+}
 
 }  // namespace cb

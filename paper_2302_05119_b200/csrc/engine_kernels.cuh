@@ -149,9 +149,9 @@ __device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const Bloc
   if (threadIdx.x == 0) {
     const int idx = n * c.S + s;
     const double h = c.lipf_hist[idx];
-    c.lup[idx] = isnan(h) ? lu : h;
+    c.lip_w[lup_idx(c, n, c.off + s)] = isnan(h) ? lu : h;
     c.lipf_hist[idx] = lu;
-    c.lu[idx] = lu;
+    c.lip_w[lu_idx(c, n, c.off + s)] = lu;
   }
   __syncthreads();
   pc.mark(c.dbg, 5);
@@ -326,6 +326,39 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
   step_and_lipschitz(c, s, 0, sm);
 }
 
+// sum over all blocks (global order) of the mode-n Lipschitz constants and of
+// their "previous" values (solver.py:422-425)
+__device__ inline void common_lip_sums(const Ctx& c, int n, double& sl, double& slp) {
+  sl = 0.0;
+  slp = 0.0;
+  for (int q = 0; q < c.S_tot; ++q) {
+    sl += c.lip[lu_idx(c, n, q)];
+    slp += c.lip[lup_idx(c, n, q)];
+  }
+}
+
+// new common columns of rows [r0, r0+rows): the partial gradients of the
+// blocks with L_u > 0 summed in block order (solver.py:444), then the
+// projected step from the extrapolated point (solver.py:447-451)
+__device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double sumL, double wc) {
+  const int L = c.counts[n];
+  const int R0 = c.R[0];
+  const double* U0c = c.U[n];
+  const double* U0p = c.Up[n];
+  for (int e = threadIdx.x; e < rows * L; e += blockDim.x) {
+    const int il = e / L, l = e - il * L;
+    const long long i = r0 + il;
+    double acc = 0.0;
+    for (int q = 0; q < c.S_tot; ++q) {
+      if (!(c.lip[lu_idx(c, n, q)] > 0.0)) continue;
+      acc += __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]);
+    }
+    const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
+    const double chat = cc + wc * (cc - cp);
+    c.cnew[i * L + l] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // mode update: extrapolate, gradient, project individual columns, partial
 // common gradient; the last CTA of each row tile forms the new common columns
@@ -351,12 +384,15 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   double* sc = P + (c.lra ? c.Rt[s] * R : 0);  // scalars
   const double* lam = c.LAM[s];
   if (threadIdx.x == 0) {
-    double sl = 0.0, slp = 0.0;
-    for (int q = 0; q < c.S; ++q) { sl += c.lu[n * c.S + q]; slp += c.lup[n * c.S + q]; }
+    double sl, slp;
+    common_lip_sums(c, n, sl, slp);
     sc[0] = sl;
     sc[1] = extrap_weight(w_hat, slp, sl, c.delta_w);
-    sc[2] = extrap_weight(w_hat, c.lup[n * c.S + s], c.lu[n * c.S + s], c.delta_w);
-    sc[3] = c.lu[n * c.S + s];
+    // own block: the written copy (current even where mode n is uncoupled
+    // and nothing is exchanged)
+    const int g = c.off + s;
+    sc[2] = extrap_weight(w_hat, c.lip_w[lup_idx(c, n, g)], c.lip_w[lu_idx(c, n, g)], c.delta_w);
+    sc[3] = c.lip_w[lu_idx(c, n, g)];
   }
   const double* stp = c.STEP[s];
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) step[e] = stp[e];
@@ -418,7 +454,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   }
   __syncthreads();
   double* Un = c.Un[s * N + n];
-  double* gcp = c.gc_part + (long long)s * c.gc_stride;
+  double* gcp = c.gc_w + (long long)(c.off + s) * c.gc_stride;
   for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
     const int il = e / R, r = e - il * R;
     const long long i = r0 + il;
@@ -432,10 +468,8 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     if (r < L) gcp[i * L + r] = g;
     else Un[i * R + r] = pos(uh[e] - g / lu);
   }
-  if (L == 0) return;
-  // every CTA of block s publishes the flag before its arrival is counted, so
-  // the last CTA of any row tile sees all S flags of this mode update
-  if (threadIdx.x == 0) c.gc_valid[s] = lu > 0.0 ? 1 : 0;
+  // sharded: the partials are all-reduced first; k_common folds them
+  if (L == 0 || c.shard) return;
   __threadfence();
   __syncthreads();
   int* flag = reinterpret_cast<int*>(sc + 4);
@@ -448,19 +482,29 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   if (!flag[0]) return;
   __threadfence();
   // last CTA of this row tile: sum the partials in block order (solver.py:444)
-  for (int e = threadIdx.x; e < rows * L; e += blockDim.x) {
-    const int il = e / L, l = e - il * L;
-    const long long i = r0 + il;
-    double acc = 0.0;
-    for (int q = 0; q < c.S; ++q) {
-      if (!__ldcg(&c.gc_valid[q])) continue;
-      acc += __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]);
-    }
-    const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
-    const double chat = cc + wc * (cc - cp);
-    c.cnew[i * L + l] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
-  }
+  common_fold(c, n, r0, rows, sumL, wc);
   if (threadIdx.x == 0) c.tile_cnt[r0 / MU_ROWS] = 0;
+}
+
+// sharded runs: new common columns of one row tile from the all-reduced
+// partials (grid: row tiles of mode n)
+__global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
+  if (stopped(c, redo)) return;
+  const int L = c.counts[n];
+  if (L == 0) return;
+  const long long In = c.dims[n];   // the common rows are shared: I_n of block 0
+  const int r0 = blockIdx.x * MU_ROWS;
+  if (r0 >= In) return;
+  const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
+  __shared__ double sc[2];
+  if (threadIdx.x == 0) {
+    double sl, slp;
+    common_lip_sums(c, n, sl, slp);
+    sc[0] = sl;
+    sc[1] = extrap_weight(redo ? 0.0 : c.st->w_hat, slp, sl, c.delta_w);
+  }
+  __syncthreads();
+  common_fold(c, n, r0, rows, sc[0], sc[1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -676,31 +720,6 @@ __device__ inline double block_res_full(const Ctx& c, int s, int bsrc) {
   return c.nsq[s] - 2.0 * lb + c.model_sq[s];
 }
 
-// sum the staged core linear terms of the fiber units into bbuf[1 - bsel]
-__device__ inline void stage_b_from_fiber(const Ctx& c) {
-  for (int s = 0; s < c.S; ++s) {
-    double* b = c.bbuf + ((long long)(1 - c.st->bsel) * c.S + s) * RSTRIDE;
-    const int R = c.R[s];
-    for (int r = 0; r < R; ++r) {
-      b[r] = c.fib_bpart[(long long)s * RSTRIDE + r];
-    }
-  }
-}
-
-__device__ inline double lra_compressed_obj(const Ctx& c) {
-  double oi = 0.0;
-  for (int s = 0; s < c.S; ++s) {
-    double rt = c.res_t[s];
-    if (qr_route_needed(c, s)) {
-      double a = 0.0;
-      for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
-      rt = a;
-    }
-    oi += 0.5 * (rt > 0.0 ? rt : 0.0);
-  }
-  return oi;
-}
-
 __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double obj_orig, double rel,
                                    int swap_t) {
   State* st = c.st;
@@ -735,72 +754,82 @@ __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double o
   st->k = k + 1;
 }
 
-// Evaluation totals and the iteration rules.  Per-block terms are formed in
-// parallel (thread s handles block s, ...) into shared memory; thread 0 then
-// folds them in block order — the reference's summation order — and applies
-// the restart / stop rules.  Launched with 256 threads and 16*S bytes of
-// dynamic shared memory.
-__global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc) {
+// Evaluation totals and the iteration rules.  Phase 1 (bit 0 of `phase`):
+// per-block terms, thread s handles local block s, written to the global
+// slots of ctl_w.  Phase 2 (bit 1): thread 0 folds the S_tot terms of ctl in
+// global block order — the reference's summation order — and applies the
+// restart / stop rules.  Single GPU runs both phases in one launch; sharded
+// runs all-reduce ctl_w into ctl between them, so every rank folds the same
+// values and takes the same decisions.
+__global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int phase) {
   State* st = c.st;
   if (st->done) return;
   if (mode == CTRL_REDO && !st->go_redo) return;
   if (!c.lra && mode == CTRL_FINISH) return;
-  extern __shared__ double csm[];
-  double* val = csm;           // per-block residual (or compressed residual)
-  double* relv = csm + c.S;    // per-block relative error contribution
   const int fast_t = (bsrc == 0);
   const bool lra_cmp = c.lra && (mode == CTRL_DECIDE || mode == CTRL_REDO);
-  for (int s = threadIdx.x; s < c.S; s += blockDim.x) {
-    if (!c.lra) {
-      if (fast_t) {
-        double* b = c.bbuf + ((long long)(1 - st->bsel) * c.S + s) * RSTRIDE;
+  const int T = c.S_tot;
+  if (phase & 1) {
+    double* val = c.ctl_w;          // per-block residual (or compressed residual)
+    double* relv = c.ctl_w + T;     // per-block relative error contribution
+    double* rt0 = c.ctl_w + 2 * T;  // lra init: compressed residual
+    for (int s = threadIdx.x; s < c.S; s += blockDim.x) {
+      const int g = c.off + s;
+      if (!c.lra) {
+        if (fast_t) {
+          double* b = c.bbuf + ((long long)(1 - st->bsel) * c.S + s) * RSTRIDE;
+          const int R = c.R[s];
+          for (int r = 0; r < R; ++r) b[r] = c.fib_bpart[(long long)s * RSTRIDE + r];
+        }
+        const double r = block_res_full(c, s, bsrc);
+        val[g] = r;
+        const double nrm = sqrt(c.nsq[s]);
+        relv[g] = nrm > 0.0 ? sqrt(r > 0.0 ? r : 0.0) / nrm : 0.0;
+      } else if (lra_cmp) {
+        double rt = c.res_t[s];
+        if (qr_route_needed(c, s)) {
+          double a = 0.0;
+          for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
+          rt = a;
+        }
+        val[g] = rt;
+      } else {
+        // original-tensor trace quantities (solver.py:519-522)
         const int R = c.R[s];
-        for (int r = 0; r < R; ++r) b[r] = c.fib_bpart[(long long)s * RSTRIDE + r];
+        const double* lam = c.LAM[s];
+        double lb = 0.0;
+        for (int r = 0; r < R; ++r) {
+          const double b = fast_t ? c.fib_bpart[(long long)s * RSTRIDE + r]
+                                  : c.borig[(long long)s * RSTRIDE + r];
+          lb = fma(lam[r], b, lb);
+        }
+        const double raw = c.nsq[s] - 2.0 * lb + c.model_sq[s];
+        val[g] = raw;   // Python max(raw, 0.0) keeps NaN / +inf (checked below)
+        const double nrm = sqrt(c.nsq[s]);
+        const double r = raw > 0.0 ? raw : 0.0;
+        relv[g] = nrm > 0.0 ? sqrt(r) / nrm : 0.0;
       }
-      const double r = block_res_full(c, s, bsrc);
-      val[s] = r;
-      const double nrm = sqrt(c.nsq[s]);
-      relv[s] = nrm > 0.0 ? sqrt(r > 0.0 ? r : 0.0) / nrm : 0.0;
-    } else if (lra_cmp) {
-      double rt = c.res_t[s];
-      if (qr_route_needed(c, s)) {
-        double a = 0.0;
-        for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
-        rt = a;
+      if (c.lra && mode == CTRL_INIT) {
+        // the iteration-0 evaluation also needs the compressed residual
+        double rt = c.res_t[s];
+        if (qr_route_needed(c, s)) {
+          double a = 0.0;
+          for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
+          rt = a;
+        }
+        rt0[g] = rt;
       }
-      val[s] = rt;
-    } else {
-      // original-tensor trace quantities (solver.py:519-522)
-      const int R = c.R[s];
-      const double* lam = c.LAM[s];
-      double lb = 0.0;
-      for (int r = 0; r < R; ++r) {
-        const double b = fast_t ? c.fib_bpart[(long long)s * RSTRIDE + r]
-                                : c.borig[(long long)s * RSTRIDE + r];
-        lb = fma(lam[r], b, lb);
-      }
-      const double raw = c.nsq[s] - 2.0 * lb + c.model_sq[s];
-      val[s] = raw;   // Python max(raw, 0.0) keeps NaN / +inf (checked below)
-      const double nrm = sqrt(c.nsq[s]);
-      const double r = raw > 0.0 ? raw : 0.0;
-      relv[s] = nrm > 0.0 ? sqrt(r) / nrm : 0.0;
-    }
-    if (c.lra && mode == CTRL_INIT) {
-      // the iteration-0 evaluation also needs the compressed residual
-      double rt = c.res_t[s];
-      if (qr_route_needed(c, s)) {
-        double a = 0.0;
-        for (int ch = 0; ch < c.qr_nchunks; ++ch) a += c.qr_part[(long long)s * c.qr_nchunks + ch];
-        rt = a;
-      }
-      csm[2 * c.S + s] = rt;
     }
   }
+  if (!(phase & 2)) return;
   __syncthreads();
   if (threadIdx.x != 0) return;
+  const double* val = c.ctl;
+  const double* relv = c.ctl + T;
+  const double* rt0 = c.ctl + 2 * T;
   if (!c.lra) {
     double oi = 0.0, rel = 0.0;
-    for (int s = 0; s < c.S; ++s) {
+    for (int s = 0; s < T; ++s) {
       const double r = val[s];
       if (!isfinite(r)) {
         st->error = CB_ERR_NONFINITE; st->err_block = s; st->err_iter = st->k;
@@ -810,7 +839,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc) {
       oi += 0.5 * r;
       rel += relv[s];
     }
-    rel /= c.S;
+    rel /= T;
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
       st->n_restarts += 1;
       st->go_redo = 1;
@@ -822,7 +851,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc) {
   // ---- lra ----
   if (lra_cmp) {
     double oi = 0.0;
-    for (int s = 0; s < c.S; ++s) oi += 0.5 * (val[s] > 0.0 ? val[s] : 0.0);
+    for (int s = 0; s < T; ++s) oi += 0.5 * (val[s] > 0.0 ? val[s] : 0.0);
     st->obj_pending = oi;
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
       st->n_restarts += 1;
@@ -834,13 +863,13 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc) {
   double oi = st->obj_pending;
   if (mode == CTRL_INIT) {
     oi = 0.0;
-    for (int s = 0; s < c.S; ++s) {
-      const double rt = csm[2 * c.S + s];
+    for (int s = 0; s < T; ++s) {
+      const double rt = rt0[s];
       oi += 0.5 * (rt > 0.0 ? rt : 0.0);
     }
   }
   double oo = 0.0, rel = 0.0;
-  for (int s = 0; s < c.S; ++s) {
+  for (int s = 0; s < T; ++s) {
     const double raw = val[s];
     if (raw != raw || raw == INFINITY) {
       st->error = CB_ERR_NONFINITE; st->err_block = s; st->err_iter = st->k;
@@ -850,8 +879,25 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc) {
     oo += 0.5 * (raw > 0.0 ? raw : 0.0);
     rel += relv[s];
   }
-  rel /= c.S;
+  rel /= T;
   accept_and_advance(c, oi, oo, rel, 0);
+}
+
+// emulated shard group exchange: recv_k <- sum_r send_r for every rank k
+// (the sends have disjoint support, so the sum is an exact gather)
+struct XsumArgs {
+  const double* send[16];
+  double* recv[16];
+  int n;
+  long long count;
+};
+
+__global__ void __launch_bounds__(256) k_xsum(XsumArgs a) {
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < a.count; e += (long long)gridDim.x * 256) {
+    double v = 0.0;
+    for (int k = 0; k < a.n; ++k) v += a.send[k][e];
+    for (int k = 0; k < a.n; ++k) a.recv[k][e] = v;
+  }
 }
 
 }  // namespace cb

@@ -41,7 +41,8 @@ __all__ = [
     "CoupledProblem", "SolverOptions", "SolveResult", "TraceRow", "solve", "objective",
     "core_gradient", "factor_gradient", "core_linear_term", "core_linear_term_lra",
     "factor_linear_term", "factor_linear_term_lra", "lipschitz_core", "lipschitz_factor",
-    "extrapolation_weight", "t_next", "init_factors",
+    "extrapolation_weight", "t_next", "init_factors", "solve_distributed",
+    "solve_emulated_shards", "shard_ranges", "ShardSpec",
 ]
 
 
@@ -400,11 +401,17 @@ class PreparedSolve:
     """A solve with its inputs resident on the device, split into
     prepare / iterate / collect so the bench can time the iterations alone."""
 
-    def __init__(self, problem, opts=None, stream=None):
+    def __init__(self, problem, opts=None, stream=None, shard=None):
         torch = D.torch_mod()
         opts = opts if opts is not None else SolverOptions()
         problem.validate()
         self.problem, self.opts = problem, opts
+        S_all = problem.n_blocks
+        self.shard = shard if shard is not None else ShardSpec(1, 0, 0, S_all, None)
+        if not (0 <= self.shard.begin < self.shard.end <= S_all):
+            raise ValueError(f"shard [{self.shard.begin}, {self.shard.end}) of {S_all} blocks is empty "
+                             "or out of range")
+        self.local = list(range(self.shard.begin, self.shard.end))
         self.stream = stream if stream is not None else torch.cuda.Stream()
         self.stream.wait_stream(torch.cuda.current_stream())
         prec = opts.precision
@@ -421,11 +428,11 @@ class PreparedSolve:
             compute = "fp64" if (problem.mode == "full" or max(problem.ranks) <= 16) else "fp32"
         self.compute_code = 1 if (prec == "fp32" and compute == "fp32") else 0
         self.als_compute_code = 1 if (prec == "fp32" and opts.compute == "fp32") else 0
-        S, N = problem.n_blocks, problem.order
+        S, N = len(self.local), problem.order
         with torch.cuda.stream(self.stream):
             self.dev = []
             self.dims = []
-            for t in problem.tensors:
+            for t in (problem.tensors[g] for g in self.local):
                 flat, dims = D.tensor_to_dev(t, prec)
                 self.dev.append(flat)
                 self.dims.append(dims)
@@ -436,31 +443,34 @@ class PreparedSolve:
         tilde_ranks = None
         if problem.mode == "lra":
             base = problem.als_options if problem.als_options is not None else AlsOptions()
-            ranks = [base.rank if base.rank is not None else r for r in problem.ranks]
+            ranks = [base.rank if base.rank is not None else problem.ranks[g] for g in self.local]
             for s, (dims, r) in enumerate(zip(self.dims, ranks)):
                 try:
                     _check_feasible(dims, r)
                 except ValueError as exc:
-                    raise ValueError(f"compression of block {s} failed: {exc}") from exc
+                    raise ValueError(f"compression of block {self.local[s]} failed: {exc}") from exc
             tic = time.perf_counter()
             with torch.cuda.stream(self.stream):
                 try:
                     self.als = als_compress_blocks(self.dev, self.dims, ranks, base.tol,
                                                    base.max_iter,
-                                                   [base.seed + s for s in range(S)],
-                                                   self.code, st, self.als_compute_code)
+                                                   [base.seed + g for g in self.local],
+                                                   self.code, st, self.als_compute_code,
+                                                   total_blocks=S_all)
                 except ValueError as exc:
                     msg = str(exc)
                     blk = 0
                     if msg.startswith("block "):
-                        blk = int(msg.split()[1].rstrip(":"))
+                        blk = self.local[int(msg.split()[1].rstrip(":"))]
                         msg = msg.split(": ", 1)[1]
                     raise ValueError(f"compression of block {blk} failed: {msg}") from exc
             self.stream.synchronize()
             self.compress_seconds = time.perf_counter() - tic
             tilde_ranks = ranks
+        # the seeded start of ALL blocks (one PCG64 stream), then this shard's
         start = init_factors(problem, opts.seed)
         self.start = start
+        local_blocks = [start.blocks[g] for g in self.local]
         desc = L.SolverDesc()
         desc.n_blocks = S
         desc.order = N
@@ -468,7 +478,7 @@ class PreparedSolve:
         flat_dims = [d for dims in self.dims for d in dims]
         self._keep.append(L.i64_array(flat_dims))
         desc.dims = ctypes.cast(self._keep[-1], L.c_i64p)
-        self._keep.append(L.int_array(problem.ranks))
+        self._keep.append(L.int_array([problem.ranks[g] for g in self.local]))
         desc.ranks = ctypes.cast(self._keep[-1], L.c_ip)
         self._keep.append(L.int_array(problem.coupled_counts))
         desc.coupled = ctypes.cast(self._keep[-1], L.c_ip)
@@ -477,8 +487,8 @@ class PreparedSolve:
         desc.dtype = self.code
         self._keep.append(L.ptr_array([D.ptr(x) for x in self.dev]))
         desc.tensors = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_vp))
-        init_f = [np.ascontiguousarray(f) for b in start.blocks for f in b.factors]
-        init_w = [np.ascontiguousarray(b.weights) for b in start.blocks]
+        init_f = [np.ascontiguousarray(f) for b in local_blocks for f in b.factors]
+        init_w = [np.ascontiguousarray(b.weights) for b in local_blocks]
         self._keep.extend([init_f, init_w])
         self._keep.append(L.dptr_array(init_f))
         desc.init_factors = ctypes.cast(self._keep[-1], ctypes.POINTER(L.c_dp))
@@ -499,7 +509,12 @@ class PreparedSolve:
         desc.delta_w = float(opts.delta_w)
         desc.tol = float(opts.tol)
         desc.max_iter = int(opts.max_iter)
-        desc.world_size = 1
+        sh = self.shard
+        desc.world_size = sh.world
+        desc.rank_id = sh.rank
+        desc.nccl_comm = sh.comm
+        desc.total_blocks = S_all
+        desc.block_offset = sh.begin
         self.t0 = time.perf_counter()
         self.engine = _Engine(desc, st)
         self.tilde_ranks = tilde_ranks
@@ -508,44 +523,184 @@ class PreparedSolve:
         iters = self.opts.max_iter if iters is None else iters
         return self.engine.run(iters)
 
-    def collect(self):
-        problem, opts = self.problem, self.opts
+    def collect_local(self):
+        """Summary, histories and this shard's blocks (and compressions)."""
         summ = self.engine.summary()
         solve_seconds = time.perf_counter() - self.t0
-        if summ.error == L.CB_ERR_NONFINITE:
-            raise FloatingPointError(
-                f"block {summ.error_block} produced a non-finite objective "
-                f"at iteration {summ.error_iter}")
-        n_iter = summ.n_iter
-        oi, oo, rel, tns = self.engine.history(n_iter + 1)
-        trace = []
-        for k in range(n_iter + 1):
-            last = k == n_iter and k > 0
-            if k == 0 or k % opts.trace_every == 0 or last:
-                trace.append(TraceRow(k, float(oo[k]), float(rel[k]), float(tns[k]) * 1e-9))
-        blocks = []
-        for s in range(problem.n_blocks):
-            facs, w = self.engine.block(s, self.dims[s], problem.ranks[s])
-            blocks.append(KruskalTensor(facs, w))
+        hist = self.engine.history(summ.n_iter + 1)
+        blocks = {}
+        for s, g in enumerate(self.local):
+            facs, w = self.engine.block(s, self.dims[s], self.problem.ranks[g])
+            blocks[g] = KruskalTensor(facs, w)
         compression = None
         if self.als is not None:
-            compression = []
-            for s in range(problem.n_blocks):
+            compression = {}
+            for s, g in enumerate(self.local):
                 facs, _, _, _, _ = self.als.block(s)
-                compression.append(KruskalTensor(facs, np.ones(self.tilde_ranks[s])))
-        reason = "tolerance" if summ.reason == 1 else "max_iterations"
-        return SolveResult(
-            factors=CoupledFactorSet(blocks, list(problem.coupled_counts)),
-            trace=trace, termination_reason=reason,
-            objective_history=[float(v) for v in oi],
-            rel_err_history=[float(v) for v in rel],
-            n_iter=n_iter, n_restarts=summ.n_restarts, solve_seconds=solve_seconds,
-            compress_seconds=self.compress_seconds, compression=compression)
+                compression[g] = KruskalTensor(facs, np.ones(self.tilde_ranks[s]))
+        return summ, hist, blocks, compression, solve_seconds
+
+    def collect(self):
+        summ, hist, blocks, compression, secs = self.collect_local()
+        return _assemble(self.problem, self.opts, summ, hist, blocks, compression, secs,
+                         self.compress_seconds)
 
     def close(self):
         self.engine.close()
         if self.als is not None:
             self.als.close()
+
+
+def _assemble(problem, opts, summ, hist, blocks, compression, solve_seconds, compress_seconds):
+    """SolveResult from the device summary/histories and {global block: model}."""
+    if summ.error == L.CB_ERR_NONFINITE:
+        raise FloatingPointError(
+            f"block {summ.error_block} produced a non-finite objective "
+            f"at iteration {summ.error_iter}")
+    n_iter = summ.n_iter
+    oi, oo, rel, tns = hist
+    trace = []
+    for k in range(n_iter + 1):
+        last = k == n_iter and k > 0
+        if k == 0 or k % opts.trace_every == 0 or last:
+            trace.append(TraceRow(k, float(oo[k]), float(rel[k]), float(tns[k]) * 1e-9))
+    S = problem.n_blocks
+    comp = None if compression is None else [compression[g] for g in range(S)]
+    reason = "tolerance" if summ.reason == 1 else "max_iterations"
+    return SolveResult(
+        factors=CoupledFactorSet([blocks[g] for g in range(S)], list(problem.coupled_counts)),
+        trace=trace, termination_reason=reason,
+        objective_history=[float(v) for v in oi[: n_iter + 1]],
+        rel_err_history=[float(v) for v in rel[: n_iter + 1]],
+        n_iter=n_iter, n_restarts=summ.n_restarts, solve_seconds=solve_seconds,
+        compress_seconds=compress_seconds, compression=comp)
+
+
+# ---------------------------------------------------------------------------
+# block sharding (SURVEY 8e): one process per GPU, each owning a contiguous
+# range of whole blocks; the couplings (per-mode Lipschitz sums, common-column
+# gradient partials, per-block evaluation terms) are all-reduced in
+# global-slot arrays, so every rank folds identical values in block order and
+# a sharded solve reproduces the single-GPU bits.
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ShardSpec:
+    world: int
+    rank: int
+    begin: int      # first global block of this rank
+    end: int        # one past the last
+    comm: object    # ncclComm_t (int address) or None: emulated group
+
+
+def shard_ranges(n_blocks, world):
+    """Contiguous block ranges per rank: rank r owns [r*S//P, (r+1)*S//P)."""
+    if world < 1 or world > n_blocks:
+        raise ValueError(f"cannot shard {n_blocks} blocks over {world} ranks")
+    return [(r * n_blocks // world, (r + 1) * n_blocks // world) for r in range(world)]
+
+
+def solve_emulated_shards(problem, opts=None, world=2):
+    """The block-sharded program on ONE GPU: `world` engine handles, one per
+    emulated rank, stepped segment by segment with the all-reduces done by a
+    summing kernel between segments (`cb_group_run`).  A verification tool
+    for the multi-GPU code path; results must equal `solve` bit for bit."""
+    torch = D.torch_mod()
+    opts = opts if opts is not None else SolverOptions()
+    stream = torch.cuda.Stream()
+    parts = []
+    try:
+        for r, (b, e) in enumerate(shard_ranges(problem.n_blocks, world)):
+            parts.append(PreparedSolve(problem, opts, stream=stream,
+                                       shard=ShardSpec(world, r, b, e, None)))
+        hs = (L.c_vp * world)(*[p.engine.h.value for p in parts])
+        summ = L.SolverSummary()
+        L.check(L.lib.cb_group_run(hs, world, int(opts.max_iter), ctypes.byref(summ)))
+        blocks, comp = {}, ({} if parts[0].als is not None else None)
+        hist, secs = None, 0.0
+        for p in parts:
+            s_, h_, b_, c_, t_ = p.collect_local()
+            blocks.update(b_)
+            if comp is not None:
+                comp.update(c_)
+            if hist is None:
+                summ, hist, secs = s_, h_, t_
+        return _assemble(problem, opts, summ, hist, blocks, comp, secs,
+                         sum(p.compress_seconds for p in parts))
+    finally:
+        for p in parts:
+            p.close()
+
+
+def nccl_comm_for(group=None):
+    """An NCCL communicator over the ranks of a torch.distributed group, built
+    from a unique id that rank 0 creates and broadcasts (object collective)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        L.check(L.lib.cb_nccl_unique_id(uid))
+    box = [bytes(uid.raw) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    uid = ctypes.create_string_buffer(box[0], 128)
+    comm = L.c_vp()
+    L.check(L.lib.cb_nccl_comm_init(uid, world, rank, ctypes.byref(comm)))
+    return comm.value
+
+
+class PreparedShardedSolve:
+    """This rank's part of a block-sharded solve (torch.distributed initialised,
+    one process per GPU).  `run`/`step_async` behave as in PreparedSolve; every
+    rank must make the same calls."""
+
+    def __init__(self, problem, opts=None, group=None):
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        self.group = group
+        self.comm = nccl_comm_for(group) if world > 1 else None
+        b, e = shard_ranges(problem.n_blocks, world)[rank]
+        self.inner = PreparedSolve(problem, opts,
+                                   shard=ShardSpec(world, rank, b, e, self.comm) if world > 1 else None)
+        self.engine, self.stream = self.inner.engine, self.inner.stream
+
+    def run(self, iters=None):
+        return self.inner.run(iters)
+
+    def collect(self):
+        """The full SolveResult on every rank (blocks gathered over the group)."""
+        import torch.distributed as dist
+        summ, hist, blocks, comp, secs = self.inner.collect_local()
+        if self.comm is None:
+            merged_b, merged_c = blocks, comp
+        else:
+            world = dist.get_world_size(self.group)
+            got = [None] * world
+            dist.all_gather_object(got, (blocks, comp), group=self.group)
+            merged_b, merged_c = {}, (None if comp is None else {})
+            for b_, c_ in got:
+                merged_b.update(b_)
+                if merged_c is not None:
+                    merged_c.update(c_)
+        return _assemble(self.inner.problem, self.inner.opts, summ, hist, merged_b, merged_c,
+                         secs, self.inner.compress_seconds)
+
+    def close(self):
+        self.inner.close()
+        if self.comm is not None:
+            L.lib.cb_nccl_comm_destroy(L.c_vp(self.comm))
+            self.comm = None
+
+
+def solve_distributed(problem, opts=None, group=None):
+    """Block-sharded `solve` over the ranks of a torch.distributed group (one
+    process per GPU, NCCL over NVLink for the couplings).  Every rank passes
+    the same problem and options and receives the full SolveResult."""
+    run = PreparedShardedSolve(problem, opts, group)
+    try:
+        run.run()
+        return run.collect()
+    finally:
+        run.close()
 
 
 def solve(problem, opts=None):
