@@ -90,7 +90,9 @@ struct cb_solver {
   // rank of an EMULATED group driven by cb_group_step: every handle of the
   // group enqueues the program one segment at a time on the same stream and
   // the exchanges between segments are done by k_xsum.
-  int world = 1, rank = 0, S_tot = 0, off = 0;
+  // shard: the sharded program (exchanges, separate send copies) runs; also
+  // with world 1 when a communicator is given (the NCCL path on one GPU)
+  int world = 1, rank = 0, S_tot = 0, off = 0, shard = 0;
   void* comm = nullptr;
   int seg_cur = 0, seg_want = -1;   // -1: emit everything; -2: count segments
   struct Xchg { double* send; double* recv; long long count; };
@@ -107,7 +109,7 @@ static inline bool emit(const cb_solver* h) {
 // exchange point: recv <- sum over ranks of send (count doubles); closes the
 // current segment
 static int xchg(cb_solver* h, double* send, double* recv, long long count) {
-  if (h->world <= 1) return CB_OK;
+  if (!h->shard) return CB_OK;
   if (h->comm) {
     if (emit(h)) {
       NcclApi& api = nccl_api();
@@ -125,12 +127,12 @@ static int xchg(cb_solver* h, double* send, double* recv, long long count) {
 // the Lipschitz constants of mode n (before its mode update), the common
 // gradient partials of mode n (after it), the per-block evaluation terms
 static int xchg_lip(cb_solver* h, int n) {
-  if (h->world <= 1 || h->counts[n] == 0) return CB_OK;
+  if (!h->shard || h->counts[n] == 0) return CB_OK;
   const long long o = lu_idx(h->ctx, n, 0);
   return xchg(h, h->ctx.lip_w + o, h->ctx.lip + o, 2LL * h->S_tot);
 }
 static int xchg_gc(cb_solver* h, int n) {
-  if (h->world <= 1 || h->counts[n] == 0) return CB_OK;
+  if (!h->shard || h->counts[n] == 0) return CB_OK;
   return xchg(h, h->ctx.gc_w, h->ctx.gc_part, (long long)h->S_tot * h->ctx.gc_stride);
 }
 
@@ -239,7 +241,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       CB_CHECK_LAUNCH();
     }
     prof(h, redo ? "redo:mode_update" : "mode_update");
-    if (h->world > 1 && h->counts[n] > 0) {
+    if (h->shard && h->counts[n] > 0) {
       if ((rc = xchg_gc(h, n))) return rc;
       if (emit(h)) {
         const int tiles = (int)((h->dims[n] + MU_ROWS - 1) / MU_ROWS);
@@ -273,7 +275,7 @@ static int enqueue_qr(cb_solver* h, int redo) {
 
 static int enqueue_control(cb_solver* h, int mode) {
   const int bsrc = h->fast3 ? 0 : 1;
-  if (h->world <= 1) {
+  if (!h->shard) {
     if (emit(h)) {
       k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 3);
       count_launch(1);
@@ -466,7 +468,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_ARG(d->order >= 1 && d->order <= CB_MAX_ORDER, "order %d outside [1, %d]", d->order, CB_MAX_ORDER);
   CB_ARG(d->dtype == CB_F32 || d->dtype == CB_F64, "bad dtype");
   const int world = d->world_size > 1 ? d->world_size : 1;
-  if (world > 1) {
+  const int shard = (world > 1 || d->nccl_comm) ? 1 : 0;
+  if (shard) {
     CB_ARG(d->order == 3, "block-sharded solves need 3-way blocks (order %d)", d->order);
     CB_ARG(d->rank_id >= 0 && d->rank_id < world, "rank %d outside [0, %d)", d->rank_id, world);
     CB_ARG(d->block_offset >= 0 && d->block_offset + d->n_blocks <= d->total_blocks,
@@ -479,10 +482,11 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   }
   cb_solver* h = new cb_solver();
   h->world = world;
-  h->rank = world > 1 ? d->rank_id : 0;
-  h->comm = world > 1 ? d->nccl_comm : nullptr;
-  h->S_tot = world > 1 ? d->total_blocks : d->n_blocks;
-  h->off = world > 1 ? d->block_offset : 0;
+  h->shard = shard;
+  h->rank = shard ? d->rank_id : 0;
+  h->comm = shard ? d->nccl_comm : nullptr;
+  h->S_tot = shard ? d->total_blocks : d->n_blocks;
+  h->off = shard ? d->block_offset : 0;
   h->st = (cudaStream_t)stream;
   h->S = d->n_blocks; h->N = d->order; h->lra = d->lra; h->update_core = d->update_core;
   h->dtype = d->dtype; h->objective = d->objective; h->delta_w = d->delta_w; h->tol = d->tol;
@@ -569,7 +573,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   h->h_MTT = MTT;
   h->h_LAM = LAM;
   Ctx& c = h->ctx;
-  c.S = S; c.S_tot = h->S_tot; c.off = h->off; c.shard = world > 1 ? 1 : 0;
+  c.S = S; c.S_tot = h->S_tot; c.off = h->off; c.shard = shard;
   c.N = N; c.lra = h->lra; c.update_core = h->update_core; c.objective = h->objective;
   c.fast3 = h->fast3; c.max_iter = h->max_iter; c.rmax = std::max(h->rmax, h->rtmax);
   for (int n = 0; n < N; ++n) c.counts[n] = h->counts[n];
@@ -602,7 +606,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   TRY(dalloc((void**)&c.lip, sizeof(double) * 2 * N * ST, A));
   TRY(dalloc((void**)&c.ctl, sizeof(double) * 3 * ST, A));
   c.lip_w = c.lip; c.ctl_w = c.ctl;
-  if (world > 1) {
+  if (shard) {
     TRY(dalloc((void**)&c.lip_w, sizeof(double) * 2 * N * ST, A));
     TRY(dalloc((void**)&c.ctl_w, sizeof(double) * 3 * ST, A));
   }
@@ -619,7 +623,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   c.gc_stride = maxIn * std::max(maxL, 1);
   TRY(dalloc((void**)&c.gc_part, sizeof(double) * ST * c.gc_stride, A));
   c.gc_w = c.gc_part;
-  if (world > 1) TRY(dalloc((void**)&c.gc_w, sizeof(double) * ST * c.gc_stride, A));
+  if (shard) TRY(dalloc((void**)&c.gc_w, sizeof(double) * ST * c.gc_stride, A));
   TRY(dalloc((void**)&c.cnew, sizeof(double) * c.gc_stride, A));
   TRY(dalloc((void**)&c.tile_cnt, sizeof(int) * (maxIn / MU_ROWS + 2), A));
   if (h->lra) {
@@ -761,7 +765,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   if (h->lra)
     CB_CUDA(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qr_smem));
   // ---- iteration 0 (an emulated group runs it through cb_group_step)
-  if (world == 1 || h->comm) {
+  if (!shard || h->comm) {
     TRY(init_evaluation(h));
     TRY(read_state(h));
     h->init_done = true;
@@ -775,7 +779,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
 
 int cb_solver_step_async(cb_solver* h) {
   CB_ARG(h, "null handle");
-  CB_ARG(h->world == 1 || h->comm, "emulated shard groups are stepped with cb_group_step");
+  CB_ARG(!h->shard || h->comm, "emulated shard groups are stepped with cb_group_step");
   if (!h->fast3) {
     int rc = generic_iteration(h);
     return rc;
@@ -829,7 +833,7 @@ int cb_solver_summary_get(cb_solver* h, cb_solver_summary* sum) {
 
 int cb_solver_run(cb_solver* h, int iters, cb_solver_summary* sum) {
   CB_ARG(h, "null handle");
-  CB_ARG(h->world == 1 || h->comm, "emulated shard groups run through cb_group_run");
+  CB_ARG(!h->shard || h->comm, "emulated shard groups run through cb_group_run");
   int rc = read_state(h);
   if (rc) return rc;
   int left = iters;

@@ -657,10 +657,11 @@ class PreparedShardedSolve:
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         self.group = group
-        self.comm = nccl_comm_for(group) if world > 1 else None
+        # a communicator even for one rank: the sharded program (exchanges in
+        # the iteration graph) then runs on a single GPU too
+        self.comm = nccl_comm_for(group)
         b, e = shard_ranges(problem.n_blocks, world)[rank]
-        self.inner = PreparedSolve(problem, opts,
-                                   shard=ShardSpec(world, rank, b, e, self.comm) if world > 1 else None)
+        self.inner = PreparedSolve(problem, opts, shard=ShardSpec(world, rank, b, e, self.comm))
         self.engine, self.stream = self.inner.engine, self.inner.stream
 
     def run(self, iters=None):
@@ -670,10 +671,10 @@ class PreparedShardedSolve:
         """The full SolveResult on every rank (blocks gathered over the group)."""
         import torch.distributed as dist
         summ, hist, blocks, comp, secs = self.inner.collect_local()
-        if self.comm is None:
+        world = dist.get_world_size(self.group)
+        if world == 1:
             merged_b, merged_c = blocks, comp
         else:
-            world = dist.get_world_size(self.group)
             got = [None] * world
             dist.all_gather_object(got, (blocks, comp), group=self.group)
             merged_b, merged_c = {}, (None if comp is None else {})

@@ -90,3 +90,27 @@ def test_shard_argument_errors(P):
     prob = P.CoupledProblem(tensors, 5, [2, 2, 2])
     with pytest.raises(ValueError):
         P.solver.solve_emulated_shards(prob, P.SolverOptions(max_iter=3), world=3)
+
+
+def test_nccl_path_single_rank_equals_single_gpu(P, tmp_path):
+    """The NCCL transport on one GPU: a world-1 NCCL communicator makes the
+    engine run the sharded program (all-reduces captured in the iteration
+    graph); the result must equal the plain solve bit for bit."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        for mode in ("full", "lra"):
+            tensors = _problem_tensors(S=3)
+            prob = P.CoupledProblem(tensors, 5, [2, 2, 2], mode=mode)
+            opts = P.SolverOptions(max_iter=40, seed=1)
+            want = P.solve(prob, opts)
+            got = P.solver.solve_distributed(prob, opts)
+            _same(got, want)
+    finally:
+        dist.destroy_process_group()
