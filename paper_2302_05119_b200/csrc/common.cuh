@@ -18,6 +18,38 @@
 
 namespace cb {
 
+// Phase timestamps (profiling builds of a run: Ctx.dbg non-null): block 0
+// accumulates the time between consecutive PH() marks into dbg[slot].
+struct PhaseClock {
+  unsigned long long last = 0;
+  long long last_clk = 0;
+  __device__ __forceinline__ unsigned long long now() const {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  }
+  __device__ __forceinline__ void start(const double* dbg) {
+    if (dbg && blockIdx.x == 0) { __syncthreads(); last = now(); last_clk = clock64(); }
+  }
+  // dbg[slot] += ns, dbg[32 + slot] += SM cycles (their ratio is the clock)
+  __device__ __forceinline__ void mark(double* dbg, int slot) {
+    if (dbg && blockIdx.x == 0) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long t = now();
+        const long long k = clock64();
+        dbg[slot] += (double)(t - last);
+        dbg[32 + slot] += (double)(k - last_clk);
+        // restart after the read-modify-write: its global round trip is
+        // charged to no phase
+        last = now();
+        last_clk = clock64();
+      }
+    }
+  }
+};
+
+
 // ----------------------------------------------------------------------------
 // deterministic block reductions (fixed shuffle tree, fixed warp order)
 // ----------------------------------------------------------------------------
@@ -185,8 +217,11 @@ __device__ inline void eigen_tail(const double* A, int R, int ld, const double* 
                                   double* vec, double* red, double shift);
 
 __device__ inline double dominant_rq(const double* A, int R, int ld, double* B, double* B2,
-                                     double* vec, double* red, double shift, double* resid_out) {
+                                     double* vec, double* red, double shift, double* resid_out,
+                                     double* dbg = nullptr) {
   const int tid = threadIdx.x, nthr = blockDim.x;
+  PhaseClock pc;
+  pc.start(dbg);
   const int Rp2 = lm_rp2(R), bld = lm_bld(R);
   unsigned* ured = reinterpret_cast<unsigned*>(red);   // 64 words = 32 doubles
   double m = 0.0;
@@ -204,6 +239,7 @@ __device__ inline double dominant_rq(const double* A, int R, int ld, double* B, 
     B[e] = v;
   }
   __syncthreads();
+  pc.mark(dbg, 10);
   // passes of four squarings (B -> B^16); after each pass the eigenpair is
   // extracted and accepted once its residual ||Av - rho v|| / ||v|| is below
   // 1e-9 ||A||, i.e. the Rayleigh quotient is within ~1e-18 ||A||^2 / gap of
@@ -225,6 +261,7 @@ __device__ inline double dominant_rq(const double* A, int R, int ld, double* B, 
         B[i * bld + j] *= ib;
       }
       __syncthreads();
+      pc.mark(dbg, 13);
     }
     if (R <= 16) {
       sq_tiles<1>(B, B2, Rp2, bld); sq_tiles<1>(B2, B, Rp2, bld);
@@ -233,10 +270,12 @@ __device__ inline double dominant_rq(const double* A, int R, int ld, double* B, 
       sq_tiles<2>(B, B2, Rp2, bld); sq_tiles<2>(B2, B, Rp2, bld);
       sq_tiles<2>(B, B2, Rp2, bld); sq_tiles<2>(B2, B, Rp2, bld);
     }
+    pc.mark(dbg, 11);
     eigen_tail(A, R, ld, B, bld, vec, red, shift);
     rho = red[36];
     resid = red[37];
     __syncthreads();
+    pc.mark(dbg, 12);
     if (resid <= 1e-9 * m) break;
   }
   if (resid_out) *resid_out = resid;
@@ -303,16 +342,19 @@ __device__ inline void eigen_tail(const double* A, int R, int ld, const double* 
 // leading dimension lm_ld(R).  All threads of the block must call it; the
 // result is returned to every thread.
 __device__ inline double block_lam_max(const double* A, int R, double* B, double* B2, double* vec,
-                                       double* red) {
+                                       double* red, double* dbg = nullptr) {
   const int ld = lm_ld(R);
   double resid;
-  const double rho = dominant_rq(A, R, ld, B, B2, vec, red, 0.0, &resid);
+  const double rho = dominant_rq(A, R, ld, B, B2, vec, red, 0.0, &resid, dbg);
+  PhaseClock pc;
+  pc.start(dbg);
   double amax = 0.0;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, j = e - i * R;
     amax = fmax(amax, fabs(A[i * ld + j]));
   }
   amax = block_max_approx(amax, reinterpret_cast<unsigned*>(red));
+  pc.mark(dbg, 14);
   if (amax == 0.0) return 0.0;
   // PSD / positive-dominant path: a converged eigenpair with rho >= 0 is the
   // spectral radius, hence lambda_max
@@ -320,6 +362,7 @@ __device__ inline double block_lam_max(const double* A, int R, double* B, double
   // otherwise shift by a spectral-radius bound so A + sI is PSD
   const double s = (rho < 0.0 && resid <= 1e-10 * amax * R) ? -rho : 2.0 * amax * R;
   const double rho2 = dominant_rq(A, R, ld, B, B2, vec, red, s, nullptr);
+  pc.mark(dbg, 15);
   const double lm = rho2 - s;
   return lm > 0.0 ? lm : 0.0;
 }

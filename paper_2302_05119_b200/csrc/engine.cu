@@ -40,6 +40,11 @@ using namespace cb;
 
 struct cb_solver {
   cudaStream_t st = nullptr;
+  // side stream of the 3-way full path: the MTTKRP of mode n runs on it
+  // concurrently with mode n's step matrix / lambda_max on `st` (fork/join by
+  // events, captured as parallel graph branches)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0, pc = 0;
   int rmax = 1, rtmax = 0, rb = 8, max_iter = 0;
   double delta_w = 0.9999, tol = 1e-8;
@@ -178,15 +183,45 @@ static int enqueue_fiber(cb_solver* h, const XArgs& a, int want_t, int want_b, i
   return CB_OK;
 }
 
-static int enqueue_slab(cb_solver* h, const XArgs& a) {
+static int enqueue_slab(cb_solver* h, const XArgs& a, cudaStream_t st) {
   if (!emit(h)) return CB_OK;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool timed = h->timing && a.gate != &h->d_state->go_redo;
-  if (timed) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
-  launch_slab(h->pc, h->rb, h->tma, a, h->d_slab, (int)h->tab.slab.size(), h->tab, h->st);
+  if (timed) { int rc = ev_pair(h, &e0, &e1, 2); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, st)); }
+  launch_slab(h->pc, h->rb, h->tma, a, h->d_slab, (int)h->tab.slab.size(), h->tab, st);
   CB_CHECK_LAUNCH();
-  if (timed) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
+  if (timed) { CB_CUDA(cudaEventRecord(e1, st)); h->t_launches += 1; h->t_bytes += (double)h->elem_total * h->elem_bytes; }
   return CB_OK;
+}
+
+// side-stream fork / join (no-ops outside the emitted segment)
+static int fork_side(cb_solver* h) {
+  if (!emit(h)) return CB_OK;
+  CB_CUDA(cudaEventRecord(h->ev_fork, h->st));
+  CB_CUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  return CB_OK;
+}
+static int join_side(cb_solver* h) {
+  if (!emit(h)) return CB_OK;
+  CB_CUDA(cudaEventRecord(h->ev_join, h->st2));
+  CB_CUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  return CB_OK;
+}
+
+// MTTKRP of mode n of the 3-way full path (contract from T, or the slab pass)
+static int enqueue_mttkrp3(cb_solver* h, int n, const XArgs& xa, int redo, cudaStream_t st) {
+  if (n < 2) {
+    if (emit(h)) {
+      launch_contract(h->pc, n, xa, n == 0 ? h->d_c0 : h->d_c1,
+                      (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
+      CB_CHECK_LAUNCH();
+    }
+    prof(h, redo ? "redo:contract" : (n == 0 ? "contract0" : "contract1"));
+    return CB_OK;
+  }
+  int rc = enqueue_slab(h, xa, st);
+  prof(h, redo ? "redo:slab" : "slab");
+  return rc;
 }
 
 // generic-order helpers (per-block launches, host-driven restart)
@@ -200,35 +235,32 @@ static int generic_mttkrp(cb_solver* h, int s, int n) {
 static int generic_rowdot_into(cb_solver* h, int s, int n, double* out);
 static int generic_residuals(cb_solver* h);
 
-// one sweep (solver.py:459-463); redo = restart sweep with w_hat = 0
+// one sweep (solver.py:459-463); redo = restart sweep with w_hat = 0.
+// 3-way full path: mode n's MTTKRP (side stream) overlaps mode n's step
+// matrix + lambda_max (k_sweep_begin for n = 0, k_step otherwise).
 static int enqueue_sweep(cb_solver* h, int redo) {
   cudaStream_t st = h->st;
   const XArgs& xa = redo ? h->xa_redo : h->xa_main;
+  const bool par = h->fast3 && !h->lra;
   int rc;
+  if (par) {
+    if ((rc = fork_side(h))) return rc;
+    if ((rc = enqueue_mttkrp3(h, 0, xa, redo, h->st2))) return rc;
+  }
   if (emit(h)) {
     k_sweep_begin<<<h->S, 256, h->blk_smem, st>>>(h->ctx, redo);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
   prof(h, redo ? "redo:sweep_begin" : "sweep_begin");
+  if (par && (rc = join_side(h))) return rc;
   if ((rc = xchg_lip(h, 0))) return rc;
   for (int n = 0; n < h->N; ++n) {
     int src = 0;
     if (h->lra) {
       src = 2;
     } else if (h->fast3) {
-      if (n < 2) {
-        if (emit(h)) {
-          launch_contract(h->pc, n, xa, n == 0 ? h->d_c0 : h->d_c1,
-                          (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
-          CB_CHECK_LAUNCH();
-        }
-        prof(h, redo ? "redo:contract" : (n == 0 ? "contract0" : "contract1"));
-      } else {
-        if ((rc = enqueue_slab(h, xa))) return rc;
-        src = 1;
-        prof(h, redo ? "redo:slab" : "slab");
-      }
+      src = n < 2 ? 0 : 1;   // MTTKRP already enqueued (overlapped)
     } else {
       for (int s = 0; s < h->S; ++s) {
         if ((rc = generic_mttkrp(h, s, n))) return rc;
@@ -251,12 +283,24 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       }
       prof(h, redo ? "redo:common" : "common");
     }
+    const bool split = par && n + 1 < h->N;
     if (emit(h)) {
-      k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo);
+      k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo, split ? 0 : 1);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
     prof(h, redo ? "redo:finalize" : "finalize");
+    if (split) {
+      if ((rc = fork_side(h))) return rc;
+      if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
+      if (emit(h)) {
+        k_step<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n + 1, redo);
+        count_launch(1);
+        CB_CHECK_LAUNCH();
+      }
+      prof(h, redo ? "redo:step" : "step");
+      if ((rc = join_side(h))) return rc;
+    }
     if (n + 1 < h->N && (rc = xchg_lip(h, n + 1))) return rc;
   }
   return CB_OK;
@@ -760,6 +804,10 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+  CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CB_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CB_CUDA(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_mode_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->mu_smem));
   if (h->lra)
@@ -1038,6 +1086,9 @@ int cb_solver_destroy(cb_solver* h) {
   if (!h) return CB_OK;
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->st2) cudaStreamDestroy(h->st2);
   for (void* p : h->allocs) cudaFree(p);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->h_state) cudaFreeHost(h->h_state);

@@ -12,35 +12,6 @@
 
 namespace cb {
 
-// Phase timestamps (profiling builds of a run: Ctx.dbg non-null): block 0
-// accumulates the time between consecutive PH() marks into dbg[slot].
-struct PhaseClock {
-  unsigned long long last = 0;
-  long long last_clk = 0;
-  __device__ __forceinline__ unsigned long long now() const {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-  }
-  __device__ __forceinline__ void start(const double* dbg) {
-    if (dbg && blockIdx.x == 0) { __syncthreads(); last = now(); last_clk = clock64(); }
-  }
-  // dbg[slot] += ns, dbg[32 + slot] += SM cycles (their ratio is the clock)
-  __device__ __forceinline__ void mark(double* dbg, int slot) {
-    if (dbg && blockIdx.x == 0) {
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const unsigned long long t = now();
-        const long long k = clock64();
-        dbg[slot] += (double)(t - last);
-        dbg[32 + slot] += (double)(k - last_clk);
-        last = t;
-        last_clk = k;
-      }
-    }
-  }
-};
-
 __device__ __forceinline__ bool stopped(const Ctx& c, int redo) {
   return redo ? (c.st->go_redo == 0) : (c.st->go_main == 0);
 }
@@ -145,7 +116,7 @@ __device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const Bloc
     step[e] = sm.lmA[i * ld + j];
   }
   pc.mark(c.dbg, 4);
-  const double lu = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+  const double lu = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.dbg);
   if (threadIdx.x == 0) {
     const int idx = n * c.S + s;
     const double h = c.lipf_hist[idx];
@@ -323,7 +294,10 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
     }
     __syncthreads();
   }
+  PhaseClock pc;
+  pc.start(c.dbg);
   step_and_lipschitz(c, s, 0, sm);
+  pc.mark(c.dbg, 9);
 }
 
 // sum over all blocks (global order) of the mode-n Lipschitz constants and of
@@ -398,6 +372,8 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) step[e] = stp[e];
   __syncthreads();
   const double sumL = sc[0], wc = sc[1], ws = sc[2], lu = sc[3];
+  PhaseClock pc;
+  pc.start(c.dbg);
   const double* Uc = c.U[s * N + n];
   const double* Upr = c.Up[s * N + n];
   const int R0 = c.R[0];
@@ -453,6 +429,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     }
   }
   __syncthreads();
+  pc.mark(c.dbg, 6);
   double* Un = c.Un[s * N + n];
   double* gcp = c.gc_w + (long long)(c.off + s) * c.gc_stride;
   for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
@@ -469,6 +446,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     else Un[i * R + r] = pos(uh[e] - g / lu);
   }
   // sharded: the partials are all-reduced first; k_common folds them
+  pc.mark(c.dbg, 7);
   if (L == 0 || c.shard) return;
   __threadfence();
   __syncthreads();
@@ -483,6 +461,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   __threadfence();
   // last CTA of this row tile: sum the partials in block order (solver.py:444)
   common_fold(c, n, r0, rows, sumL, wc);
+  pc.mark(c.dbg, 8);
   if (threadIdx.x == 0) c.tile_cnt[r0 / MU_ROWS] = 0;
 }
 
@@ -512,7 +491,9 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
 // gram / cross gram (solver.py:452-457, :367-371), then the next mode's step
 // matrix and Lipschitz constant, or the evaluation quantities after mode N-1.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo) {
+// with_step = 0: the next mode's step matrix is left to k_step, which the 3-way
+// path runs concurrently with the next MTTKRP (they share no inputs)
+__global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int with_step) {
   if (stopped(c, redo)) return;
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
@@ -539,12 +520,22 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo) {
   __syncthreads();
   pc.mark(c.dbg, 1);
   if (n + 1 < N) {
-    step_and_lipschitz(c, s, n + 1, sm);
-    pc.mark(c.dbg, 2);
+    if (with_step) {
+      step_and_lipschitz(c, s, n + 1, sm);
+      pc.mark(c.dbg, 2);
+    }
   } else {
     final_quantities(c, s, sm);
     pc.mark(c.dbg, 3);
   }
+}
+
+// step matrix and Lipschitz constant of mode n for every block (solver.py:402-406)
+__global__ void __launch_bounds__(256) k_step(Ctx c, int n, int redo) {
+  if (stopped(c, redo)) return;
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  step_and_lipschitz(c, blockIdx.x, n, sm);
 }
 
 // restore curr <- prev and refresh caches (solver.py:538-543)
