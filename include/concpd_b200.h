@@ -214,6 +214,11 @@ int cb_solver_set_timing(cb_solver* h, int on);
  * graph while on): on=1 starts, on=0 stops and writes "label count ms" lines */
 int cb_solver_profile(cb_solver* h, int on, char* out, int cap);
 int cb_solver_timing(cb_solver* h, int kind, double* ms, long long* launches, double* bytes);
+/* iteration timeline (profiling): op 1 enables (re-captures the iteration
+ * graph with in-kernel timestamps) and resets, 2 resets, 0 synchronises and
+ * copies per kernel slot {earliest CTA start, latest CTA end} (globaltimer
+ * ns, 2*24 entries; slot ids in csrc/xpass.cuh TlSlot), -1 disables. */
+int cb_solver_timeline(cb_solver* h, int op, unsigned long long* out, int cap);
 int cb_solver_destroy(cb_solver* h);
 
 /* Emulated shard group: the handles of ranks 0..n-1 (created with

@@ -100,6 +100,7 @@ _sig("cb_solver_block_factors", c_int, [c_vp, c_int, ctypes.POINTER(c_dp), c_dp]
 _sig("cb_solver_set_timing", c_int, [c_vp, c_int])
 _sig("cb_solver_profile", c_int, [c_vp, c_int, ctypes.c_char_p, c_int])
 _sig("cb_solver_timing", c_int, [c_vp, c_int, c_dp, ctypes.POINTER(ctypes.c_longlong), c_dp])
+_sig("cb_solver_timeline", c_int, [c_vp, c_int, ctypes.POINTER(ctypes.c_ulonglong), c_int])
 _sig("cb_solver_destroy", c_int, [c_vp])
 _sig("cb_group_step", c_int, [ctypes.POINTER(c_vp), c_int, c_int])
 _sig("cb_group_run", c_int, [ctypes.POINTER(c_vp), c_int, c_int, ctypes.POINTER(SolverSummary)])
@@ -115,7 +116,8 @@ EXPORTED = [
     "cb_als_create", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
     "cb_als_destroy", "cb_solver_create", "cb_solver_run", "cb_solver_step_async",
     "cb_solver_summary_get", "cb_solver_history", "cb_solver_block_factors",
-    "cb_solver_set_timing", "cb_solver_timing", "cb_solver_profile", "cb_solver_destroy",
+    "cb_solver_set_timing", "cb_solver_timing", "cb_solver_profile", "cb_solver_timeline",
+    "cb_solver_destroy",
     "cb_group_step", "cb_group_run", "cb_nccl_unique_id",
     "cb_nccl_comm_init", "cb_nccl_comm_destroy",
 ]

@@ -260,7 +260,7 @@ static int als_sweep(cb_als* h) {
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
       } else {
         launch_slab(h->pc, h->rb, h->tma, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab, st);
-        src = 1;
+        src = h->tab.slab_direct ? 0 : 1;   // the row-dot kernel writes MTT itself
       }
       CB_CHECK_LAUNCH();
     } else {
@@ -456,6 +456,11 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     xa.MTT = c.MTT; xa.gate = nullptr; xa.active = c.active;
     xa.ktime = nullptr;
     xa.slab_stage_rows = h->tab.slab_rows;
+    {
+      int* d_s3;
+      TRY(upload(h->tab.s3_first, &d_s3, A, st));
+      xa.s3_first = d_s3;
+    }
     xa.fib_first = c.fib_first; xa.blk_cnt = blk_cnt; xa.bsum = bsum; xa.rsum = rsum;
   } else {
     size_t kr = 0;

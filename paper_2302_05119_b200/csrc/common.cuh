@@ -213,10 +213,10 @@ __device__ __forceinline__ void sq_tiles(const double* B, double* B2, int Rp2, i
   __syncthreads();
 }
 
-__device__ inline void eigen_tail(const double* A, int R, int ld, const double* B, int bld,
+static __device__ __noinline__ void eigen_tail(const double* A, int R, int ld, const double* B, int bld,
                                   double* vec, double* red, double shift);
 
-__device__ inline double dominant_rq(const double* A, int R, int ld, double* B, double* B2,
+static __device__ __noinline__ double dominant_rq(const double* A, int R, int ld, double* B, double* B2,
                                      double* vec, double* red, double shift, double* resid_out,
                                      double* dbg = nullptr) {
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -285,7 +285,7 @@ __device__ inline double dominant_rq(const double* A, int R, int ld, double* B, 
 // warp 0: eigenvector from the column of B with the largest diagonal, one
 // power step with the original (shifted) matrix, Rayleigh quotient and
 // residual -> red[36], red[37]; ends with a block barrier
-__device__ inline void eigen_tail(const double* A, int R, int ld, const double* B, int bld,
+static __device__ __noinline__ void eigen_tail(const double* A, int R, int ld, const double* B, int bld,
                                   double* vec, double* red, double shift) {
   const int tid = threadIdx.x;
   if (tid < 32) {
@@ -341,7 +341,7 @@ __device__ inline void eigen_tail(const double* A, int R, int ld, const double* 
 // lambda_max(A) clamped at 0 (0 for the exact zero matrix).  A in smem with
 // leading dimension lm_ld(R).  All threads of the block must call it; the
 // result is returned to every thread.
-__device__ inline double block_lam_max(const double* A, int R, double* B, double* B2, double* vec,
+static __device__ __noinline__ double block_lam_max(const double* A, int R, double* B, double* B2, double* vec,
                                        double* red, double* dbg = nullptr) {
   const int ld = lm_ld(R);
   double resid;

@@ -6,6 +6,8 @@
 // the 3-way fast path one iteration is captured once in a CUDA graph and
 // replayed.  The host polls the device `done` flag every few iterations.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -45,6 +47,9 @@ struct cb_solver {
   // events, captured as parallel graph branches)
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t st3 = nullptr;     // capture stream of the conditional restart body
+  bool cond_capture = false;
+  bool in_body = false;
   int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0, pc = 0;
   int rmax = 1, rtmax = 0, rb = 8, max_iter = 0;
   double delta_w = 0.9999, tol = 1e-8;
@@ -241,7 +246,9 @@ static int generic_residuals(cb_solver* h);
 static int enqueue_sweep(cb_solver* h, int redo) {
   cudaStream_t st = h->st;
   const XArgs& xa = redo ? h->xa_redo : h->xa_main;
-  const bool par = h->fast3 && !h->lra;
+  // no side stream inside the conditional restart body (rarely executed; keeps
+  // that capture single-stream)
+  const bool par = h->fast3 && !h->lra && !h->in_body;
   int rc;
   if (par) {
     if ((rc = fork_side(h))) return rc;
@@ -260,7 +267,9 @@ static int enqueue_sweep(cb_solver* h, int redo) {
     if (h->lra) {
       src = 2;
     } else if (h->fast3) {
-      src = n < 2 ? 0 : 1;   // MTTKRP already enqueued (overlapped)
+      src = (n < 2 || h->tab.slab_direct) ? 0 : 1;
+      // overlapped runs enqueued this MTTKRP on the side stream already
+      if (!par && (rc = enqueue_mttkrp3(h, n, xa, redo, st))) return rc;
     } else {
       for (int s = 0; s < h->S; ++s) {
         if ((rc = generic_mttkrp(h, s, n))) return rc;
@@ -359,7 +368,7 @@ static int enqueue_eval_full(cb_solver* h, int redo) {
   if (h->fast3) {
     XArgs a = redo ? h->xa_redo : h->xa_main;
     a.t_other = 1;   // write the non-accepted T buffer
-    return enqueue_fiber(h, a, 1, 1, h->objective == 0 ? 1 : 0);
+    return enqueue_fiber(h, a, 1, h->ctx.b_mtt ? 0 : 1, h->objective == 0 ? 1 : 0);
   }
   // generic: b from the last mode's MTTKRP (solver.py:506-509), residuals
   for (int s = 0; s < h->S; ++s) {
@@ -382,6 +391,56 @@ static int enqueue_trace_lra(cb_solver* h) {
 }
 
 // one full APG iteration (solver.py:586-610), device-gated
+// restart branch (solver.py:594-599): restore, sweep with w_hat = 0,
+// re-evaluate, accept; every kernel is gated on go_redo
+static int enqueue_redo_branch(cb_solver* h) {
+  int rc;
+  if ((rc = enqueue_restore(h))) return rc;
+  if ((rc = enqueue_sweep(h, 1))) return rc;
+  if (!h->lra) {
+    if ((rc = enqueue_eval_full(h, 1))) return rc;
+    prof(h, "redo:fiber");
+  } else if ((rc = enqueue_qr(h, 1))) {
+    return rc;
+  }
+  return enqueue_control(h, CTRL_REDO);
+}
+
+// Under graph capture (h->cond_capture) the restart branch becomes the body of
+// a conditional IF node, so an iteration without restart launches none of its
+// ~15 kernels; otherwise it is enqueued inline as gated no-ops.
+static int enqueue_redo(cb_solver* h) {
+  if (!h->cond_capture) return enqueue_redo_branch(h);
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CB_CUDA(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h->ctx.cond;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CB_CUDA(cudaGraphAddNode(&node, g, deps, nd, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CB_CUDA(cudaStreamUpdateCaptureDependencies(h->st, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaStream_t main = h->st;
+  h->st = h->st3;
+  CB_CUDA(cudaStreamBeginCaptureToGraph(h->st3, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal));
+  h->in_body = true;
+  int rc = enqueue_redo_branch(h);
+  h->in_body = false;
+  cudaGraph_t done_body;
+  cudaError_t e = cudaStreamEndCapture(h->st3, &done_body);
+  h->st = main;
+  if (rc) return rc;
+  CB_CUDA(e);
+  return CB_OK;
+}
+
+// one full APG iteration (solver.py:586-610), device-gated
 static int enqueue_iteration(cb_solver* h) {
   int rc;
   prof(h, "(start)");
@@ -390,20 +449,12 @@ static int enqueue_iteration(cb_solver* h) {
     if ((rc = enqueue_eval_full(h, 0))) return rc;
     prof(h, "fiber");
     if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
-    // restart branch (no-ops unless go_redo)
-    if ((rc = enqueue_restore(h))) return rc;
-    if ((rc = enqueue_sweep(h, 1))) return rc;
-    if ((rc = enqueue_eval_full(h, 1))) return rc;
-    prof(h, "redo:fiber");
-    if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
+    if ((rc = enqueue_redo(h))) return rc;
   } else {
     if ((rc = enqueue_sweep(h, 0))) return rc;
     if ((rc = enqueue_qr(h, 0))) return rc;
     if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
-    if ((rc = enqueue_restore(h))) return rc;
-    if ((rc = enqueue_sweep(h, 1))) return rc;
-    if ((rc = enqueue_qr(h, 1))) return rc;
-    if ((rc = enqueue_control(h, CTRL_REDO))) return rc;
+    if ((rc = enqueue_redo(h))) return rc;
     if ((rc = enqueue_trace_lra(h))) return rc;
     prof(h, "trace_fiber");
     if ((rc = enqueue_control(h, CTRL_FINISH))) return rc;
@@ -766,6 +817,15 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     xa.MTT = c.MTT; xa.active = nullptr;
     xa.ktime = nullptr;
     xa.slab_stage_rows = h->tab.slab_rows;
+    {
+      int* d_s3;
+      TRY(upload(h->tab.s3_first, &d_s3, A, st));
+      xa.s3_first = d_s3;
+    }
+    // with the row-dot mode-2 kernel, the core linear term b is staged from
+    // its MTTKRP output (solver.py:506-509) in k_finalize of the last mode,
+    // so the evaluation fiber pass only forms T
+    c.b_mtt = (h->tab.slab_direct && !h->lra) ? 1 : 0;
     if (c.dbg) {
       TRY(dalloc((void**)&h->ktime, sizeof(unsigned long long) * 8, A));
       const unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, ~0ull, 0};
@@ -806,6 +866,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+  CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CB_CUDA(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
@@ -837,12 +898,26 @@ int cb_solver_step_async(cb_solver* h) {
     cudaGraph_t g;
     cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
+      // conditional restart branch (not with NCCL exchanges inside it)
+      if (!h->shard && !getenv("CB_NO_COND")) {
+        cudaGraph_t cg;
+        cudaStreamCaptureStatus cs;
+        if (cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, nullptr, nullptr) == cudaSuccess &&
+            cudaGraphConditionalHandleCreate(&h->ctx.cond, cg, 0, cudaGraphCondAssignDefault) ==
+                cudaSuccess) {
+          h->ctx.use_cond = 1;
+          h->cond_capture = true;
+        }
+      }
       const long long before = cb_launch_count();
       int rc = enqueue_iteration(h);
       h->launches_per_iter = cb_launch_count() - before;
+      h->ctx.use_cond = 0;
+      h->cond_capture = false;
       cudaError_t e2 = cudaStreamEndCapture(h->st, &g);
       if (rc == CB_OK && e2 == cudaSuccess) {
-        if (cudaGraphInstantiate(&h->gexec, g, 0) != cudaSuccess) {
+        cudaError_t e3 = cudaGraphInstantiate(&h->gexec, g, 0);
+        if (e3 != cudaSuccess) {
           h->gexec = nullptr;
           h->graph_ok = false;
         }
@@ -989,6 +1064,38 @@ int cb_solver_profile(cb_solver* h, int on, char* out, int cap) {
   return CB_OK;
 }
 
+int cb_solver_timeline(cb_solver* h, int op, unsigned long long* out, int cap) {
+  CB_ARG(h, "null handle");
+  const size_t bytes = sizeof(unsigned long long) * 2 * TL_NSLOT;
+  if (op == 1 && !h->ctx.tl) {
+    CB_CUDA(cudaMalloc((void**)&h->ctx.tl, bytes));
+    h->allocs.push_back(h->ctx.tl);
+    h->xa_main.tl = h->ctx.tl;
+    h->xa_redo.tl = h->ctx.tl;
+    if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }   // recapture
+  }
+  if (op == -1 && h->ctx.tl) {
+    h->ctx.tl = nullptr;
+    h->xa_main.tl = nullptr;
+    h->xa_redo.tl = nullptr;
+    if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+    return CB_OK;
+  }
+  if (!h->ctx.tl) return CB_OK;
+  if (op == 1 || op == 2) {
+    // begin slots (even) start at ~0 for atomicMin, end slots at 0
+    std::vector<unsigned long long> init(2 * TL_NSLOT);
+    for (int k = 0; k < TL_NSLOT; ++k) { init[2 * k] = ~0ull; init[2 * k + 1] = 0ull; }
+    CB_CUDA(cudaMemcpyAsync(h->ctx.tl, init.data(), bytes, cudaMemcpyHostToDevice, h->st));
+    CB_CUDA(cudaStreamSynchronize(h->st));
+    return CB_OK;
+  }
+  CB_CUDA(cudaStreamSynchronize(h->st));
+  CB_ARG(out && cap >= 2 * TL_NSLOT, "timeline buffer needs %d entries", 2 * TL_NSLOT);
+  CB_CUDA(cudaMemcpy(out, h->ctx.tl, bytes, cudaMemcpyDeviceToHost));
+  return CB_OK;
+}
+
 int cb_solver_set_timing(cb_solver* h, int on) {
   CB_ARG(h, "null handle");
   h->timing = on != 0;
@@ -1089,6 +1196,7 @@ int cb_solver_destroy(cb_solver* h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->st2) cudaStreamDestroy(h->st2);
+  if (h->st3) cudaStreamDestroy(h->st3);
   for (void* p : h->allocs) cudaFree(p);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->h_state) cudaFreeHost(h->h_state);

@@ -93,6 +93,12 @@ struct Ctx {
   double* h_orig;
   double* h_rel;
   double* h_tns;
+  // graph-captured iterations: the restart branch is the body of a
+  // conditional (IF) node that k_control switches on
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+  unsigned long long* tl;     // profiling only: iteration timeline (TlSlot)
+  int b_mtt;                  // b from the last mode's MTTKRP in k_finalize (3-way row-dot path)
 };
 
 __host__ __device__ inline long long lu_idx(const Ctx& c, int n, int g) {

@@ -18,6 +18,12 @@ struct XTables {
   int sb = 1;
   long long fib_rows = 0;    // max i2 rows of a fiber unit (A2 rows staged per CTA)
   long long slab_rows = 0;   // A0+A1 rows the slab kernel stages (0: read through L1)
+  // row-dot mode-2 kernel (xpass3.cuh): writes MTT[s] directly when set
+  int slab_direct = 0;
+  int s3_nslot = 0;
+  int s3_tma = 0;             // rows 16-B aligned: bulk-copy ring usable
+  long long s3_max_i0 = 1;
+  std::vector<int> s3_first;  // S+1
 };
 
 enum { PC_F64 = 0, PC_F32_F64 = 1, PC_F32 = 2 };

@@ -50,7 +50,7 @@ __host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
 
 // out[P x Q] = A^T B with A rows x P, B rows x Q (row-major), whole block,
 // fixed summation order over rows (deterministic).
-__device__ inline void block_gram(const double* __restrict__ A, int P, const double* __restrict__ B,
+static __device__ __noinline__ void block_gram(const double* __restrict__ A, int P, const double* __restrict__ B,
                            int Q, long long rows, double* __restrict__ out, const BlockSmem& sm) {
   double* As = sm.gr;
   double* Bs = sm.gr + 32 * sm.gw;
@@ -86,7 +86,7 @@ __device__ inline void block_gram(const double* __restrict__ A, int P, const dou
 // Hadamard product of the block's grams over modes != skip (mode order,
 // starting from ones: solver.py:352-358) times optional lam lam^T, into the
 // lam_max matrix slot (leading dim lm_ld(R)).  Returns via smem.
-__device__ inline void build_gram_product(const Ctx& c, int s, int skip, bool times_lamlam,
+static __device__ __noinline__ void build_gram_product(const Ctx& c, int s, int skip, bool times_lamlam,
                                    const BlockSmem& sm) {
   const int R = c.R[s];
   const int ld = lm_ld(R);
@@ -104,7 +104,7 @@ __device__ inline void build_gram_product(const Ctx& c, int s, int skip, bool ti
 
 // step(n) = (hadamard_{m != n} G) o lam lam^T, its lambda_max and the
 // Lipschitz history update (solver.py:402-406).
-__device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const BlockSmem& sm) {
+static __device__ __noinline__ void step_and_lipschitz(const Ctx& c, int s, int n, const BlockSmem& sm) {
   const int R = c.R[s];
   const int ld = lm_ld(R);
   PhaseClock pc;
@@ -130,7 +130,7 @@ __device__ inline void step_and_lipschitz(const Ctx& c, int s, int n, const Bloc
 
 // Final per-block quantities of an evaluation: model_sq = lam^T (had G) lam and
 // for lra inner = lam^T (had C)^T w~, res_t (solver.py:513-515).
-__device__ inline void final_quantities(const Ctx& c, int s, const BlockSmem& sm) {
+static __device__ __noinline__ void final_quantities(const Ctx& c, int s, const BlockSmem& sm) {
   const int R = c.R[s];
   const int ld = lm_ld(R);
   const double* lam = c.LAM[s];
@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(256) k_init_block(Ctx c) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
   if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_SWEEP);
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
   const int s = blockIdx.x;
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
   pc.start(c.dbg);
   step_and_lipschitz(c, s, 0, sm);
   pc.mark(c.dbg, 9);
+  tl_end(c.tl, TL_SWEEP);
 }
 
 // sum over all blocks (global order) of the mode-n Lipschitz constants and of
@@ -341,6 +343,7 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
 __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int src,
                                                       const RowUnit* __restrict__ units) {
   if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_MU + n);
   extern __shared__ double smd[];
   const RowUnit u = units[blockIdx.x];
   const int s = u.s;
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   }
   // sharded: the partials are all-reduced first; k_common folds them
   pc.mark(c.dbg, 7);
+  tl_end(c.tl, TL_MU + n);
   if (L == 0 || c.shard) return;
   __threadfence();
   __syncthreads();
@@ -462,6 +466,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   // last CTA of this row tile: sum the partials in block order (solver.py:444)
   common_fold(c, n, r0, rows, sumL, wc);
   pc.mark(c.dbg, 8);
+  tl_end(c.tl, TL_MU + n);
   if (threadIdx.x == 0) c.tile_cnt[r0 / MU_ROWS] = 0;
 }
 
@@ -469,6 +474,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
 // partials (grid: row tiles of mode n)
 __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
   if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_COMMON + n);
   const int L = c.counts[n];
   if (L == 0) return;
   const long long In = c.dims[n];   // the common rows are shared: I_n of block 0
@@ -484,6 +490,7 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
   }
   __syncthreads();
   common_fold(c, n, r0, rows, sc[0], sc[1]);
+  tl_end(c.tl, TL_COMMON + n);
 }
 
 // ---------------------------------------------------------------------------
@@ -495,6 +502,7 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
 // path runs concurrently with the next MTTKRP (they share no inputs)
 __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int with_step) {
   if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_FIN + n);
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
   const int s = blockIdx.x;
@@ -525,17 +533,32 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
       pc.mark(c.dbg, 2);
     }
   } else {
+    if (c.b_mtt) {
+      // staged core linear term b[r] = sum_i U_{N-1}[i, r] MTTKRP_{N-1}[i, r]
+      // (solver.py:506-509); warp per r, lanes over rows, fixed order
+      const double* M = c.MTT[s];
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      for (int r = wid; r < R; r += blockDim.x >> 5) {
+        double v = 0.0;
+        for (long long i = lane; i < In; i += 32) v = fma(Uc[i * R + r], M[i * R + r], v);
+        v = warp_sum(v);
+        if (lane == 0) c.fib_bpart[(long long)s * RSTRIDE + r] = v;
+      }
+    }
     final_quantities(c, s, sm);
     pc.mark(c.dbg, 3);
   }
+  tl_end(c.tl, TL_FIN + n);
 }
 
 // step matrix and Lipschitz constant of mode n for every block (solver.py:402-406)
 __global__ void __launch_bounds__(256) k_step(Ctx c, int n, int redo) {
   if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_STEP + n - 1);
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
   step_and_lipschitz(c, blockIdx.x, n, sm);
+  tl_end(c.tl, TL_STEP + n - 1);
 }
 
 // restore curr <- prev and refresh caches (solver.py:538-543)
@@ -760,6 +783,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
   const int fast_t = (bsrc == 0);
   const bool lra_cmp = c.lra && (mode == CTRL_DECIDE || mode == CTRL_REDO);
   const int T = c.S_tot;
+  tl_begin(c.tl, TL_CONTROL);
   if (phase & 1) {
     double* val = c.ctl_w;          // per-block residual (or compressed residual)
     double* relv = c.ctl_w + T;     // per-block relative error contribution
@@ -812,6 +836,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
       }
     }
   }
+  tl_end(c.tl, TL_CONTROL);
   if (!(phase & 2)) return;
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -834,6 +859,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
       st->n_restarts += 1;
       st->go_redo = 1;
+      if (c.use_cond) cudaGraphSetConditional(c.cond, 1u);   // run the restart branch
       return;
     }
     accept_and_advance(c, oi, oi, rel, fast_t);
@@ -847,6 +873,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
       st->n_restarts += 1;
       st->go_redo = 1;
+      if (c.use_cond) cudaGraphSetConditional(c.cond, 1u);
     }
     return;
   }

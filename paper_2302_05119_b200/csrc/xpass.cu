@@ -19,6 +19,7 @@
 #include "ops_internal.h"
 #include "status.h"
 #include "xpass2.cuh"
+#include "xpass3.cuh"
 
 namespace cb {
 
@@ -59,7 +60,8 @@ static void fib2_combo(bool tma, int want_t, int want_b, int want_res, const XAr
   // (T, B, RES) combinations used by the engines; T-only runs the RES variant
   if (want_t && want_b && want_res) fib2_go<TE, TC, RB, true, true, true>(tma, a, u, n, t, st);
   else if (want_t && want_b) fib2_go<TE, TC, RB, true, true, false>(tma, a, u, n, t, st);
-  else if (want_t) fib2_go<TE, TC, RB, true, false, true>(tma, a, u, n, t, st);
+  else if (want_t && want_res) fib2_go<TE, TC, RB, true, false, true>(tma, a, u, n, t, st);
+  else if (want_t) fib2_go<TE, TC, RB, true, false, false>(tma, a, u, n, t, st);
   else fib2_go<TE, TC, RB, false, true, false>(tma, a, u, n, t, st);
 }
 
@@ -77,7 +79,7 @@ static void fiber_dispatch(int pc, int rb, bool tma, int want_t, int want_b, int
 
 void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
-  const int combos[4][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {0, 1, 0}};
+  const int combos[5][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {1, 0, 0}, {0, 1, 0}};
   for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, t, 0);
 }
 
@@ -86,6 +88,44 @@ void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res
   if (n <= 0) return;
   fiber_dispatch(pc, rb, tma, want_t, want_b, want_res, a, u, n, t, st);
   count_launch(1);
+}
+
+template <typename TE, int RB>
+static void slab3_go(bool tma, const XArgs& a, const XTables& t, cudaStream_t st, bool prep) {
+  const int ntasks = t.s3_first.back();
+  const int S = (int)t.s3_first.size() - 1;
+  const int grid = std::max(1, std::min((ntasks + S3_WARPS - 1) / S3_WARPS, 148));
+  const int rows = slab3_rows(t.s3_max_i0, (int)sizeof(TE));
+  const size_t sm = tma ? slab3_smem(t.s3_max_i0, (int)sizeof(TE), rows) : 0;
+#define S3_LAUNCH(NS)                                                                            \
+  do {                                                                                           \
+    if (tma) {                                                                                   \
+      if (prep) {                                                                                \
+        cudaFuncSetAttribute(slab3_kernel<TE, RB, NS, S3_RING>,                                  \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);              \
+        return;                                                                                  \
+      }                                                                                          \
+      slab3_kernel<TE, RB, NS, S3_RING><<<grid, S3_WARPS * 32, sm, st>>>(a, a.s3_first, S, ntasks, \
+                                                                         rows);                  \
+    } else if (!prep) {                                                                          \
+      slab3_kernel<TE, RB, NS, 0><<<grid, S3_WARPS * 32, 0, st>>>(a, a.s3_first, S, ntasks, rows); \
+    }                                                                                            \
+  } while (0)
+  switch (t.s3_nslot) {
+    case 1: S3_LAUNCH(1); break;
+    case 2: S3_LAUNCH(2); break;
+    case 3: S3_LAUNCH(3); break;
+    default: S3_LAUNCH(4); break;
+  }
+#undef S3_LAUNCH
+}
+
+template <typename TE>
+static void slab3_dispatch(int rb, bool tma, const XArgs& a, const XTables& t, cudaStream_t st,
+                           bool prep) {
+  if (rb <= 8) slab3_go<TE, 8>(tma, a, t, st, prep);
+  else if (rb <= 12) slab3_go<TE, 12>(tma, a, t, st, prep);
+  else slab3_go<TE, 16>(tma, a, t, st, prep);
 }
 
 template <typename TE, typename TC, int RB>
@@ -113,11 +153,25 @@ static void slab_dispatch(int pc, int rb, bool tma, const XArgs& a, const SlabUn
 
 void prepare_slab(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
+  if (t.slab_direct) {
+    const bool ring = tma && t.s3_tma;
+    if (pc == PC_F64) slab3_dispatch<double>(rb, ring, a, t, 0, true);
+    else slab3_dispatch<float>(rb, ring, a, t, 0, true);
+    return;
+  }
   slab_dispatch(pc, rb, tma, a, nullptr, -1, t, 0);
 }
 
 void launch_slab(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, int n,
                  const XTables& t, cudaStream_t st) {
+  if (t.slab_direct) {
+    // fp64 arithmetic (the row-dot kernel has no fp32-arithmetic variant)
+    const bool ring = tma && t.s3_tma;
+    if (pc == PC_F64) slab3_dispatch<double>(rb, ring, a, t, st, false);
+    else slab3_dispatch<float>(rb, ring, a, t, st, false);
+    count_launch(1);
+    return;
+  }
   if (n <= 0) return;
   slab_dispatch(pc, rb, tma, a, u, n, t, st);
   count_launch(1);
@@ -207,6 +261,18 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   }
   const long long ring = 128 + (long long)S2_NST * tile * kc * pc_storage_bytes(pc);
   t.slab_rows = (ring + ab * rb * tcb <= 200 * 1024) ? ab : 0;
+  // row-dot mode-2 kernel where the shapes allow it (arithmetic always fp64)
+  t.slab_direct = (pc != PC_F32 && slab3_ok(S, dims, rb) && !getenv("CB_NO_SLAB3")) ? 1 : 0;
+  t.s3_nslot = slab3_nslot(S, dims);
+  t.s3_max_i0 = 1;
+  t.s3_tma = 1;
+  for (int s = 0; s < S; ++s) {
+    t.s3_max_i0 = std::max(t.s3_max_i0, dims[3 * s]);
+    // every row (and so every stage) 16-B aligned
+    if ((dims[3 * s] * pc_storage_bytes(pc)) % 16 != 0) t.s3_tma = 0;
+  }
+  t.s3_first.assign(S + 1, 0);
+  for (int s = 0; s < S; ++s) t.s3_first[s + 1] = t.s3_first[s] + (int)dims[3 * s + 2];
 }
 
 }  // namespace cb

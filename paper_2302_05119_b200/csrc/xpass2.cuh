@@ -81,6 +81,7 @@ fiber2_kernel(XArgs a, const FibUnit* __restrict__ units, int use_tma) {
   const int s = u.s;
   if (a.active && !a.active[s]) return;
   ktime_begin(a.ktime);
+  tl_begin(a.tl, TL_FIBER);
   const int R = a.R[s];
   const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1], I2 = a.dims[3 * s + 2];
   const long long J = I0 * I1;
@@ -280,6 +281,7 @@ fiber2_kernel(XArgs a, const FibUnit* __restrict__ units, int use_tma) {
     }
   }
   ktime_end(a.ktime);
+  tl_end(a.tl, TL_FIBER);
 }
 
 // ---------------------------------------------------------------------------
@@ -299,6 +301,7 @@ slab2_kernel(XArgs a, const SlabUnit* __restrict__ units, int use_tma) {
   const int s = u.s;
   if (a.active && !a.active[s]) return;
   ktime_begin(a.ktime ? a.ktime + 4 : nullptr);
+  tl_begin(a.tl, TL_SLAB);
   const int R = a.R[s];
   const long long I0 = a.dims[3 * s], I1 = a.dims[3 * s + 1], I2 = a.dims[3 * s + 2];
   const long long J = I0 * I1;
@@ -415,6 +418,7 @@ slab2_kernel(XArgs a, const SlabUnit* __restrict__ units, int use_tma) {
     __syncthreads();
   }
   ktime_end(a.ktime ? a.ktime + 4 : nullptr);
+  tl_end(a.tl, TL_SLAB);
 }
 
 }  // namespace cb
