@@ -460,6 +460,9 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       int* d_s3;
       TRY(upload(h->tab.s3_first, &d_s3, A, st));
       xa.s3_first = d_s3;
+      int* d_f3;
+      TRY(upload(h->tab.f3_first, &d_f3, A, st));
+      xa.f3_first = d_f3;
     }
     xa.fib_first = c.fib_first; xa.blk_cnt = blk_cnt; xa.bsum = bsum; xa.rsum = rsum;
   } else {

@@ -18,6 +18,13 @@
 
 namespace cb {
 
+// Programmatic dependent launch: kernels of the iteration are launched with
+// programmatic stream serialization, so a kernel's CTAs may be scheduled while
+// its predecessor drains; every kernel therefore waits here (first statement)
+// before touching anything the predecessor wrote.  A no-op for ordinary
+// launches.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Phase timestamps (profiling builds of a run: Ctx.dbg non-null): block 0
 // accumulates the time between consecutive PH() marks into dbg[slot].
 struct PhaseClock {

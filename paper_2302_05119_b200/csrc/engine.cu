@@ -18,6 +18,7 @@
 #include "ops_internal.h"
 #include "status.h"
 #include "engine_host.h"
+#include "launch.cuh"
 #include "nccl_shim.h"
 
 namespace cb {
@@ -255,7 +256,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
     if ((rc = enqueue_mttkrp3(h, 0, xa, redo, h->st2))) return rc;
   }
   if (emit(h)) {
-    k_sweep_begin<<<h->S, 256, h->blk_smem, st>>>(h->ctx, redo);
+    launch_k(k_sweep_begin, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, redo);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -277,7 +278,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       prof(h, "generic_mttkrp");
     }
     if (emit(h)) {
-      k_mode_update<<<h->n_rows[n], 256, h->mu_smem, st>>>(h->ctx, n, redo, src, h->d_rows[n]);
+      launch_k(k_mode_update, dim3(h->n_rows[n]), dim3(256), h->mu_smem, st, h->ctx, n, redo, src, h->d_rows[n]);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
@@ -286,7 +287,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       if ((rc = xchg_gc(h, n))) return rc;
       if (emit(h)) {
         const int tiles = (int)((h->dims[n] + MU_ROWS - 1) / MU_ROWS);
-        k_common<<<tiles, 256, 0, st>>>(h->ctx, n, redo);
+        launch_k(k_common, dim3(tiles), dim3(256), 0, st, h->ctx, n, redo);
         count_launch(1);
         CB_CHECK_LAUNCH();
       }
@@ -294,7 +295,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
     }
     const bool split = par && n + 1 < h->N;
     if (emit(h)) {
-      k_finalize<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n, redo, split ? 0 : 1);
+      launch_k(k_finalize, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, n, redo, split ? 0 : 1);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
@@ -303,7 +304,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       if ((rc = fork_side(h))) return rc;
       if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
       if (emit(h)) {
-        k_step<<<h->S, 256, h->blk_smem, st>>>(h->ctx, n + 1, redo);
+        launch_k(k_step, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, n + 1, redo);
         count_launch(1);
         CB_CHECK_LAUNCH();
       }
@@ -317,9 +318,9 @@ static int enqueue_sweep(cb_solver* h, int redo) {
 
 static int enqueue_qr(cb_solver* h, int redo) {
   if (!emit(h)) return CB_OK;
-  k_qr_factor<<<h->S * h->N, 256, h->qr_smem, h->st>>>(h->ctx, redo);
+  launch_k(k_qr_factor, dim3(h->S * h->N), dim3(256), h->qr_smem, h->st, h->ctx, redo);
   prof(h, redo ? "redo:qr_factor" : "qr_factor");
-  k_qr_core<<<h->S * h->ctx.qr_nchunks, 256, 0, h->st>>>(h->ctx, redo);
+  launch_k(k_qr_core, dim3(h->S * h->ctx.qr_nchunks), dim3(256), 0, h->st, h->ctx, redo);
   prof(h, redo ? "redo:qr_core" : "qr_core");
   count_launch(2);
   CB_CHECK_LAUNCH();
@@ -330,7 +331,7 @@ static int enqueue_control(cb_solver* h, int mode) {
   const int bsrc = h->fast3 ? 0 : 1;
   if (!h->shard) {
     if (emit(h)) {
-      k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 3);
+      launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 3);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
@@ -338,14 +339,14 @@ static int enqueue_control(cb_solver* h, int mode) {
     return CB_OK;
   }
   if (emit(h)) {
-    k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 1);
+    launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 1);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
   int rc = xchg(h, h->ctx.ctl_w, h->ctx.ctl, 3LL * h->S_tot);
   if (rc) return rc;
   if (emit(h)) {
-    k_control<<<1, 256, 0, h->st>>>(h->ctx, mode, bsrc, 2);
+    launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 2);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -355,7 +356,7 @@ static int enqueue_control(cb_solver* h, int mode) {
 
 static int enqueue_restore(cb_solver* h) {
   if (emit(h)) {
-    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -478,7 +479,7 @@ static int generic_iteration(cb_solver* h) {
   if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
   if ((rc = read_state(h))) return rc;
   if (h->h_state->go_redo) {
-    k_restore<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx);
     count_launch(1);
     CB_CHECK_LAUNCH();
     if ((rc = enqueue_sweep(h, 1))) return rc;
@@ -525,7 +526,7 @@ static int generic_residuals(cb_solver* h) {
 static int init_evaluation(cb_solver* h) {
   int rc;
   if (emit(h)) {
-    k_init_block<<<h->S, 256, h->blk_smem, h->st>>>(h->ctx);
+    launch_k(k_init_block, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -821,6 +822,9 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       int* d_s3;
       TRY(upload(h->tab.s3_first, &d_s3, A, st));
       xa.s3_first = d_s3;
+      int* d_f3;
+      TRY(upload(h->tab.f3_first, &d_f3, A, st));
+      xa.f3_first = d_f3;
     }
     // with the row-dot mode-2 kernel, the core linear term b is staged from
     // its MTTKRP output (solver.py:506-509) in k_finalize of the last mode,
@@ -1160,7 +1164,7 @@ int cb_group_step(cb_solver* const* hs, int n, int program) {
         a.recv[k] = hs[k]->pending[x].recv;
       }
       const int blocks = (int)std::min<long long>(148 * 4, (a.count + 255) / 256);
-      k_xsum<<<std::max(blocks, 1), 256, 0, hs[0]->st>>>(a);
+      launch_k(k_xsum, dim3(std::max(blocks, 1)), dim3(256), 0, hs[0]->st, a);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }

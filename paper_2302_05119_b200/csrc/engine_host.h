@@ -16,6 +16,7 @@ struct XTables {
   std::vector<int> slab_nchunk; // S
   std::vector<RowUnit> c0, c1;
   int sb = 1;
+  int fib_tj = 1;             // fiber tile: columns per thread (JT = 256 * fib_tj)
   long long fib_rows = 0;    // max i2 rows of a fiber unit (A2 rows staged per CTA)
   long long slab_rows = 0;   // A0+A1 rows the slab kernel stages (0: read through L1)
   // row-dot mode-2 kernel (xpass3.cuh): writes MTT[s] directly when set
@@ -23,7 +24,14 @@ struct XTables {
   int s3_nslot = 0;
   int s3_tma = 0;             // rows 16-B aligned: bulk-copy ring usable
   long long s3_max_i0 = 1;
+  long long s3_a1_rows = 1;
   std::vector<int> s3_first;  // S+1
+  // warp-task T pass (xpass3.cuh fiber3_kernel) for T-only fiber launches
+  int fiber_direct = 0;
+  int f3_rb = 16;             // exact small rank bucket of the T pass (8, 10, 12, 16)
+  int f3_tma = 0;
+  long long f3_a2_rows = 1;
+  std::vector<int> f3_first;  // S+1 cumulative I1 (task ranges)
 };
 
 enum { PC_F64 = 0, PC_F32_F64 = 1, PC_F32 = 2 };

@@ -179,6 +179,7 @@ static __device__ __noinline__ void final_quantities(const Ctx& c, int s, const 
 // init: grams, cross grams, ||M~||^2, Lipschitz histories unset
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_init_block(Ctx c) {
+  griddep_wait();
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
   const int s = blockIdx.x;
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(256) k_init_block(Ctx c) {
 // sweep begin: core update (solver.py:375-395) and the mode-0 step matrix
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_SWEEP);
   extern __shared__ double smd[];
@@ -342,6 +344,7 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int src,
                                                       const RowUnit* __restrict__ units) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_MU + n);
   extern __shared__ double smd[];
@@ -473,6 +476,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
 // sharded runs: new common columns of one row tile from the all-reduced
 // partials (grid: row tiles of mode n)
 __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_COMMON + n);
   const int L = c.counts[n];
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
 // with_step = 0: the next mode's step matrix is left to k_step, which the 3-way
 // path runs concurrently with the next MTTKRP (they share no inputs)
 __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int with_step) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_FIN + n);
   extern __shared__ double smd[];
@@ -553,6 +558,7 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
 
 // step matrix and Lipschitz constant of mode n for every block (solver.py:402-406)
 __global__ void __launch_bounds__(256) k_step(Ctx c, int n, int redo) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_STEP + n - 1);
   extern __shared__ double smd[];
@@ -563,6 +569,7 @@ __global__ void __launch_bounds__(256) k_step(Ctx c, int n, int redo) {
 
 // restore curr <- prev and refresh caches (solver.py:538-543)
 __global__ void __launch_bounds__(256) k_restore(Ctx c) {
+  griddep_wait();
   if (c.st->go_redo == 0) return;
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
@@ -594,6 +601,7 @@ __device__ __forceinline__ bool qr_route_needed(const Ctx& c, int s) {
 }
 
 __global__ void __launch_bounds__(256) k_qr_factor(Ctx c, int redo) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   const int s = blockIdx.x / c.N;
   const int n = blockIdx.x - s * c.N;
@@ -669,6 +677,7 @@ __global__ void __launch_bounds__(256) k_qr_factor(Ctx c, int redo) {
 // ||core||^2 with core[a_0..a_{N-1}] = sum_q wts[q] prod_m Rm[a_m, q],
 // wts = [w~, -lam] (solver.py:476-482).  Grid: S * qr_nchunks.
 __global__ void __launch_bounds__(256) k_qr_core(Ctx c, int redo) {
+  griddep_wait();
   if (stopped(c, redo)) return;
   const int s = blockIdx.x / c.qr_nchunks;
   const int ch = blockIdx.x - s * c.qr_nchunks;
@@ -776,6 +785,7 @@ __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double o
 // runs all-reduce ctl_w into ctl between them, so every rank folds the same
 // values and takes the same decisions.
 __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int phase) {
+  griddep_wait();
   State* st = c.st;
   if (st->done) return;
   if (mode == CTRL_REDO && !st->go_redo) return;
@@ -911,6 +921,7 @@ struct XsumArgs {
 };
 
 __global__ void __launch_bounds__(256) k_xsum(XsumArgs a) {
+  griddep_wait();
   for (long long e = blockIdx.x * 256LL + threadIdx.x; e < a.count; e += (long long)gridDim.x * 256) {
     double v = 0.0;
     for (int k = 0; k < a.n; ++k) v += a.send[k][e];

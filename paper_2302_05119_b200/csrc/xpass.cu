@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "engine_host.h"
+#include "launch.cuh"
 #include "ops_internal.h"
 #include "status.h"
 #include "xpass2.cuh"
@@ -42,16 +43,29 @@ static int pc_storage_bytes(int pc) { return pc == PC_F64 ? 8 : 4; }
   }
 
 // n < 0: set the dynamic shared-memory attribute (call outside graph capture)
-template <typename TE, typename TC, int RB, bool T, bool B, bool S>
-static void fib2_go(bool tma, const XArgs& a, const FibUnit* u, int n, const XTables& t,
-                    cudaStream_t st) {
-  const size_t sm = fiber2_smem<TE, TC, RB>(t.fib_rows);
+template <typename TE, typename TC, int RB, bool T, bool B, bool S, int TJ>
+static void fib2_go_tj(bool tma, const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                       cudaStream_t st) {
+  const size_t sm = fiber2_smem<TE, TC, RB>(t.fib_rows, TJ);
   if (n < 0) {
-    cudaFuncSetAttribute(fiber2_kernel<TE, TC, RB, T, B, S>,
+    cudaFuncSetAttribute(fiber2_kernel<TE, TC, RB, T, B, S, TJ>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     return;
   }
-  fiber2_kernel<TE, TC, RB, T, B, S><<<n, X2_THREADS, sm, st>>>(a, u, tma ? 1 : 0);
+  launch_k(fiber2_kernel<TE, TC, RB, T, B, S, TJ>, dim3(n), dim3(X2_THREADS), sm, st, a, u,
+           tma ? 1 : 0);
+}
+
+// the fiber tile TJ (columns per thread) is chosen by build_xtables: the
+// register-budget default x2_tile, halved when that leaves SMs idle
+template <typename TE, typename TC, int RB, bool T, bool B, bool S>
+static void fib2_go(bool tma, const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                    cudaStream_t st) {
+  constexpr int TD = x2_tile(RB, sizeof(TC));
+  if (t.fib_tj == TD) fib2_go_tj<TE, TC, RB, T, B, S, TD>(tma, a, u, n, t, st);
+  else if (TD >= 2 && t.fib_tj == (TD >= 2 ? TD / 2 : 1))
+    fib2_go_tj<TE, TC, RB, T, B, S, (TD >= 2 ? TD / 2 : 1)>(tma, a, u, n, t, st);
+  else fib2_go_tj<TE, TC, RB, T, B, S, 1>(tma, a, u, n, t, st);
 }
 
 template <typename TE, typename TC, int RB>
@@ -77,14 +91,53 @@ static void fiber_dispatch(int pc, int rb, bool tma, int want_t, int want_b, int
   }
 }
 
+template <typename TE, int RB>
+static void fiber3_go(bool tma, const XArgs& a, const XTables& t, cudaStream_t st, bool prep) {
+  (void)tma;
+  const int ntasks = t.f3_first.back();
+  const int S = (int)t.f3_first.size() - 1;
+  const int grid = std::max(1, std::min((ntasks + F3_WARPS - 1) / F3_WARPS, 148 * 2));
+  const int a2r = (int)t.f3_a2_rows;
+  const size_t sm = fiber3_smem(a2r, RB);
+  if (prep) {
+    cudaFuncSetAttribute(fiber3_kernel<TE, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    return;
+  }
+  launch_k(fiber3_kernel<TE, RB>, dim3(grid), dim3(F3_WARPS * 32), sm, st, a, a.f3_first, S,
+           ntasks, a2r);
+}
+
+template <typename TE>
+static void fiber3_dispatch(int rb, bool tma, const XArgs& a, const XTables& t, cudaStream_t st,
+                            bool prep) {
+  if (rb <= 8) fiber3_go<TE, 8>(tma, a, t, st, prep);
+  else if (rb <= 10) fiber3_go<TE, 10>(tma, a, t, st, prep);
+  else if (rb <= 12) fiber3_go<TE, 12>(tma, a, t, st, prep);
+  else fiber3_go<TE, 16>(tma, a, t, st, prep);
+}
+
 void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
+  if (t.fiber_direct) {
+    const bool ring = tma && t.f3_tma;
+    if (pc == PC_F64) fiber3_dispatch<double>(t.f3_rb, ring, a, t, 0, true);
+    else fiber3_dispatch<float>(t.f3_rb, ring, a, t, 0, true);
+  }
   const int combos[5][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {1, 0, 0}, {0, 1, 0}};
   for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, t, 0);
 }
 
 void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, const XTables& t, cudaStream_t st) {
+  static const bool f3_on = getenv("CB_F3_ON") != nullptr;
+  if (want_t && !want_b && !want_res && t.fiber_direct && f3_on) {
+    const bool ring = tma && t.f3_tma;
+    if (pc == PC_F64) fiber3_dispatch<double>(t.f3_rb, ring, a, t, st, false);
+    else fiber3_dispatch<float>(t.f3_rb, ring, a, t, st, false);
+    count_launch(1);
+    return;
+  }
   if (n <= 0) return;
   fiber_dispatch(pc, rb, tma, want_t, want_b, want_res, a, u, n, t, st);
   count_launch(1);
@@ -94,9 +147,10 @@ template <typename TE, int RB>
 static void slab3_go(bool tma, const XArgs& a, const XTables& t, cudaStream_t st, bool prep) {
   const int ntasks = t.s3_first.back();
   const int S = (int)t.s3_first.size() - 1;
-  const int grid = std::max(1, std::min((ntasks + S3_WARPS - 1) / S3_WARPS, 148));
+  const int grid = std::max(1, std::min((ntasks + S3_WARPS - 1) / S3_WARPS, 148 * 4));
   const int rows = slab3_rows(t.s3_max_i0, (int)sizeof(TE));
-  const size_t sm = tma ? slab3_smem(t.s3_max_i0, (int)sizeof(TE), rows) : 0;
+  const int a1r = (int)t.s3_a1_rows;
+  const size_t sm = slab3_smem(t.s3_max_i0, (int)sizeof(TE), rows, a1r, RB, tma);
 #define S3_LAUNCH(NS)                                                                            \
   do {                                                                                           \
     if (tma) {                                                                                   \
@@ -105,10 +159,16 @@ static void slab3_go(bool tma, const XArgs& a, const XTables& t, cudaStream_t st
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);              \
         return;                                                                                  \
       }                                                                                          \
-      slab3_kernel<TE, RB, NS, S3_RING><<<grid, S3_WARPS * 32, sm, st>>>(a, a.s3_first, S, ntasks, \
-                                                                         rows);                  \
-    } else if (!prep) {                                                                          \
-      slab3_kernel<TE, RB, NS, 0><<<grid, S3_WARPS * 32, 0, st>>>(a, a.s3_first, S, ntasks, rows); \
+      launch_k(slab3_kernel<TE, RB, NS, S3_RING>, dim3(grid), dim3(S3_WARPS * 32), sm, st, a,    \
+               a.s3_first, S, ntasks, rows, a1r);                                                \
+    } else {                                                                                     \
+      if (prep) {                                                                                \
+        cudaFuncSetAttribute(slab3_kernel<TE, RB, NS, 0>,                                        \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);              \
+        return;                                                                                  \
+      }                                                                                          \
+      launch_k(slab3_kernel<TE, RB, NS, 0>, dim3(grid), dim3(S3_WARPS * 32), sm, st, a,          \
+               a.s3_first, S, ntasks, rows, a1r);                                                \
     }                                                                                            \
   } while (0)
   switch (t.s3_nslot) {
@@ -124,6 +184,7 @@ template <typename TE>
 static void slab3_dispatch(int rb, bool tma, const XArgs& a, const XTables& t, cudaStream_t st,
                            bool prep) {
   if (rb <= 8) slab3_go<TE, 8>(tma, a, t, st, prep);
+  else if (rb <= 10) slab3_go<TE, 10>(tma, a, t, st, prep);
   else if (rb <= 12) slab3_go<TE, 12>(tma, a, t, st, prep);
   else slab3_go<TE, 16>(tma, a, t, st, prep);
 }
@@ -137,7 +198,7 @@ static void slab2_go(bool tma, const XArgs& a, const SlabUnit* u, int n, const X
                          (int)sm);
     return;
   }
-  slab2_kernel<TE, TC, RB><<<n, X2_THREADS, sm, st>>>(a, u, tma ? 1 : 0);
+  launch_k(slab2_kernel<TE, TC, RB>, dim3(n), dim3(X2_THREADS), sm, st, a, u, tma ? 1 : 0);
 }
 
 static void slab_dispatch(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, int n,
@@ -155,8 +216,8 @@ void prepare_slab(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
   if (t.slab_direct) {
     const bool ring = tma && t.s3_tma;
-    if (pc == PC_F64) slab3_dispatch<double>(rb, ring, a, t, 0, true);
-    else slab3_dispatch<float>(rb, ring, a, t, 0, true);
+    if (pc == PC_F64) slab3_dispatch<double>(t.f3_rb, ring, a, t, 0, true);
+    else slab3_dispatch<float>(t.f3_rb, ring, a, t, 0, true);
     return;
   }
   slab_dispatch(pc, rb, tma, a, nullptr, -1, t, 0);
@@ -167,8 +228,8 @@ void launch_slab(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, in
   if (t.slab_direct) {
     // fp64 arithmetic (the row-dot kernel has no fp32-arithmetic variant)
     const bool ring = tma && t.s3_tma;
-    if (pc == PC_F64) slab3_dispatch<double>(rb, ring, a, t, st, false);
-    else slab3_dispatch<float>(rb, ring, a, t, st, false);
+    if (pc == PC_F64) slab3_dispatch<double>(t.f3_rb, ring, a, t, st, false);
+    else slab3_dispatch<float>(t.f3_rb, ring, a, t, st, false);
     count_launch(1);
     return;
   }
@@ -182,11 +243,11 @@ void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
   if (n <= 0) return;
   const bool tf = pc == PC_F32;   // T is stored in the fiber pass arithmetic type
   if (mode == 0) {
-    if (tf) contract0_kernel<float><<<n, 256, 0, st>>>(a, u);
-    else contract0_kernel<double><<<n, 256, 0, st>>>(a, u);
+    if (tf) launch_k(contract0_kernel<float>, dim3(n), dim3(256), 0, st, a, u);
+    else launch_k(contract0_kernel<double>, dim3(n), dim3(256), 0, st, a, u);
   } else {
-    if (tf) contract1_kernel<float><<<n, 256, 0, st>>>(a, u);
-    else contract1_kernel<double><<<n, 256, 0, st>>>(a, u);
+    if (tf) launch_k(contract1_kernel<float>, dim3(n), dim3(256), 0, st, a, u);
+    else launch_k(contract1_kernel<double>, dim3(n), dim3(256), 0, st, a, u);
   }
   count_launch(1);
 }
@@ -209,14 +270,54 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   const int tcb = pc_compute_bytes(pc);
   const int tile = x2_tile(rb, tcb);
   const long long target_per_block = (148LL * 2 + s_total - 1) / std::max(s_total, 1);
+  // warp-task T pass (xpass3.cuh) where the shapes allow it; it writes T
+  // unsplit, so every T producer then uses nsplit = 1
+  {
+    long long a2r = 1;
+    for (int s = 0; s < S; ++s) a2r = std::max(a2r, dims[3 * s + 2]);
+    t.f3_a2_rows = a2r;
+    int rmax = 1;
+    for (int s = 0; s < S; ++s) rmax = std::max(rmax, R[s]);
+    t.f3_rb = rmax <= 8 ? 8 : rmax <= 10 ? 10 : rmax <= 12 ? 12 : 16;
+    // pair loads / stores need even J; A2 copies must fit (2 CTAs per SM)
+    bool even = true;
+    for (int s = 0; s < S; ++s) even = even && (dims[3 * s] * dims[3 * s + 1]) % 2 == 0;
+    const int f3rb = rmax <= 8 ? 8 : rmax <= 10 ? 10 : rmax <= 12 ? 12 : 16;
+    t.fiber_direct = (pc != PC_F32 && rmax <= 16 && even &&
+                      fiber3_smem(a2r, f3rb) <= 96 * 1024 && !getenv("CB_NO_FIBER3")) ? 1 : 0;
+    t.f3_first.assign(S + 1, 0);
+    for (int s = 0; s < S; ++s) {
+      const long long J = dims[3 * s] * dims[3 * s + 1];
+      t.f3_first[s + 1] = t.f3_first[s] + (int)((J + F3_CH - 1) / F3_CH);
+    }
+  }
   t.fib.clear(); t.fib_first.assign(S + 1, 0); t.nsplit.assign(S, 1);
-  const long long JT = (long long)X2_THREADS * tile;
+  // fiber tile: halve TJ while the unsplit (nsplit 1) decomposition leaves SMs idle
+  {
+    int tj = tile;
+    long long units = 0;
+    auto count = [&](int tjv) {
+      long long u = 0;
+      for (int s = 0; s < S; ++s) {
+        const long long J = dims[3 * s] * dims[3 * s + 1];
+        u += (J + (long long)X2_THREADS * tjv - 1) / ((long long)X2_THREADS * tjv);
+      }
+      return u;
+    };
+    units = count(tj);
+    // (halving measured slower on c2: TJ 2 with 200 units 50 us vs TJ 4 with
+    // 100 units 34 us; opt-in for experiments)
+    static const bool halve = getenv("CB_FIB_HALVE") != nullptr;
+    while (halve && t.fiber_direct && tj > 1 && units < 148) { tj /= 2; units = count(tj); }
+    t.fib_tj = tj;
+  }
+  const long long JT = (long long)X2_THREADS * t.fib_tj;
   for (int s = 0; s < S; ++s) {
     const long long J = dims[3 * s] * dims[3 * s + 1];
     const long long I2 = dims[3 * s + 2];
     const long long tiles = (J + JT - 1) / JT;
     int ns = 1;
-    while (tiles * ns < target_per_block && I2 / (ns * 2) >= 2 * F2_CH) ns *= 2;
+    while (!t.fiber_direct && tiles * ns < target_per_block && I2 / (ns * 2) >= 2 * F2_CH) ns *= 2;
     t.nsplit[s] = ns;
     t.fib_first[s] = (int)t.fib.size();
     for (int sp = 0; sp < ns; ++sp)
@@ -264,6 +365,10 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   // row-dot mode-2 kernel where the shapes allow it (arithmetic always fp64)
   t.slab_direct = (pc != PC_F32 && slab3_ok(S, dims, rb) && !getenv("CB_NO_SLAB3")) ? 1 : 0;
   t.s3_nslot = slab3_nslot(S, dims);
+  t.s3_a1_rows = 1;
+  for (int s = 0; s < S; ++s) t.s3_a1_rows = std::max(t.s3_a1_rows, dims[3 * s + 1]);
+  // per-warp A1 copies must fit beside the ring
+  if ((size_t)S3_WARPS * t.s3_a1_rows * t.f3_rb * 8 > 96 * 1024) t.slab_direct = 0;
   t.s3_max_i0 = 1;
   t.s3_tma = 1;
   for (int s = 0; s < S; ++s) {

@@ -61,6 +61,7 @@ struct XArgs {
   unsigned long long* tl;        // profiling only: iteration timeline (TlSlot)
   long long slab_stage_rows;     // factor rows the slab kernel may stage in smem (0: none)
   const int* s3_first;           // slab3: S+1 cumulative slab counts (task ranges)
+  const int* f3_first;           // fiber3: S+1 cumulative fiber-row counts
 };
 
 // In-kernel wall time of a whole launch (first CTA start -> last CTA end),
@@ -119,6 +120,7 @@ __device__ __forceinline__ void* tbuf(const XArgs& a, int s) {
 template <typename TE>
 __global__ void __launch_bounds__(256)
 contract0_kernel(XArgs a, const RowUnit* __restrict__ units) {
+  griddep_wait();
   if (gated(a)) return;
   const RowUnit u = units[blockIdx.x];
   const int s = u.s;
@@ -156,6 +158,7 @@ contract0_kernel(XArgs a, const RowUnit* __restrict__ units) {
 template <typename TE>
 __global__ void __launch_bounds__(256)
 contract1_kernel(XArgs a, const RowUnit* __restrict__ units) {
+  griddep_wait();
   if (gated(a)) return;
   const RowUnit u = units[blockIdx.x];
   const int s = u.s;

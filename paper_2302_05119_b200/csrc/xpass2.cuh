@@ -32,8 +32,8 @@ __host__ __device__ constexpr int x2_tile(int rb, int tc_bytes) {
 
 // dynamic smem: X ring + the unit's A2 rows (max_rows x RB, TC), staged once
 template <typename TE, typename TC, int RB>
-__host__ __device__ constexpr size_t fiber2_smem(long long max_rows) {
-  return 128 + (size_t)F2_NST * F2_CH * X2_THREADS * x2_tile(RB, sizeof(TC)) * sizeof(TE) +
+__host__ __device__ constexpr size_t fiber2_smem(long long max_rows, int tj) {
+  return 128 + (size_t)F2_NST * F2_CH * X2_THREADS * tj * sizeof(TE) +
          (size_t)max_rows * RB * sizeof(TC);
 }
 
@@ -71,10 +71,11 @@ __device__ __forceinline__ void load_row(const TC* __restrict__ p, TC (&v)[RB]) 
 // ---------------------------------------------------------------------------
 // fiber pass, unit = (block, i2 split, j-tile of 256*TJ columns)
 // ---------------------------------------------------------------------------
-template <typename TE, typename TC, int RB, bool STORE_T, bool WANT_B, bool WANT_RES>
+template <typename TE, typename TC, int RB, bool STORE_T, bool WANT_B, bool WANT_RES, int TJ_>
 __global__ void __launch_bounds__(X2_THREADS)
 fiber2_kernel(XArgs a, const FibUnit* __restrict__ units, int use_tma) {
-  constexpr int TJ = x2_tile(RB, sizeof(TC));
+  griddep_wait();
+  constexpr int TJ = TJ_;
   constexpr int JT = X2_THREADS * TJ;
   if (gated(a)) return;
   const FibUnit u = units[blockIdx.x];
@@ -293,6 +294,7 @@ fiber2_kernel(XArgs a, const FibUnit* __restrict__ units, int use_tma) {
 template <typename TE, typename TC, int RB>
 __global__ void __launch_bounds__(X2_THREADS)
 slab2_kernel(XArgs a, const SlabUnit* __restrict__ units, int use_tma) {
+  griddep_wait();
   constexpr int TM = x2_tile(RB, sizeof(TC));
   constexpr int S2_KC = s2_kc(RB, sizeof(TC));
   constexpr int PER_T = S2_KC / X2_THREADS;   // j per thread per stage

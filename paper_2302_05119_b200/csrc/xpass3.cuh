@@ -20,7 +20,7 @@
 
 namespace cb {
 
-constexpr int S3_WARPS = 8;
+constexpr int S3_WARPS = 4;
 constexpr int S3_HDR = 256;  // mbarriers: S3_WARPS x ring slots (<= 4) x 8 B
 constexpr int S3_PD = 3;    // rows prefetched ahead per warp
 
@@ -49,13 +49,18 @@ __device__ __forceinline__ double warp_fold(double (&v)[VP], int lane) {
 }
 
 // tasks: global slab index t in [0, ntasks); block s owns [task_first[s], task_first[s+1]).
-// RING > 0: each warp streams its task's rows (one contiguous span of X)
-// through a private RING-stage shared-memory ring of `rows` rows per stage,
-// filled by 1-D bulk copies issued by lane 0 (needs 16-B aligned rows);
-// RING == 0: rows are prefetched S3_PD deep into registers with __ldg.
+// Per task the lane accumulates, over the I1 rows, acc[k][r] += x[i0_k] A1[i1, r]
+// (A1 row: broadcast L1 read, prefetched one row ahead); at the end of the
+// task it forms v[r] = sum_k A0[i0_k, r] acc[k][r] and folds v across the warp
+// once.  RING > 0: the task's rows (one contiguous span of X) stream through a
+// private RING-stage shared-memory ring of `rows` rows per stage, one bulk
+// copy per stage issued by lane 0 (needs 16-B aligned rows); RING == 0: rows
+// are prefetched S3_PD deep into registers with __ldg.
 template <typename TE, int RB, int NSLOT, int RING>
-__global__ void __launch_bounds__(S3_WARPS * 32, 1)
-slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int rows) {
+__global__ void __launch_bounds__(S3_WARPS * 32, 3)
+slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int rows,
+             int a1_rows) {
+  griddep_wait();
   if (gated(a)) return;
   tl_begin(a.tl, TL_SLAB);
   constexpr int VP = s3_vp(RB);
@@ -65,15 +70,17 @@ slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int
   const bool writer = (lane & ((32 / VP) - 1)) == 0;
   extern __shared__ __align__(128) unsigned char s3sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(s3sm) + warp * (RING > 0 ? RING : 1);
+  // per warp: A1 copy [a1_rows][RB] (fp64, zero-padded), then the X ring
+  double* a1s = reinterpret_cast<double*>(s3sm + S3_HDR) + (size_t)warp * a1_rows * RB;
+  TE* ring_base = reinterpret_cast<TE*>(reinterpret_cast<double*>(s3sm + S3_HDR) +
+                                        (size_t)S3_WARPS * a1_rows * RB);
   int cur = -1;
-  double a0[NSLOT][RB];
   const TE* X = nullptr;
-  const double* A1 = nullptr;
+  const double* A0 = nullptr;
   long long I0 = 0, J = 0;
   int I1 = 0, R = 0;
   int s = 0;
   uint32_t phase_bits = 0;      // RING: parity per ring slot
-  TE* ring = nullptr;
   if constexpr (RING > 0) {
     if (lane == 0)
       for (int q = 0; q < RING; ++q) mbar_init(&bar[q], 1);
@@ -90,21 +97,37 @@ slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int
       I1 = (int)a.dims[3 * s + 1];
       J = I0 * I1;
       X = reinterpret_cast<const TE*>(a.X[s]);
-      A1 = a.U[3 * s + 1];
-      const double* A0 = a.U[3 * s];
-#pragma unroll
-      for (int k = 0; k < NSLOT; ++k) {
-        const long long i0 = lane + 32 * k;
-#pragma unroll
-        for (int r = 0; r < RB; ++r) a0[k][r] = (i0 < I0 && r < R) ? __ldg(A0 + i0 * R + r) : 0.0;
+      A0 = a.U[3 * s];
+      const double* A1 = a.U[3 * s + 1];
+      __syncwarp();
+      for (long long e = lane; e < (long long)I1 * RB; e += 32) {
+        const long long q = e / RB;
+        const int r = (int)(e - q * RB);
+        a1s[e] = r < R ? __ldg(A1 + q * R + r) : 0.0;
       }
+      __syncwarp();
     }
     const long long i2 = t - task_first[s];
     const TE* xs = X + i2 * J;
-    double acc = 0.0;
+    double acc[NSLOT][RB];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[k][r] = 0.0;
+    auto row = [&](const TE* xr, int i1, bool from_ring) {
+      double an[RB];            // A1 row (broadcast shared-memory read)
+      load_row<double, RB>(a1s + (size_t)i1 * RB, an);
+#pragma unroll
+      for (int k = 0; k < NSLOT; ++k) {
+        const long long i0 = lane + 32 * k;
+        const double x = i0 < I0 ? (double)(from_ring ? xr[i0] : __ldg(xr + i0)) : 0.0;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[k][r] = fma(x, an[r], acc[k][r]);
+      }
+    };
     if constexpr (RING > 0) {
       const long long stage_elems = (long long)rows * I0;
-      ring = reinterpret_cast<TE*>(s3sm + S3_HDR) + (size_t)warp * RING * stage_elems;
+      TE* ring = ring_base + (size_t)warp * RING * stage_elems;
       const int nst = (I1 + rows - 1) / rows;
       auto issue = [&](int k) {
         const int q = k % RING;
@@ -116,7 +139,6 @@ slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int
       };
       if (lane == 0)
         for (int k = 0; k < nst && k < RING; ++k) issue(k);
-      double a1n = (vi < R && I1 > 0) ? __ldg(A1 + vi) : 0.0;
       for (int k = 0; k < nst; ++k) {
         const int q = k % RING;
         mbar_wait(&bar[q], (phase_bits >> q) & 1u);
@@ -124,23 +146,7 @@ slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int
         const TE* xr = ring + (size_t)q * stage_elems;
         const int r0 = k * rows;
         const int nr = I1 - r0 < rows ? I1 - r0 : rows;
-        for (int rr = 0; rr < nr; ++rr) {
-          const int i1 = r0 + rr;
-          double v[VP];
-#pragma unroll
-          for (int r = 0; r < VP; ++r) v[r] = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < NSLOT; ++kk) {
-            const long long i0 = lane + 32 * kk;
-            const double x = i0 < I0 ? (double)xr[rr * I0 + i0] : 0.0;
-#pragma unroll
-            for (int r = 0; r < RB; ++r) v[r] = fma(x, a0[kk][r], v[r]);
-          }
-          const double a1 = a1n;
-          a1n = (vi < R && i1 + 1 < I1) ? __ldg(A1 + (long long)(i1 + 1) * R + vi) : 0.0;
-          const double w = warp_fold<VP>(v, lane);
-          acc = fma(w, a1, acc);
-        }
+        for (int rr = 0; rr < nr; ++rr) row(xr + (size_t)rr * I0, r0 + rr, true);
         __syncwarp();   // slot consumed by every lane
         if (lane == 0 && k + RING < nst) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -148,59 +154,147 @@ slab3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int
         }
       }
     } else {
-      TE xb[S3_PD][NSLOT];
-      double a1b[S3_PD];
+      for (int i1 = 0; i1 < I1; ++i1) row(xs + (long long)i1 * I0, i1, false);
+    }
+    // v[r] = sum_k A0[i0_k, r] acc[k][r], then one warp fold
+    double v[VP];
 #pragma unroll
-      for (int p = 0; p < S3_PD; ++p) {
+    for (int r = 0; r < VP; ++r) v[r] = 0.0;
 #pragma unroll
-        for (int k = 0; k < NSLOT; ++k) {
-          const long long i0 = lane + 32 * k;
-          xb[p][k] = (p < I1 && i0 < I0) ? __ldg(xs + (long long)p * I0 + i0) : TE(0);
-        }
-        a1b[p] = (p < I1 && vi < R) ? __ldg(A1 + (long long)p * R + vi) : 0.0;
-      }
-      for (int i1 = 0; i1 < I1; i1 += S3_PD) {
+    for (int k = 0; k < NSLOT; ++k) {
+      const long long i0 = lane + 32 * k;
+      if (i0 < I0) {
 #pragma unroll
-        for (int p = 0; p < S3_PD; ++p) {
-          if (i1 + p < I1) {
-            double v[VP];
-#pragma unroll
-            for (int r = 0; r < VP; ++r) v[r] = 0.0;
-#pragma unroll
-            for (int k = 0; k < NSLOT; ++k) {
-              const double x = (double)xb[p][k];
-#pragma unroll
-              for (int r = 0; r < RB; ++r) v[r] = fma(x, a0[k][r], v[r]);
-            }
-            const double a1 = a1b[p];
-            // refill this ring slot with row i1 + p + PD
-            const int nx = i1 + p + S3_PD;
-#pragma unroll
-            for (int k = 0; k < NSLOT; ++k) {
-              const long long i0 = lane + 32 * k;
-              xb[p][k] = (nx < I1 && i0 < I0) ? __ldg(xs + (long long)nx * I0 + i0) : TE(0);
-            }
-            a1b[p] = (nx < I1 && vi < R) ? __ldg(A1 + (long long)nx * R + vi) : 0.0;
-            const double w = warp_fold<VP>(v, lane);
-            acc = fma(w, a1, acc);
-          }
-        }
+        for (int r = 0; r < RB; ++r)
+          if (r < R) v[r] = fma(__ldg(A0 + i0 * R + r), acc[k][r], v[r]);
       }
     }
-    if (writer && vi < R) a.MTT[s][i2 * R + vi] = acc;
+    const double w = warp_fold<VP>(v, lane);
+    if (writer && vi < R) a.MTT[s][i2 * R + vi] = w;
   }
   tl_end(a.tl, TL_SLAB);
 }
 
-constexpr int S3_RING = 4;
+constexpr int S3_RING = 3;
 
-// rows per ring stage (~4 KB per stage) and the kernel's dynamic smem
+// rows per ring stage (~2 KB per stage) and the kernel's dynamic smem
 inline int slab3_rows(long long max_i0, int elem) {
-  const long long per = 4096 / (max_i0 * elem);
+  const long long per = 2048 / (max_i0 * elem);
   return (int)(per < 1 ? 1 : per);
 }
-inline size_t slab3_smem(long long max_i0, int elem, int rows) {
-  return S3_HDR + (size_t)S3_WARPS * S3_RING * rows * max_i0 * elem;
+inline size_t slab3_smem(long long max_i0, int elem, int rows, long long a1_rows, int rb,
+                         bool ring) {
+  return S3_HDR + (size_t)S3_WARPS * a1_rows * rb * 8 +
+         (ring ? (size_t)S3_WARPS * S3_RING * rows * max_i0 * elem : 0);
+}
+
+// ---------------------------------------------------------------------------
+// T pass of the 3-way full path as warp tasks:
+//   T[r][j] = sum_{i2} X[j + J i2] A2[i2, r],   j = i0 + I0 i1 flattened
+// One warp owns one task (block s, 64 consecutive j) and walks the I2 rows of
+// that chunk (a 256-byte fp32 segment per row, rows J apart); lane l holds
+// the adjacent pair j = j0 + 2l, 2l + 1 (one 8-byte load per row, F3_PD rows
+// prefetched in registers) and accumulates 2 x RB fp64 sums.  A2 is staged
+// per warp in shared memory (broadcast 16-byte reads per row).  No cross-lane
+// reduction, no partials: T is written once.  Small per-lane state keeps two
+// CTAs per SM resident.  (Plain loads: per-row bulk copies would be 256-byte
+// TMA operations, whose issue rate, not bandwidth, then bounds the pass.)
+// ---------------------------------------------------------------------------
+constexpr int F3_WARPS = 8;
+constexpr int F3_PD = 4;
+constexpr int F3_CH = 64;        // j per task
+
+template <typename TE> struct Pair2;
+template <> struct Pair2<float> { typedef float2 T; };
+template <> struct Pair2<double> { typedef double2 T; };
+
+template <typename TE, int RB>
+__global__ void __launch_bounds__(F3_WARPS * 32, 2)
+fiber3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int a2_rows) {
+  griddep_wait();
+  if (gated(a)) return;
+  tl_begin(a.tl, TL_FIBER);
+  typedef typename Pair2<TE>::T P2;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  extern __shared__ __align__(128) unsigned char f3sm[];
+  double* a2s = reinterpret_cast<double*>(f3sm) + (size_t)warp * a2_rows * RB;
+  int cur = -1, s = 0, R = 0;
+  long long I2 = 0, J = 0;
+  const TE* X = nullptr;
+  double* T = nullptr;
+  for (int t = blockIdx.x * F3_WARPS + warp; t < ntasks; t += gridDim.x * F3_WARPS) {
+    while (s + 1 < S && t >= task_first[s + 1]) ++s;
+    if (a.active && !a.active[s]) continue;
+    if (s != cur) {
+      cur = s;
+      R = a.R[s];
+      I2 = a.dims[3 * s + 2];
+      J = a.dims[3 * s] * a.dims[3 * s + 1];
+      X = reinterpret_cast<const TE*>(a.X[s]);
+      T = reinterpret_cast<double*>(tbuf(a, s));
+      const double* A2 = a.U[3 * s + 2];
+      __syncwarp();
+      for (long long e = lane; e < I2 * RB; e += 32) {
+        const long long q = e / RB;
+        const int r = (int)(e - q * RB);
+        a2s[e] = r < R ? __ldg(A2 + q * R + r) : 0.0;
+      }
+      __syncwarp();
+    }
+    const long long j0 = (long long)(t - task_first[s]) * F3_CH;
+    const long long jl = j0 + 2 * lane;           // this lane's pair
+    const bool full = jl + 1 < J;
+    const bool half = jl < J;
+    const TE* xs = X + jl;
+    double acc0[RB], acc1[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) { acc0[r] = 0.0; acc1[r] = 0.0; }
+    P2 xb[F3_PD];
+#pragma unroll
+    for (int p = 0; p < F3_PD; ++p) {
+      if (p < I2 && full) xb[p] = __ldg(reinterpret_cast<const P2*>(xs + J * p));
+      else { xb[p].x = (p < I2 && half) ? __ldg(xs + J * p) : TE(0); xb[p].y = TE(0); }
+    }
+    for (long long i2 = 0; i2 < I2; i2 += F3_PD) {
+#pragma unroll
+      for (int p = 0; p < F3_PD; ++p) {
+        if (i2 + p < I2) {
+          const double x0 = (double)xb[p].x, x1 = (double)xb[p].y;
+          const long long nx = i2 + p + F3_PD;
+          if (nx < I2 && full) xb[p] = __ldg(reinterpret_cast<const P2*>(xs + J * nx));
+          else { xb[p].x = (nx < I2 && half) ? __ldg(xs + J * nx) : TE(0); xb[p].y = TE(0); }
+          double av[RB];
+          load_row<double, RB>(a2s + (i2 + p) * RB, av);
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            acc0[r] = fma(x0, av[r], acc0[r]);
+            acc1[r] = fma(x1, av[r], acc1[r]);
+          }
+        }
+      }
+    }
+    if (half) {
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        if (r < R) {
+          if (full) {
+            double2 v;
+            v.x = acc0[r];
+            v.y = acc1[r];
+            // T rows are J apart: 16-byte aligned when J is even (host checks)
+            *reinterpret_cast<double2*>(T + (long long)r * J + jl) = v;
+          } else {
+            T[(long long)r * J + jl] = acc0[r];
+          }
+        }
+    }
+  }
+  tl_end(a.tl, TL_FIBER);
+}
+
+inline size_t fiber3_smem(long long a2_rows, int rb) {
+  return (size_t)F3_WARPS * a2_rows * rb * 8;
 }
 
 // usable for these shapes?  (all blocks)
