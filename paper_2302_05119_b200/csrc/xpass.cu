@@ -25,7 +25,8 @@
 namespace cb {
 
 int rank_bucket(int r) {
-  return r <= 8 ? 8 : r <= 12 ? 12 : r <= 16 ? 16 : r <= 24 ? 24 : r <= 32 ? 32 : r <= 40 ? 40 : 64;
+  return r <= 8 ? 8 : r <= 10 ? 10 : r <= 12 ? 12 : r <= 16 ? 16 : r <= 24 ? 24 : r <= 32 ? 32
+         : r <= 40 ? 40 : 64;
 }
 int pc_compute_bytes(int pc) { return pc == PC_F32 ? 4 : 8; }
 static int pc_storage_bytes(int pc) { return pc == PC_F64 ? 8 : 4; }
@@ -34,6 +35,7 @@ static int pc_storage_bytes(int pc) { return pc == PC_F64 ? 8 : 4; }
 #define CB_RB_SWITCH(RBV, CALL)                     \
   switch (RBV) {                                    \
     case 8: { constexpr int RB = 8; CALL; } break;  \
+    case 10: { constexpr int RB = 10; CALL; } break; \
     case 12: { constexpr int RB = 12; CALL; } break; \
     case 16: { constexpr int RB = 16; CALL; } break; \
     case 24: { constexpr int RB = 24; CALL; } break; \
@@ -62,9 +64,9 @@ template <typename TE, typename TC, int RB, bool T, bool B, bool S>
 static void fib2_go(bool tma, const XArgs& a, const FibUnit* u, int n, const XTables& t,
                     cudaStream_t st) {
   constexpr int TD = x2_tile(RB, sizeof(TC));
-  if (t.fib_tj == TD) fib2_go_tj<TE, TC, RB, T, B, S, TD>(tma, a, u, n, t, st);
-  else if (TD >= 2 && t.fib_tj == (TD >= 2 ? TD / 2 : 1))
-    fib2_go_tj<TE, TC, RB, T, B, S, (TD >= 2 ? TD / 2 : 1)>(tma, a, u, n, t, st);
+  if (t.fib_tj >= TD) fib2_go_tj<TE, TC, RB, T, B, S, TD>(tma, a, u, n, t, st);
+  else if (t.fib_tj == 3) fib2_go_tj<TE, TC, RB, T, B, S, (TD >= 3 ? 3 : 1)>(tma, a, u, n, t, st);
+  else if (t.fib_tj == 2) fib2_go_tj<TE, TC, RB, T, B, S, (TD >= 2 ? 2 : 1)>(tma, a, u, n, t, st);
   else fib2_go_tj<TE, TC, RB, T, B, S, 1>(tma, a, u, n, t, st);
 }
 
@@ -305,10 +307,19 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
       return u;
     };
     units = count(tj);
-    // (halving measured slower on c2: TJ 2 with 200 units 50 us vs TJ 4 with
-    // 100 units 34 us; opt-in for experiments)
-    static const bool halve = getenv("CB_FIB_HALVE") != nullptr;
-    while (halve && t.fiber_direct && tj > 1 && units < 148) { tj /= 2; units = count(tj); }
+    // unsplit T pass: pick TJ (<= the register-budget tile) minimising waves x TJ,
+    // the per-SM makespan in column-rows (c2: TJ 3 -> 140 units in one wave)
+    static const bool tj_search = getenv("CB_FIB_TJSEARCH") != nullptr;   // measured slower on c2
+    if (t.fiber_direct && tj_search) {
+      long long best = -1;
+      for (int c : {tile, 3, 2, 1}) {
+        if (c > tile) continue;
+        const long long u = count(c);
+        const long long cost = ((u + 147) / 148) * c;
+        if (best < 0 || cost < best) { best = cost; tj = c; units = u; }
+      }
+    }
+    if (getenv("CB_FIB_TJ")) tj = std::max(1, std::min(tile, atoi(getenv("CB_FIB_TJ"))));
     t.fib_tj = tj;
   }
   const long long JT = (long long)X2_THREADS * t.fib_tj;

@@ -50,8 +50,14 @@ __host__ __device__ constexpr size_t slab2_smem(long long kr_rows) {
 // R-wide row of TC values from shared memory as 16-byte vectors
 template <typename TC, int RB>
 __device__ __forceinline__ void load_row(const TC* __restrict__ p, TC (&v)[RB]) {
-  static_assert((RB * sizeof(TC)) % 16 == 0, "rank bucket must fill 16-byte vectors");
+  // 16-byte vectors while they fit (rows must start 16-byte aligned when
+  // RB * sizeof(TC) is a multiple of 16), then a scalar tail
   constexpr int PER = 16 / sizeof(TC);
+  if constexpr ((RB * sizeof(TC)) % 16 != 0) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) v[r] = p[r];
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < RB / PER; ++q) {
     if constexpr (sizeof(TC) == 8) {
@@ -169,6 +175,7 @@ fiber2_kernel(XArgs a, const FibUnit* __restrict__ units, int use_tma) {
     const TC* as = a2t + (size_t)k * F2_CH * RB;
     if (use_tma) mbar_wait(&bar[slot], (uint32_t)((k / F2_NST) & 1));
     const TE* xs = xbuf + (size_t)slot * F2_CH * JT + threadIdx.x;
+#pragma unroll 2
     for (int q = 0; q < nr; ++q) {
       TC x[TJ];
 #pragma unroll
