@@ -248,7 +248,7 @@ def run_ours(args):
             "peak_source": peak_kind, "kernels": kinds}
     # ---- e2e: public API on host buffers (H2D of inputs + D2H of results) --
     host = [np.asarray(t, dtype=np.float64) for t in tensors]
-    e2e_iters = K
+    e2e_iters = spec.max_iter           # the config's own run length (c2: 500 iterations)
     torch.cuda.synchronize()
     tic = time.perf_counter()
     e2e_problem = P.CoupledProblem(host, spec.rank, list(spec.coupled), mode=spec.mode)

@@ -369,7 +369,20 @@ static int enqueue_eval_full(cb_solver* h, int redo) {
   if (h->fast3) {
     XArgs a = redo ? h->xa_redo : h->xa_main;
     a.t_other = 1;   // write the non-accepted T buffer
-    return enqueue_fiber(h, a, 1, h->ctx.b_mtt ? 0 : 1, h->objective == 0 ? 1 : 0);
+    int rc;
+    if (!h->ctx.ld_pre)
+      return enqueue_fiber(h, a, 1, h->ctx.b_mtt ? 0 : 1, h->objective == 0 ? 1 : 0);
+    // per-block evaluation algebra beside the fiber pass (side stream)
+    const bool par = !h->in_body;
+    if (par && (rc = fork_side(h))) return rc;
+    if (emit(h)) {
+      launch_k(k_eval_side, dim3(h->S), dim3(256), h->blk_smem, par ? h->st2 : h->st, h->ctx, redo);
+      count_launch(1);
+      CB_CHECK_LAUNCH();
+    }
+    if ((rc = enqueue_fiber(h, a, 1, 0, h->objective == 0 ? 1 : 0))) return rc;
+    if (par && (rc = join_side(h))) return rc;
+    return CB_OK;
   }
   // generic: b from the last mode's MTTKRP (solver.py:506-509), residuals
   for (int s = 0; s < h->S; ++s) {
@@ -696,6 +709,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   c.dbg = nullptr;
   if (getenv("CB_PHASES")) TRY(dalloc((void**)&c.dbg, sizeof(double) * 64, A));
   TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
+  TRY(dalloc((void**)&c.ldcore, sizeof(double) * S, A));
   // coupling arrays in global block slots; separate send copies when sharded
   // (their foreign slots stay zero: the all-reduce is an exact all-gather)
   const int ST = h->S_tot;
@@ -830,6 +844,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     // its MTTKRP output (solver.py:506-509) in k_finalize of the last mode,
     // so the evaluation fiber pass only forms T
     c.b_mtt = (h->tab.slab_direct && !h->lra) ? 1 : 0;
+    c.ld_pre = (c.b_mtt && !getenv("CB_NO_LDPRE")) ? 1 : 0;
     if (c.dbg) {
       TRY(dalloc((void**)&h->ktime, sizeof(unsigned long long) * 8, A));
       const unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, ~0ull, 0};
@@ -869,6 +884,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));

@@ -99,6 +99,11 @@ struct Ctx {
   int use_cond;
   unsigned long long* tl;     // profiling only: iteration timeline (TlSlot)
   int b_mtt;                  // b from the last mode's MTTKRP in k_finalize (3-way row-dot path)
+  // 3-way full path: the evaluation's per-block algebra (b, model_sq) and the
+  // NEXT iteration's core Lipschitz constant run in k_eval_side beside the
+  // fiber pass; k_sweep_begin then reads ldcore instead of a lambda_max
+  int ld_pre;
+  double* ldcore;             // S
 };
 
 __host__ __device__ inline long long lu_idx(const Ctx& c, int n, int g) {

@@ -230,6 +230,10 @@ __global__ void __launch_bounds__(256) k_init_block(Ctx c) {
     __syncthreads();
   }
   final_quantities(c, s, sm);
+  if (c.ld_pre && c.update_core) {
+    const double ld = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+    if (threadIdx.x == 0) c.ldcore[s] = ld;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -249,7 +253,11 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
   double* lamp = c.LAMP[s];
   if (c.update_core) {
     build_gram_product(c, s, -1, false, sm);
-    const double ldv = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+    // main sweeps of the 3-way full path: L_d was formed beside the previous
+    // evaluation's fiber pass (k_eval_side) from these same grams
+    const double ldv = (!redo && c.ld_pre)
+                           ? c.ldcore[s]
+                           : block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
     double* sc = sm.misc + 192;
     if (threadIdx.x == 0) {
       const double h = c.lipc_hist[s];
@@ -537,7 +545,7 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
       step_and_lipschitz(c, s, n + 1, sm);
       pc.mark(c.dbg, 2);
     }
-  } else {
+  } else if (!c.ld_pre) {
     if (c.b_mtt) {
       // staged core linear term b[r] = sum_i U_{N-1}[i, r] MTTKRP_{N-1}[i, r]
       // (solver.py:506-509); warp per r, lanes over rows, fixed order
@@ -554,6 +562,38 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
     pc.mark(c.dbg, 3);
   }
   tl_end(c.tl, TL_FIN + n);
+}
+
+// evaluation algebra of the 3-way full path, run beside the fiber pass:
+// b[r] = sum_i U_{N-1}[i, r] MTTKRP_{N-1}[i, r] (solver.py:506-509), the
+// evaluation quantities (final_quantities), and the next sweep's core
+// Lipschitz constant lambda_max(hadamard_n G_n) (solver.py:375-379)
+__device__ inline void eval_side_block(const Ctx& c, int s, const BlockSmem& sm) {
+  const int N = c.N;
+  const int R = c.R[s];
+  const long long In = c.dims[s * N + N - 1];
+  const double* Uc = c.U[s * N + N - 1];
+  const double* M = c.MTT[s];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int r = wid; r < R; r += blockDim.x >> 5) {
+    double v = 0.0;
+    for (long long i = lane; i < In; i += 32) v = fma(Uc[i * R + r], M[i * R + r], v);
+    v = warp_sum(v);
+    if (lane == 0) c.fib_bpart[(long long)s * RSTRIDE + r] = v;
+  }
+  final_quantities(c, s, sm);   // leaves hadamard_n G_n in sm.lmA
+  if (c.update_core) {
+    const double ld = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+    if (threadIdx.x == 0) c.ldcore[s] = ld;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_eval_side(Ctx c, int redo) {
+  griddep_wait();
+  if (stopped(c, redo)) return;
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  eval_side_block(c, blockIdx.x, sm);
 }
 
 // step matrix and Lipschitz constant of mode n for every block (solver.py:402-406)
