@@ -51,6 +51,8 @@ struct cb_solver {
   cudaStream_t st3 = nullptr;     // capture stream of the conditional restart body
   bool cond_capture = false;
   bool in_body = false;
+  bool fused = false;          // k_mode_fused replaces k_mode_update + k_finalize
+  size_t fused_smem = 0;
   int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0, pc = 0;
   int rmax = 1, rtmax = 0, rb = 8, max_iter = 0;
   double delta_w = 0.9999, tol = 1e-8;
@@ -277,6 +279,17 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       }
       prof(h, "generic_mttkrp");
     }
+    const bool split = par && n + 1 < h->N;
+    if (h->fused) {
+      // mode update + finalize in one cooperative launch (one CTA per block)
+      if (emit(h)) {
+        CB_CUDA(launch_coop(k_mode_fused, dim3(h->S), dim3(256), h->fused_smem, st, h->ctx, n,
+                            redo, src, split ? 0 : 1));
+        count_launch(1);
+        CB_CHECK_LAUNCH();
+      }
+      prof(h, redo ? "redo:mode_fused" : "mode_fused");
+    } else {
     if (emit(h)) {
       launch_k(k_mode_update, dim3(h->n_rows[n]), dim3(256), h->mu_smem, st, h->ctx, n, redo, src, h->d_rows[n]);
       count_launch(1);
@@ -293,13 +306,13 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       }
       prof(h, redo ? "redo:common" : "common");
     }
-    const bool split = par && n + 1 < h->N;
     if (emit(h)) {
       launch_k(k_finalize, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, n, redo, split ? 0 : 1);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
     prof(h, redo ? "redo:finalize" : "finalize");
+    }
     if (split) {
       if ((rc = fork_side(h))) return rc;
       if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
@@ -885,6 +898,21 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  // fused mode update: single GPU, all S CTAs co-resident (cooperative)
+  h->fused_smem = std::max(h->blk_smem, h->mu_smem);
+  CB_CUDA(cudaFuncSetAttribute(k_mode_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)h->fused_smem));
+  {
+    int dev = 0, per_sm = 0, sms = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mode_fused, 256, h->fused_smem);
+    // opt-in: measured slower on c2 (phase A serialises the row tiles of a
+    // block in one CTA; phase B's block-order fold is a chain of L2 reads)
+    h->fused = !h->shard && coop && per_sm >= 1 && S <= per_sm * sms && getenv("CB_FUSED");
+    TRY(dalloc((void**)&c.gbar, sizeof(unsigned), A));
+  }
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));

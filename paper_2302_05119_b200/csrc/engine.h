@@ -104,6 +104,7 @@ struct Ctx {
   // fiber pass; k_sweep_begin then reads ldcore instead of a lambda_max
   int ld_pre;
   double* ldcore;             // S
+  unsigned* gbar;             // grid-barrier counter of k_mode_fused (monotonic)
 };
 
 __host__ __device__ inline long long lu_idx(const Ctx& c, int n, int g) {
