@@ -63,6 +63,18 @@ int cb_mttkrp(int dtype, const void* X, int order, const int64_t* dims,
               const double* const* factors, int rank, int mode, double* out,
               void* stream);
 
+/* Batched core linear term b_s = (A0 (.) A1 (.) A2 of block s)^T vec(X_s) on the
+ * tensor cores (tcgen05 kind::i8, exact int32 accumulation over byte-sliced
+ * fixed-point operands, ~2^-20 relative per product, unbiased).  fp32 3-way
+ * blocks (I0 % 4 == 0, I0 <= 512, rank <= 64); `tensors` and `factors` are
+ * host arrays of device pointers (n_blocks and 3*n_blocks), `dims` is
+ * n_blocks x 3, out is a device array of n_blocks x 64 doubles (row s holds
+ * b_s[0..rank_s)).  Synchronous.  Replaces solver.py:215-218
+ * core_linear_term (and the lra trace term solver.py:519-522). */
+int cb_core_linear_term_tc(int n_blocks, const void* const* tensors, const int64_t* dims,
+                           const double* const* factors, const int* ranks, double* out,
+                           void* stream);
+
 /* Khatri-Rao product of `nmats` row-major matrices (first slowest), out has
  * prod(rows) x rank entries.  Replaces tensor_ops.py:66-85 khatri_rao. */
 int cb_khatri_rao(const double* const* mats, int nmats, const int64_t* rows, int rank,

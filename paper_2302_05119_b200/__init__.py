@@ -24,6 +24,7 @@ from .solver import (
     TraceRow,
     core_gradient,
     core_linear_term,
+    core_linear_terms_tc,
     core_linear_term_lra,
     extrapolation_weight,
     factor_gradient,

@@ -75,6 +75,8 @@ _sig("cb_abi_version", c_int, [])
 _sig("cb_launch_count", ctypes.c_longlong, [])
 _sig("cb_launch_count_reset", None, [])
 _sig("cb_mttkrp", c_int, [c_int, c_vp, c_int, c_i64p, ctypes.POINTER(c_vp), c_int, c_int, c_vp, c_vp])
+_sig("cb_core_linear_term_tc", c_int, [c_int, ctypes.POINTER(c_vp), c_i64p, ctypes.POINTER(c_vp),
+                                        c_ip, c_vp, c_vp])
 _sig("cb_khatri_rao", c_int, [ctypes.POINTER(c_vp), c_int, c_i64p, c_int, c_vp, c_vp])
 _sig("cb_hadamard_gram", c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64p, c_int, c_int,
                                  c_int, c_int, c_vp, c_vp])
@@ -111,7 +113,7 @@ _sig("cb_nccl_comm_destroy", c_int, [c_vp])
 # every symbol the header declares (checked by tests/test_boundary.py)
 EXPORTED = [
     "cb_last_error", "cb_abi_version", "cb_launch_count", "cb_launch_count_reset",
-    "cb_mttkrp", "cb_khatri_rao", "cb_hadamard_gram", "cb_spectral_norm_batched",
+    "cb_mttkrp", "cb_core_linear_term_tc", "cb_khatri_rao", "cb_hadamard_gram", "cb_spectral_norm_batched",
     "cb_tensor_stats", "cb_kruskal_residual", "cb_rowdot", "cb_gemm", "cb_factor_gradient",
     "cb_als_create", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
     "cb_als_destroy", "cb_solver_create", "cb_solver_run", "cb_solver_step_async",

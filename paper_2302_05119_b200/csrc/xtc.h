@@ -1,0 +1,38 @@
+// Tensor-core trace pass (tcgen05 kind::i8, exact int32 accumulation over
+// byte-sliced fixed-point operands) for 3-way fp32 blocks:
+//
+//   b_s[r] = sum_{i0,i1,i2} X_s[i0,i1,i2] A0[i0,r] A1[i1,r] A2[i2,r]
+//
+// the core linear term of the reference (`solver.py:215-218`, staged at
+// `:506-511`) and the lra original-tensor trace term (`solver.py:519-522`).
+// See xtc.cu for the algorithm and DESIGN.md §5 for the roofline.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "xpass.cuh"
+
+namespace cb {
+
+struct XtcPlan;
+
+// usable for these blocks?  fp32 storage, I0 % 4 == 0 (TMA row pitch),
+// I0 <= XTC_MAX_I0, rank <= 64, 16-byte aligned tensors
+bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R);
+
+// plan for S blocks (device fp32 tensors X[s], dims S x 3, ranks R[s]):
+// per-block tensor maps, unit tables, the per-block fixed-point exponent of X
+// (one max|X| pass, enqueued on `st`), operand images and partial buffers
+int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
+                    cudaStream_t st, XtcPlan** out);
+void xtc_plan_destroy(XtcPlan* p);
+
+// b_s into bsum[s * RSTRIDE + r] (r < R[s]); factors from U (device array of
+// S*3 pointers, the engine's XArgs.U), skipped when *gate == 0 (gate may be
+// null).  Two launches: operand prep + the streaming MMA kernel.
+int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
+              cudaStream_t st);
+
+// algorithmic bytes streamed per xtc_trace call (sum_s |X_s| * 4)
+double xtc_bytes(const XtcPlan* p);
+
+}  // namespace cb

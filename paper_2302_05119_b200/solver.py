@@ -38,7 +38,7 @@ from .kruskal import CoupledFactorSet, KruskalTensor
 from .tensor_ops import hadamard_gram, spectral_norm
 
 __all__ = [
-    "CoupledProblem", "SolverOptions", "SolveResult", "TraceRow", "solve", "objective",
+    "CoupledProblem", "SolverOptions", "core_linear_terms_tc", "SolveResult", "TraceRow", "solve", "objective",
     "core_gradient", "factor_gradient", "core_linear_term", "core_linear_term_lra",
     "factor_linear_term", "factor_linear_term_lra", "lipschitz_core", "lipschitz_factor",
     "extrapolation_weight", "t_next", "init_factors", "solve_distributed",
@@ -263,6 +263,30 @@ def core_linear_term(tensor, factors):
     out = torch.empty(rank, dtype=torch.float64, device=flat.device)
     L.check(L.lib.cb_rowdot(D.ptr(dev[0]), D.ptr(mtt), dims[0], rank, D.ptr(out), D.stream()))
     return D.to_host(out)
+
+
+def core_linear_terms_tc(tensors, factor_sets):
+    """Batched core linear terms b_s = (U_kr,s)^T vec(M_s) of 3-way blocks on
+    the tensor cores (`cb_core_linear_term_tc`: tcgen05 kind::i8 over
+    byte-sliced fixed-point operands, exact int32 accumulation, ~2^-20
+    relative per product).  The tensors are cast to fp32 (the throughput-mode
+    storage); returns a list of R_s-vectors (solver.py:215-218)."""
+    torch = D.torch_mod()
+    devs, dims, ranks, facs = [], [], [], []
+    for t, fs in zip(tensors, factor_sets):
+        flat, d = D.tensor_to_dev(np.asarray(t), "fp32")
+        if len(d) != 3:
+            raise ValueError("the tensor-core trace pass needs 3-way blocks")
+        devs.append(flat)
+        dims.extend(int(x) for x in d)
+        ranks.append(int(np.asarray(fs[0]).shape[1]))
+        facs.extend(D.to_dev_f64(f) for f in fs)
+    out = torch.zeros((len(devs), 64), dtype=torch.float64, device=devs[0].device)
+    L.check(L.lib.cb_core_linear_term_tc(len(devs), L.ptr_array([D.ptr(x) for x in devs]),
+                                         L.i64_array(dims), L.ptr_array([D.ptr(x) for x in facs]),
+                                         L.int_array(ranks), D.ptr(out), D.stream()))
+    host = D.to_host(out)
+    return [host[s, :r].copy() for s, r in enumerate(ranks)]
 
 
 def _gemm(a, b, ta=False, tb=False, alpha=1.0):

@@ -1,0 +1,112 @@
+"""GPU parity of the tensor-core trace pass (`cb_core_linear_term_tc`,
+csrc/xtc.cu) against the oracle's core linear term (oracle/concpd_oracle.py
+`core_term`, reference solver.py:215-218), fp64 on the same fp32-rounded
+inputs.
+
+The pass rounds X to 2^-21 of its block maximum and A0 to 2^-23 of each
+column maximum (unbiased) and accumulates exactly in int32; the bound
+asserted is 2e-7 relative to sum |X||A0||A1||A2| per rank column (observed
+~2e-8), plus bitwise determinism and independence of the batching."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import concpd_oracle as O
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2302_05119_b200 as P
+    return P
+
+
+def _block(rng, dims, rank, signed=False):
+    f = [rng.random((d, rank)) for d in dims]
+    if signed:
+        f = [x - 0.5 for x in f]
+    x = O.dense_from_model(f, np.ones(rank)) + 0.1 * rng.standard_normal(dims)
+    if not signed:
+        x = np.maximum(x, 0.0)
+    x = np.asfortranarray(x.astype(np.float32))
+    g = [rng.random((d, rank)) - (0.5 if signed else 0.0) for d in dims]
+    return x, g
+
+
+def _want(x, g):
+    x64 = np.asarray(x, dtype=np.float64)
+    want = O.core_term(x64, g)
+    scale = O.core_term(np.abs(x64), [np.abs(a) for a in g])
+    return want, scale
+
+
+SHAPES = [
+    ((400, 12, 30), 40),     # c5-like rank, 13 chunks incl. a 16-column tail
+    ((112, 92, 40), 20),     # c3 mode sizes (shortened), J tail tile
+    ((64, 71, 60), 30),      # c4 shape
+    ((100, 100, 10), 10),    # c2 modes, N bucket 16
+    ((36, 5, 7), 64),        # rank 64 bucket, a single partial tile
+    ((4, 3, 2), 3),          # tiny
+]
+
+
+@pytest.mark.parametrize("signed", [False, True])
+def test_tc_trace_matches_oracle(P, signed):
+    rng = np.random.default_rng(11 if signed else 7)
+    for dims, rank in SHAPES:
+        x, g = _block(rng, dims, rank, signed)
+        got = P.core_linear_terms_tc([x], [g])[0]
+        want, scale = _want(x, g)
+        err = np.abs(got - want) / scale
+        # relative to sum |.| (signed data cancels inside b); tiny blocks do
+        # not average the 2^-21 input rounding, so they get the per-product
+        # bound
+        tol = 2e-7 if x.size >= 10000 else 4e-6
+        assert err.max() < (2.5 * tol if signed else tol), (dims, rank, err.max())
+
+
+def test_tc_trace_batched_ragged_and_deterministic(P):
+    rng = np.random.default_rng(3)
+    blocks = [_block(rng, d, r) for d, r in SHAPES[:4]]
+    # ranks differ per block: the N bucket is the maximum
+    xs = [b[0] for b in blocks]
+    gs = [b[1] for b in blocks]
+    got = P.core_linear_terms_tc(xs, gs)
+    again = P.core_linear_terms_tc(xs, gs)
+    for a, b in zip(got, again):
+        assert np.array_equal(a, b)              # bitwise run-to-run
+    for s, (x, g) in enumerate(blocks):
+        want, scale = _want(x, g)
+        assert (np.abs(got[s] - want) / scale).max() < 2e-7
+    # a block's result does not depend on its batch neighbours (fixed units)
+    single = P.core_linear_terms_tc([xs[1]], [gs[1]])[0]
+    # (alone it may use a smaller N bucket: same products, same fold order)
+    assert np.array_equal(single, got[1])
+
+
+def test_tc_trace_zero_and_scaled(P):
+    rng = np.random.default_rng(5)
+    x, g = _block(rng, (64, 20, 20), 8)
+    z = np.zeros_like(x)
+    assert np.array_equal(P.core_linear_terms_tc([z], [g])[0], np.zeros(8))
+    # power-of-two scalings are exact in the fixed-point representation
+    a = P.core_linear_terms_tc([x], [g])[0]
+    b = P.core_linear_terms_tc([np.asfortranarray(x * np.float32(1024.0))], [g])[0]
+    np.testing.assert_array_equal(b, a * 1024.0)
+
+
+def test_tc_trace_c5_block(P):
+    """One full c5 block (400^3 fp32, R = 40): the size the roofline runs on."""
+    from paper_2302_05119_b200.configs import generate_config
+    xs, spec = generate_config("c5", blocks=[0])
+    rng = np.random.default_rng(0)
+    g = [rng.random((d, spec.rank)) for d in spec.dims]
+    got = P.core_linear_terms_tc(xs, [g])[0]
+    x64 = np.asarray(xs[0], dtype=np.float64)
+    want = O.core_term(x64, g)
+    rel = np.abs(got - want) / np.abs(want)
+    assert rel.max() < 1e-7, rel.max()
