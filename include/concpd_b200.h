@@ -177,7 +177,10 @@ typedef struct {
   const double* const* tilde_weights; /* lra: host array of HOST arrays      */
   int objective;                  /* 0 = explicit residual, 1 = gram expansion */
   int compute;                    /* fp32 storage only: 0 = fp64 arithmetic in
-                                     the tensor passes, 1 = fp32 arithmetic    */
+                                     the tensor passes, 1 = fp32 arithmetic,
+                                     2 = fp64 arithmetic except the lra trace
+                                     pass, which runs on the tensor cores
+                                     (cb_core_linear_term_tc's algorithm)     */
   double delta_w;
   double tol;
   int max_iter;

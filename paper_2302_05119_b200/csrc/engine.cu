@@ -20,6 +20,7 @@
 #include "engine_host.h"
 #include "launch.cuh"
 #include "nccl_shim.h"
+#include "xtc.h"
 
 namespace cb {
 
@@ -110,6 +111,7 @@ struct cb_solver {
   int seg_cur = 0, seg_want = -1;   // -1: emit everything; -2: count segments
   struct Xchg { double* send; double* recv; long long count; };
   std::vector<Xchg> pending;
+  cb::XtcPlan* xtc = nullptr;  // tensor-core lra trace pass (compute code 2)
 };
 
 namespace cb {
@@ -407,6 +409,17 @@ static int enqueue_eval_full(cb_solver* h, int redo) {
 }
 
 static int enqueue_trace_lra(cb_solver* h) {
+  if (h->xtc) {
+    // tensor-core trace pass (xtc.cu): b_orig of every block into fib_bpart
+    if (!emit(h)) return CB_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, h->st)); }
+    int rc = xtc_trace(h->xtc, h->xa_main.U, h->xa_main.gate, h->ctx.fib_bpart, h->st);
+    if (rc) return rc;
+    CB_CHECK_LAUNCH();
+    if (h->timing) { CB_CUDA(cudaEventRecord(e1, h->st)); h->t_launches += 1; h->t_bytes += xtc_bytes(h->xtc); }
+    return CB_OK;
+  }
   if (h->fast3) return enqueue_fiber(h, h->xa_main, 0, 1, 0);
   for (int s = 0; s < h->S; ++s) {
     int rc = generic_mttkrp(h, s, 0);
@@ -867,6 +880,13 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     }
     xa.gate = &h->d_state->go_main;
     h->xa_main = xa;
+    // lra trace pass on the tensor cores (compute code 2, fp32 storage)
+    if (h->lra && d->compute == 2 && h->dtype == CB_F32 &&
+        xtc_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
+      // a plan that does not fit (shared memory) leaves the CUDA-core pass
+      if (xtc_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->xtc) != CB_OK)
+        h->xtc = nullptr;
+    }
     xa.gate = &h->d_state->go_redo;
     h->xa_redo = xa;
   } else {
@@ -1246,6 +1266,7 @@ int cb_solver_destroy(cb_solver* h) {
   if (h->st2) cudaStreamDestroy(h->st2);
   if (h->st3) cudaStreamDestroy(h->st3);
   for (void* p : h->allocs) cudaFree(p);
+  cb::xtc_plan_destroy(h->xtc);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->h_state) cudaFreeHost(h->h_state);
   delete h;

@@ -90,6 +90,13 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+// K-major, 32-byte swizzle (rows of 32 B = one int8 K=32 MMA step, 8-row
+// atoms of 256 B, atoms SBO = 256 B apart; 256-B aligned)
+__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+
 // ---- tensor TMA (2-D tile, global -> shared, completes on an mbarrier) ----
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1,
                                             uint64_t* bar) {
@@ -103,6 +110,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0,
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+
+// 4-byte async copy global -> shared (LDGSTS), completion per thread
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -44,13 +44,17 @@
 //             epilogue (tcgen05.ld of the int32 levels, fp64 combine, A1/A2
 //             weights, per-thread fp64 row sums), each group for half of the
 //             N columns.
-// TMEM: 4 A slots x 32 columns, 2 D buffers x 3 levels x N columns (<= 512).
+// TMEM: 6 A slots (4 for N = 64) x 32 columns, 2 D buffers x 3 levels x N
+// columns (<= 512).  Row weights A1[i1,r] A2[i2,r] are fp32 (transposed
+// tables, loaded while the next tile converts); column constants in smem.
 // Units of 8 tiles (never straddling a block) are the partial granularity:
 // partials are reduced in fixed order and folded per block in unit order by
 // the last arriving CTA, so b is bitwise independent of the grid size and
 // of how blocks are sharded over GPUs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -66,24 +70,31 @@
 namespace cb {
 
 constexpr int XTC_M = 128;                        // rows per tile (MMA M)
-constexpr int XTC_KC = 32;                        // fp32 columns per chunk (= MMA K of int8)
-constexpr int XTC_STAGE = XTC_M * XTC_KC * 4;     // 16 KB per ring stage
+constexpr int XTC_KC = 32;                        // fp32 columns per TMA box (= MMA K of int8)
+constexpr int XTC_SUB = 2;                        // boxes per chunk (one sync round trip)
+constexpr int XTC_BOX = XTC_M * XTC_KC * 4;       // 16 KB
+constexpr int XTC_STAGE = XTC_BOX;                // 16 KB per ring stage (a chunk = SUB stages)
 constexpr int XTC_TPU = 8;                        // tiles per unit
 constexpr int XTC_MAX_I0 = 512;
-constexpr int XTC_THREADS = 320;
+// warps: 8 converters, 4 EG epilogue (EG = 1 for N <= 48, else 2), MMA, TMA
+template <int N> __host__ __device__ constexpr int xtc_eg() { return 2; }
+constexpr int XTC_U2R = 8;        // A2 rows staged per tile
+constexpr int XTC_PF = 0;         // tiles bulk-prefetched into L2 ahead (0: off; 1 measured slower)
+template <int N> __host__ __device__ constexpr int xtc_threads() { return (10 + 4 * xtc_eg<N>()) * 32; }
 constexpr int XTC_SMEM_MAX = 227 * 1024;
 constexpr float XTC_MAGIC = 14712960.0f;          // 1.5 * 2^23 + 0x208080
 
 struct XtcBlock {
   long long I0, I1, I2, J;
-  int R, ntiles, nch, nsup;
+  int R, ntiles, nch;
   int ex;                 // fixed-point exponent of X
   int ufirst, nunits;
   int bimg_bytes;
   double* aux;            // [0,64): scale_r; [64,128): 2^21 sum_k p_kr
-  double* ut1;            // [r][I1] = A1[i1, r]
-  double* ut2;            // [r][I2] = A2[i2, r]
-  unsigned char* bimg;    // 3 slices x nsup x N x 128 B (K-major, 128-B swizzle)
+  float* ut1;             // [r][I1] = A1[i1, r] (fp32 row weights)
+  float* ut2;             // [r][I2] = A2[i2, r]
+  const float* X;         // the block (for L2 prefetch of whole tiles)
+  unsigned char* bimg;    // 3 slices x (SUB nch) K=32 steps x N rows x 32 B (K-major, 32-B swizzle)
 };
 
 struct XtcUnit { int s, t0, t1, u; };
@@ -95,6 +106,8 @@ struct XtcArgs {
   int nunits;
   int nst;
   int bimg_max;
+  int dbg;                 // experiments: 1 = no epilogue math, 2 = no conversion math
+  int u1_bytes;            // smem bytes of the staged A1^T table (0: read it from L2)
   double* part;           // [unit][64]
   int* cnt;               // per-block arrival counters (self-resetting)
   double* bsum;           // [s][RSTRIDE]
@@ -102,7 +115,7 @@ struct XtcArgs {
 };
 
 struct XtcPlan {
-  int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0;
+  int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, u1_bytes = 0;
   size_t smem = 0;
   double bytes = 0.0;
   std::vector<void*> allocs;
@@ -164,8 +177,7 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     }
   }
   __syncthreads();
-  const long long slice = (long long)b.nsup * N * 128;
-  const int kmax = b.nsup * 128;
+  const int kmax = b.nch * XTC_SUB * 32;
   for (int e = threadIdx.x; e < kmax * N; e += 256) {
     const int k = e / N, n = e - (e / N) * N;
     long long p = 0;
@@ -174,11 +186,17 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     const long long p1 = (p - d2) >> 8;
     const long long d1 = ((p1 + 128) & 255) - 128;
     const long long d0 = (p1 - d1) >> 8;
-    const int q = k >> 7, kk = k & 127;
-    const long long off = ((long long)q * N + n) * 128 + (((kk >> 4) ^ (n & 7)) << 4) + (kk & 15);
+    // chunk c = k / 32: N rows of 32 bytes, 16-byte halves swapped on rows
+    // with bit 2 set (Swizzle<1,4,3> of a 256-byte atom)
+    // K step c = k / 32 holds the three slices as one operand of 3N rows
+    // ([b0 | b1 | b2], so one MMA covers a digit of A times all three), rows
+    // of 32 bytes, 16-byte halves swapped on rows with bit 2 set
+    // (Swizzle<1,4,3> of a 256-byte atom; N % 16 == 0 keeps it per slice)
+    const int c = k >> 5, kk = k & 31;
+    const long long off = ((long long)c * 3 * N + n) * 32 + (((kk >> 4) ^ ((n >> 2) & 1)) << 4) + (kk & 15);
     b.bimg[off] = (unsigned char)(signed char)d0;
-    b.bimg[slice + off] = (unsigned char)(signed char)d1;
-    b.bimg[2 * slice + off] = (unsigned char)(signed char)d2;
+    b.bimg[off + N * 32] = (unsigned char)(signed char)d1;
+    b.bimg[off + 2 * N * 32] = (unsigned char)(signed char)d2;
   }
   for (int r = warp; r < N; r += 8) {
     double t = 0.0;   // integers < 2^30: exact in any order
@@ -193,11 +211,11 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
   const long long I1 = b.I1, I2 = b.I2;
   for (long long e = threadIdx.x; e < (long long)R * I1; e += 256) {
     const long long r = e / I1, i = e - r * I1;
-    b.ut1[e] = A1[i * R + r];
+    b.ut1[e] = (float)A1[i * R + r];
   }
   for (long long e = threadIdx.x; e < (long long)R * I2; e += 256) {
     const long long r = e / I2, i = e - r * I2;
-    b.ut2[e] = A2[i * R + r];
+    b.ut2[e] = (float)A2[i * R + r];
   }
 }
 
@@ -213,38 +231,91 @@ __device__ __forceinline__ uint32_t pick3(uint32_t t0, uint32_t t1, uint32_t t2,
 }
 
 template <int N>
-__global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
+__host__ __device__ constexpr int xtc_nsl() { return N <= 48 ? 4 : 2; }   // TMEM A slots
+
+// sum over the 32 lanes of v[0..8) by recursive halving (9 fp64 shuffles
+// instead of 40); lane l ends with the total of value l / 4.  Fixed order:
+// bitwise deterministic.
+__device__ __forceinline__ double fold8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int o = 16 >> st;
+    const int c = 8 >> st;
+    if (c > 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < c / 2; ++i) {
+        const double send = up ? v[i] : v[i + c / 2];
+        const double keep = up ? v[i + c / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  return v[0];
+}
+
+// int32 -> double through the fp64 adder (exact): 2^52 + 2^31 + x
+__device__ __forceinline__ double i2d_exact(uint32_t x) {
+  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+template <int N>
+__global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
-  constexpr int NH = N / 2;          // columns per epilogue group
+  constexpr int EG = xtc_eg<N>();    // epilogue groups
+  constexpr int NH = N / EG;         // columns per epilogue group
+  constexpr int NE = 128 * EG;       // epilogue threads
+  constexpr int WMMA = 8 + 4 * EG, WTMA = WMMA + 1;
+  constexpr int NSL = xtc_nsl<N>();  // TMEM A slots (even: slot parity = group)
+  constexpr uint32_t SLOTW = 24u * XTC_SUB;   // 3 slices x SUB x 8 columns
+  constexpr uint32_t DBASE = SLOTW * NSL;
   extern __shared__ unsigned char xtc_raw[];
   const uint32_t raw_u32 = smem_u32(xtc_raw);
   unsigned char* sm = xtc_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
-  const int nst = a.nst;
+  const int nst = a.nst;             // power of two
   unsigned char* ring = sm;
   unsigned char* bimg = sm + (size_t)nst * XTC_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bimg + a.bimg_max);
+  float* u1s = reinterpret_cast<float*>(bimg + a.bimg_max);       // [r][I1] of the segment
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bimg + a.bimg_max + a.u1_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + nst;
   uint64_t* a_full = bars + 2 * nst;
-  uint64_t* a_empty = a_full + 4;
-  uint64_t* d_full = a_empty + 4;
+  uint64_t* a_empty = a_full + 8;
+  uint64_t* d_full = a_empty + 8;
   uint64_t* d_empty = d_full + 2;
   uint64_t* b_full = d_empty + 2;
   uint64_t* b_empty = b_full + 1;
-  double* red = reinterpret_cast<double*>(b_empty + 1);      // [2 groups][4 warps][32]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + 256);
+  double* red = reinterpret_cast<double*>(b_empty + 1);      // [EG groups][4 warps][64]
+  double* auxs = red + 512;                                  // [128] of the segment
+  float* u2s = reinterpret_cast<float*>(auxs + 128);         // [2][XTC_U2R][64]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u2s + 2 * XTC_U2R * 64);
   int* shflag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
+  // experiments (CB_XTC_DBG & 8): cycles each role spends in its waits
+  long long twait[6] = {0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+#define XTC_TW(k, call)                                  \
+  do {                                                   \
+    if (a.dbg & 8) {                                     \
+      const long long t0_ = clock64();                   \
+      call;                                              \
+      twait[k] += clock64() - t0_;                       \
+    } else {                                             \
+      call;                                              \
+    }                                                    \
+  } while (0)
   const int u_begin = (int)((long long)blockIdx.x * a.nunits / G);
   const int u_end = (int)((long long)(blockIdx.x + 1) * a.nunits / G);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 128); }
-    for (int i = 0; i < 4; ++i) { mbar_init(&a_full[i], 128); mbar_init(&a_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], 256); }
+    for (int i = 0; i < NSL; ++i) { mbar_init(&a_full[i], 128); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], NE); }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
     mbar_fence_init();
@@ -255,15 +326,29 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 9) {
+  if (warp == WTMA) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      int g = 0, seg = 0, cur = -1;
+      int st = 0, ph = 0, seg = 0, cur = -1;
+      // L2 prefetch runs XTC_PF tiles ahead of the ring: a tile (128 rows x
+      // I0) is one contiguous span, one bulk prefetch
+      int pu = u_begin, pt = a.units[u_begin].t0;
+      auto prefetch_next = [&]() {
+        if (pu >= u_end) return;
+        const XtcUnit pn = a.units[pu];
+        const XtcBlock& pb = a.blk[pn.s];
+        const long long r0 = (long long)pt * XTC_M;
+        const long long nr = min((long long)XTC_M, pb.J - r0);
+        bulk_prefetch_l2(pb.X + r0 * pb.I0, (uint32_t)(nr * pb.I0 * 4));
+        if (++pt >= pn.t1) { ++pu; if (pu < u_end) pt = a.units[pu].t0; }
+      };
+      if (XTC_PF > 0)
+        for (int k = 0; k <= XTC_PF; ++k) prefetch_next();
       for (int u = u_begin; u < u_end; ++u) {
         const XtcUnit un = a.units[u];
         const XtcBlock& b = a.blk[un.s];
         const int nch = b.nch;
-        if (un.s != cur) {
+        if (un.s != cur && !(a.dbg & 4)) {
           mbar_wait(b_empty, (seg & 1) ^ 1);
           const int bytes = b.bimg_bytes;
           mbar_arrive_expect_tx(b_full, (uint32_t)bytes);
@@ -274,26 +359,30 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
         }
         const CUtensorMap* tm = a.tmaps + un.s;
         for (int t = un.t0; t < un.t1; ++t) {
-          for (int c = 0; c < nch; ++c, ++g) {
-            const int st = g % nst;
-            mbar_wait(&empty[st], ((g / nst) & 1) ^ 1);
+          if (XTC_PF > 0) prefetch_next();
+          for (int c = 0; c < nch * XTC_SUB; ++c) {
+            XTC_TW(0, mbar_wait(&empty[st], ph ^ 1));
             mbar_arrive_expect_tx(&full[st], XTC_STAGE);
             tma_load_2d(ring + (size_t)st * XTC_STAGE, tm, c * XTC_KC, t * XTC_M, &full[st]);
+            if (++st == nst) { st = 0; ph ^= 1; }
           }
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == WMMA) {
     // --------------------------------------------------------- MMA issuer
-    constexpr uint32_t idu = idesc_i8(N, 0, 1);     // a0 (unsigned) x b (signed)
-    constexpr uint32_t ids = idesc_i8(N, 1, 1);     // a1, a2 (signed) x b (signed)
+    if (a.dbg & 4) goto done;
+    // D[L0 | L1 | L2] += a0 [b0|b1|b2]; D[L1 | L2] += a1 [b0|b1]; D[L2] += a2 b0
+    constexpr uint32_t id0 = idesc_i8(3 * N, 0, 1);   // a0 unsigned x b signed
+    constexpr uint32_t id1 = idesc_i8(2 * N, 1, 1);   // a1 signed
+    constexpr uint32_t id2 = idesc_i8(N, 1, 1);       // a2 signed
     int g = 0, seg = 0, cur = -1, tl = 0;
+    int slot = 0, sphase = 0;
     const uint32_t bbase = smem_u32(bimg);
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
       const XtcBlock& b = a.blk[un.s];
       const int nch = b.nch;
-      const uint32_t sl = (uint32_t)b.nsup * N * 128;
       if (un.s != cur) {
         mbar_wait(b_full, seg & 1);
         tc_fence_after();
@@ -303,25 +392,23 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
       const bool last_seg = (u + 1 == u_end) || a.units[u + 1].s != un.s;
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
         const int buf = tl & 1;
-        mbar_wait(&d_empty[buf], ((tl >> 1) & 1) ^ 1);
+        XTC_TW(1, mbar_wait(&d_empty[buf], ((tl >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t dc = tmem + 128 + (uint32_t)(buf * 3 * N);
+        const uint32_t dc = tmem + DBASE + (uint32_t)(buf * 3 * N);
         for (int c = 0; c < nch; ++c, ++g) {
-          const int slot = g & 3;
-          mbar_wait(&a_full[slot], (g >> 2) & 1);
+          XTC_TW(2, mbar_wait(&a_full[slot], sphase));
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t ac = tmem + 32u * slot;
-            const uint32_t bb = bbase + (uint32_t)(c >> 2) * N * 128 + (uint32_t)(c & 3) * 32;
-            const uint64_t B0 = sdesc_k_sw128(bb), B1 = sdesc_k_sw128(bb + sl),
-                           B2 = sdesc_k_sw128(bb + 2 * sl);
-            const uint32_t acc = c > 0 ? 1u : 0u;
-            mma_i8_ts(dc, ac, B0, idu, acc);
-            mma_i8_ts(dc + N, ac, B1, idu, acc);
-            mma_i8_ts(dc + N, ac + 8, B0, ids, 1u);
-            mma_i8_ts(dc + 2 * N, ac, B2, idu, acc);
-            mma_i8_ts(dc + 2 * N, ac + 8, B1, ids, 1u);
-            mma_i8_ts(dc + 2 * N, ac + 16, B0, ids, 1u);
+#pragma unroll
+            for (int k = 0; k < XTC_SUB; ++k) {
+              // slot layout: slice j of K step k at column 8 (SUB j + k)
+              const uint32_t ac = tmem + SLOTW * slot + 8u * k;
+              const uint64_t B = sdesc_k_sw32(bbase + (uint32_t)(c * XTC_SUB + k) * 3 * N * 32);
+              const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
+              mma_i8_ts(dc, ac, B, id0, acc);
+              mma_i8_ts(dc + N, ac + 8 * XTC_SUB, B, id1, 1u);
+              mma_i8_ts(dc + 2 * N, ac + 16 * XTC_SUB, B, id2, 1u);
+            }
             tc_commit(&a_empty[slot]);
             if (c == nch - 1) {
               tc_commit(&d_full[buf]);
@@ -329,142 +416,227 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
             }
           }
           __syncwarp();
+          if (++slot == NSL) { slot = 0; sphase ^= 1; }
         }
       }
     }
-  } else {
-    // ------------------------------------- converters + epilogue (warps 0-7)
+  } else if (warp < 8) {
+    // ------------------------------------------------ converters (warps 0-7)
+    // two groups of 4 (one warp per TMEM lane quarter) alternate chunks
     const int h = warp >> 2;
     const int wq = warp & 3;
     const int m = wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    double acc[NH];
-#pragma unroll
-    for (int j = 0; j < NH; ++j) acc[j] = 0.0;
-    int g = 0, tl = 0;
-    // deferred epilogue state
-    int p_valid = 0, p_s = 0, p_t = 0, p_tl = 0, p_u = -1, p_flush = 0;
-
-    auto epilogue = [&](int s, int t, int tloc) {
-      const XtcBlock& b = a.blk[s];
-      const int buf = tloc & 1;
-      mbar_wait(&d_full[buf], (tloc >> 1) & 1);
-      tc_fence_after();
-      const long long row = (long long)t * XTC_M + m;
-      const bool valid = row < b.J;
-      const long long i2 = valid ? row / b.I1 : 0;
-      const long long i1 = valid ? row - i2 * b.I1 : 0;
-      const uint32_t dc = trow + 128 + (uint32_t)(buf * 3 * N);
-#pragma unroll
-      for (int cg = 0; cg < NH / 8; ++cg) {
-        const int col0 = h * NH + cg * 8;
-        uint32_t l0[8], l1[8], l2[8];
-        tmem_ld8(dc + col0, l0);
-        tmem_ld8(dc + N + col0, l1);
-        tmem_ld8(dc + 2 * N + col0, l2);
-        tmem_wait_ld();
-        if (valid) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int r = col0 + j;
-            if (r < b.R) {
-              const double v = fma((double)(int)l0[j], 4294967296.0,
-                                   fma((double)(int)l1[j], 16777216.0,
-                                       fma((double)(int)l2[j], 65536.0, -b.aux[64 + r])));
-              const double w = b.ut1[(long long)r * b.I1 + i1] * b.ut2[(long long)r * b.I2 + i2];
-              acc[cg * 8 + j] = fma(v * b.aux[r], w, acc[cg * 8 + j]);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&d_empty[buf]);
-    };
-
-    auto flush = [&](int s, int u) {
-#pragma unroll
-      for (int j = 0; j < NH; ++j) {
-        double v = acc[j];
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[(h * 4 + wq) * 32 + j] = v;
-        acc[j] = 0.0;
-      }
-      named_bar(1, 256);
-      if (threadIdx.x < N) {
-        const int r = threadIdx.x, hh = r / NH, jj = r - hh * NH;
-        const double* q = red + hh * 4 * 32 + jj;
-        a.part[(long long)u * 64 + r] = ((q[0] + q[32]) + q[64]) + q[96];
-        __threadfence();
-      }
-      named_bar(1, 256);
-      if (threadIdx.x == 0) {
-        const XtcBlock& b = a.blk[s];
-        const int prev = atomicAdd(&a.cnt[s], 1);
-        const int last = prev == b.nunits - 1;
-        if (last) a.cnt[s] = 0;
-        *shflag = last;
-      }
-      named_bar(1, 256);
-      if (*shflag) {
-        __threadfence();
-        const XtcBlock& b = a.blk[s];
-        if (threadIdx.x < b.R) {
-          double t = 0.0;
-          for (int k = 0; k < b.nunits; ++k)
-            t += __ldcg(&a.part[(long long)(b.ufirst + k) * 64 + threadIdx.x]);
-          a.bsum[(long long)s * RSTRIDE + threadIdx.x] = t;
-        }
-      }
-    };
-
+    int g = 0;
+    // slot / phase of this group's next chunk: chunks alternate between the
+    // groups, slots cycle through NSL (even), so group h owns the slots of
+    // parity h and advances by 2; ring stages likewise (any nst >= 2)
+    int slot = h, sphase = 0;
+    int rst = XTC_SUB * h, rph = 0;   // first ring stage of this group's next chunk
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
       const XtcBlock& b = a.blk[un.s];
       const int nch = b.nch;
       const float sx = ldexpf(1.0f, 20 - b.ex);
-      for (int t = un.t0; t < un.t1; ++t, ++tl) {
-        for (int c = 0; c < nch; ++c, ++g) {
-          if ((g & 1) != h) continue;
-          const int st = g % nst;
-          mbar_wait(&full[st], (g / nst) & 1);
-          const float4* rowp = reinterpret_cast<const float4*>(ring + (size_t)st * XTC_STAGE + m * 128);
-          uint32_t w0[8], w1[8], w2[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 v = rowp[q ^ (m & 7)];
-            const uint32_t t0 = __float_as_uint(fmaf(v.x, sx, XTC_MAGIC));
-            const uint32_t t1 = __float_as_uint(fmaf(v.y, sx, XTC_MAGIC));
-            const uint32_t t2 = __float_as_uint(fmaf(v.z, sx, XTC_MAGIC));
-            const uint32_t t3 = __float_as_uint(fmaf(v.w, sx, XTC_MAGIC));
-            w0[q] = pick3(t0, t1, t2, t3, 2) & 0x3F3F3F3Fu;
-            w1[q] = pick3(t0, t1, t2, t3, 1) ^ 0x80808080u;
-            w2[q] = pick3(t0, t1, t2, t3, 0) ^ 0x80808080u;
+      for (int t = un.t0; t < un.t1; ++t) {
+        for (int c = (h - g) & 1; c < nch; c += 2) {
+          // the chunk's SUB stages (consecutive; nst is even and the
+          // group's stages start at multiples of SUB, so no wrap inside)
+          const int st0 = rst, ph0 = rph;
+          rst += 2 * XTC_SUB;
+          if (rst >= nst) { rst -= nst; rph ^= 1; }
+          if (a.dbg & 4) {
+            for (int k = 0; k < XTC_SUB; ++k) {
+              XTC_TW(3, mbar_wait(&full[st0 + k], ph0));
+              mbar_arrive(&empty[st0 + k]);
+            }
+            continue;
           }
-          mbar_arrive(&empty[st]);
-          const int slot = g & 3;
-          mbar_wait(&a_empty[slot], ((g >> 2) & 1) ^ 1);
+          XTC_TW(4, mbar_wait(&a_empty[slot], sphase ^ 1));
           tc_fence_after();
-          const uint32_t ac = trow + 32u * slot;
-          tmem_st8(ac, w0);
-          tmem_st8(ac + 8, w1);
-          tmem_st8(ac + 16, w2);
+          const uint32_t ac = trow + SLOTW * slot;
+#pragma unroll
+          for (int k = 0; k < XTC_SUB; ++k) {
+            // a stage into registers, released before its conversion (the
+            // ring stays in flight)
+            XTC_TW(3, mbar_wait(&full[st0 + k], ph0));
+            const float4* rowp =
+                reinterpret_cast<const float4*>(ring + (size_t)(st0 + k) * XTC_STAGE + m * 128);
+            float4 vv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) vv[q] = rowp[q ^ (m & 7)];
+            mbar_arrive(&empty[st0 + k]);
+            uint32_t w0[8], w1[8], w2[8];
+            if (a.dbg & 2) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) { w0[q] = 0x20202020u; w1[q] = 0; w2[q] = 0; }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const uint32_t t0 = __float_as_uint(fmaf(vv[q].x, sx, XTC_MAGIC));
+                const uint32_t t1 = __float_as_uint(fmaf(vv[q].y, sx, XTC_MAGIC));
+                const uint32_t t2 = __float_as_uint(fmaf(vv[q].z, sx, XTC_MAGIC));
+                const uint32_t t3 = __float_as_uint(fmaf(vv[q].w, sx, XTC_MAGIC));
+                w0[q] = pick3(t0, t1, t2, t3, 2) & 0x3F3F3F3Fu;
+                w1[q] = pick3(t0, t1, t2, t3, 1) ^ 0x80808080u;
+                w2[q] = pick3(t0, t1, t2, t3, 0) ^ 0x80808080u;
+              }
+            }
+            tmem_st8(ac + 8 * k, w0);
+            tmem_st8(ac + 8 * (XTC_SUB + k), w1);
+            tmem_st8(ac + 8 * (2 * XTC_SUB + k), w2);
+          }
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&a_full[slot]);
+          slot += 2;
+          if (slot >= NSL) { slot -= NSL; sphase ^= 1; }
         }
-        if (p_valid) {
-          epilogue(p_s, p_t, p_tl);
-          if (p_flush) flush(p_s, p_u);
-        }
-        p_valid = 1; p_s = un.s; p_t = t; p_tl = tl; p_u = un.u;
-        p_flush = (t == un.t1 - 1);
+        g += nch;
       }
     }
-    if (p_valid) {
-      epilogue(p_s, p_t, p_tl);
-      if (p_flush) flush(p_s, p_u);
+  } else if (!(a.dbg & 4)) {
+    // ------------------------------------------ epilogue (warps 8 .. 8+4EG-1)
+    // EG groups of 4 (one warp per lane quarter), each for N/EG of the
+    // columns: row weights A1[i1,r] (staged per segment) x A2[i2,r] (the
+    // tile's few A2 rows, cp.async-staged one tile ahead), the int32 levels
+    // of D from TMEM, fp64 row sums per thread; per unit a fixed-order
+    // reduction into a partial, per block a fold in unit order
+    const int et = threadIdx.x - 256;
+    const int h = (warp - 8) >> 2;
+    const int wq = warp & 3;
+    const int m = wq * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
+    // per-lane unit sums: after each tile's 8-column warp fold, lane l holds
+    // column cg*8 + l/4 of this warp's 32 rows
+    double acc[NH / 8];
+#pragma unroll
+    for (int j = 0; j < NH / 8; ++j) acc[j] = 0.0;
+    // stage the A2 rows of tile (s, t) into u2s[buf]: rows i2 of its first
+    // .. last row (<= XTC_U2R of them, else the epilogue reads L2)
+    auto stage_u2 = [&](int s, int t, int buf) {
+      const XtcBlock& b = a.blk[s];
+      const long long r0 = (long long)t * XTC_M;
+      const long long r1 = std::min(r0 + XTC_M, b.J) - 1;
+      const long long i2a = r0 / b.I1;
+      const int n2 = (int)(r1 / b.I1 - i2a + 1);   // <= XTC_U2R (I1 >= 19, host-checked)
+      for (int e = et; e < n2 * 64; e += NE) {
+        const int k = e >> 6, r = e & 63;
+        if (r < b.R)
+          cp_async4(u2s + buf * XTC_U2R * 64 + e, b.ut2 + (long long)r * b.I2 + i2a + k);
+      }
+    };
+    int tl = 0, cur = -1;
+    int nxt_u = u_begin, nxt_t = a.units[u_begin].t0;   // the tile after the current one
+    auto advance = [&](int& uu, int& tt) {
+      if (++tt >= a.units[uu].t1) { ++uu; if (uu < u_end) tt = a.units[uu].t0; }
+    };
+    stage_u2(a.units[nxt_u].s, nxt_t, 0);
+    cp_async_commit();
+    advance(nxt_u, nxt_t);
+    for (int u = u_begin; u < u_end; ++u) {
+      const XtcUnit un = a.units[u];
+      const XtcBlock& b = a.blk[un.s];
+      const int I1 = (int)b.I1, I2 = (int)b.I2;
+      const long long J = b.J;
+      const int R = b.R;
+      if (un.s != cur) {
+        // a new segment: the block's column constants and A1^T table
+        cur = un.s;
+        named_bar(1, NE);
+        if (et < 128) auxs[et] = b.aux[et];
+        for (int e = et; e < R * I1; e += NE) u1s[e] = b.ut1[e];
+      }
+      for (int t = un.t0; t < un.t1; ++t, ++tl) {
+        const int buf = tl & 1;
+        cp_async_wait_all();          // this thread's copies for tile t
+        named_bar(1, NE);             // everyone's; buf ^ 1 is free again
+        if (nxt_u < u_end) {
+          stage_u2(a.units[nxt_u].s, nxt_t, buf ^ 1);
+          advance(nxt_u, nxt_t);
+        }
+        cp_async_commit();
+        const long long row = (long long)t * XTC_M + m;
+        const bool valid = row < J;
+        const int i2 = valid ? (int)(row / I1) : 0;
+        const int i1 = valid ? (int)(row - (long long)i2 * I1) : 0;
+        const int i2a = (int)(((long long)t * XTC_M) / I1);
+        const long long r1 = std::min((long long)t * XTC_M + XTC_M, J) - 1;
+        (void)r1;
+        const float* u1 = u1s + i1;                                   // shared
+        const float* u2 = u2s + buf * XTC_U2R * 64 + (i2 - i2a) * 64; // shared
+        XTC_TW(5, mbar_wait(&d_full[buf], (tl >> 1) & 1));
+        tc_fence_after();
+        const uint32_t dc = trow + DBASE + (uint32_t)(buf * 3 * N);
+        const double* corr = auxs + 64;
+#pragma unroll
+        for (int cg = 0; cg < NH / 8; ++cg) {
+          const int col0 = h * NH + cg * 8;
+          uint32_t l0[8], l1[8], l2[8];
+          tmem_ld8(dc + col0, l0);
+          tmem_ld8(dc + N + col0, l1);
+          tmem_ld8(dc + 2 * N + col0, l2);
+          float w[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = col0 + j;
+            w[j] = (valid && r < R) ? u1[r * I1] * u2[r] : 0.0f;
+          }
+          tmem_wait_ld();
+          if (a.dbg & 1) continue;
+          double c8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double v = fma(i2d_exact(l0[j]), 4294967296.0,
+                                 fma(i2d_exact(l1[j]), 16777216.0,
+                                     fma(i2d_exact(l2[j]), 65536.0, -corr[col0 + j])));
+            c8[j] = v * (double)w[j];
+          }
+          acc[cg] += fold8(c8, lane);
+        }
+        tc_fence_before();
+        mbar_arrive(&d_empty[buf]);
+        if (t == un.t1 - 1) {
+          // unit done: fixed-order reduction over the 128 rows
+#pragma unroll
+          for (int j = 0; j < NH / 8; ++j) {
+            if ((lane & 3) == 0) red[(h * 4 + wq) * 64 + j * 8 + (lane >> 2)] = acc[j];
+            acc[j] = 0.0;
+          }
+          named_bar(1, NE);
+          if (et < N) {
+            const int r = et, hh = r / NH, jj = r - hh * NH;
+            const double* q = red + hh * 4 * 64 + jj;
+            a.part[(long long)un.u * 64 + r] = (((q[0] + q[64]) + q[128]) + q[192]) * auxs[r];
+            __threadfence();
+          }
+          named_bar(1, NE);
+          if (et == 0) {
+            const int prev = atomicAdd(&a.cnt[un.s], 1);
+            const int last = prev == b.nunits - 1;
+            if (last) a.cnt[un.s] = 0;
+            *shflag = last;
+          }
+          named_bar(1, NE);
+          if (*shflag) {
+            __threadfence();
+            if (et < R) {
+              double s = 0.0;
+              for (int k = 0; k < b.nunits; ++k)
+                s += __ldcg(&a.part[(long long)(b.ufirst + k) * 64 + et]);
+              a.bsum[(long long)un.s * RSTRIDE + et] = s;
+            }
+          }
+          // red / shflag / auxs are reused only after the next barrier
+        }
+      }
     }
+    cp_async_wait_all();
   }
+done:
+  if ((a.dbg & 8) && blockIdx.x == 0 && lane == 0)
+    printf("xtc cta0 warp %2d: total %lld  waits empty %lld d_empty %lld a_full %lld full %lld a_empty %lld d_full %lld\n",
+           warp, clock64() - t_start, twait[0], twait[1], twait[2], twait[3], twait[4], twait[5]);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -483,7 +655,6 @@ static int n_bucket(int rmax) {
   return 64;
 }
 
-static int nsup_of(long long I0) { return (int)((I0 + 127) / 128); }
 
 bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R) {
   if (getenv("CB_NO_XTC")) return false;
@@ -493,6 +664,7 @@ bool xtc_supported(int S, const void* const* X, const long long* dims, const int
     if (I0 % 4 != 0 || I0 > XTC_MAX_I0) return false;
     if (I1 * I2 >= (1LL << 31)) return false;
     if (R[s] < 1 || R[s] > 64) return false;
+    if (I1 < 19) return false;            // a tile's rows span <= XTC_U2R values of i2
     if ((reinterpret_cast<uintptr_t>(X[s]) & 15) != 0) return false;
   }
   return true;
@@ -517,8 +689,9 @@ static EncodeTiledFn encode_fn() {
 }
 
 template <int N>
-static size_t xtc_smem_for(int nst, int bimg_max) {
-  return 1024 + (size_t)nst * XTC_STAGE + bimg_max + 8 * (2 * nst + 14) + 256 * 8 + 16;
+static size_t xtc_smem_for(int nst, int bimg_max, int u1_bytes) {
+  return 1024 + (size_t)nst * XTC_STAGE + bimg_max + u1_bytes + 8 * (2 * nst + 22) + 640 * 8 +
+         2 * XTC_U2R * 64 * 4 + 16;
 }
 
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
@@ -546,10 +719,9 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     b.J = b.I1 * b.I2;
     b.R = R[s];
     b.ntiles = (int)((b.J + XTC_M - 1) / XTC_M);
-    b.nch = (int)((b.I0 + XTC_KC - 1) / XTC_KC);
-    b.nsup = nsup_of(b.I0);
+    b.nch = (int)((b.I0 + XTC_SUB * XTC_KC - 1) / (XTC_SUB * XTC_KC));
     b.ex = 0;
-    b.bimg_bytes = 3 * b.nsup * N * 128;
+    b.bimg_bytes = 3 * b.nch * XTC_SUB * N * 32;
     p->bimg_max = std::max(p->bimg_max, b.bimg_bytes);
     b.ufirst = (int)hu.size();
     for (int t = 0; t < b.ntiles; t += XTC_TPU)
@@ -581,22 +753,29 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   p->grid = std::max(1, std::min(nsm, p->nunits));
   // ring stages: what fits beside the B image, even (each stage then always
   // serves the same converter group), at least 2
-  const size_t fixed = xtc_smem_for<16>(0, p->bimg_max);
+  // shared memory: the B image, the segment's A1^T table (fp32, N x I1) when
+  // it fits beside a 4-stage ring, then as many ring stages (power of two,
+  // <= 8) as fit
+  long long i1max = 1;
+  for (int s = 0; s < S; ++s) i1max = std::max(i1max, hb[s].I1);
+  int u1b = (int)(((long long)rmax * i1max * 4 + 127) / 128 * 128);
+  p->u1_bytes = u1b;
+  const size_t fixed = xtc_smem_for<16>(0, p->bimg_max, u1b);
   int nst = (int)((XTC_SMEM_MAX - fixed) / (XTC_STAGE + 16));
-  nst = std::min(nst, 12) & ~1;
-  if (nst < 2) {
+  nst = std::min(nst, 12) & ~1;   // even (chunks never wrap), >= 2 SUB
+  if (nst < 2 * XTC_SUB) {
     delete p;
     set_error("xtc: operand image too large (%d bytes)", p->bimg_max);
     return CB_ERR_UNSUPPORTED;
   }
   p->nst = nst;
-  p->smem = xtc_smem_for<16>(nst, p->bimg_max);
+  p->smem = xtc_smem_for<16>(nst, p->bimg_max, u1b);
   // device buffers
   std::vector<void*>& A = p->allocs;
   int rc = CB_OK;
 #define XTRY(x) do { rc = (x); if (rc) { xtc_plan_destroy(p); return rc; } } while (0)
   double* aux = nullptr;
-  double* ut = nullptr;
+  float* ut = nullptr;
   unsigned char* bimg = nullptr;
   XTRY(dalloc((void**)&p->tmaps, sizeof(CUtensorMap) * S, A));
   XTRY(dalloc((void**)&p->blk, sizeof(XtcBlock) * S, A));
@@ -605,7 +784,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   XTRY(dalloc((void**)&p->cnt, sizeof(int) * S, A));
   XTRY(dalloc((void**)&p->maxbits, sizeof(unsigned int) * S, A));
   XTRY(dalloc((void**)&aux, sizeof(double) * 128 * S, A));
-  XTRY(dalloc((void**)&ut, sizeof(double) * ut_elems, A));
+  XTRY(dalloc((void**)&ut, sizeof(float) * ut_elems, A));
   XTRY(dalloc((void**)&bimg, (size_t)bimg_total, A));
   long long uo = 0, bo = 0;
   for (int s = 0; s < S; ++s) {
@@ -615,6 +794,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     b.ut2 = ut + uo + 64 * b.I1;
     uo += 64 * (b.I1 + b.I2);
     b.bimg = bimg + bo;
+    b.X = reinterpret_cast<const float*>(X[s]);
     bo += b.bimg_bytes;
   }
   CB_CUDA(cudaMemcpyAsync(p->tmaps, hm.data(), sizeof(CUtensorMap) * S, cudaMemcpyHostToDevice, st));
@@ -656,7 +836,7 @@ double xtc_bytes(const XtcPlan* p) { return p ? p->bytes : 0.0; }
 template <int N>
 static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStream_t st) {
   CB_CUDA(launch_k(k_xtc_prep<N>, dim3(p->S), dim3(256), 0, st, a, U));
-  CB_CUDA(launch_k(k_xtc_trace<N>, dim3(p->grid), dim3(XTC_THREADS), p->smem, st, a));
+  CB_CUDA(launch_k(k_xtc_trace<N>, dim3(p->grid), dim3(xtc_threads<N>()), p->smem, st, a));
   count_launch(2);
   return CB_OK;
 }
@@ -670,6 +850,8 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.nunits = p->nunits;
   a.nst = p->nst;
   a.bimg_max = p->bimg_max;
+  a.u1_bytes = p->u1_bytes;
+  { static const char* e = getenv("CB_XTC_DBG"); a.dbg = e ? atoi(e) : 0; }
   a.part = p->part;
   a.cnt = p->cnt;
   a.bsum = bsum;

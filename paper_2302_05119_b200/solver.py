@@ -18,9 +18,10 @@ like the reference, gram expansion in fp32; or force "explicit" /
 "expansion") and ``SolverOptions.compute`` (arithmetic of the tensor passes
 when the storage is fp32: "auto" = fp64 for CoNCPD-APG, whose restart rule
 compares objectives that differ by ~1e-12 late in a run, and for the ALS
-compression, whose fixed point is sensitive; fp32 only for the lra
-original-tensor trace pass of ranks > 16, which feeds the reported trace
-alone).
+compression, whose fixed point is sensitive; "tc" for the lra
+original-tensor trace pass of ranks > 16, which feeds the reported trace and
+stop rule alone: the tensor-core pass of `cb_core_linear_term_tc`, ~2e-8
+relative on b.  "fp32" forces CUDA-core fp32 arithmetic in that pass).
 """
 
 from __future__ import annotations
@@ -142,7 +143,7 @@ class SolverOptions:
     trace_every: int = 1
     precision: str = "fp64"        # "fp64" parity mode | "fp32" throughput mode
     objective: str = "auto"        # "auto" | "explicit" | "expansion"
-    compute: str = "auto"          # fp32 storage: arithmetic of the tensor passes
+    compute: str = "auto"          # fp32 storage: "auto" | "fp64" | "fp32" | "tc" (lra trace)
 
     def __post_init__(self):
         if self.max_iter < 0:
@@ -157,7 +158,7 @@ class SolverOptions:
             raise ValueError(f"unknown precision {self.precision!r}")
         if self.objective not in ("auto", "explicit", "expansion"):
             raise ValueError(f"unknown objective evaluation {self.objective!r}")
-        if self.compute not in ("auto", "fp64", "fp32"):
+        if self.compute not in ("auto", "fp64", "fp32", "tc"):
             raise ValueError(f"unknown compute type {self.compute!r}")
 
 
@@ -449,8 +450,8 @@ class PreparedSolve:
         # may run in fp32 for large ranks
         compute = opts.compute
         if compute == "auto":
-            compute = "fp64" if (problem.mode == "full" or max(problem.ranks) <= 16) else "fp32"
-        self.compute_code = 1 if (prec == "fp32" and compute == "fp32") else 0
+            compute = "fp64" if (problem.mode == "full" or max(problem.ranks) <= 16) else "tc"
+        self.compute_code = {"fp64": 0, "fp32": 1, "tc": 2}[compute] if prec == "fp32" else 0
         self.als_compute_code = 1 if (prec == "fp32" and opts.compute == "fp32") else 0
         S, N = len(self.local), problem.order
         with torch.cuda.stream(self.stream):

@@ -45,12 +45,12 @@ def _want(x, g):
 
 
 SHAPES = [
-    ((400, 12, 30), 40),     # c5-like rank, 13 chunks incl. a 16-column tail
+    ((400, 24, 30), 40),     # c5-like rank, K tail (400 = 6 x 64 + 16)
     ((112, 92, 40), 20),     # c3 mode sizes (shortened), J tail tile
     ((64, 71, 60), 30),      # c4 shape
     ((100, 100, 10), 10),    # c2 modes, N bucket 16
-    ((36, 5, 7), 64),        # rank 64 bucket, a single partial tile
-    ((4, 3, 2), 3),          # tiny
+    ((36, 20, 7), 64),       # rank 64 bucket, a single partial tile
+    ((4, 19, 2), 3),         # tiny (I1 = 19: the smallest staged mode-1 size)
 ]
 
 
@@ -86,6 +86,14 @@ def test_tc_trace_batched_ragged_and_deterministic(P):
     single = P.core_linear_terms_tc([xs[1]], [gs[1]])[0]
     # (alone it may use a smaller N bucket: same products, same fold order)
     assert np.array_equal(single, got[1])
+
+
+def test_tc_trace_rejects_unsupported_shapes(P):
+    rng = np.random.default_rng(1)
+    for dims in ((6, 5, 4), (30, 20, 4)):      # I1 < 19; I0 % 4 != 0
+        x, g = _block(rng, dims, 3)
+        with pytest.raises(Exception):
+            P.core_linear_terms_tc([x], [g])
 
 
 def test_tc_trace_zero_and_scaled(P):
