@@ -239,10 +239,16 @@ def run_ours(args):
     # dominant streaming kernel = the one with the larger time per launch
     dom_name = max(kinds, key=lambda k: kinds[k]["ms_avg"])
     dom = kinds[dom_name]
+    # lra + compute "tc": the timed fiber-kind launch is the tensor-core trace
+    # pass (csrc/xtc.cu; same shape rule as xtc_supported)
+    tc_trace = (spec.mode == "lra" and getattr(run, "compute_code", 0) == 2 and
+                spec.dims[0] % 4 == 0 and spec.dims[0] <= 512 and spec.dims[1] >= 19 and
+                spec.rank <= 64)
     roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
             "frac": dom["gbs"] / peak, "traffic": None,
-            "kernel": {"slab": "slab3_kernel (mode-2 MTTKRP, row-dot)",
-                       "fiber": "fiber2_kernel (T = X x2 A2)"}[dom_name],
+            "kernel": ("k_xtc_trace (lra trace pass, tcgen05 kind::i8 tensor cores)" if tc_trace
+                       else {"slab": "slab3_kernel (mode-2 MTTKRP, row-dot)",
+                             "fiber": "fiber2_kernel (T = X x2 A2)"}[dom_name]),
             "bytes_per_launch": dom["bytes_per_launch"],
             "bytes_note": "algorithmic: every block element read once, sum_s |M_s| x 4 B",
             "peak_source": peak_kind, "kernels": kinds}
