@@ -815,6 +815,11 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   if (h->fast3) {
     build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab, h->S_tot);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
+    if (!h->tab.fib4.empty()) {
+      FibUnit* d4;
+      TRY(upload(h->tab.fib4, &d4, A, st));
+      h->tab.d_fib4 = d4;
+    }
     TRY(upload(h->tab.slab, &h->d_slab, A, st));
     TRY(upload(h->tab.c0, &h->d_c0, A, st));
     TRY(upload(h->tab.c1, &h->d_c1, A, st));

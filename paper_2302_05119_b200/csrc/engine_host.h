@@ -17,6 +17,11 @@ struct XTables {
   std::vector<RowUnit> c0, c1;
   int sb = 1;
   int fib_tj = 1;             // fiber tile: columns per thread (JT = 256 * fib_tj)
+  // fiber4 (xpass4.cuh) T-only units: its own tile (T is per column, so the
+  // tile does not change any bit; chosen to fill the SMs)
+  std::vector<FibUnit> fib4;
+  int fib4_tj = 0;
+  const FibUnit* d_fib4 = nullptr;   // device copy (set by the engine)
   long long fib_rows = 0;    // max i2 rows of a fiber unit (A2 rows staged per CTA)
   long long slab_rows = 0;   // A0+A1 rows the slab kernel stages (0: read through L1)
   // row-dot mode-2 kernel (xpass3.cuh): writes MTT[s] directly when set

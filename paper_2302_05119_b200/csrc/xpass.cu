@@ -21,6 +21,7 @@
 #include "status.h"
 #include "xpass2.cuh"
 #include "xpass3.cuh"
+#include "xpass4.cuh"
 
 namespace cb {
 
@@ -119,8 +120,45 @@ static void fiber3_dispatch(int rb, bool tma, const XArgs& a, const XTables& t, 
   else fiber3_go<TE, 16>(tma, a, t, st, prep);
 }
 
+// warp-specialised T pass (xpass4.cuh): T-only launches, fp32 storage with
+// fp64 arithmetic, unsplit T, rank bucket <= 16, bulk-copy rows
+static bool fiber4_ok(int pc, int rb, bool tma, const XTables& t) {
+  static const bool off = getenv("CB_NO_F4") != nullptr;
+  return !off && pc == PC_F32_F64 && rb <= 16 && tma && t.fiber_direct && t.fib4_tj > 0;
+}
+
+template <int RB, int TJ>
+static void fiber4_go(const XArgs& a, const FibUnit* u, int n, const XTables& t, cudaStream_t st,
+                      bool prep) {
+  const size_t sm = fiber4_smem<float>(t.fib_rows, RB, TJ);
+  if (prep) {
+    cudaFuncSetAttribute(fiber4_kernel<float, RB, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    return;
+  }
+  launch_k(fiber4_kernel<float, RB, TJ>, dim3(n), dim3(F4_THREADS), sm, st, a, u);
+}
+
+template <int RB>
+static void fiber4_tj(const XArgs& a, const FibUnit* u, int n, const XTables& t, cudaStream_t st,
+                      bool prep) {
+  if (t.fib4_tj >= 4) fiber4_go<RB, 4>(a, u, n, t, st, prep);
+  else if (t.fib4_tj == 3) fiber4_go<RB, 3>(a, u, n, t, st, prep);
+  else if (t.fib4_tj == 2) fiber4_go<RB, 2>(a, u, n, t, st, prep);
+  else fiber4_go<RB, 1>(a, u, n, t, st, prep);
+}
+
+static void fiber4_dispatch(int rb, const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                            cudaStream_t st, bool prep) {
+  if (rb <= 8) fiber4_tj<8>(a, u, n, t, st, prep);
+  else if (rb <= 10) fiber4_tj<10>(a, u, n, t, st, prep);
+  else if (rb <= 12) fiber4_tj<12>(a, u, n, t, st, prep);
+  else fiber4_tj<16>(a, u, n, t, st, prep);
+}
+
 void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
+  if (fiber4_ok(pc, rb, tma, t)) fiber4_dispatch(rb, a, nullptr, 0, t, 0, true);
   if (t.fiber_direct) {
     const bool ring = tma && t.f3_tma;
     if (pc == PC_F64) fiber3_dispatch<double>(t.f3_rb, ring, a, t, 0, true);
@@ -132,6 +170,11 @@ void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
 
 void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, const XTables& t, cudaStream_t st) {
+  if (want_t && !want_b && !want_res && n > 0 && t.d_fib4 && fiber4_ok(pc, rb, tma, t)) {
+    fiber4_dispatch(rb, a, t.d_fib4, (int)t.fib4.size(), t, st, false);
+    count_launch(1);
+    return;
+  }
   static const bool f3_on = getenv("CB_F3_ON") != nullptr;
   if (want_t && !want_b && !want_res && t.fiber_direct && f3_on) {
     const bool ring = tma && t.f3_tma;
@@ -335,6 +378,26 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
       for (long long j0 = 0; j0 < J; j0 += JT) t.fib.push_back(FibUnit{s, sp, j0});
   }
   t.fib_first[S] = (int)t.fib.size();
+  // fiber4 units: the tile minimising waves x TJ over this engine's blocks
+  t.fib4.clear();
+  t.fib4_tj = 0;
+  if (t.fiber_direct && pc == PC_F32_F64 && rb <= 16) {
+    long long best = -1;
+    for (int c : {4, 3, 2, 1}) {
+      long long u = 0;
+      for (int s = 0; s < S; ++s) {
+        const long long J = dims[3 * s] * dims[3 * s + 1];
+        u += (J + 256LL * c - 1) / (256LL * c);
+      }
+      const long long cost = ((u + 147) / 148) * c;
+      if (best < 0 || cost < best) { best = cost; t.fib4_tj = c; }
+    }
+    const long long JT4 = 256LL * t.fib4_tj;
+    for (int s = 0; s < S; ++s) {
+      const long long J = dims[3 * s] * dims[3 * s + 1];
+      for (long long j0 = 0; j0 < J; j0 += JT4) t.fib4.push_back(FibUnit{s, 0, j0});
+    }
+  }
   t.sb = tile;
   const int kc = s2_kc(rb, tcb);
   t.slab.clear(); t.slab_first.assign(S, 0); t.slab_nchunk.assign(S, 1);
