@@ -23,7 +23,18 @@ namespace cb {
 // its predecessor drains; every kernel therefore waits here (first statement)
 // before touching anything the predecessor wrote.  A no-op for ordinary
 // launches.
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The trigger (launch_dependents) is issued first: the next kernel's CTAs are
+// scheduled as soon as every CTA of this one is running, and sit in their own
+// griddep_wait() until this grid has completed and flushed (the wait, not
+// the trigger, carries the memory ordering), so the launch latency of the
+// serial iteration chain overlaps the running kernel.  CB_NO_EARLY_TRIGGER
+// builds keep the implicit trigger at exit.
+__device__ __forceinline__ void griddep_wait() {
+#ifndef CB_NO_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 // Phase timestamps (profiling builds of a run: Ctx.dbg non-null): block 0
 // accumulates the time between consecutive PH() marks into dbg[slot].
