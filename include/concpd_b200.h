@@ -135,7 +135,9 @@ typedef struct {
   double tol;                     /* AlsOptions.tol                         */
   int max_iter;                   /* AlsOptions.max_iter                    */
   int compute;                    /* fp32 storage only: 0 = fp64 arithmetic in
-                                     the tensor passes, 1 = fp32 arithmetic  */
+                                     the tensor passes, 1 = fp32 arithmetic,
+                                     2 = fp64 except the mode-2 MTTKRP of
+                                     ranks > 16, on the tensor cores (xtc)  */
   int total_blocks;               /* blocks of the whole (sharded) problem;
                                      fixes each block's work decomposition so
                                      a shard reproduces the unsharded bits

@@ -17,6 +17,7 @@
 #include "engine_host.h"
 #include "ops_internal.h"
 #include "status.h"
+#include "xtc.h"
 
 namespace cb {
 
@@ -211,6 +212,7 @@ using namespace cb;
 
 struct cb_als {
   cudaStream_t st = nullptr;
+  cb::XtcPlan* xtc = nullptr;   // mode-2 MTTKRP on the tensor cores (compute code 2)
   int S = 0, N = 0, dtype = CB_F64, max_iter = 0, rmax = 1, rb = 8, fast3 = 0, pc = 0;
   double tol = 1e-4;
   std::vector<long long> dims;
@@ -259,8 +261,14 @@ static int als_sweep(cb_als* h) {
         launch_contract(h->pc, n, h->xa, n == 0 ? h->d_c0 : h->d_c1,
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
       } else {
-        launch_slab(h->pc, h->rb, h->tma, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab, st);
-        src = h->tab.slab_direct ? 0 : 1;   // the row-dot kernel writes MTT itself
+        if (h->xtc) {
+          // tensor-core mode-2 MTTKRP (xtc.cu), written into MTT
+          int rc = xtc_mode2(h->xtc, h->xa.U, h->xa.active, h->xa.MTT, st);
+          if (rc) return rc;
+        } else {
+          launch_slab(h->pc, h->rb, h->tma, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab, st);
+          src = h->tab.slab_direct ? 0 : 1;   // the row-dot kernel writes MTT itself
+        }
       }
       CB_CHECK_LAUNCH();
     } else {
@@ -299,6 +307,7 @@ int cb_als_destroy(cb_als* h) {
   if (!h) return CB_OK;
   if (h->st) cudaStreamSynchronize(h->st);
   for (void* p : h->allocs) cudaFree(p);
+  cb::xtc_plan_destroy(h->xtc);
   if (h->h_state) cudaFreeHost(h->h_state);
   delete h;
   return CB_OK;
@@ -456,6 +465,17 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     xa.MTT = c.MTT; xa.gate = nullptr; xa.active = c.active;
     xa.ktime = nullptr;
     xa.slab_stage_rows = h->tab.slab_rows;
+    // compute code 2 (fp32 storage, ranks > 16 where the row-dot kernel does
+    // not apply): the mode-2 MTTKRP on the tensor cores; a plan that does not
+    // fit leaves the CUDA-core slab pass
+    if (d->compute == 2 && h->dtype == CB_F32 && !h->tab.slab_direct &&
+        xtc_supported(S, h->X.data(), h->dims.data(), h->R.data()) && !getenv("CB_NO_XTC_ALS")) {
+      bool i1_ok = true;
+      for (int s = 0; s < S; ++s) i1_ok = i1_ok && h->dims[3 * s + 1] >= 32;
+      if (i1_ok &&
+          xtc_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->xtc, 1) != CB_OK)
+        h->xtc = nullptr;
+    }
     {
       int* d_s3;
       TRY(upload(h->tab.s3_first, &d_s3, A, st));

@@ -118,3 +118,34 @@ def test_tc_trace_c5_block(P):
     want = O.core_term(x64, g)
     rel = np.abs(got - want) / np.abs(want)
     assert rel.max() < 1e-7, rel.max()
+
+
+def test_tc_mode2_als_matches_fp64_als(P):
+    """ALS compression with the mode-2 MTTKRP on the tensor cores
+    (SolverOptions(compute="tc"), csrc/xtc.cu xtc_mode2) against the fp64
+    passes: the relative-error history within 1e-5 relative per sweep on these
+    small blocks (128K elements: the 2^-21 input rounding averages over few
+    products; 2e-11 measured on 400^3 c5 blocks, tools/als_probe.py)."""
+    import torch
+    from paper_2302_05119_b200 import _lib as L
+    from paper_2302_05119_b200 import _device as D
+    from paper_2302_05119_b200.cpd_als import als_compress_blocks
+    rng = np.random.default_rng(21)
+    shapes = [((64, 40, 50), 20), ((96, 36, 30), 20)]
+    devs, dims = [], []
+    for d, r in shapes:
+        x, _ = _block(rng, d, r)
+        flat, dd = D.tensor_to_dev(x, "fp32")
+        devs.append(flat)
+        dims.append(dd)
+    st = L.c_vp(torch.cuda.current_stream().cuda_stream)
+    out = {}
+    for code in (0, 2):
+        h = als_compress_blocks(devs, dims, [20, 20], 1e-30, 12, [0, 1], L.CB_F32, st, code,
+                                total_blocks=2)
+        out[code] = [h.block(s)[2] for s in range(2)]
+        h.close()
+    for s in range(2):
+        a, b = np.asarray(out[0][s]), np.asarray(out[2][s])
+        assert len(a) == len(b) == 12
+        np.testing.assert_allclose(b, a, rtol=1e-5, atol=0)
