@@ -17,6 +17,7 @@
 #include "engine_host.h"
 #include "ops_internal.h"
 #include "status.h"
+#include "xslab5.h"
 #include "xtc.h"
 
 namespace cb {
@@ -213,6 +214,7 @@ using namespace cb;
 struct cb_als {
   cudaStream_t st = nullptr;
   cb::XtcPlan* xtc = nullptr;   // mode-2 MTTKRP on the tensor cores (compute code 2)
+  cb::Sl5Plan* sl5 = nullptr;   // fp64 mode-2 MTTKRP for ranks > 16 (xslab5.cu)
   int S = 0, N = 0, dtype = CB_F64, max_iter = 0, rmax = 1, rb = 8, fast3 = 0, pc = 0;
   double tol = 1e-4;
   std::vector<long long> dims;
@@ -265,6 +267,10 @@ static int als_sweep(cb_als* h) {
           // tensor-core mode-2 MTTKRP (xtc.cu), written into MTT
           int rc = xtc_mode2(h->xtc, h->xa.U, h->xa.active, h->xa.MTT, st);
           if (rc) return rc;
+        } else if (h->sl5) {
+          // fp64 GEMM-tiled mode-2 MTTKRP (xslab5.cu), written into MTT
+          int rc = sl5_mode2(h->sl5, h->xa.U, h->xa.active, h->xa.MTT, st);
+          if (rc) return rc;
         } else {
           launch_slab(h->pc, h->rb, h->tma, h->xa, h->d_slab, (int)h->tab.slab.size(), h->tab, st);
           src = h->tab.slab_direct ? 0 : 1;   // the row-dot kernel writes MTT itself
@@ -308,6 +314,7 @@ int cb_als_destroy(cb_als* h) {
   if (h->st) cudaStreamSynchronize(h->st);
   for (void* p : h->allocs) cudaFree(p);
   cb::xtc_plan_destroy(h->xtc);
+  cb::sl5_plan_destroy(h->sl5);
   if (h->h_state) cudaFreeHost(h->h_state);
   delete h;
   return CB_OK;
@@ -475,6 +482,12 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       if (i1_ok &&
           xtc_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->xtc, 1) != CB_OK)
         h->xtc = nullptr;
+    }
+    // fp64 arithmetic with ranks > 16: the GEMM-tiled mode-2 pass
+    if (!h->xtc && h->pc == PC_F32_F64 && !h->tab.slab_direct &&
+        sl5_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
+      if (sl5_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->sl5) != CB_OK)
+        h->sl5 = nullptr;
     }
     {
       int* d_s3;
