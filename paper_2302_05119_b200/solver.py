@@ -59,9 +59,11 @@ def _is_torch(t):
 class CoupledProblem:
     """S nonnegative tensors decomposed jointly (solver.py:60-135).
 
-    ``tensors`` may be numpy arrays (cast to float64 like the reference) or
-    CUDA torch tensors already resident on the device (kept as given; an
-    fp32 tensor stored first-index-fastest is used without any copy).
+    ``tensors`` may be numpy arrays (cast to float64 like the reference,
+    except float32 arrays, which are kept: the cast is exact and the fp32
+    throughput mode uploads them without a float64 detour) or CUDA torch
+    tensors already resident on the device (kept as given; an fp32 tensor
+    stored first-index-fastest is used without any copy).
     """
 
     tensors: list
@@ -72,7 +74,8 @@ class CoupledProblem:
     als_options: AlsOptions = None
 
     def __post_init__(self):
-        self.tensors = [t if _is_torch(t) else np.asarray(t, dtype=float) for t in self.tensors]
+        self.tensors = [t if (_is_torch(t) or (isinstance(t, np.ndarray) and t.dtype == np.float32))
+                        else np.asarray(t, dtype=float) for t in self.tensors]
         if isinstance(self.ranks, (int, np.integer)):
             self.ranks = [int(self.ranks)] * len(self.tensors)
         self.ranks = [int(r) for r in self.ranks]
@@ -86,7 +89,10 @@ class CoupledProblem:
     def order(self):
         return self.tensors[0].ndim
 
-    def validate(self):
+    def validate(self, check_values=True):
+        """The reference's checks (solver.py:96-135).  ``check_values=False``
+        skips the per-element finite / nonnegative scan (the single-process
+        solve runs it on the device after the upload, same messages)."""
         if not self.tensors:
             raise ValueError("no tensors")
         if self.mode not in ("full", "lra"):
@@ -95,11 +101,8 @@ class CoupledProblem:
         for s, t in enumerate(self.tensors):
             if t.ndim != order:
                 raise ValueError(f"block {s} has order {t.ndim}, expected {order}")
-            finite, nonneg = _value_checks(t)
-            if not finite:
-                raise ValueError(f"block {s} contains non-finite values")
-            if not nonneg:
-                raise ValueError(f"block {s} contains negative entries")
+            if check_values:
+                _raise_values(s, t)
         if len(self.ranks) != len(self.tensors):
             raise ValueError("one rank per block required")
         if any(r < 1 for r in self.ranks):
@@ -114,6 +117,14 @@ class CoupledProblem:
                 sizes = sorted({int(t.shape[n]) for t in self.tensors})
                 if len(sizes) != 1:
                     raise ValueError(f"mode {n} is coupled but block sizes differ: {sizes}")
+
+
+def _raise_values(s, t):
+    finite, nonneg = _value_checks(t)
+    if not finite:
+        raise ValueError(f"block {s} contains non-finite values")
+    if not nonneg:
+        raise ValueError(f"block {s} contains negative entries")
 
 
 def _value_checks(t):
@@ -429,7 +440,8 @@ class PreparedSolve:
     def __init__(self, problem, opts=None, stream=None, shard=None):
         torch = D.torch_mod()
         opts = opts if opts is not None else SolverOptions()
-        problem.validate()
+        # single process: the element scan runs on the device after upload
+        problem.validate(check_values=shard is not None)
         self.problem, self.opts = problem, opts
         S_all = problem.n_blocks
         self.shard = shard if shard is not None else ShardSpec(1, 0, 0, S_all, None)
@@ -463,8 +475,10 @@ class PreparedSolve:
         with torch.cuda.stream(self.stream):
             self.dev = []
             self.dims = []
-            for t in (problem.tensors[g] for g in self.local):
+            for g, t in zip(self.local, (problem.tensors[g] for g in self.local)):
                 flat, dims = D.tensor_to_dev(t, prec)
+                if shard is None:
+                    _raise_values(g, flat)
                 self.dev.append(flat)
                 self.dims.append(dims)
         st = L.c_vp(self.stream.cuda_stream)
