@@ -60,6 +60,7 @@ struct Sl5Args {
   double* const* mtt;        // S outputs (I2 x R)
   int S;
   long long i2max;
+  const int* gate;           // skip when *gate == 0 (the engine's gated restart copies)
 };
 
 struct Sl5Plan {
@@ -83,6 +84,7 @@ __device__ __forceinline__ void sl5_tma(void* dst, const void* tmap, int c0, int
 template <int RB>
 __global__ void __launch_bounds__(SL5_THREADS, 1) k_sl5_dpass(Sl5Args a) {
   griddep_wait();
+  if (a.gate && *a.gate == 0) return;
   constexpr int CG = RB / 4;                   // columns per thread
   extern __shared__ unsigned char sl5_raw[];
   const uint32_t raw_u32 = smem_u32(sl5_raw);
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_sl5_dpass(Sl5Args a) {
 // M2[i2, r] = sum_{i1} A1[i1, r] D[r][i1 + I1 i2]: one warp per (s, i2, r)
 __global__ void __launch_bounds__(256) k_sl5_contract(Sl5Args a) {
   griddep_wait();
+  if (a.gate && *a.gate == 0) return;
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)a.S * a.i2max * 64;
   for (long long w = (blockIdx.x * 256LL + threadIdx.x) >> 5; w < nw;
@@ -220,6 +223,9 @@ __global__ void __launch_bounds__(256) k_sl5_contract(Sl5Args a) {
 // host side
 // --------------------------------------------------------------------------
 static int sl5_rb(int rmax) {
+  if (rmax <= 8) return 8;
+  if (rmax <= 12) return 12;
+  if (rmax <= 16) return 16;
   if (rmax <= 24) return 24;
   if (rmax <= 32) return 32;
   if (rmax <= 40) return 40;
@@ -317,6 +323,9 @@ int sl5_plan_create(int S, const void* const* X, const long long* dims, const in
   CB_CUDA(cudaFuncSetAttribute(k_sl5_dpass<RBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                (int)p->smem))
   switch (p->rb) {
+    case 8: SL5_ATTR(8); break;
+    case 12: SL5_ATTR(12); break;
+    case 16: SL5_ATTR(16); break;
     case 24: SL5_ATTR(24); break;
     case 32: SL5_ATTR(32); break;
     case 40: SL5_ATTR(40); break;
@@ -335,7 +344,7 @@ void sl5_plan_destroy(Sl5Plan* p) {
 }
 
 int sl5_mode2(Sl5Plan* p, const double* const* U_dev, const int* active, double* const* mtt,
-              cudaStream_t st) {
+              cudaStream_t st, const int* gate) {
   Sl5Args a;
   memset(&a, 0, sizeof(a));
   a.tmaps = p->tmaps;
@@ -347,7 +356,11 @@ int sl5_mode2(Sl5Plan* p, const double* const* U_dev, const int* active, double*
   a.mtt = mtt;
   a.S = p->S;
   a.i2max = p->i2max;
+  a.gate = gate;
   switch (p->rb) {
+    case 8: CB_CUDA(launch_k(k_sl5_dpass<8>, dim3(p->grid), dim3(SL5_THREADS), p->smem, st, a)); break;
+    case 12: CB_CUDA(launch_k(k_sl5_dpass<12>, dim3(p->grid), dim3(SL5_THREADS), p->smem, st, a)); break;
+    case 16: CB_CUDA(launch_k(k_sl5_dpass<16>, dim3(p->grid), dim3(SL5_THREADS), p->smem, st, a)); break;
     case 24: CB_CUDA(launch_k(k_sl5_dpass<24>, dim3(p->grid), dim3(SL5_THREADS), p->smem, st, a)); break;
     case 32: CB_CUDA(launch_k(k_sl5_dpass<32>, dim3(p->grid), dim3(SL5_THREADS), p->smem, st, a)); break;
     case 40: CB_CUDA(launch_k(k_sl5_dpass<40>, dim3(p->grid), dim3(SL5_THREADS), p->smem, st, a)); break;

@@ -14,6 +14,6 @@ int sl5_plan_create(int S, const void* const* X, const long long* dims, const in
 void sl5_plan_destroy(Sl5Plan* p);
 // mtt[s] (device array of S pointers) <- M2 (I2 x R) of every active block
 int sl5_mode2(Sl5Plan* p, const double* const* U_dev, const int* active, double* const* mtt,
-              cudaStream_t st);
+              cudaStream_t st, const int* gate = nullptr);
 
 }  // namespace cb
