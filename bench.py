@@ -248,7 +248,10 @@ def run_ours(args):
             "frac": dom["gbs"] / peak, "traffic": None,
             "kernel": ("k_xtc_trace (lra trace pass, tcgen05 kind::i8 tensor cores)" if tc_trace
                        else {"slab": "slab3_kernel (mode-2 MTTKRP, row-dot)",
-                             "fiber": "fiber2_kernel (T = X x2 A2)"}[dom_name]),
+                             "fiber": ("fiber4_kernel (T = X x3 A2, warp-specialised ring)"
+                                       if (spec.mode == "full" and prec == "fp32" and
+                                           spec.rank <= 16)
+                                       else "fiber2_kernel (T = X x3 A2)")}[dom_name]),
             "bytes_per_launch": dom["bytes_per_launch"],
             "bytes_note": "algorithmic: every block element read once, sum_s |M_s| x 4 B",
             "peak_source": peak_kind, "kernels": kinds}

@@ -36,8 +36,11 @@ if has launches; then
   echo "launches rc=$?" | tee -a $OUT/status.txt
 fi
 if has full; then
-  timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k 'regex:slab3|fiber3|contract' -s 30 -c 6 -o $OUT/full -f \
+  # conditional graph nodes block kernel-level profiling: plain graph here
+  CB_NO_COND=1 timeout 1200 ncu --set full --clock-control none --import-source on \
+    -k 'regex:slab3|fiber4' -s 20 -c 4 -o /tmp/full -f \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/ncu_full.log 2>&1
   echo "full rc=$?" | tee -a $OUT/status.txt
+  python tools/ncu_summary.py /tmp/full.ncu-rep 10 > $OUT/full_summary.txt 2>&1
+  python tools/ncu_lines.py /tmp/full.ncu-rep 25 > $OUT/full_lines.txt 2>&1
 fi
