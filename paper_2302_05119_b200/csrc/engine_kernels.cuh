@@ -24,10 +24,14 @@ struct BlockSmem {
   double* lmB2;
   double* vec;
   double* red;
-  double* gr;     // gram staging 2 * 32 * gw
+  double* gr;     // gram staging 2 * gram_rows(gw) * gw
   int gw;
   double* misc;   // 4 * 64
 };
+
+// rows staged per gram chunk: small ranks stage up to 128 rows at once, so
+// a whole factor (I_n <= 128) arrives in one round trip of loads
+__host__ __device__ __forceinline__ int gram_rows(int gw) { return gw <= 16 ? 128 : 32; }
 
 __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
   BlockSmem b;
@@ -40,29 +44,33 @@ __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
   b.red = b.vec + 128;
   b.gr = b.red + 40;
   b.gw = gw;
-  b.misc = b.gr + 2 * 32 * gw;
+  b.misc = b.gr + 2 * gram_rows(gw) * gw;
   return b;
 }
 
 __host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
-  return sizeof(double) * ((size_t)lm_smem_doubles(rmax) + 2 * 32 * (size_t)gw + 4 * 64 + 8);
+  return sizeof(double) * ((size_t)lm_smem_doubles(rmax) + 2 * (size_t)gram_rows(gw) * gw + 4 * 64 + 8);
 }
 
 // out[P x Q] = A^T B with A rows x P, B rows x Q (row-major), whole block,
 // fixed summation order over rows (deterministic).
 static __device__ __noinline__ void block_gram(const double* __restrict__ A, int P, const double* __restrict__ B,
                            int Q, long long rows, double* __restrict__ out, const BlockSmem& sm) {
+  const int CH = gram_rows(sm.gw);
   double* As = sm.gr;
-  double* Bs = sm.gr + 32 * sm.gw;
+  // a gram of one matrix with itself reads one staged copy
+  const bool same = (A == B) && (P == Q);
+  double* Bs = same ? As : sm.gr + CH * sm.gw;
   const int nout = P * Q;
   double acc[16];
 #pragma unroll
   for (int t = 0; t < 16; ++t) acc[t] = 0.0;
-  for (long long c0 = 0; c0 < rows; c0 += 32) {
-    const int nr = (int)(rows - c0 < 32 ? rows - c0 : 32);
+  for (long long c0 = 0; c0 < rows; c0 += CH) {
+    const int nr = (int)(rows - c0 < CH ? rows - c0 : CH);
     __syncthreads();
     for (int e = threadIdx.x; e < nr * P; e += blockDim.x) As[e] = A[c0 * P + e];
-    for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) Bs[e] = B[c0 * Q + e];
+    if (!same)
+      for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) Bs[e] = B[c0 * Q + e];
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
@@ -706,11 +714,28 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
   const double* Un = c.Un[s * N + n];
   PhaseClock pc;
   pc.start(c.dbg);
-  for (long long e = threadIdx.x; e < In * R; e += blockDim.x) {
-    const long long i = e / R;
-    const int r = (int)(e - i * R);
-    Upr[e] = Uc[e];
-    Uc[e] = r < L ? c.cnew[i * L + r] : Un[e];
+  // prev <- curr, curr <- new: all loads of a batch in flight before its
+  // stores (the pointers may alias as far as the compiler knows)
+  for (long long base = 0; base < In * R; base += 8LL * blockDim.x) {
+    double cu[8], nv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long e = base + threadIdx.x + (long long)k * blockDim.x;
+      if (e < In * R) {
+        const long long i = e / R;
+        const int r = (int)(e - i * R);
+        cu[k] = Uc[e];
+        nv[k] = r < L ? c.cnew[i * L + r] : Un[e];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long e = base + threadIdx.x + (long long)k * blockDim.x;
+      if (e < In * R) {
+        Upr[e] = cu[k];
+        Uc[e] = nv[k];
+      }
+    }
   }
   __syncthreads();
   pc.mark(c.dbg, 0);
