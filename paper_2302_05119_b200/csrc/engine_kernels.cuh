@@ -31,7 +31,7 @@ struct BlockSmem {
 
 // rows staged per gram chunk: small ranks stage up to 128 rows at once, so
 // a whole factor (I_n <= 128) arrives in one round trip of loads
-__host__ __device__ __forceinline__ int gram_rows(int gw) { return gw <= 16 ? 128 : 32; }
+__host__ __device__ __forceinline__ int gram_rows(int gw) { return gw <= 16 ? 128 : 64; }
 
 __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
   BlockSmem b;
@@ -53,7 +53,10 @@ __host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
 }
 
 // out[P x Q] = A^T B with A rows x P, B rows x Q (row-major), whole block,
-// fixed summation order over rows (deterministic).
+// fixed summation order over rows (deterministic: every output is one fma
+// chain over the rows in order, whatever the staging).  Rows are staged in
+// chunks of gram_rows(gw) (one round trip of loads per chunk); each thread
+// owns a 4 x 4 register tile of outputs (16 FMAs per 8 shared loads per row).
 static __device__ __noinline__ void block_gram(const double* __restrict__ A, int P, const double* __restrict__ B,
                            int Q, long long rows, double* __restrict__ out, const BlockSmem& sm) {
   const int CH = gram_rows(sm.gw);
@@ -61,10 +64,19 @@ static __device__ __noinline__ void block_gram(const double* __restrict__ A, int
   // a gram of one matrix with itself reads one staged copy
   const bool same = (A == B) && (P == Q);
   double* Bs = same ? As : sm.gr + CH * sm.gw;
-  const int nout = P * Q;
-  double acc[16];
+  // small grams (P Q <= 256): one output per thread (more parallel rows
+  // chains); larger: 4 x 4 tiles
+  const bool t1 = P * Q <= 256;
+  const int TP = t1 ? 1 : 4;
+  const int ntp = (P + TP - 1) / TP, ntq = (Q + TP - 1) / TP;
+  const int tile = threadIdx.x;                 // ntp * ntq <= 256 for P, Q <= 64
+  const bool owner = tile < ntp * ntq;
+  const int p0 = owner ? (tile / ntq) * TP : 0, q0 = owner ? (tile % ntq) * TP : 0;
+  double acc[4][4];
 #pragma unroll
-  for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
   for (long long c0 = 0; c0 < rows; c0 += CH) {
     const int nr = (int)(rows - c0 < CH ? rows - c0 : CH);
     __syncthreads();
@@ -72,21 +84,32 @@ static __device__ __noinline__ void block_gram(const double* __restrict__ A, int
     if (!same)
       for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) Bs[e] = B[c0 * Q + e];
     __syncthreads();
+    if (owner && t1) {
+      double sacc = acc[0][0];
+      for (int i = 0; i < nr; ++i) sacc = fma(As[i * P + p0], Bs[i * Q + q0], sacc);
+      acc[0][0] = sacc;
+    } else if (owner) {
+      for (int i = 0; i < nr; ++i) {
+        double a4[4], b4[4];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int o = threadIdx.x + t * 256;
-      if (o < nout) {
-        const int p = o / Q, q = o - p * Q;
-        double s = acc[t];
-        for (int i = 0; i < nr; ++i) s = fma(As[i * P + p], Bs[i * Q + q], s);
-        acc[t] = s;
+        for (int u = 0; u < 4; ++u) a4[u] = p0 + u < P ? As[i * P + p0 + u] : 0.0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b4[v] = q0 + v < Q ? Bs[i * Q + q0 + v] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(a4[u], b4[v], acc[u][v]);
       }
     }
   }
+  if (owner && t1) {
+    out[p0 * Q + q0] = acc[0][0];
+  } else if (owner) {
 #pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const int o = threadIdx.x + t * 256;
-    if (o < nout) out[o] = acc[t];
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (p0 + u < P && q0 + v < Q) out[(p0 + u) * Q + q0 + v] = acc[u][v];
   }
   __syncthreads();
 }

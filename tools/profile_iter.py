@@ -15,7 +15,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 flush_on = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 spec = CONFIGS[name]
-tensors, _ = generate_config(name)
+nblk = int(os.environ.get("TL_BLOCKS", "0"))
+tensors, _ = generate_config(name, blocks=range(nblk) if nblk else None)
 prob = P.CoupledProblem([np.asarray(t, dtype=float) for t in tensors], spec.rank, list(spec.coupled), mode=spec.mode)
 run = PreparedSolve(prob, P.SolverOptions(max_iter=iters + 12, tol=float(np.nextafter(0, 1)), precision=spec.dtype))
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
