@@ -348,9 +348,17 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
 __device__ inline void common_lip_sums(const Ctx& c, int n, double& sl, double& slp) {
   sl = 0.0;
   slp = 0.0;
-  for (int q = 0; q < c.S_tot; ++q) {
-    sl += c.lip[lu_idx(c, n, q)];
-    slp += c.lip[lup_idx(c, n, q)];
+  for (int q0 = 0; q0 < c.S_tot; q0 += 8) {
+    double a8[8], b8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = q0 + k;
+      a8[k] = q < c.S_tot ? c.lip[lu_idx(c, n, q)] : 0.0;
+      b8[k] = q < c.S_tot ? c.lip[lup_idx(c, n, q)] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (q0 + k < c.S_tot) { sl += a8[k]; slp += b8[k]; }
   }
 }
 
@@ -365,12 +373,23 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
   for (int e = threadIdx.x; e < rows * L; e += blockDim.x) {
     const int il = e / L, l = e - il * L;
     const long long i = r0 + il;
+    // partials of the blocks with L_u > 0, added in block order; loads in
+    // batches of 8 issued before their adds (latency, not bandwidth, bound)
     double acc = 0.0;
-    for (int q = 0; q < c.S_tot; ++q) {
-      if (!(c.lip[lu_idx(c, n, q)] > 0.0)) continue;
-      acc += __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]);
-    }
     const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
+    for (int q0 = 0; q0 < c.S_tot; q0 += 8) {
+      double g8[8];
+      bool on[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int q = q0 + k;
+        on[k] = q < c.S_tot && c.lip[lu_idx(c, n, q)] > 0.0;
+        g8[k] = q < c.S_tot ? __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (on[k]) acc += g8[k];
+    }
     const double chat = cc + wc * (cc - cp);
     c.cnew[i * L + l] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
   }
