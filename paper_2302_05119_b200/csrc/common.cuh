@@ -236,7 +236,7 @@ static __device__ __noinline__ void eigen_tail(const double* A, int R, int ld, c
 
 static __device__ __noinline__ double dominant_rq(const double* A, int R, int ld, double* B, double* B2,
                                      double* vec, double* red, double shift, double* resid_out,
-                                     double* dbg = nullptr) {
+                                     double* dbg = nullptr, double* m_out = nullptr) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   PhaseClock pc;
   pc.start(dbg);
@@ -248,6 +248,7 @@ static __device__ __noinline__ double dominant_rq(const double* A, int R, int ld
     m = fmax(m, fabs(A[i * ld + j] + (i == j ? shift : 0.0)));
   }
   m = block_max_approx(m, ured);
+  if (m_out) *m_out = m;
   if (m == 0.0) { if (resid_out) *resid_out = 0.0; return 0.0; }
   const double inv0 = 1.0 / m;
   for (int e = tid; e < Rp2 * bld; e += nthr) {
@@ -363,15 +364,12 @@ static __device__ __noinline__ double block_lam_max(const double* A, int R, doub
                                        double* red, double* dbg = nullptr) {
   const int ld = lm_ld(R);
   double resid;
-  const double rho = dominant_rq(A, R, ld, B, B2, vec, red, 0.0, &resid, dbg);
+  // the unshifted pass's max |A| is the amax of the acceptance test (the
+  // same block_max_approx of the same entries; no second reduction)
+  double amax = 0.0;
+  const double rho = dominant_rq(A, R, ld, B, B2, vec, red, 0.0, &resid, dbg, &amax);
   PhaseClock pc;
   pc.start(dbg);
-  double amax = 0.0;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, j = e - i * R;
-    amax = fmax(amax, fabs(A[i * ld + j]));
-  }
-  amax = block_max_approx(amax, reinterpret_cast<unsigned*>(red));
   pc.mark(dbg, 14);
   if (amax == 0.0) return 0.0;
   // PSD / positive-dominant path: a converged eigenpair with rho >= 0 is the
