@@ -260,15 +260,26 @@ def run_ours(args):
     # user holds it; the solve keeps fp32 input without a float64 detour)
     host = [np.asarray(t) for t in tensors]
     e2e_iters = spec.max_iter           # the config's own run length (c2: 500 iterations)
-    torch.cuda.synchronize()
-    tic = time.perf_counter()
-    e2e_problem = P.CoupledProblem(host, spec.rank, list(spec.coupled), mode=spec.mode)
-    e2e_opts = P.SolverOptions(max_iter=e2e_iters, tol=TINY_TOL, seed=0, precision=prec)
-    res = solve_distributed(e2e_problem, e2e_opts) if world > 1 else P.solve(e2e_problem, e2e_opts)
-    if world > 1:
-        t = torch.tensor([time.perf_counter() - tic], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    e2e_s = float(t.item()) if world > 1 else time.perf_counter() - tic
+    # median of up to 3 complete solve() calls (each one end to end: checks,
+    # upload, engine setup, graph capture, iterations, download); one call
+    # when a call takes more than 10 s
+    e2e_times = []
+    for rep in range(3):
+        torch.cuda.synchronize()
+        tic = time.perf_counter()
+        e2e_problem = P.CoupledProblem(host, spec.rank, list(spec.coupled), mode=spec.mode)
+        e2e_opts = P.SolverOptions(max_iter=e2e_iters, tol=TINY_TOL, seed=0, precision=prec)
+        res = (solve_distributed(e2e_problem, e2e_opts) if world > 1
+               else P.solve(e2e_problem, e2e_opts))
+        dt = time.perf_counter() - tic
+        if world > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e_times.append(dt)
+        if dt > 10.0:
+            break
+    e2e_s = statistics.median(e2e_times)
     elem = sum(int(np.prod(t.shape)) for t in tensors)
     h2d = elem * (4 if prec == "fp32" else 8) + sum(
         8 * (sum(t.shape) * spec.rank + spec.rank) for t in tensors)
@@ -278,7 +289,8 @@ def run_ours(args):
            "h2d_bytes_per_step": h2d / max(res.n_iter, 1),
            "d2h_bytes_per_step": d2h / max(res.n_iter, 1),
            "step": f"one solve() call of {res.n_iter} iterations on host numpy inputs, "
-                   "incl. validation, upload, engine setup, graph capture and result download"}
+                   "incl. validation, upload, engine setup, graph capture and result download "
+                   f"(median of {len(e2e_times)} calls)"}
     # ---- CPU baseline: the oracle port on a bounded sample -----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
