@@ -21,6 +21,7 @@ struct XTables {
   // tile does not change any bit; chosen to fill the SMs)
   std::vector<FibUnit> fib4;
   int fib4_tj = 0;
+  int fib_unsplit = 0;              // every block's fiber units cover all of I2 (nsplit 1)
   const FibUnit* d_fib4 = nullptr;   // device copy (set by the engine)
   long long fib_rows = 0;    // max i2 rows of a fiber unit (A2 rows staged per CTA)
   long long slab_rows = 0;   // A0+A1 rows the slab kernel stages (0: read through L1)

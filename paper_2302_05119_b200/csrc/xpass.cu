@@ -156,9 +156,39 @@ static void fiber4_dispatch(int rb, const XArgs& a, const FibUnit* u, int n, con
   else fiber4_tj<16>(a, u, n, t, st, prep);
 }
 
+// T + explicit residual (the ALS sweep's fiber pass) for ranks > 16 on the
+// fiber4 ring, over the fiber2 unit table (same units, same partial slots)
+static bool fiber4res_ok(int pc, int rb, bool tma, const XTables& t) {
+  static const bool off = getenv("CB_NO_F4RES") != nullptr;
+  return !off && pc == PC_F32_F64 && rb >= 24 && tma && t.fib_unsplit &&
+         t.fib_tj == x2_tile(rb, 8);
+}
+
+template <int RB>
+static void fiber4res_go(const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                         cudaStream_t st, bool prep) {
+  constexpr int TJ = x2_tile(RB, 8);
+  const size_t sm = fiber4_smem<float>(t.fib_rows, RB, TJ);
+  if (prep) {
+    cudaFuncSetAttribute(fiber4_kernel<float, RB, TJ, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return;
+  }
+  launch_k(fiber4_kernel<float, RB, TJ, true>, dim3(n), dim3(F4_THREADS), sm, st, a, u);
+}
+
+static void fiber4res_dispatch(int rb, const XArgs& a, const FibUnit* u, int n, const XTables& t,
+                               cudaStream_t st, bool prep) {
+  if (rb <= 24) fiber4res_go<24>(a, u, n, t, st, prep);
+  else if (rb <= 32) fiber4res_go<32>(a, u, n, t, st, prep);
+  else if (rb <= 40) fiber4res_go<40>(a, u, n, t, st, prep);
+  else fiber4res_go<64>(a, u, n, t, st, prep);
+}
+
 void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
   if (fiber4_ok(pc, rb, tma, t)) fiber4_dispatch(rb, a, nullptr, 0, t, 0, true);
+  if (fiber4res_ok(pc, rb, tma, t)) fiber4res_dispatch(rb, a, nullptr, 0, t, 0, true);
   if (t.fiber_direct) {
     const bool ring = tma && t.f3_tma;
     if (pc == PC_F64) fiber3_dispatch<double>(t.f3_rb, ring, a, t, 0, true);
@@ -170,6 +200,11 @@ void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
 
 void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res, const XArgs& a,
                   const FibUnit* u, int n, const XTables& t, cudaStream_t st) {
+  if (want_t && want_res && !want_b && n > 0 && fiber4res_ok(pc, rb, tma, t)) {
+    fiber4res_dispatch(rb, a, u, n, t, st, false);
+    count_launch(1);
+    return;
+  }
   if (want_t && !want_b && !want_res && n > 0 && t.d_fib4 && fiber4_ok(pc, rb, tma, t)) {
     fiber4_dispatch(rb, a, t.d_fib4, (int)t.fib4.size(), t, st, false);
     count_launch(1);
@@ -378,6 +413,8 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
       for (long long j0 = 0; j0 < J; j0 += JT) t.fib.push_back(FibUnit{s, sp, j0});
   }
   t.fib_first[S] = (int)t.fib.size();
+  t.fib_unsplit = 1;
+  for (int s = 0; s < S; ++s) t.fib_unsplit = t.fib_unsplit && t.nsplit[s] == 1;
   // fiber4 units: the tile minimising waves x TJ over this engine's blocks
   t.fib4.clear();
   t.fib4_tj = 0;

@@ -28,7 +28,10 @@ __host__ __device__ constexpr size_t fiber4_smem(long long a2_rows, int rb, int 
   return 128 + (size_t)F4_NST * F4_ROWS * F4_CONS * tj * sizeof(TE) + (size_t)a2_rows * rb * 8;
 }
 
-template <typename TE, int RB, int TJ>
+// RES: also the explicit residual sum_(j,i2) (X - [[lam; A0, A1, A2]])^2 of
+// the unit into a.rpart[unit], folded per block in unit order by the last
+// arriving CTA into a.rsum[s] (the ALS stop rule, cpd_als.py:101-110)
+template <typename TE, int RB, int TJ, bool RES = false>
 __global__ void __launch_bounds__(F4_THREADS)
 fiber4_kernel(XArgs a, const FibUnit* __restrict__ units) {
   griddep_wait();
@@ -99,6 +102,22 @@ fiber4_kernel(XArgs a, const FibUnit* __restrict__ units) {
   for (int t = 0; t < TJ; ++t)
 #pragma unroll
     for (int r = 0; r < RB; ++r) acc[t][r] = 0.0;
+  // RES: the model's row weights lam_r A0[i0, r] A1[i1, r] of this column
+  double w[RES ? TJ : 1][RES ? RB : 1];
+  double res = 0.0;
+  if constexpr (RES) {
+    const double* lam = a.LAM ? a.LAM[s] : nullptr;
+    const double* A0 = a.U[3 * s];
+    const double* A1 = a.U[3 * s + 1];
+#pragma unroll
+    for (int t = 0; t < TJ; ++t) {
+      const long long i1 = ok[t] ? jq[t] / I0 : 0;
+      const long long i0 = ok[t] ? jq[t] - i1 * I0 : 0;
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        w[t][r] = (r < R && ok[t]) ? (lam ? lam[r] : 1.0) * A0[i0 * R + r] * A1[i1 * R + r] : 0.0;
+    }
+  }
   for (int k = 0; k < nstages; ++k) {
     const int slot = k % F4_NST;
     const long long r0 = (long long)k * F4_ROWS;
@@ -120,6 +139,15 @@ fiber4_kernel(XArgs a, const FibUnit* __restrict__ units) {
 #pragma unroll
         for (int t = 0; t < TJ; ++t) acc[t][r] = fma(x[t], av[r], acc[t][r]);
       }
+      if constexpr (RES) {
+#pragma unroll
+        for (int t = 0; t < TJ; ++t) {
+          double m = 0.0;
+#pragma unroll
+          for (int r = 0; r < RB; ++r) m = fma(w[t][r], av[r], m);
+          if (ok[t]) { const double d = x[t] - m; res = fma(d, d, res); }
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -132,6 +160,32 @@ fiber4_kernel(XArgs a, const FibUnit* __restrict__ units) {
       for (int r = 0; r < RB; ++r)
         if (r < R) T[(long long)r * J + jq[t]] = acc[t][r];
     }
+  if constexpr (RES) {
+    // unit partial: warp sums, then the 8 warps in order (consumers only)
+    __shared__ double red4[F4_CONS / 32];
+    __shared__ int last4;
+    for (int o = 16; o; o >>= 1) res += __shfl_xor_sync(0xffffffffu, res, o);
+    if (lane == 0) red4[warp] = res;
+    asm volatile("bar.sync 1, %0;" ::"r"(F4_CONS) : "memory");
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < F4_CONS / 32; ++q) t += red4[q];
+      a.rpart[blockIdx.x] = t;
+      __threadfence();
+      const int first = a.fib_first[s], nunits = a.fib_first[s + 1] - first;
+      last4 = atomicAdd(&a.blk_cnt[s], 1) == nunits - 1;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(F4_CONS) : "memory");
+    if (last4 && threadIdx.x == 0) {
+      // the block's units in unit order
+      __threadfence();
+      const int first = a.fib_first[s], nunits = a.fib_first[s + 1] - first;
+      double t = 0.0;
+      for (int q = 0; q < nunits; ++q) t += __ldcg(&a.rpart[first + q]);
+      a.rsum[s] = t;
+      a.blk_cnt[s] = 0;
+    }
+  }
   tl_end(a.tl, TL_FIBER);
 }
 
