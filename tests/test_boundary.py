@@ -48,6 +48,28 @@ def test_solver_options_validation_matches_reference():
         SolverOptions(trace_every=0)
     with pytest.raises(ValueError, match="precision"):
         SolverOptions(precision="fp16")
+    # additions (defaulted): arithmetic of the fp32-storage tensor passes
+    for ok in ("auto", "fp64", "fp32", "tc"):
+        SolverOptions(precision="fp32", compute=ok)
+    with pytest.raises(ValueError, match="compute"):
+        SolverOptions(compute="int8")
+
+
+def test_float32_inputs_kept_and_value_checks():
+    """float32 numpy blocks are kept (the cast to float64 is exact); value
+    checks on host arrays give the reference's messages either way."""
+    from paper_2302_05119_b200 import CoupledProblem
+    x32 = np.ones((3, 4, 5), dtype=np.float32)
+    p = CoupledProblem([x32], 2, [0, 0, 0])
+    assert p.tensors[0].dtype == np.float32 and p.tensors[0] is x32
+    p64 = CoupledProblem([x32.astype(np.int64)], 2, [0, 0, 0])
+    assert p64.tensors[0].dtype == np.float64
+    bad = x32.copy()
+    bad[0, 0, 0] = -1.0
+    with pytest.raises(ValueError, match="negative"):
+        CoupledProblem([bad], 2, [0, 0, 0]).validate()
+    # the single-process solve defers the element scan to the device
+    CoupledProblem([bad], 2, [0, 0, 0]).validate(check_values=False)
 
 
 def test_problem_validation_messages_match_reference():
