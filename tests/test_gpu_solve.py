@@ -187,3 +187,20 @@ def test_device_resident_fp32_inputs(P):
     res_host = P.solve(P.CoupledProblem([t.astype(np.float32).astype(float) for t in tensors], 4, [2, 2, 2]),
                        P.SolverOptions(max_iter=40, seed=1, precision="fp32"))
     assert res_dev.objective_history == res_host.objective_history
+
+
+def test_device_value_checks_raise_reference_messages(P):
+    """The single-process solve scans the uploaded blocks on the device; the
+    errors are the reference's (solver.py:114-117), with the block index."""
+    rng = np.random.default_rng(4)
+    good = rng.random((6, 5, 4)).astype(np.float32)
+    bad = good.copy()
+    bad[1, 2, 3] = -0.5
+    with pytest.raises(ValueError, match="block 1 contains negative entries"):
+        P.solve(P.CoupledProblem([good, bad], 2, [0, 0, 0]),
+                P.SolverOptions(max_iter=2, precision="fp32"))
+    nan = good.copy()
+    nan[0, 0, 0] = np.nan
+    with pytest.raises(ValueError, match="block 0 contains non-finite values"):
+        P.solve(P.CoupledProblem([nan, good], 2, [0, 0, 0]),
+                P.SolverOptions(max_iter=2, precision="fp32"))
