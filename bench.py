@@ -244,8 +244,19 @@ def run_ours(args):
     tc_trace = (spec.mode == "lra" and getattr(run, "compute_code", 0) == 2 and
                 spec.dims[0] % 4 == 0 and spec.dims[0] <= 512 and spec.dims[1] >= 19 and
                 spec.rank <= 64)
+    # DRAM bytes (read + write) per launch of the dominant kernel from one
+    # ncu --set full capture (committed summaries; ncu cannot run in here)
+    kname = ("xtc" if tc_trace else
+             ("fiber4" if (dom_name == "fiber" and spec.mode == "full" and prec == "fp32" and
+                           spec.rank <= 16) else dom_name))
+    traffic_tab = {
+        ("c2", "slab"): (40.187648e6, "profiles/r01e_c2_streaming_ncu_summary.txt"),
+        ("c2", "fiber4"): (40.101120e6 + 9.216e3, "profiles/r01e_c2_streaming_ncu_summary.txt"),
+        ("c5", "xtc"): (16.518760e9 + 41.288448e6, "profiles/r01c_xtc_c5_ncu_summary.txt"),
+    }
+    traffic, traffic_src = traffic_tab.get((spec.name, kname), (None, None))
     roof = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
-            "frac": dom["gbs"] / peak, "traffic": None,
+            "frac": dom["gbs"] / peak, "traffic": traffic, "traffic_source": traffic_src,
             "kernel": ("k_xtc_trace (lra trace pass, tcgen05 kind::i8 tensor cores)" if tc_trace
                        else {"slab": "slab3_kernel (mode-2 MTTKRP, row-dot)",
                              "fiber": ("fiber4_kernel (T = X x3 A2, warp-specialised ring)"
