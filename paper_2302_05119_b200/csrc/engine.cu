@@ -112,6 +112,12 @@ struct cb_solver {
   struct Xchg { double* send; double* recv; long long count; };
   std::vector<Xchg> pending;
   cb::XtcPlan* xtc = nullptr;  // tensor-core lra trace pass (compute code 2)
+  // pipelined lra (single GPU, tensor-core trace): the trace pass of
+  // iteration k streams beside the sweep of k+1 (see enqueue_pipe_step)
+  bool pipe = false;
+  bool pipe_pending = false;     // an iteration's trace + FINISH not yet enqueued
+  cudaGraphExec_t gexec_pipe = nullptr;
+  long long launches_per_pipe = 0;
 };
 
 namespace cb {
@@ -342,11 +348,11 @@ static int enqueue_qr(cb_solver* h, int redo) {
   return CB_OK;
 }
 
-static int enqueue_control(cb_solver* h, int mode) {
+static int enqueue_control(cb_solver* h, int mode, int extra = 0) {
   const int bsrc = h->fast3 ? 0 : 1;
   if (!h->shard) {
     if (emit(h)) {
-      launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 3);
+      launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 3 | extra);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
@@ -371,7 +377,7 @@ static int enqueue_control(cb_solver* h, int mode) {
 
 static int enqueue_restore(cb_solver* h) {
   if (emit(h)) {
-    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx);
+    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx, 0);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -502,6 +508,74 @@ static int enqueue_iteration(cb_solver* h) {
   return CB_OK;
 }
 
+// ---- pipelined lra iteration (single GPU, tensor-core trace pass) ---------
+// The trace pass only feeds FINISH (trace, histories, stop rule), never the
+// next sweep, so iteration k's streaming pass (16 GB on c5) runs on the side
+// stream beside the sweep + QR route of iteration k+1:
+//   prologue (k = 1):  sweep, qr, DECIDE (advances the momentum), redo, prep
+//   step (k -> k+1):   [st2: trace(k)] || [st: sweep(k+1), qr(k+1)] -> join
+//                      -> FINISH(k) (snapshots of lam_k / model_sq_k) ->
+//                      rollback if it stopped (k_restore, gate 1) -> DECIDE
+//                      (k+1) -> redo -> prep(k+1) + snapshots
+//   drain:             trace(k), FINISH(k) (no speculative sweep to undo)
+// The arithmetic is that of the classic order, so results are identical.
+static int enqueue_pipe_prep(cb_solver* h) {
+  if (!emit(h)) return CB_OK;
+  int rc = xtc_trace(h->xtc, h->xa_main.U, h->xa_main.gate, h->ctx.fib_bpart, h->st, 1);
+  if (rc) return rc;
+  launch_k(k_pipe_snap, dim3(h->S), dim3(64), 0, h->st, h->ctx);
+  count_launch(1);
+  CB_CHECK_LAUNCH();
+  return CB_OK;
+}
+
+static int enqueue_pipe_stream(cb_solver* h, cudaStream_t st) {
+  if (!emit(h)) return CB_OK;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) { int rc = ev_pair(h, &e0, &e1, 1); if (rc) return rc; CB_CUDA(cudaEventRecord(e0, st)); }
+  int rc = xtc_trace(h->xtc, h->xa_main.U, h->xa_main.gate, h->ctx.fib_bpart, st, 2);
+  if (rc) return rc;
+  CB_CHECK_LAUNCH();
+  if (h->timing) { CB_CUDA(cudaEventRecord(e1, st)); h->t_launches += 1; h->t_bytes += xtc_bytes(h->xtc); }
+  return CB_OK;
+}
+
+static int enqueue_pipe_prologue(cb_solver* h) {
+  int rc;
+  if ((rc = enqueue_sweep(h, 0))) return rc;
+  if ((rc = enqueue_qr(h, 0))) return rc;
+  if ((rc = enqueue_control(h, CTRL_DECIDE, 16))) return rc;
+  if ((rc = enqueue_redo(h))) return rc;
+  return enqueue_pipe_prep(h);
+}
+
+static int enqueue_pipe_step(cb_solver* h) {
+  int rc;
+  if ((rc = fork_side(h))) return rc;
+  if ((rc = enqueue_pipe_stream(h, h->st2))) return rc;
+  if ((rc = enqueue_sweep(h, 0))) return rc;
+  if ((rc = enqueue_qr(h, 0))) return rc;
+  if ((rc = join_side(h))) return rc;
+  if ((rc = enqueue_control(h, CTRL_FINISH, 16 | 32))) return rc;
+  if (emit(h)) {
+    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx, 1);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
+  if ((rc = enqueue_control(h, CTRL_DECIDE, 16))) return rc;
+  if ((rc = enqueue_redo(h))) return rc;
+  return enqueue_pipe_prep(h);
+}
+
+static int pipe_drain(cb_solver* h) {
+  if (!h->pipe_pending) return CB_OK;
+  int rc;
+  if ((rc = enqueue_pipe_stream(h, h->st))) return rc;
+  if ((rc = enqueue_control(h, CTRL_FINISH, 16))) return rc;
+  h->pipe_pending = false;
+  return CB_OK;
+}
+
 static int read_state(cb_solver* h) {
   CB_CUDA(cudaMemcpyAsync(h->h_state, h->d_state, sizeof(State), cudaMemcpyDeviceToHost, h->st));
   CB_CUDA(cudaStreamSynchronize(h->st));
@@ -518,7 +592,7 @@ static int generic_iteration(cb_solver* h) {
   if ((rc = enqueue_control(h, CTRL_DECIDE))) return rc;
   if ((rc = read_state(h))) return rc;
   if (h->h_state->go_redo) {
-    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx);
+    launch_k(k_restore, dim3(h->S), dim3(256), h->blk_smem, h->st, h->ctx, 0);
     count_launch(1);
     CB_CHECK_LAUNCH();
     if ((rc = enqueue_sweep(h, 1))) return rc;
@@ -754,6 +828,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   TRY(dalloc((void**)&c.tsq, sizeof(double) * S, A));
   TRY(dalloc((void**)&c.res, sizeof(double) * S, A));
   TRY(dalloc((void**)&c.borig, sizeof(double) * S * RSTRIDE, A));
+  TRY(dalloc((void**)&c.lam_snap, sizeof(double) * S * 64, A));
+  TRY(dalloc((void**)&c.msq_snap, sizeof(double) * S, A));
   int maxL = 0;
   for (int n = 0; n < N; ++n) maxL = std::max(maxL, h->counts[n]);
   c.gc_stride = maxIn * std::max(maxL, 1);
@@ -891,6 +967,22 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       // a plan that does not fit (shared memory) leaves the CUDA-core pass
       if (xtc_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->xtc) != CB_OK)
         h->xtc = nullptr;
+      // pipelined only when the trace pass is large enough to hide the sweep
+      // behind (c3, c5); on small blocks (c4: 35 MB) the extra snapshot /
+      // rollback work costs more than it hides (measured)
+      h->pipe = h->xtc != nullptr && !shard && !getenv("CB_NO_PIPE") &&
+                (xtc_bytes(h->xtc) >= 64e6 || getenv("CB_PIPE"));
+      if (h->pipe) {
+        // leave SMs for the sweep that runs beside the trace: its per-block
+        // CTAs (several per SM), measured best near S / 3 on c5
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        int reserve = (S + 2) / 3;
+        if (getenv("CB_PIPE_RESERVE")) reserve = atoi(getenv("CB_PIPE_RESERVE"));
+        reserve = std::max(0, std::min(reserve, nsm / 3));
+        xtc_set_grid_cap(h->xtc, nsm - reserve);
+      }
     }
     xa.gate = &h->d_state->go_redo;
     h->xa_redo = xa;
@@ -966,6 +1058,60 @@ int cb_solver_step_async(cb_solver* h) {
     int rc = generic_iteration(h);
     return rc;
   }
+  if (h->pipe && !h->timing && !h->profile) {
+    if (!h->pipe_pending) {
+      // a new pipeline: iteration k+1's sweep .. prep, eagerly
+      int rc = enqueue_pipe_prologue(h);
+      if (rc) return rc;
+      h->pipe_pending = true;
+      return CB_OK;
+    }
+    if (!h->gexec_pipe && h->graph_ok) {
+      cudaGraph_t g;
+      cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        if (!getenv("CB_NO_COND")) {
+          cudaGraph_t cg;
+          cudaStreamCaptureStatus cs;
+          if (cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, nullptr, nullptr) == cudaSuccess &&
+              cudaGraphConditionalHandleCreate(&h->ctx.cond, cg, 0, cudaGraphCondAssignDefault) ==
+                  cudaSuccess) {
+            h->ctx.use_cond = 1;
+            h->cond_capture = true;
+          }
+        }
+        const long long before = cb_launch_count();
+        int rc = enqueue_pipe_step(h);
+        h->launches_per_pipe = cb_launch_count() - before;
+        h->ctx.use_cond = 0;
+        h->cond_capture = false;
+        cudaError_t e2 = cudaStreamEndCapture(h->st, &g);
+        if (rc == CB_OK && e2 == cudaSuccess) {
+          if (cudaGraphInstantiate(&h->gexec_pipe, g, 0) != cudaSuccess) {
+            h->gexec_pipe = nullptr;
+            h->graph_ok = false;
+          }
+          cudaGraphDestroy(g);
+        } else {
+          h->graph_ok = false;
+        }
+        cudaGetLastError();
+      } else {
+        h->graph_ok = false;
+        cudaGetLastError();
+      }
+    }
+    if (h->gexec_pipe) {
+      CB_CUDA(cudaGraphLaunch(h->gexec_pipe, h->st));
+      count_launch(h->launches_per_pipe);
+      return CB_OK;
+    }
+    return enqueue_pipe_step(h);
+  }
+  if (h->pipe) {
+    int rc = pipe_drain(h);   // the classic iteration (timing / profile modes)
+    if (rc) return rc;
+  }
   if (h->timing || h->profile) return enqueue_iteration(h);
   if (!h->gexec && h->graph_ok) {
     cudaGraph_t g;
@@ -1014,7 +1160,9 @@ int cb_solver_step_async(cb_solver* h) {
 
 int cb_solver_summary_get(cb_solver* h, cb_solver_summary* sum) {
   CB_ARG(h && sum, "null handle");
-  int rc = read_state(h);
+  int rc = pipe_drain(h);
+  if (rc) return rc;
+  rc = read_state(h);
   if (rc) return rc;
   const State& s = *h->h_state;
   sum->n_iter = s.n_hist > 0 ? s.n_hist - 1 : 0;
@@ -1043,6 +1191,7 @@ int cb_solver_run(cb_solver* h, int iters, cb_solver_summary* sum) {
     rc = read_state(h);
     if (rc) return rc;
   }
+  if ((rc = pipe_drain(h))) return rc;
   if (sum) return cb_solver_summary_get(h, sum);
   return CB_OK;
 }
@@ -1050,7 +1199,9 @@ int cb_solver_run(cb_solver* h, int iters, cb_solver_summary* sum) {
 int cb_solver_history(cb_solver* h, double* obj_int, double* obj_orig, double* rel, double* t_ns,
                       int cap) {
   CB_ARG(h, "null handle");
-  int rc = read_state(h);
+  int rc = pipe_drain(h);
+  if (rc) return rc;
+  rc = read_state(h);
   if (rc) return rc;
   const int n = std::min(cap, h->h_state->n_hist);
   if (n <= 0) return CB_OK;
@@ -1065,6 +1216,10 @@ int cb_solver_history(cb_solver* h, double* obj_int, double* obj_orig, double* r
 int cb_solver_block_factors(cb_solver* h, int block, double* const* host_factors,
                             double* host_weights) {
   CB_ARG(h && block >= 0 && block < h->S, "bad block %d", block);
+  {
+    int rc = pipe_drain(h);
+    if (rc) return rc;
+  }
   for (int n = 0; n < h->N; ++n) {
     if (!host_factors || !host_factors[n]) continue;
     CB_CUDA(cudaMemcpyAsync(host_factors[n], h->h_U[block * h->N + n],
@@ -1146,6 +1301,7 @@ int cb_solver_timeline(cb_solver* h, int op, unsigned long long* out, int cap) {
     h->xa_main.tl = h->ctx.tl;
     h->xa_redo.tl = h->ctx.tl;
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }   // recapture
+    if (h->gexec_pipe) { cudaGraphExecDestroy(h->gexec_pipe); h->gexec_pipe = nullptr; }
   }
   if (op == -1 && h->ctx.tl) {
     h->ctx.tl = nullptr;
@@ -1266,6 +1422,7 @@ int cb_solver_destroy(cb_solver* h) {
   if (!h) return CB_OK;
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gexec_pipe) cudaGraphExecDestroy(h->gexec_pipe);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->st2) cudaStreamDestroy(h->st2);

@@ -22,7 +22,7 @@ struct State {
   int error, err_block, err_iter;
   int tsel, bsel;     // accepted T / b buffers
   int n_hist;         // history entries written (n_iter + 1)
-  int pad;
+  int rollback;       // pipelined lra: the stop came after a speculative sweep (undo it)
   double t_k;
   double w_hat;       // extrapolation weight of the current (main) sweep
   double rel_prev;    // RelErr of the last accepted iteration
@@ -67,6 +67,8 @@ struct Ctx {
   double* nsq;                // S ||M_s||^2
   double* bbuf;               // 2 * S * RSTRIDE staged core linear terms
   double* model_sq;           // S lam^T (hadamard G) lam
+  double* lam_snap;           // S * 64: lam of the iteration whose trace is in flight (pipelined lra)
+  double* msq_snap;           // S: its model_sq
   double* inner;              // S (lra) lam^T (hadamard C)^T w~
   double* res_t;              // S (lra) compressed residual by expansion
   double* tsq;                // S (lra) ||M~||^2

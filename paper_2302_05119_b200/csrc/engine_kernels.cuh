@@ -853,9 +853,11 @@ __global__ void __launch_bounds__(256) k_step(Ctx c, int n, int redo) {
 }
 
 // restore curr <- prev and refresh caches (solver.py:538-543)
-__global__ void __launch_bounds__(256) k_restore(Ctx c) {
+// gate 0: the restart branch (go_redo); gate 1: the pipelined lra rollback
+// of a speculative sweep after a stop (rollback)
+__global__ void __launch_bounds__(256) k_restore(Ctx c, int gate) {
   griddep_wait();
-  if (c.st->go_redo == 0) return;
+  if (gate == 0 ? c.st->go_redo == 0 : c.st->rollback == 0) return;
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
   const int s = blockIdx.x;
@@ -1028,8 +1030,17 @@ __device__ inline double block_res_full(const Ctx& c, int s, int bsrc) {
   return c.nsq[s] - 2.0 * lb + c.model_sq[s];
 }
 
+// momentum: advance t_k / w_hat here (classic order); the pipelined lra
+// iteration advances them at DECIDE instead (the next sweep starts before
+// this FINISH).  rollback_on_stop: that next sweep was speculative.
+__device__ inline void advance_momentum(State* st) {
+  const double t_new = t_next(st->t_k);
+  st->w_hat = (st->t_k - 1.0) / t_new;
+  st->t_k = t_new;
+}
+
 __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double obj_orig, double rel,
-                                   int swap_t) {
+                                   int swap_t, bool momentum = true, bool rollback_on_stop = false) {
   State* st = c.st;
   const int k = st->k;
   c.h_obj[k] = obj_int;
@@ -1053,12 +1064,11 @@ __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double o
   if (stop) {
     st->done = 1;
     st->go_main = 0;
+    if (rollback_on_stop) st->rollback = 1;
     return;
   }
   // momentum for the next iteration (solver.py:588-590)
-  const double t_new = t_next(st->t_k);
-  st->w_hat = (st->t_k - 1.0) / t_new;
-  st->t_k = t_new;
+  if (momentum) advance_momentum(st);
   st->k = k + 1;
 }
 
@@ -1077,6 +1087,11 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
   if (!c.lra && mode == CTRL_FINISH) return;
   const int fast_t = (bsrc == 0);
   const bool lra_cmp = c.lra && (mode == CTRL_DECIDE || mode == CTRL_REDO);
+  // pipelined lra (phase bit 4): FINISH reads the snapshots of its
+  // iteration's lam / model_sq and leaves the momentum to DECIDE, which
+  // advances it; bit 5: the stop rolls back a speculative sweep
+  const bool pipe = (phase & 16) != 0;
+  const bool rb_on_stop = (phase & 32) != 0;
   const int T = c.S_tot;
   tl_begin(c.tl, TL_CONTROL);
   if (phase & 1) {
@@ -1106,14 +1121,14 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
       } else {
         // original-tensor trace quantities (solver.py:519-522)
         const int R = c.R[s];
-        const double* lam = c.LAM[s];
+        const double* lam = pipe ? c.lam_snap + (long long)s * 64 : c.LAM[s];
         double lb = 0.0;
         for (int r = 0; r < R; ++r) {
           const double b = fast_t ? c.fib_bpart[(long long)s * RSTRIDE + r]
                                   : c.borig[(long long)s * RSTRIDE + r];
           lb = fma(lam[r], b, lb);
         }
-        const double raw = c.nsq[s] - 2.0 * lb + c.model_sq[s];
+        const double raw = c.nsq[s] - 2.0 * lb + (pipe ? c.msq_snap[s] : c.model_sq[s]);
         val[g] = raw;   // Python max(raw, 0.0) keeps NaN / +inf (checked below)
         const double nrm = sqrt(c.nsq[s]);
         const double r = raw > 0.0 ? raw : 0.0;
@@ -1165,6 +1180,7 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
     double oi = 0.0;
     for (int s = 0; s < T; ++s) oi += 0.5 * (val[s] > 0.0 ? val[s] : 0.0);
     st->obj_pending = oi;
+    if (mode == CTRL_DECIDE && pipe) advance_momentum(st);
     if (mode == CTRL_DECIDE && oi >= st->obj_prev) {
       st->n_restarts += 1;
       st->go_redo = 1;
@@ -1193,7 +1209,18 @@ __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int 
     rel += relv[s];
   }
   rel /= T;
-  accept_and_advance(c, oi, oo, rel, 0);
+  accept_and_advance(c, oi, oo, rel, 0, !(pipe && mode == CTRL_FINISH), rb_on_stop);
+}
+
+// pipelined lra: lam and model_sq of the iteration whose trace pass runs
+// beside the next (speculative) sweep, read by its FINISH
+__global__ void __launch_bounds__(64) k_pipe_snap(Ctx c) {
+  griddep_wait();
+  if (c.st->go_main == 0) return;
+  const int s = blockIdx.x;
+  const int R = c.R[s];
+  for (int r = threadIdx.x; r < R; r += blockDim.x) c.lam_snap[(long long)s * 64 + r] = c.LAM[s][r];
+  if (threadIdx.x == 0) c.msq_snap[s] = c.model_sq[s];
 }
 
 // emulated shard group exchange: recv_k <- sum_r send_r for every rank k

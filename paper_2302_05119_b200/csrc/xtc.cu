@@ -121,6 +121,7 @@ struct XtcArgs {
 
 struct XtcPlan {
   int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, u1_bytes = 0, ntiles = 0;
+  int grid_cap = 0;          // > 0: at most this many CTAs (SMs left to concurrent work)
   long long i2max = 1;
   double* m2part = nullptr;
   size_t smem = 0;
@@ -904,16 +905,29 @@ void xtc_plan_destroy(XtcPlan* p) {
 
 double xtc_bytes(const XtcPlan* p) { return p ? p->bytes : 0.0; }
 
+void xtc_set_grid_cap(XtcPlan* p, int cap) {
+  if (p) p->grid_cap = cap;
+}
+
 template <int N>
-static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStream_t st) {
-  CB_CUDA(launch_k(k_xtc_prep<N>, dim3(p->S), dim3(256), 0, st, a, U));
-  CB_CUDA(launch_k(k_xtc_trace<N>, dim3(p->grid), dim3(xtc_threads<N>()), p->smem, st, a));
-  count_launch(2);
+static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStream_t st,
+                  int parts = 3) {
+  if (parts & 1) {
+    CB_CUDA(launch_k(k_xtc_prep<N>, dim3(p->S), dim3(256), 0, st, a, U));
+    count_launch(1);
+  }
+  if (parts & 2) {
+    const int grid = p->grid_cap > 0 ? std::min(p->grid, p->grid_cap) : p->grid;
+    CB_CUDA(launch_k(k_xtc_trace<N>, dim3(grid), dim3(xtc_threads<N>()), p->smem, st, a));
+    count_launch(1);
+  }
   return CB_OK;
 }
 
+// parts: 1 = operand prep only (snapshots the factors), 2 = the streaming
+// pass only (reads only the prepared operands), 3 = both
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
-              cudaStream_t st) {
+              cudaStream_t st, int parts) {
   XtcArgs a;
   a.tmaps = p->tmaps;
   a.blk = p->blk;
@@ -931,10 +945,10 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.m2part = nullptr;
   a.active = nullptr;
   switch (p->N) {
-    case 16: return xtc_go<16>(p, a, U_dev, st);
-    case 32: return xtc_go<32>(p, a, U_dev, st);
-    case 48: return xtc_go<48>(p, a, U_dev, st);
-    default: return xtc_go<64>(p, a, U_dev, st);
+    case 16: return xtc_go<16>(p, a, U_dev, st, parts);
+    case 32: return xtc_go<32>(p, a, U_dev, st, parts);
+    case 48: return xtc_go<48>(p, a, U_dev, st, parts);
+    default: return xtc_go<64>(p, a, U_dev, st, parts);
   }
 }
 

@@ -30,7 +30,7 @@ void xtc_plan_destroy(XtcPlan* p);
 // S*3 pointers, the engine's XArgs.U), skipped when *gate == 0 (gate may be
 // null).  Two launches: operand prep + the streaming MMA kernel.
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
-              cudaStream_t st);
+              cudaStream_t st, int parts = 3);
 
 // mode-2 MTTKRP on the same pipeline (the ALS compression of rank > 16
 // blocks; plan created with mode2 = 1, I1 >= 32): mtt[s] (device array of S
@@ -38,6 +38,10 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
 // blocks with active[s] == 0 are skipped.  Three launches (prep, stream, fold).
 int xtc_mode2(XtcPlan* p, const double* const* U_dev, const int* active, double* const* mtt,
               cudaStream_t st);
+
+// cap the streaming kernel's persistent grid (0: one CTA per SM), leaving
+// SMs to work that runs beside it (the pipelined lra sweep)
+void xtc_set_grid_cap(XtcPlan* p, int cap);
 
 // algorithmic bytes streamed per xtc_trace call (sum_s |X_s| * 4)
 double xtc_bytes(const XtcPlan* p);
