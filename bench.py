@@ -250,8 +250,8 @@ def run_ours(args):
              ("fiber4" if (dom_name == "fiber" and spec.mode == "full" and prec == "fp32" and
                            spec.rank <= 16) else dom_name))
     traffic_tab = {
-        ("c2", "slab"): (40.187648e6, "profiles/r01e_c2_streaming_ncu_summary.txt"),
-        ("c2", "fiber4"): (40.101120e6 + 9.216e3, "profiles/r01e_c2_streaming_ncu_summary.txt"),
+        ("c2", "slab"): (40.186624e6, "profiles/r01f_c2_streaming_ncu_summary.txt"),
+        ("c2", "fiber4"): (40.100096e6 + 18.944e3, "profiles/r01f_c2_streaming_ncu_summary.txt"),
         ("c5", "xtc"): (16.518760e9 + 41.288448e6, "profiles/r01c_xtc_c5_ncu_summary.txt"),
     }
     traffic, traffic_src = traffic_tab.get((spec.name, kname), (None, None))

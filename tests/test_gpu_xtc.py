@@ -149,3 +149,32 @@ def test_tc_mode2_als_matches_fp64_als(P):
         a, b = np.asarray(out[0][s]), np.asarray(out[2][s])
         assert len(a) == len(b) == 12
         np.testing.assert_allclose(b, a, rtol=1e-5, atol=0)
+
+
+@pytest.mark.parametrize("tol,max_iter", [(1e-30, 40), (1e-5, 400)])
+def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, monkeypatch, tol, max_iter):
+    """The pipelined lra iteration (csrc/engine.cu enqueue_pipe_*: the trace of
+    iteration k beside the sweep of k+1, snapshots, rollback on stop) returns
+    the unpipelined solve's factors, histories and stop iteration bitwise,
+    both at max_iter and at an early tol stop (the rollback path)."""
+    rng = np.random.default_rng(33)
+    tensors = [_block(rng, (64, 40, 30), 20)[0] for _ in range(3)]
+    out = {}
+    for pipe in (True, False):
+        monkeypatch.delenv("CB_PIPE", raising=False)
+        monkeypatch.delenv("CB_NO_PIPE", raising=False)
+        monkeypatch.setenv("CB_PIPE" if pipe else "CB_NO_PIPE", "1")
+        prob = P.CoupledProblem(tensors, 20, [5, 5, 0], mode="lra")
+        out[pipe] = P.solve(prob, P.SolverOptions(max_iter=max_iter, tol=tol, seed=5,
+                                                  precision="fp32", compute="tc"))
+    a, b = out[True], out[False]
+    assert a.n_iter == b.n_iter and a.termination_reason == b.termination_reason
+    if tol > 1e-20:
+        assert a.n_iter < max_iter            # the stop (and rollback) path ran
+    assert a.objective_history == b.objective_history
+    assert a.rel_err_history == b.rel_err_history
+    assert a.n_restarts == b.n_restarts
+    for ba, bb in zip(a.factors.blocks, b.factors.blocks):
+        np.testing.assert_array_equal(ba.weights, bb.weights)
+        for fa, fb in zip(ba.factors, bb.factors):
+            np.testing.assert_array_equal(fa, fb)
