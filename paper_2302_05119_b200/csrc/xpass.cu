@@ -156,6 +156,34 @@ static void fiber4_dispatch(int rb, const XArgs& a, const FibUnit* u, int n, con
   else fiber4_tj<16>(a, u, n, t, st, prep);
 }
 
+// resident fiber4 CTAs per SM for tile TJ (registers of the compiled kernel,
+// its ring + A2 shared memory, 288 threads), used by the CB_F4_OCC tile model
+// (c2: TJ 1 runs 4 CTAs / 32 consumer warps per SM)
+template <int RB>
+static int fiber4_occ_rb(int tj, long long a2_rows) {
+  cudaFuncAttributes fa{};
+  cudaError_t e;
+  if (tj >= 4) e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 4>);
+  else if (tj == 3) e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 3>);
+  else if (tj == 2) e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 2>);
+  else e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 1>);
+  if (e != cudaSuccess) { (void)cudaGetLastError(); return 1; }
+  const long long warps = F4_THREADS / 32;
+  const long long regs_warp = ((long long)fa.numRegs * 32 + 255) / 256 * 256;
+  const long long by_regs = 65536 / std::max(1LL, regs_warp * warps);
+  const long long smem = (long long)fiber4_smem<float>(a2_rows, RB, tj) + 1024;
+  const long long by_smem = (228LL * 1024) / smem;
+  const long long by_thr = 2048 / F4_THREADS;
+  return (int)std::max(1LL, std::min({by_regs, by_smem, by_thr}));
+}
+
+static int fiber4_occ(int rb, int tj, long long a2_rows) {
+  if (rb <= 8) return fiber4_occ_rb<8>(tj, a2_rows);
+  if (rb <= 10) return fiber4_occ_rb<10>(tj, a2_rows);
+  if (rb <= 12) return fiber4_occ_rb<12>(tj, a2_rows);
+  return fiber4_occ_rb<16>(tj, a2_rows);
+}
+
 // T + explicit residual (the ALS sweep's fiber pass) for ranks > 16 on the
 // fiber4 ring, over the fiber2 unit table (same units, same partial slots)
 static bool fiber4res_ok(int pc, int rb, bool tma, const XTables& t) {
@@ -415,10 +443,19 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   t.fib_first[S] = (int)t.fib.size();
   t.fib_unsplit = 1;
   for (int s = 0; s < S; ++s) t.fib_unsplit = t.fib_unsplit && t.nsplit[s] == 1;
-  // fiber4 units: the tile minimising waves x TJ over this engine's blocks
+  // fiber4 units: the tile minimising waves x TJ over this engine's blocks,
+  // a wave being 148 CTAs.  CB_F4_OCC counts 148 x the resident CTAs per SM
+  // instead: on c2 that picks TJ 1 (4 CTAs per SM), the kernel drops from 34
+  // to 25 us but the step slows 6.33k -> 6.17k it/s, because the T pass runs
+  // on the side stream beside k_sweep_begin / k_step (the critical path) and
+  // at 4 CTAs per SM it leaves those R x R kernels no SM (profiles/r01h_*).
+  // CB_F4_TJ: fixed tile.
   t.fib4.clear();
   t.fib4_tj = 0;
   if (t.fiber_direct && pc == PC_F32_F64 && rb <= 16) {
+    static const bool flat = getenv("CB_F4_OCC") == nullptr;
+    long long i2max = 1;
+    for (int s = 0; s < S; ++s) i2max = std::max(i2max, dims[3 * s + 2]);
     long long best = -1;
     for (int c : {4, 3, 2, 1}) {
       long long u = 0;
@@ -426,9 +463,11 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
         const long long J = dims[3 * s] * dims[3 * s + 1];
         u += (J + 256LL * c - 1) / (256LL * c);
       }
-      const long long cost = ((u + 147) / 148) * c;
+      const long long slots = 148LL * (flat ? 1 : fiber4_occ(rb, c, i2max));
+      const long long cost = ((u + slots - 1) / slots) * c;
       if (best < 0 || cost < best) { best = cost; t.fib4_tj = c; }
     }
+    if (getenv("CB_F4_TJ")) t.fib4_tj = std::max(1, std::min(4, atoi(getenv("CB_F4_TJ"))));
     const long long JT4 = 256LL * t.fib4_tj;
     for (int s = 0; s < S; ++s) {
       const long long J = dims[3 * s] * dims[3 * s + 1];
