@@ -197,6 +197,10 @@ typedef struct {
   void* nccl_comm;                /* ncclComm_t created by cb_nccl_comm_init */
   int total_blocks;               /* S over all ranks                        */
   int block_offset;               /* global index of this rank's first block */
+  /* lra with the tensor-core trace pass: iteration k's trace pass streams
+   * beside iteration k+1's sweep (results bitwise those of the serial order).
+   * 0 = auto (on when the trace pass streams >= 64 MB), 1 = on, 2 = off. */
+  int pipeline;
 } cb_solver_desc;
 
 typedef struct {

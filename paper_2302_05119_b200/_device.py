@@ -41,6 +41,10 @@ def tensor_to_dev(t, dtype="fp64"):
         dims = tuple(int(d) for d in t.shape)
         if t.is_cuda and t.dtype == want and tuple(t.stride()) == fortran_strides(dims):
             return t.as_strided((t.numel(),), (1,)), dims      # already first-index-fastest
+        if not t.is_cuda and t.dtype == want and tuple(t.stride()) == fortran_strides(dims):
+            # host buffer already first-index-fastest (pinned: asynchronous DMA)
+            flat = t.as_strided((t.numel(),), (1,))
+            return flat.to(device=device(), non_blocking=t.is_pinned()), dims
         perm = tuple(range(t.ndim - 1, -1, -1))
         flat = t.permute(*perm).contiguous().reshape(-1)   # Fortran order of t
         return flat.to(device=device(), dtype=want), dims
@@ -49,6 +53,22 @@ def tensor_to_dev(t, dtype="fp64"):
     np_dtype = np.float64 if dtype == "fp64" else np.float32
     flat = np.ravel(np.asarray(a, dtype=np_dtype), order="F")
     return torch.from_numpy(np.ascontiguousarray(flat)).to(device()), dims
+
+
+def source_dtype(t):
+    """"fp32" for float32 input (numpy or torch), else "fp64" (the
+    reference casts everything else to float64, solver.py:91)."""
+    dt = getattr(t, "dtype", None)
+    if dt is None:
+        return "fp64"
+    torch = torch_mod()
+    return "fp32" if dt in (np.float32, torch.float32) else "fp64"
+
+
+def cast_flat(flat, dtype):
+    """Device-side cast of a flat buffer to the solve precision."""
+    torch = torch_mod()
+    return flat.to(torch.float64 if dtype == "fp64" else torch.float32)
 
 
 def fortran_strides(dims):

@@ -45,7 +45,7 @@ class SolverDesc(ctypes.Structure):
         ("tilde_factors", ctypes.POINTER(c_dp)), ("tilde_weights", ctypes.POINTER(c_dp)),
         ("objective", c_int), ("compute", c_int), ("delta_w", c_dbl), ("tol", c_dbl), ("max_iter", c_int),
         ("world_size", c_int), ("rank_id", c_int), ("nccl_comm", c_vp),
-        ("total_blocks", c_int), ("block_offset", c_int),
+        ("total_blocks", c_int), ("block_offset", c_int), ("pipeline", c_int),
     ]
 
 

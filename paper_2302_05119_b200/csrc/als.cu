@@ -476,7 +476,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     // not apply): the mode-2 MTTKRP on the tensor cores; a plan that does not
     // fit leaves the CUDA-core slab pass
     if (d->compute == 2 && h->dtype == CB_F32 && !h->tab.slab_direct &&
-        xtc_supported(S, h->X.data(), h->dims.data(), h->R.data()) && !getenv("CB_NO_XTC_ALS")) {
+        xtc_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
       bool i1_ok = true;
       for (int s = 0; s < S; ++s) i1_ok = i1_ok && h->dims[3 * s + 1] >= 32;
       if (i1_ok &&

@@ -52,8 +52,6 @@ struct cb_solver {
   cudaStream_t st3 = nullptr;     // capture stream of the conditional restart body
   bool cond_capture = false;
   bool in_body = false;
-  bool fused = false;          // k_mode_fused replaces k_mode_update + k_finalize
-  size_t fused_smem = 0;
   int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0, pc = 0;
   int rmax = 1, rtmax = 0, rb = 8, max_iter = 0;
   double delta_w = 0.9999, tol = 1e-8;
@@ -85,7 +83,6 @@ struct cb_solver {
   bool timing = false;
   bool profile = false;
   bool tma = false;             // bulk-copy streaming path usable
-  unsigned long long* ktime = nullptr;   // in-kernel launch timers (CB_PHASES)
   std::vector<cudaEvent_t> mpool;
   std::vector<const char*> mlabels;
   size_t mused = 0;
@@ -288,16 +285,6 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       prof(h, "generic_mttkrp");
     }
     const bool split = par && n + 1 < h->N;
-    if (h->fused) {
-      // mode update + finalize in one cooperative launch (one CTA per block)
-      if (emit(h)) {
-        CB_CUDA(launch_coop(k_mode_fused, dim3(h->S), dim3(256), h->fused_smem, st, h->ctx, n,
-                            redo, src, split ? 0 : 1));
-        count_launch(1);
-        CB_CHECK_LAUNCH();
-      }
-      prof(h, redo ? "redo:mode_fused" : "mode_fused");
-    } else {
     if (emit(h)) {
       launch_k(k_mode_update, dim3(h->n_rows[n]), dim3(256), h->mu_smem, st, h->ctx, n, redo, src, h->d_rows[n]);
       count_launch(1);
@@ -320,7 +307,6 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       CB_CHECK_LAUNCH();
     }
     prof(h, redo ? "redo:finalize" : "finalize");
-    }
     if (split) {
       if ((rc = fork_side(h))) return rc;
       if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
@@ -807,7 +793,6 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   }
   TRY(dalloc((void**)&c.lipc_hist, sizeof(double) * S, A));
   c.dbg = nullptr;
-  if (getenv("CB_PHASES")) TRY(dalloc((void**)&c.dbg, sizeof(double) * 64, A));
   TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
   TRY(dalloc((void**)&c.ldcore, sizeof(double) * S, A));
   // coupling arrays in global block slots; separate send copies when sharded
@@ -951,14 +936,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     // its MTTKRP output (solver.py:506-509) in k_finalize of the last mode,
     // so the evaluation fiber pass only forms T
     c.b_mtt = (h->tab.slab_direct && !h->lra) ? 1 : 0;
-    c.ld_pre = (c.b_mtt && !getenv("CB_NO_LDPRE")) ? 1 : 0;
-    if (c.dbg) {
-      TRY(dalloc((void**)&h->ktime, sizeof(unsigned long long) * 8, A));
-      const unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, ~0ull, 0};
-      CB_CUDA(cudaMemcpyAsync(h->ktime, init, sizeof(init), cudaMemcpyHostToDevice, st));
-      CB_CUDA(cudaStreamSynchronize(st));
-      xa.ktime = h->ktime;
-    }
+    c.ld_pre = c.b_mtt;
     xa.gate = &h->d_state->go_main;
     h->xa_main = xa;
     // lra trace pass on the tensor cores (compute code 2, fp32 storage)
@@ -970,8 +948,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       // pipelined only when the trace pass is large enough to hide the sweep
       // behind (c3, c5); on small blocks (c4: 35 MB) the extra snapshot /
       // rollback work costs more than it hides (measured)
-      h->pipe = h->xtc != nullptr && !shard && !getenv("CB_NO_PIPE") &&
-                (xtc_bytes(h->xtc) >= 64e6 || getenv("CB_PIPE"));
+      h->pipe = h->xtc != nullptr && !shard && d->pipeline != 2 &&
+                (xtc_bytes(h->xtc) >= 64e6 || d->pipeline == 1);
       if (h->pipe) {
         // leave SMs for the sweep that runs beside the trace: its per-block
         // CTAs (several per SM), measured best near S / 3 on c5
@@ -979,7 +957,6 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         int reserve = (S + 2) / 3;
-        if (getenv("CB_PIPE_RESERVE")) reserve = atoi(getenv("CB_PIPE_RESERVE"));
         reserve = std::max(0, std::min(reserve, nsm / 3));
         xtc_set_grid_cap(h->xtc, nsm - reserve);
       }
@@ -1015,21 +992,6 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
-  // fused mode update: single GPU, all S CTAs co-resident (cooperative)
-  h->fused_smem = std::max(h->blk_smem, h->mu_smem);
-  CB_CUDA(cudaFuncSetAttribute(k_mode_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)h->fused_smem));
-  {
-    int dev = 0, per_sm = 0, sms = 0, coop = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mode_fused, 256, h->fused_smem);
-    // opt-in: measured slower on c2 (phase A serialises the row tiles of a
-    // block in one CTA; phase B's block-order fold is a chain of L2 reads)
-    h->fused = !h->shard && coop && per_sm >= 1 && S <= per_sm * sms && getenv("CB_FUSED");
-    TRY(dalloc((void**)&c.gbar, sizeof(unsigned), A));
-  }
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
@@ -1070,7 +1032,7 @@ int cb_solver_step_async(cb_solver* h) {
       cudaGraph_t g;
       cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
       if (e == cudaSuccess) {
-        if (!getenv("CB_NO_COND")) {
+        {
           cudaGraph_t cg;
           cudaStreamCaptureStatus cs;
           if (cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, nullptr, nullptr) == cudaSuccess &&
@@ -1118,7 +1080,7 @@ int cb_solver_step_async(cb_solver* h) {
     cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
       // conditional restart branch (not with NCCL exchanges inside it)
-      if (!h->shard && !getenv("CB_NO_COND")) {
+      if (!h->shard) {
         cudaGraph_t cg;
         cudaStreamCaptureStatus cs;
         if (cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, nullptr, nullptr) == cudaSuccess &&
@@ -1273,18 +1235,6 @@ int cb_solver_profile(cb_solver* h, int on, char* out, int cap) {
         s += line;
       }
   }
-  if (h->ktime) {
-    unsigned long long kt[8];
-    CB_CUDA(cudaMemcpy(kt, h->ktime, sizeof(kt), cudaMemcpyDeviceToHost));
-    if (kt[1]) {
-      snprintf(line, sizeof(line), "kernel:fiber %llu %.6f\n", kt[1], kt[0] * 1e-6);
-      s += line;
-    }
-    if (kt[5]) {
-      snprintf(line, sizeof(line), "kernel:slab %llu %.6f\n", kt[5], kt[4] * 1e-6);
-      s += line;
-    }
-  }
   if (out && cap > 0) {
     strncpy(out, s.c_str(), cap - 1);
     out[cap - 1] = 0;
@@ -1307,7 +1257,9 @@ int cb_solver_timeline(cb_solver* h, int op, unsigned long long* out, int cap) {
     h->ctx.tl = nullptr;
     h->xa_main.tl = nullptr;
     h->xa_redo.tl = nullptr;
+    // both iteration graphs captured the timeline pointer: recapture them
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+    if (h->gexec_pipe) { cudaGraphExecDestroy(h->gexec_pipe); h->gexec_pipe = nullptr; }
     return CB_OK;
   }
   if (!h->ctx.tl) return CB_OK;

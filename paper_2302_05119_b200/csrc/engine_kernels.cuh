@@ -531,184 +531,6 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   if (threadIdx.x == 0) c.tile_cnt[r0 / MU_ROWS] = 0;
 }
 
-// ---------------------------------------------------------------------------
-// Fused mode update + finalize, one CTA per block (single-GPU runs with
-// S <= co-resident CTAs; cooperative launch): phase A forms, tile by tile, the
-// extrapolated point, gradient, new individual columns and the common-gradient
-// partial of this block; a grid-wide barrier; phase B folds the common
-// columns (every CTA the same sums in block order, solver.py:444-451), writes
-// prev <- curr, curr <- [c_new | individual], refreshes the gram and, unless
-// split off, the next mode's step matrix and Lipschitz constant.  Replaces
-// k_mode_update + k_finalize (one launch and one dependency fewer per mode).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned arrive = atomicAdd(bar, 1u);
-    const unsigned target = (arrive / n + 1u) * n;
-    unsigned seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
-    } while ((int)(seen - target) < 0);
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(256) k_mode_fused(Ctx c, int n, int redo, int src,
-                                                    int with_step) {
-  griddep_wait();
-  if (stopped(c, redo)) return;
-  tl_begin(c.tl, TL_MU + n);
-  extern __shared__ double smd[];
-  const int s = blockIdx.x;
-  const int R = c.R[s];
-  const int N = c.N;
-  const int L = c.counts[n];
-  const long long In = c.dims[s * N + n];
-  const double w_hat = redo ? 0.0 : c.st->w_hat;
-  // phase-A smem: step | uh | mt | P | scalars; phase B reuses the whole area
-  double* step = smd;
-  double* uh = step + R * R;
-  double* mt = uh + MU_ROWS * R;
-  double* P = mt + MU_ROWS * R;
-  double* sc = P + (c.lra ? c.Rt[s] * R : 0);
-  const double* lam = c.LAM[s];
-  if (threadIdx.x == 0) {
-    double sl, slp;
-    common_lip_sums(c, n, sl, slp);
-    sc[0] = sl;
-    sc[1] = extrap_weight(w_hat, slp, sl, c.delta_w);
-    const int g = c.off + s;
-    sc[2] = extrap_weight(w_hat, c.lip_w[lup_idx(c, n, g)], c.lip_w[lu_idx(c, n, g)], c.delta_w);
-    sc[3] = c.lip_w[lu_idx(c, n, g)];
-  }
-  const double* stp = c.STEP[s];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) step[e] = stp[e];
-  if (src == 2) {
-    const int Rt = c.Rt[s];
-    for (int e = threadIdx.x; e < Rt * R; e += blockDim.x) {
-      double v = 0.0;
-      bool first = true;
-      for (int m = 0; m < N; ++m) {
-        if (m == n) continue;
-        const double gg = c.C[s * N + m][e];
-        v = first ? gg : v * gg;
-        first = false;
-      }
-      P[e] = first ? 1.0 : v;
-    }
-  }
-  __syncthreads();
-  const double sumL = sc[0], wc = sc[1], ws = sc[2], lu = sc[3];
-  double* Uc = c.U[s * N + n];
-  double* Upr = c.Up[s * N + n];
-  double* Un = c.Un[s * N + n];
-  const int R0 = c.R[0];
-  const double* U0c = c.U[n];
-  const double* U0p = c.Up[n];
-  double* gcp = c.gc_w + (long long)(c.off + s) * c.gc_stride;
-  for (long long r0 = 0; r0 < In; r0 += MU_ROWS) {
-    const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
-    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
-      const int il = e / R, r = e - il * R;
-      const long long i = r0 + il;
-      double v;
-      if (r < L) {
-        const double cc = U0c[i * R0 + r], cp = U0p[i * R0 + r];
-        v = cc + wc * (cc - cp);
-      } else {
-        const double cur = Uc[i * R + r], prv = Upr[i * R + r];
-        v = cur + ws * (cur - prv);
-      }
-      uh[e] = v;
-      if (src == 0) {
-        mt[e] = c.MTT[s][i * R + r];
-      } else if (src == 1) {
-        const int sb = c.slab_sb;
-        const long long gq = i / sb;
-        const int m = (int)(i - gq * sb);
-        const int nch = c.slab_nchunk[s];
-        const long long base = c.slab_first[s] + gq * nch;
-        double a = 0.0;
-        for (int ch = 0; ch < nch; ++ch) a += c.slab_part[((base + ch) * sb + m) * RSTRIDE + r];
-        mt[e] = a;
-      } else {
-        const int Rt = c.Rt[s];
-        const double* Ut = c.Ut[s * N + n];
-        const double* tw = c.TW[s];
-        double a = 0.0;
-        for (int q = 0; q < Rt; ++q) a = fma(Ut[i * Rt + q] * tw[q], P[q * R + r], a);
-        mt[e] = a;
-      }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
-      const int il = e / R, r = e - il * R;
-      const long long i = r0 + il;
-      if (lu == 0.0) {
-        if (r >= L) Un[i * R + r] = Uc[i * R + r];
-        continue;
-      }
-      double gv = 0.0;
-      for (int q = 0; q < R; ++q) gv = fma(uh[il * R + q], step[q * R + r], gv);
-      gv -= mt[e] * lam[r];
-      if (r < L) gcp[i * L + r] = gv;
-      else Un[i * R + r] = pos(uh[e] - gv / lu);
-    }
-    __syncthreads();
-  }
-  tl_end(c.tl, TL_MU + n);
-  // ---- all blocks' partials written: fold the common columns
-  if (L > 0) grid_barrier(c.gbar, (unsigned)gridDim.x);
-  tl_begin(c.tl, TL_FIN + n);
-  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
-  for (long long e = threadIdx.x; e < In * R; e += blockDim.x) {
-    const long long i = e / R;
-    const int r = (int)(e - i * R);
-    const double cur = Uc[e];
-    double nv;
-    if (r < L) {
-      // c_new[i, r] (solver.py:444-451): the same sums in block order on every
-      // CTA.  The common columns are bit-identical copies in every block, so
-      // this block's own (not block 0's, which its CTA may be rewriting) serve
-      double acc = 0.0;
-      for (int q = 0; q < c.S_tot; ++q) {
-        if (!(c.lip[lu_idx(c, n, q)] > 0.0)) continue;
-        acc += __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + r]);
-      }
-      const double cp = Upr[e];
-      const double chat = cur + wc * (cur - cp);
-      nv = sumL > 0.0 ? pos(chat - acc / sumL) : cur;
-    } else {
-      nv = Un[e];
-    }
-    Upr[e] = cur;
-    Uc[e] = nv;
-  }
-  __syncthreads();
-  block_gram(Uc, R, Uc, R, In, c.G[s * N + n], sm);
-  if (c.lra) block_gram(c.Ut[s * N + n], c.Rt[s], Uc, R, In, c.C[s * N + n], sm);
-  __syncthreads();
-  if (n + 1 < N) {
-    if (with_step) step_and_lipschitz(c, s, n + 1, sm);
-  } else if (!c.ld_pre) {
-    if (c.b_mtt) {
-      const double* M = c.MTT[s];
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      for (int r = wid; r < R; r += blockDim.x >> 5) {
-        double v = 0.0;
-        for (long long i = lane; i < In; i += 32) v = fma(Uc[i * R + r], M[i * R + r], v);
-        v = warp_sum(v);
-        if (lane == 0) c.fib_bpart[(long long)s * RSTRIDE + r] = v;
-      }
-    }
-    final_quantities(c, s, sm);
-  }
-  tl_end(c.tl, TL_FIN + n);
-}
-
 // sharded runs: new common columns of one row tile from the all-reduced
 // partials (grid: row tiles of mode n)
 __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
@@ -1082,7 +904,13 @@ __device__ inline void accept_and_advance(const Ctx& c, double obj_int, double o
 __global__ void __launch_bounds__(256) k_control(Ctx c, int mode, int bsrc, int phase) {
   griddep_wait();
   State* st = c.st;
-  if (st->done) return;
+  if (st->done) {
+    // pipelined lra: the DECIDE after a stop follows the rollback restore
+    // (k_restore gate 1) of the same step; clear the flag so later steps of
+    // the host's polling chunk do not repeat that restore
+    if (mode == CTRL_DECIDE && threadIdx.x == 0) st->rollback = 0;
+    return;
+  }
   if (mode == CTRL_REDO && !st->go_redo) return;
   if (!c.lra && mode == CTRL_FINISH) return;
   const int fast_t = (bsrc == 0);

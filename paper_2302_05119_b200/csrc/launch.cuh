@@ -2,7 +2,7 @@
 // cudaLaunchAttributeProgrammaticStreamSerialization, so inside the iteration
 // graph consecutive kernels get programmatic edges and the next kernel's CTAs
 // are scheduled while the previous one drains (each kernel starts with
-// griddep_wait()).  CB_NO_PDL=1 turns it off.
+// griddep_wait()).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdlib.h>
@@ -10,11 +10,6 @@
 #include <utility>
 
 namespace cb {
-
-inline bool pdl_enabled() {
-  static const bool on = getenv("CB_NO_PDL") == nullptr;
-  return on;
-}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -28,7 +23,7 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

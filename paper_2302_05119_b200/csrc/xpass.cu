@@ -94,37 +94,10 @@ static void fiber_dispatch(int pc, int rb, bool tma, int want_t, int want_b, int
   }
 }
 
-template <typename TE, int RB>
-static void fiber3_go(bool tma, const XArgs& a, const XTables& t, cudaStream_t st, bool prep) {
-  (void)tma;
-  const int ntasks = t.f3_first.back();
-  const int S = (int)t.f3_first.size() - 1;
-  const int grid = std::max(1, std::min((ntasks + F3_WARPS - 1) / F3_WARPS, 148 * 2));
-  const int a2r = (int)t.f3_a2_rows;
-  const size_t sm = fiber3_smem(a2r, RB);
-  if (prep) {
-    cudaFuncSetAttribute(fiber3_kernel<TE, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    return;
-  }
-  launch_k(fiber3_kernel<TE, RB>, dim3(grid), dim3(F3_WARPS * 32), sm, st, a, a.f3_first, S,
-           ntasks, a2r);
-}
-
-template <typename TE>
-static void fiber3_dispatch(int rb, bool tma, const XArgs& a, const XTables& t, cudaStream_t st,
-                            bool prep) {
-  if (rb <= 8) fiber3_go<TE, 8>(tma, a, t, st, prep);
-  else if (rb <= 10) fiber3_go<TE, 10>(tma, a, t, st, prep);
-  else if (rb <= 12) fiber3_go<TE, 12>(tma, a, t, st, prep);
-  else fiber3_go<TE, 16>(tma, a, t, st, prep);
-}
-
 // warp-specialised T pass (xpass4.cuh): T-only launches, fp32 storage with
 // fp64 arithmetic, unsplit T, rank bucket <= 16, bulk-copy rows
 static bool fiber4_ok(int pc, int rb, bool tma, const XTables& t) {
-  static const bool off = getenv("CB_NO_F4") != nullptr;
-  return !off && pc == PC_F32_F64 && rb <= 16 && tma && t.fiber_direct && t.fib4_tj > 0;
+  return pc == PC_F32_F64 && rb <= 16 && tma && t.fiber_direct && t.fib4_tj > 0;
 }
 
 template <int RB, int TJ>
@@ -156,39 +129,10 @@ static void fiber4_dispatch(int rb, const XArgs& a, const FibUnit* u, int n, con
   else fiber4_tj<16>(a, u, n, t, st, prep);
 }
 
-// resident fiber4 CTAs per SM for tile TJ (registers of the compiled kernel,
-// its ring + A2 shared memory, 288 threads), used by the CB_F4_OCC tile model
-// (c2: TJ 1 runs 4 CTAs / 32 consumer warps per SM)
-template <int RB>
-static int fiber4_occ_rb(int tj, long long a2_rows) {
-  cudaFuncAttributes fa{};
-  cudaError_t e;
-  if (tj >= 4) e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 4>);
-  else if (tj == 3) e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 3>);
-  else if (tj == 2) e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 2>);
-  else e = cudaFuncGetAttributes(&fa, fiber4_kernel<float, RB, 1>);
-  if (e != cudaSuccess) { (void)cudaGetLastError(); return 1; }
-  const long long warps = F4_THREADS / 32;
-  const long long regs_warp = ((long long)fa.numRegs * 32 + 255) / 256 * 256;
-  const long long by_regs = 65536 / std::max(1LL, regs_warp * warps);
-  const long long smem = (long long)fiber4_smem<float>(a2_rows, RB, tj) + 1024;
-  const long long by_smem = (228LL * 1024) / smem;
-  const long long by_thr = 2048 / F4_THREADS;
-  return (int)std::max(1LL, std::min({by_regs, by_smem, by_thr}));
-}
-
-static int fiber4_occ(int rb, int tj, long long a2_rows) {
-  if (rb <= 8) return fiber4_occ_rb<8>(tj, a2_rows);
-  if (rb <= 10) return fiber4_occ_rb<10>(tj, a2_rows);
-  if (rb <= 12) return fiber4_occ_rb<12>(tj, a2_rows);
-  return fiber4_occ_rb<16>(tj, a2_rows);
-}
-
 // T + explicit residual (the ALS sweep's fiber pass) for ranks > 16 on the
 // fiber4 ring, over the fiber2 unit table (same units, same partial slots)
 static bool fiber4res_ok(int pc, int rb, bool tma, const XTables& t) {
-  static const bool off = getenv("CB_NO_F4RES") != nullptr;
-  return !off && pc == PC_F32_F64 && rb >= 24 && tma && t.fib_unsplit &&
+  return pc == PC_F32_F64 && rb >= 24 && tma && t.fib_unsplit &&
          t.fib_tj == x2_tile(rb, 8);
 }
 
@@ -217,11 +161,6 @@ void prepare_fiber(int pc, int rb, bool tma, const XTables& t) {
   XArgs a{};
   if (fiber4_ok(pc, rb, tma, t)) fiber4_dispatch(rb, a, nullptr, 0, t, 0, true);
   if (fiber4res_ok(pc, rb, tma, t)) fiber4res_dispatch(rb, a, nullptr, 0, t, 0, true);
-  if (t.fiber_direct) {
-    const bool ring = tma && t.f3_tma;
-    if (pc == PC_F64) fiber3_dispatch<double>(t.f3_rb, ring, a, t, 0, true);
-    else fiber3_dispatch<float>(t.f3_rb, ring, a, t, 0, true);
-  }
   const int combos[5][3] = {{1, 1, 1}, {1, 1, 0}, {1, 0, 1}, {1, 0, 0}, {0, 1, 0}};
   for (auto& c : combos) fiber_dispatch(pc, rb, tma, c[0], c[1], c[2], a, nullptr, -1, t, 0);
 }
@@ -235,14 +174,6 @@ void launch_fiber(int pc, int rb, bool tma, int want_t, int want_b, int want_res
   }
   if (want_t && !want_b && !want_res && n > 0 && t.d_fib4 && fiber4_ok(pc, rb, tma, t)) {
     fiber4_dispatch(rb, a, t.d_fib4, (int)t.fib4.size(), t, st, false);
-    count_launch(1);
-    return;
-  }
-  static const bool f3_on = getenv("CB_F3_ON") != nullptr;
-  if (want_t && !want_b && !want_res && t.fiber_direct && f3_on) {
-    const bool ring = tma && t.f3_tma;
-    if (pc == PC_F64) fiber3_dispatch<double>(t.f3_rb, ring, a, t, st, false);
-    else fiber3_dispatch<float>(t.f3_rb, ring, a, t, st, false);
     count_launch(1);
     return;
   }
@@ -361,7 +292,6 @@ void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
 }
 
 bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes) {
-  if (getenv("CB_NO_TMA")) return false;
   for (int s = 0; s < S; ++s) {
     const long long J = dims[3 * s] * dims[3 * s + 1];
     if ((J * elem_bytes) % 16 != 0) return false;
@@ -392,7 +322,7 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
     for (int s = 0; s < S; ++s) even = even && (dims[3 * s] * dims[3 * s + 1]) % 2 == 0;
     const int f3rb = rmax <= 8 ? 8 : rmax <= 10 ? 10 : rmax <= 12 ? 12 : 16;
     t.fiber_direct = (pc != PC_F32 && rmax <= 16 && even &&
-                      fiber3_smem(a2r, f3rb) <= 96 * 1024 && !getenv("CB_NO_FIBER3")) ? 1 : 0;
+                      fiber3_smem(a2r, f3rb) <= 96 * 1024) ? 1 : 0;
     t.f3_first.assign(S + 1, 0);
     for (int s = 0; s < S; ++s) {
       const long long J = dims[3 * s] * dims[3 * s + 1];
@@ -400,34 +330,8 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
     }
   }
   t.fib.clear(); t.fib_first.assign(S + 1, 0); t.nsplit.assign(S, 1);
-  // fiber tile: halve TJ while the unsplit (nsplit 1) decomposition leaves SMs idle
-  {
-    int tj = tile;
-    long long units = 0;
-    auto count = [&](int tjv) {
-      long long u = 0;
-      for (int s = 0; s < S; ++s) {
-        const long long J = dims[3 * s] * dims[3 * s + 1];
-        u += (J + (long long)X2_THREADS * tjv - 1) / ((long long)X2_THREADS * tjv);
-      }
-      return u;
-    };
-    units = count(tj);
-    // unsplit T pass: pick TJ (<= the register-budget tile) minimising waves x TJ,
-    // the per-SM makespan in column-rows (c2: TJ 3 -> 140 units in one wave)
-    static const bool tj_search = getenv("CB_FIB_TJSEARCH") != nullptr;   // measured slower on c2
-    if (t.fiber_direct && tj_search) {
-      long long best = -1;
-      for (int c : {tile, 3, 2, 1}) {
-        if (c > tile) continue;
-        const long long u = count(c);
-        const long long cost = ((u + 147) / 148) * c;
-        if (best < 0 || cost < best) { best = cost; tj = c; units = u; }
-      }
-    }
-    if (getenv("CB_FIB_TJ")) tj = std::max(1, std::min(tile, atoi(getenv("CB_FIB_TJ"))));
-    t.fib_tj = tj;
-  }
+  // fiber tile: the register-budget tile (fiber2 units)
+  t.fib_tj = tile;
   const long long JT = (long long)X2_THREADS * t.fib_tj;
   for (int s = 0; s < S; ++s) {
     const long long J = dims[3 * s] * dims[3 * s + 1];
@@ -444,18 +348,14 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   t.fib_unsplit = 1;
   for (int s = 0; s < S; ++s) t.fib_unsplit = t.fib_unsplit && t.nsplit[s] == 1;
   // fiber4 units: the tile minimising waves x TJ over this engine's blocks,
-  // a wave being 148 CTAs.  CB_F4_OCC counts 148 x the resident CTAs per SM
-  // instead: on c2 that picks TJ 1 (4 CTAs per SM), the kernel drops from 34
-  // to 25 us but the step slows 6.33k -> 6.17k it/s, because the T pass runs
-  // on the side stream beside k_sweep_begin / k_step (the critical path) and
-  // at 4 CTAs per SM it leaves those R x R kernels no SM (profiles/r01h_*).
-  // CB_F4_TJ: fixed tile.
+  // a wave being 148 CTAs (one per SM).  Counting several resident CTAs per
+  // SM instead (c2: TJ 1, 4 CTAs per SM) made the kernel faster (34 -> 25 us)
+  // but the step slower (6.33k -> 6.17k it/s): the T pass runs on the side
+  // stream beside k_sweep_begin / k_step, the critical path, and at 4 CTAs
+  // per SM it leaves those R x R kernels no SM (profiles/r01h_*).
   t.fib4.clear();
   t.fib4_tj = 0;
   if (t.fiber_direct && pc == PC_F32_F64 && rb <= 16) {
-    static const bool flat = getenv("CB_F4_OCC") == nullptr;
-    long long i2max = 1;
-    for (int s = 0; s < S; ++s) i2max = std::max(i2max, dims[3 * s + 2]);
     long long best = -1;
     for (int c : {4, 3, 2, 1}) {
       long long u = 0;
@@ -463,11 +363,10 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
         const long long J = dims[3 * s] * dims[3 * s + 1];
         u += (J + 256LL * c - 1) / (256LL * c);
       }
-      const long long slots = 148LL * (flat ? 1 : fiber4_occ(rb, c, i2max));
+      const long long slots = 148LL;
       const long long cost = ((u + slots - 1) / slots) * c;
       if (best < 0 || cost < best) { best = cost; t.fib4_tj = c; }
     }
-    if (getenv("CB_F4_TJ")) t.fib4_tj = std::max(1, std::min(4, atoi(getenv("CB_F4_TJ"))));
     const long long JT4 = 256LL * t.fib4_tj;
     for (int s = 0; s < S; ++s) {
       const long long J = dims[3 * s] * dims[3 * s + 1];
@@ -513,7 +412,7 @@ void build_xtables(int S, const long long* dims, const int* R, int rb, int pc, X
   const long long ring = 128 + (long long)S2_NST * tile * kc * pc_storage_bytes(pc);
   t.slab_rows = (ring + ab * rb * tcb <= 200 * 1024) ? ab : 0;
   // row-dot mode-2 kernel where the shapes allow it (arithmetic always fp64)
-  t.slab_direct = (pc != PC_F32 && slab3_ok(S, dims, rb) && !getenv("CB_NO_SLAB3")) ? 1 : 0;
+  t.slab_direct = (pc != PC_F32 && slab3_ok(S, dims, rb)) ? 1 : 0;
   t.s3_nslot = slab3_nslot(S, dims);
   t.s3_a1_rows = 1;
   for (int s = 0; s < S; ++s) t.s3_a1_rows = std::max(t.s3_a1_rows, dims[3 * s + 1]);

@@ -188,110 +188,10 @@ inline size_t slab3_smem(long long max_i0, int elem, int rows, long long a1_rows
          (ring ? (size_t)S3_WARPS * S3_RING * rows * max_i0 * elem : 0);
 }
 
-// ---------------------------------------------------------------------------
-// T pass of the 3-way full path as warp tasks:
-//   T[r][j] = sum_{i2} X[j + J i2] A2[i2, r],   j = i0 + I0 i1 flattened
-// One warp owns one task (block s, 64 consecutive j) and walks the I2 rows of
-// that chunk (a 256-byte fp32 segment per row, rows J apart); lane l holds
-// the adjacent pair j = j0 + 2l, 2l + 1 (one 8-byte load per row, F3_PD rows
-// prefetched in registers) and accumulates 2 x RB fp64 sums.  A2 is staged
-// per warp in shared memory (broadcast 16-byte reads per row).  No cross-lane
-// reduction, no partials: T is written once.  Small per-lane state keeps two
-// CTAs per SM resident.  (Plain loads: per-row bulk copies would be 256-byte
-// TMA operations, whose issue rate, not bandwidth, then bounds the pass.)
-// ---------------------------------------------------------------------------
+// Sizing rule of the unsplit T pass (T = X x3 A2 written once per block,
+// the fiber4 kernel of xpass4.cuh): A2 staged per warp must fit.
 constexpr int F3_WARPS = 8;
-constexpr int F3_PD = 4;
-constexpr int F3_CH = 64;        // j per task
-
-template <typename TE> struct Pair2;
-template <> struct Pair2<float> { typedef float2 T; };
-template <> struct Pair2<double> { typedef double2 T; };
-
-template <typename TE, int RB>
-__global__ void __launch_bounds__(F3_WARPS * 32, 2)
-fiber3_kernel(XArgs a, const int* __restrict__ task_first, int S, int ntasks, int a2_rows) {
-  griddep_wait();
-  if (gated(a)) return;
-  tl_begin(a.tl, TL_FIBER);
-  typedef typename Pair2<TE>::T P2;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  extern __shared__ __align__(128) unsigned char f3sm[];
-  double* a2s = reinterpret_cast<double*>(f3sm) + (size_t)warp * a2_rows * RB;
-  int cur = -1, s = 0, R = 0;
-  long long I2 = 0, J = 0;
-  const TE* X = nullptr;
-  double* T = nullptr;
-  for (int t = blockIdx.x * F3_WARPS + warp; t < ntasks; t += gridDim.x * F3_WARPS) {
-    while (s + 1 < S && t >= task_first[s + 1]) ++s;
-    if (a.active && !a.active[s]) continue;
-    if (s != cur) {
-      cur = s;
-      R = a.R[s];
-      I2 = a.dims[3 * s + 2];
-      J = a.dims[3 * s] * a.dims[3 * s + 1];
-      X = reinterpret_cast<const TE*>(a.X[s]);
-      T = reinterpret_cast<double*>(tbuf(a, s));
-      const double* A2 = a.U[3 * s + 2];
-      __syncwarp();
-      for (long long e = lane; e < I2 * RB; e += 32) {
-        const long long q = e / RB;
-        const int r = (int)(e - q * RB);
-        a2s[e] = r < R ? __ldg(A2 + q * R + r) : 0.0;
-      }
-      __syncwarp();
-    }
-    const long long j0 = (long long)(t - task_first[s]) * F3_CH;
-    const long long jl = j0 + 2 * lane;           // this lane's pair
-    const bool full = jl + 1 < J;
-    const bool half = jl < J;
-    const TE* xs = X + jl;
-    double acc0[RB], acc1[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) { acc0[r] = 0.0; acc1[r] = 0.0; }
-    P2 xb[F3_PD];
-#pragma unroll
-    for (int p = 0; p < F3_PD; ++p) {
-      if (p < I2 && full) xb[p] = __ldg(reinterpret_cast<const P2*>(xs + J * p));
-      else { xb[p].x = (p < I2 && half) ? __ldg(xs + J * p) : TE(0); xb[p].y = TE(0); }
-    }
-    for (long long i2 = 0; i2 < I2; i2 += F3_PD) {
-#pragma unroll
-      for (int p = 0; p < F3_PD; ++p) {
-        if (i2 + p < I2) {
-          const double x0 = (double)xb[p].x, x1 = (double)xb[p].y;
-          const long long nx = i2 + p + F3_PD;
-          if (nx < I2 && full) xb[p] = __ldg(reinterpret_cast<const P2*>(xs + J * nx));
-          else { xb[p].x = (nx < I2 && half) ? __ldg(xs + J * nx) : TE(0); xb[p].y = TE(0); }
-          double av[RB];
-          load_row<double, RB>(a2s + (i2 + p) * RB, av);
-#pragma unroll
-          for (int r = 0; r < RB; ++r) {
-            acc0[r] = fma(x0, av[r], acc0[r]);
-            acc1[r] = fma(x1, av[r], acc1[r]);
-          }
-        }
-      }
-    }
-    if (half) {
-#pragma unroll
-      for (int r = 0; r < RB; ++r)
-        if (r < R) {
-          if (full) {
-            double2 v;
-            v.x = acc0[r];
-            v.y = acc1[r];
-            // T rows are J apart: 16-byte aligned when J is even (host checks)
-            *reinterpret_cast<double2*>(T + (long long)r * J + jl) = v;
-          } else {
-            T[(long long)r * J + jl] = acc0[r];
-          }
-        }
-    }
-  }
-  tl_end(a.tl, TL_FIBER);
-}
+constexpr int F3_CH = 64;        // j per unit of the f3 table
 
 inline size_t fiber3_smem(long long a2_rows, int rb) {
   return (size_t)F3_WARPS * a2_rows * rb * 8;

@@ -238,7 +238,6 @@ static size_t sl5_smem(long long kpad, int rb) {
 }
 
 bool sl5_supported(int S, const void* const* X, const long long* dims, const int* R) {
-  if (getenv("CB_NO_SL5")) return false;
   int rmax = 1;
   long long kmax = 1;
   for (int s = 0; s < S; ++s) {

@@ -725,7 +725,6 @@ static int n_bucket(int rmax) {
 
 
 bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R) {
-  if (getenv("CB_NO_XTC")) return false;
   for (int s = 0; s < S; ++s) {
     const long long I0 = dims[3 * s], I1 = dims[3 * s + 1], I2 = dims[3 * s + 2];
     if (I0 < 1 || I1 < 1 || I2 < 1) return false;
@@ -936,7 +935,7 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.nst = p->nst;
   a.bimg_max = p->bimg_max;
   a.u1_bytes = p->u1_bytes;
-  { static const char* e = getenv("CB_XTC_DBG"); a.dbg = e ? atoi(e) : 0; }
+  a.dbg = 0;
   a.part = p->part;
   a.cnt = p->cnt;
   a.bsum = bsum;

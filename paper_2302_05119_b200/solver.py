@@ -90,19 +90,31 @@ class CoupledProblem:
         return self.tensors[0].ndim
 
     def validate(self, check_values=True):
-        """The reference's checks (solver.py:96-135).  ``check_values=False``
-        skips the per-element finite / nonnegative scan (the single-process
-        solve runs it on the device after the upload, same messages)."""
+        """The reference's checks in the reference's order (solver.py:96-135):
+        per block its order, then its values; then ranks and coupled counts.
+        ``check_values=False`` skips the per-element finite / nonnegative scan
+        (the single-process solve runs the same loop with the scan on the
+        device, in the input's own dtype, right after each upload)."""
+        self._validate_head()
+        for s, t in enumerate(self.tensors):
+            self._validate_block(s, t)
+            if check_values:
+                _raise_values(s, t)
+        self._validate_tail()
+
+    def _validate_head(self):
         if not self.tensors:
             raise ValueError("no tensors")
         if self.mode not in ("full", "lra"):
             raise ValueError(f"unknown mode {self.mode!r}")
+
+    def _validate_block(self, s, t):
         order = self.tensors[0].ndim
-        for s, t in enumerate(self.tensors):
-            if t.ndim != order:
-                raise ValueError(f"block {s} has order {t.ndim}, expected {order}")
-            if check_values:
-                _raise_values(s, t)
+        if t.ndim != order:
+            raise ValueError(f"block {s} has order {t.ndim}, expected {order}")
+
+    def _validate_tail(self):
+        order = self.tensors[0].ndim
         if len(self.ranks) != len(self.tensors):
             raise ValueError("one rank per block required")
         if any(r < 1 for r in self.ranks):
@@ -155,6 +167,7 @@ class SolverOptions:
     precision: str = "fp64"        # "fp64" parity mode | "fp32" throughput mode
     objective: str = "auto"        # "auto" | "explicit" | "expansion"
     compute: str = "auto"          # fp32 storage: "auto" | "fp64" | "fp32" | "tc" (lra trace)
+    pipeline: str = "auto"         # lra tensor-core trace beside the next sweep: "auto" | "on" | "off"
 
     def __post_init__(self):
         if self.max_iter < 0:
@@ -171,6 +184,8 @@ class SolverOptions:
             raise ValueError(f"unknown objective evaluation {self.objective!r}")
         if self.compute not in ("auto", "fp64", "fp32", "tc"):
             raise ValueError(f"unknown compute type {self.compute!r}")
+        if self.pipeline not in ("auto", "on", "off"):
+            raise ValueError(f"unknown pipeline mode {self.pipeline!r}")
 
 
 @dataclass(frozen=True)
@@ -440,8 +455,13 @@ class PreparedSolve:
     def __init__(self, problem, opts=None, stream=None, shard=None):
         torch = D.torch_mod()
         opts = opts if opts is not None else SolverOptions()
-        # single process: the element scan runs on the device after upload
-        problem.validate(check_values=shard is not None)
+        # sharded: every rank validates all blocks on the host; single
+        # process: the same checks in the same order, the element scan on the
+        # device in each block's own dtype before the downcast to `precision`
+        if shard is not None:
+            problem.validate()
+        else:
+            problem._validate_head()
         self.problem, self.opts = problem, opts
         S_all = problem.n_blocks
         self.shard = shard if shard is not None else ShardSpec(1, 0, 0, S_all, None)
@@ -475,12 +495,20 @@ class PreparedSolve:
         with torch.cuda.stream(self.stream):
             self.dev = []
             self.dims = []
-            for g, t in zip(self.local, (problem.tensors[g] for g in self.local)):
-                flat, dims = D.tensor_to_dev(t, prec)
+            for g in (range(S_all) if shard is None else self.local):
+                t = problem.tensors[g]
                 if shard is None:
-                    _raise_values(g, flat)
+                    problem._validate_block(g, t)
+                    src, dims = D.tensor_to_dev(t, D.source_dtype(t))
+                    _raise_values(g, src)
+                    flat = src if D.source_dtype(t) == prec else D.cast_flat(src, prec)
+                    del src
+                else:
+                    flat, dims = D.tensor_to_dev(t, prec)
                 self.dev.append(flat)
                 self.dims.append(dims)
+            if shard is None:
+                problem._validate_tail()
         st = L.c_vp(self.stream.cuda_stream)
         # lra stage 1: batched device ALS (solver.py:556-573)
         self.compress_seconds = 0.0
@@ -560,6 +588,7 @@ class PreparedSolve:
         desc.nccl_comm = sh.comm
         desc.total_blocks = S_all
         desc.block_offset = sh.begin
+        desc.pipeline = {"auto": 0, "on": 1, "off": 2}[opts.pipeline]
         self.t0 = time.perf_counter()
         self.engine = _Engine(desc, st)
         self.tilde_ranks = tilde_ranks

@@ -152,7 +152,7 @@ def test_tc_mode2_als_matches_fp64_als(P):
 
 
 @pytest.mark.parametrize("tol,max_iter", [(1e-30, 40), (1e-5, 400)])
-def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, monkeypatch, tol, max_iter):
+def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, tol, max_iter):
     """The pipelined lra iteration (csrc/engine.cu enqueue_pipe_*: the trace of
     iteration k beside the sweep of k+1, snapshots, rollback on stop) returns
     the unpipelined solve's factors, histories and stop iteration bitwise,
@@ -161,12 +161,10 @@ def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, monkeypatch, tol, max
     tensors = [_block(rng, (64, 40, 30), 20)[0] for _ in range(3)]
     out = {}
     for pipe in (True, False):
-        monkeypatch.delenv("CB_PIPE", raising=False)
-        monkeypatch.delenv("CB_NO_PIPE", raising=False)
-        monkeypatch.setenv("CB_PIPE" if pipe else "CB_NO_PIPE", "1")
         prob = P.CoupledProblem(tensors, 20, [5, 5, 0], mode="lra")
         out[pipe] = P.solve(prob, P.SolverOptions(max_iter=max_iter, tol=tol, seed=5,
-                                                  precision="fp32", compute="tc"))
+                                                  precision="fp32", compute="tc",
+                                                  pipeline="on" if pipe else "off"))
     a, b = out[True], out[False]
     assert a.n_iter == b.n_iter and a.termination_reason == b.termination_reason
     if tol > 1e-20:

@@ -56,14 +56,20 @@ def main():
                 print(f"   {lab:24s} {d[k]} {u}")
         rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
         if rd is not None and wr is not None:
-            ur = units[col["dram__bytes_read.sum"]]
-            print(f"   traffic (read+write)     {rd + wr:.3f} {ur}")
+            # each column carries its own unit (ncu picks byte/Kbyte/Mbyte/Gbyte
+            # per metric): convert both to bytes before adding
+            rd *= BYTE_SCALE.get(units[col["dram__bytes_read.sum"]].lower(), 1.0)
+            wr *= BYTE_SCALE.get(units[col["dram__bytes_write.sum"]].lower(), 1.0)
+            print(f"   traffic (read+write)     {(rd + wr) / 1e6:.3f} MB")
         st = [(k, num(k)) for k in hdr
               if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")]
         st = sorted([s for s in st if s[1]], key=lambda s: -s[1])[:6]
         print("   top stalls (warps per issue): " + ", ".join(
             f"{k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]}={v:.2f}"
             for k, v in st))
+
+
+BYTE_SCALE = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12}
 
 
 if __name__ == "__main__":
