@@ -118,6 +118,28 @@ int cb_factor_gradient(const double* u_hat, int64_t rows, const double* gram_ski
                        void* stream);
 
 /* ------------------------------------------------------------------------
+ * Seeded synthetic blocks on the device (the input pipeline).
+ * X = [[weights; factors]] (weights NULL = ones), fp64 arithmetic, written
+ * first-index-fastest.  Replaces the O(|M| R) part of synth.generate
+ * (synth.py:77-112: reconstruct, kruskal.py:112-119) and add_noise
+ * (metrics.py:207-223); the factors are drawn by the caller (numpy, the
+ * reference's SeedSequence children).
+ * ---------------------------------------------------------------------- */
+
+/* out2 (device, 2 doubles) = {sum of x^2, max x} of the clean block
+ * (add_noise's signal power mean(X^2) = out2[0] / |M|, metrics.py:218). */
+int cb_synth_stats(int order, const int64_t* dims, const double* const* factors,
+                   const double* weights, int rank, double* out2, void* stream);
+
+/* out = noise(scale * X): noise 0 none; 1 + sigma z then clip at 0
+ * (metrics.py:220-221); 2 + sigma z then clip to [0, 1]; 3 * exp(sigma z).
+ * z: standard normals from Philox4x32-10 keyed by `seed`, counter = (element
+ * index, block), so a block does not depend on launch shape or block order. */
+int cb_synth_fill(int dtype, void* out, int order, const int64_t* dims,
+                  const double* const* factors, const double* weights, int rank, double scale,
+                  int noise, double sigma, uint64_t seed, int block, void* stream);
+
+/* ------------------------------------------------------------------------
  * CP-ALS compression engine (cpd_als.py:52-120), batched over blocks.
  * Each block is an independent ALS fit with its own stop rule.
  * ---------------------------------------------------------------------- */

@@ -14,8 +14,10 @@ noise drawn over the logical shape in C order, result clipped at 0).
 
 Tensors are returned as numpy arrays of logical shape ``dims`` stored in
 Fortran (first-index-fastest) order — the physical layout the device kernels
-read (`tensor_ops.py:1-15`).  Host-side generation only (SURVEY §8f rank 1
-lists on-device generation as a later item).
+read (`tensor_ops.py:1-15`).  This module is numpy-only (the bench's
+reference arm loads it by path without the native library);
+``synth.generate_config_device`` is the on-device generator of the same
+recipes for throughput runs.
 """
 
 from __future__ import annotations
@@ -24,7 +26,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["ConfigSpec", "CONFIGS", "generate_config", "config_tensor_block"]
+__all__ = ["ConfigSpec", "CONFIGS", "generate_config", "config_tensor_block",
+           "config_block_factors", "shared_prefixes"]
 
 
 @dataclass(frozen=True)
@@ -85,23 +88,33 @@ def _reconstruct_f(factors):
     return flat.reshape(a0.shape[0], a1.shape[0], a2.shape[0], order="F")
 
 
-def _shared_prefixes(spec, children):
+def shared_prefixes(spec, children):
+    """The common prefixes (I_n x L_n per mode) from child 0."""
     rng_c = np.random.default_rng(children[0])
     return [_draw(rng_c, spec.factor_dist, (spec.dims[n], spec.coupled[n]))
             for n in range(3)]
 
 
-def config_tensor_block(spec, s, seed=0, children=None, common=None):
-    """Generate block ``s`` of a config: returns (tensor_fp64_F, true_factors)."""
-    if children is None:
-        children = np.random.SeedSequence(seed).spawn(2 * spec.n_blocks + 1)
-    if common is None:
-        common = _shared_prefixes(spec, children)
+def config_block_factors(spec, s, children, common):
+    """Block ``s``'s true factors: the common prefix plus its individual
+    columns from child 1+2s (unit weights)."""
     rng_s = np.random.default_rng(children[1 + 2 * s])
     facs = []
     for n in range(3):
         own = _draw(rng_s, spec.factor_dist, (spec.dims[n], spec.rank - spec.coupled[n]))
         facs.append(np.hstack([common[n], own]) if spec.coupled[n] else own)
+    return facs
+
+
+def config_tensor_block(spec, s, seed=0, children=None, common=None):
+    """Generate block ``s`` of a config on the host: returns (tensor_fp64_F,
+    true_factors).  ``synth.generate_config_device`` runs the same recipe with
+    the reconstruction and the noise on the GPU."""
+    if children is None:
+        children = np.random.SeedSequence(seed).spawn(2 * spec.n_blocks + 1)
+    if common is None:
+        common = shared_prefixes(spec, children)
+    facs = config_block_factors(spec, s, children, common)
     clean = _reconstruct_f(facs)
     if spec.noise == "gauss01":
         clean = clean / clean.max()
@@ -131,7 +144,7 @@ def generate_config(name, seed=0, blocks=None, dtype=None):
     """
     spec = CONFIGS[name]
     children = np.random.SeedSequence(seed).spawn(2 * spec.n_blocks + 1)
-    common = _shared_prefixes(spec, children)
+    common = shared_prefixes(spec, children)
     idx = range(spec.n_blocks) if blocks is None else blocks
     want = dtype or spec.dtype
     np_dtype = np.float64 if want == "fp64" else np.float32

@@ -213,6 +213,8 @@ class SolveResult:
     solve_seconds: float = 0.0
     compress_seconds: float = 0.0
     compression: list = None
+    # additions (defaulted): ALS sweeps per block of the lra compression
+    compression_iters: list = None
 
 
 # ---------------------------------------------------------------------------
@@ -452,16 +454,15 @@ class PreparedSolve:
     """A solve with its inputs resident on the device, split into
     prepare / iterate / collect so the bench can time the iterations alone."""
 
-    def __init__(self, problem, opts=None, stream=None, shard=None):
+    def __init__(self, problem, opts=None, stream=None, shard=None, agree=None):
         torch = D.torch_mod()
         opts = opts if opts is not None else SolverOptions()
-        # sharded: every rank validates all blocks on the host; single
-        # process: the same checks in the same order, the element scan on the
-        # device in each block's own dtype before the downcast to `precision`
-        if shard is not None:
-            problem.validate()
-        else:
-            problem._validate_head()
+        # the reference's checks in its order (per block: order, values; then
+        # ranks / counts).  The element scan runs on the device in each
+        # block's own dtype before the downcast to `precision`; a sharded rank
+        # scans its own blocks and `agree` (PreparedShardedSolve: an
+        # all-reduce) makes every rank raise the same first error
+        problem._validate_head()
         self.problem, self.opts = problem, opts
         S_all = problem.n_blocks
         self.shard = shard if shard is not None else ShardSpec(1, 0, 0, S_all, None)
@@ -495,20 +496,30 @@ class PreparedSolve:
         with torch.cuda.stream(self.stream):
             self.dev = []
             self.dims = []
-            for g in (range(S_all) if shard is None else self.local):
-                t = problem.tensors[g]
-                if shard is None:
+            first_bad, bad_msg = None, None     # (block, 0 order / 1 values)
+            for g, t in enumerate(problem.tensors):
+                try:
                     problem._validate_block(g, t)
-                    src, dims = D.tensor_to_dev(t, D.source_dtype(t))
+                except ValueError as exc:
+                    first_bad, bad_msg = (g, 0), exc
+                    break
+                if g not in self.local:
+                    continue
+                src, dims = D.tensor_to_dev(t, D.source_dtype(t))
+                try:
                     _raise_values(g, src)
-                    flat = src if D.source_dtype(t) == prec else D.cast_flat(src, prec)
-                    del src
-                else:
-                    flat, dims = D.tensor_to_dev(t, prec)
+                except ValueError as exc:
+                    first_bad, bad_msg = (g, 1), exc
+                    break
+                flat = src if D.source_dtype(t) == prec else D.cast_flat(src, prec)
+                del src
                 self.dev.append(flat)
                 self.dims.append(dims)
-            if shard is None:
-                problem._validate_tail()
+            if agree is not None:
+                first_bad, bad_msg = agree(first_bad, bad_msg, problem)
+            if bad_msg is not None:
+                raise bad_msg
+            problem._validate_tail()
         st = L.c_vp(self.stream.cuda_stream)
         # lra stage 1: batched device ALS (solver.py:556-573)
         self.compress_seconds = 0.0
@@ -610,8 +621,9 @@ class PreparedSolve:
         if self.als is not None:
             compression = {}
             for s, g in enumerate(self.local):
-                facs, _, _, _, _ = self.als.block(s)
+                facs, _, _, its, _ = self.als.block(s)
                 compression[g] = KruskalTensor(facs, np.ones(self.tilde_ranks[s]))
+                compression[g].als_iters = its
         return summ, hist, blocks, compression, solve_seconds
 
     def collect(self):
@@ -640,6 +652,7 @@ def _assemble(problem, opts, summ, hist, blocks, compression, solve_seconds, com
             trace.append(TraceRow(k, float(oo[k]), float(rel[k]), float(tns[k]) * 1e-9))
     S = problem.n_blocks
     comp = None if compression is None else [compression[g] for g in range(S)]
+    comp_iters = None if comp is None else [getattr(k, "als_iters", None) for k in comp]
     reason = "tolerance" if summ.reason == 1 else "max_iterations"
     return SolveResult(
         factors=CoupledFactorSet([blocks[g] for g in range(S)], list(problem.coupled_counts)),
@@ -647,7 +660,7 @@ def _assemble(problem, opts, summ, hist, blocks, compression, solve_seconds, com
         objective_history=[float(v) for v in oi[: n_iter + 1]],
         rel_err_history=[float(v) for v in rel[: n_iter + 1]],
         n_iter=n_iter, n_restarts=summ.n_restarts, solve_seconds=solve_seconds,
-        compress_seconds=compress_seconds, compression=comp)
+        compress_seconds=compress_seconds, compression=comp, compression_iters=comp_iters)
 
 
 # ---------------------------------------------------------------------------
@@ -706,6 +719,34 @@ def solve_emulated_shards(problem, opts=None, world=2):
             p.close()
 
 
+def _agree_first_error(first_bad, msg, problem, group):
+    """Every rank raises the group's first validation error in the
+    reference's order: the smallest block, an order error before a value
+    error of the same block (only the owner of a block scans its values)."""
+    import torch
+    import torch.distributed as dist
+    code = 2 * problem.n_blocks if first_bad is None else 2 * first_bad[0] + first_bad[1]
+    t = torch.tensor([code], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    best = int(t.item())
+    if best >= 2 * problem.n_blocks:
+        return None, None
+    g, kind = divmod(best, 2)
+    if kind == 0:
+        # every rank checks every block's order: all found it themselves
+        return (g, 0), ValueError(f"block {g} has order {problem.tensors[g].ndim}, "
+                                  f"expected {problem.tensors[0].ndim}")
+    # a value error, found by the rank owning block g: one more exchange
+    # tells the others which of the two checks failed (same message as
+    # _raise_values on every rank)
+    mine = first_bad is not None and first_bad == (g, 1)
+    kinds = torch.tensor([(1 if "non-finite" in str(msg) else 2) if mine else 0],
+                         dtype=torch.int64, device="cuda")
+    dist.all_reduce(kinds, op=dist.ReduceOp.MAX, group=group)
+    which = "contains non-finite values" if int(kinds.item()) == 1 else "contains negative entries"
+    return (g, 1), ValueError(f"block {g} {which}")
+
+
 def nccl_comm_for(group=None):
     """An NCCL communicator over the ranks of a torch.distributed group, built
     from a unique id that rank 0 creates and broadcasts (object collective)."""
@@ -735,7 +776,8 @@ class PreparedShardedSolve:
         # the iteration graph) then runs on a single GPU too
         self.comm = nccl_comm_for(group)
         b, e = shard_ranges(problem.n_blocks, world)[rank]
-        self.inner = PreparedSolve(problem, opts, shard=ShardSpec(world, rank, b, e, self.comm))
+        self.inner = PreparedSolve(problem, opts, shard=ShardSpec(world, rank, b, e, self.comm),
+                                   agree=lambda fb, msg, prob: _agree_first_error(fb, msg, prob, group))
         self.engine, self.stream = self.inner.engine, self.inner.stream
 
     def run(self, iters=None):
