@@ -140,6 +140,30 @@ int cb_synth_fill(int dtype, void* out, int order, const int64_t* dims,
                   int noise, double sigma, uint64_t seed, int block, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Post-solve metrics on the device (metrics.py:71-156).
+ * ---------------------------------------------------------------------- */
+
+/* out2 (device) = {||X - [[weights; factors]]||^2, ||X||^2}: rel_err / psnr of
+ * a Kruskal model without forming it (metrics.py:51-81, :140-156). */
+int cb_model_residual(int dtype, const void* X, int order, const int64_t* dims,
+                      const double* const* factors, const double* weights, int rank,
+                      double* out2, void* stream);
+
+/* out2 (device) = {||A - B||^2, ||A||^2} of two dense buffers of n elements
+ * (rel_err / psnr of a dense reconstruction). */
+int cb_diff_sq(int dtype_a, const void* A, int dtype_b, const void* B, int64_t n, double* out2,
+               void* stream);
+
+/* Performance index of n_pairs (estimate, truth) factor pairs (device,
+ * row-major rows[p] x rank, rank >= 2): out[p] (device) as in
+ * performance_index (metrics.py:84-124) with pinv(E) T = (E^T E)^{-1} E^T T;
+ * deficient[p] (device) = 1 where E looks rank-deficient (the reference's
+ * warning). */
+int cb_performance_index(int n_pairs, const double* const* estimated, const double* const* truth,
+                         const int64_t* rows, int rank, double* out, int* deficient,
+                         void* stream);
+
+/* ------------------------------------------------------------------------
  * CP-ALS compression engine (cpd_als.py:52-120), batched over blocks.
  * Each block is an independent ALS fit with its own stop rule.
  * ---------------------------------------------------------------------- */

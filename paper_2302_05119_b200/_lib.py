@@ -91,6 +91,11 @@ _sig("cb_factor_gradient", c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c
 _sig("cb_synth_stats", c_int, [c_int, c_i64p, ctypes.POINTER(c_vp), c_vp, c_int, c_vp, c_vp])
 _sig("cb_synth_fill", c_int, [c_int, c_vp, c_int, c_i64p, ctypes.POINTER(c_vp), c_vp, c_int, c_dbl,
                               c_int, c_dbl, ctypes.c_uint64, c_int, c_vp])
+_sig("cb_model_residual", c_int, [c_int, c_vp, c_int, c_i64p, ctypes.POINTER(c_vp), c_vp, c_int,
+                                  c_vp, c_vp])
+_sig("cb_diff_sq", c_int, [c_int, c_vp, c_int, c_vp, c_i64, c_vp, c_vp])
+_sig("cb_performance_index", c_int, [c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64p,
+                                     c_int, c_vp, c_vp, c_vp])
 _sig("cb_als_create", c_int, [ctypes.POINTER(AlsDesc), c_vp, ctypes.POINTER(c_vp)])
 _sig("cb_als_run", c_int, [c_vp])
 _sig("cb_als_block_result", c_int, [c_vp, c_int, c_dp, c_ip, c_ip, c_dp, ctypes.POINTER(c_dp)])
@@ -118,7 +123,8 @@ EXPORTED = [
     "cb_last_error", "cb_abi_version", "cb_launch_count", "cb_launch_count_reset",
     "cb_mttkrp", "cb_core_linear_term_tc", "cb_khatri_rao", "cb_hadamard_gram", "cb_spectral_norm_batched",
     "cb_tensor_stats", "cb_kruskal_residual", "cb_rowdot", "cb_gemm", "cb_factor_gradient",
-    "cb_synth_stats", "cb_synth_fill",
+    "cb_synth_stats", "cb_synth_fill", "cb_model_residual", "cb_diff_sq",
+    "cb_performance_index",
     "cb_als_create", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
     "cb_als_destroy", "cb_solver_create", "cb_solver_run", "cb_solver_step_async",
     "cb_solver_summary_get", "cb_solver_history", "cb_solver_block_factors",

@@ -49,8 +49,10 @@ struct SynthArgs {
   int noise;                  // 0 none, 1 add + clip >= 0, 2 add + clip [0, 1], 3 x exp(sigma z)
   double scale, sigma;
   uint32_t key0, key1, blk;
-  // stats pass: per-CTA partials {sum x^2, max x}
+  // stats pass: per-CTA partials {sum x^2, max x}; residual pass: the
+  // tensor X (dtype) and partials {sum (X - x)^2, sum X^2}
   double* part;
+  const void* X;
 };
 
 // Philox4x32-10 (Salmon et al., SC'11), counter (c0..c3), key (k0, k1)
@@ -115,6 +117,13 @@ __global__ void __launch_bounds__(SYN_THREADS) k_synth(SynthArgs a) {
       if (PASS == 0) {
         ss = fma(x, x, ss);
         mx = fmax(mx, x);
+      } else if (PASS == 2) {
+        const uint64_t idx = (uint64_t)i0 + (uint64_t)I0 * (uint64_t)(j0 + cj);
+        const double t = a.dtype == CB_F32 ? (double)static_cast<const float*>(a.X)[idx]
+                                           : static_cast<const double*>(a.X)[idx];
+        const double d = t - x;
+        ss = fma(d, d, ss);
+        mx = fma(t, t, mx);
       } else {
         const uint64_t idx = (uint64_t)i0 + (uint64_t)I0 * (uint64_t)(j0 + cj);
         x *= a.scale;
@@ -130,15 +139,18 @@ __global__ void __launch_bounds__(SYN_THREADS) k_synth(SynthArgs a) {
       }
     }
   }
-  if (PASS == 0) {
+  if (PASS != 1) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     ss = warp_sum(ss);
-    mx = warp_max(mx);
+    mx = PASS == 0 ? warp_max(mx) : warp_sum(mx);
     if (lane == 0) { red[0][wid] = ss; red[1][wid] = mx; }
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0.0, m = 0.0;
-      for (int k = 0; k < SYN_THREADS / 32; ++k) { s += red[0][k]; m = fmax(m, red[1][k]); }
+      for (int k = 0; k < SYN_THREADS / 32; ++k) {
+        s += red[0][k];
+        m = PASS == 0 ? fmax(m, red[1][k]) : m + red[1][k];
+      }
       const int64_t p = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
       a.part[2 * p] = s;
       a.part[2 * p + 1] = m;
@@ -147,17 +159,20 @@ __global__ void __launch_bounds__(SYN_THREADS) k_synth(SynthArgs a) {
 }
 
 // fixed-order fold of the per-CTA partials (one warp, lanes strided, then
-// the lanes in order)
-__global__ void k_synth_fold(const double* part, int64_t n, double* out2) {
+// the lanes in order); second component: max (stats) or sum (residual)
+__global__ void k_synth_fold(const double* part, int64_t n, double* out2, int second_sum) {
   double s = 0.0, m = 0.0;
-  for (int64_t p = threadIdx.x; p < n; p += 32) { s += part[2 * p]; m = fmax(m, part[2 * p + 1]); }
+  for (int64_t p = threadIdx.x; p < n; p += 32) {
+    s += part[2 * p];
+    m = second_sum ? m + part[2 * p + 1] : fmax(m, part[2 * p + 1]);
+  }
   __shared__ double ls[32], lm[32];
   ls[threadIdx.x] = s;
   lm[threadIdx.x] = m;
   __syncwarp();
   if (threadIdx.x == 0) {
     double t = 0.0, u = 0.0;
-    for (int k = 0; k < 32; ++k) { t += ls[k]; u = fmax(u, lm[k]); }
+    for (int k = 0; k < 32; ++k) { t += ls[k]; u = second_sum ? u + lm[k] : fmax(u, lm[k]); }
     out2[0] = t;
     out2[1] = u;
   }
@@ -210,7 +225,7 @@ int cb_synth_stats(int order, const int64_t* dims, const double* const* factors,
   const int64_t np = (int64_t)grid.x * grid.y;
   CB_CUDA(cudaMallocAsync((void**)&a.part, sizeof(double) * 2 * np, st));
   synth_dispatch<0>(a, grid, st);
-  k_synth_fold<<<1, 32, 0, st>>>(a.part, np, out2);
+  k_synth_fold<<<1, 32, 0, st>>>(a.part, np, out2, 0);
   count_launch(2);
   CB_CHECK_LAUNCH();
   CB_CUDA(cudaFreeAsync(a.part, st));
@@ -238,6 +253,30 @@ int cb_synth_fill(int dtype, void* out, int order, const int64_t* dims,
   synth_dispatch<1>(a, grid, (cudaStream_t)stream);
   count_launch(1);
   CB_CHECK_LAUNCH();
+  return CB_OK;
+}
+
+/* out2 = {||X - [[weights; factors]]||^2, ||X||^2} by the generator's tiled
+ * reconstruction (no dense model is formed). */
+int cb_model_residual(int dtype, const void* X, int order, const int64_t* dims,
+                      const double* const* factors, const double* weights, int rank,
+                      double* out2, void* stream) {
+  CB_ARG(X && dims && factors && out2, "null argument");
+  CB_ARG(dtype == CB_F32 || dtype == CB_F64, "bad dtype");
+  SynthArgs a{};
+  dim3 grid;
+  int rc = synth_args(a, order, dims, factors, weights, rank, grid);
+  if (rc) return rc;
+  a.X = X;
+  a.dtype = dtype;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t np = (int64_t)grid.x * grid.y;
+  CB_CUDA(cudaMallocAsync((void**)&a.part, sizeof(double) * 2 * np, st));
+  synth_dispatch<2>(a, grid, st);
+  k_synth_fold<<<1, 32, 0, st>>>(a.part, np, out2, 1);
+  count_launch(2);
+  CB_CHECK_LAUNCH();
+  CB_CUDA(cudaFreeAsync(a.part, st));
   return CB_OK;
 }
 

@@ -1,0 +1,70 @@
+"""Where the c5 solve() wall clock goes: upload + value checks, ALS
+compression, seeded start, engine create (incl. iteration-0 evaluation),
+first step (graph capture), the iterations, result download."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2302_05119_b200 as P  # noqa: E402
+from paper_2302_05119_b200 import solver as S  # noqa: E402
+from paper_2302_05119_b200.synth import generate_config_device  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+dev, spec = generate_config_device(name)
+host = []
+for t in dev:
+    h = torch.empty_strided(t.shape, t.stride(), dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    host.append(h)
+del dev
+torch.cuda.synchronize()
+torch.cuda.empty_cache()
+marks = []
+
+
+def mark(label):
+    torch.cuda.synchronize()
+    marks.append((label, time.perf_counter()))
+
+
+orig_create = S._Engine.__init__
+
+
+def timed_create(self, desc, stream):
+    mark("before engine create (upload, checks, ALS, seeded start)")
+    orig_create(self, desc, stream)
+    mark("engine create (allocs, tables, xtc plan, ||M||^2, iteration-0 evaluation)")
+
+
+S._Engine.__init__ = timed_create
+orig_als = S.als_compress_blocks
+
+
+def timed_als(*a, **k):
+    mark("upload + value checks")
+    h = orig_als(*a, **k)
+    mark("ALS compression")
+    return h
+
+
+S.als_compress_blocks = timed_als
+prob = P.CoupledProblem(host, spec.rank, list(spec.coupled), mode=spec.mode)
+opts = P.SolverOptions(max_iter=spec.max_iter, tol=float(np.nextafter(0, 1)), seed=0,
+                       precision=spec.dtype)
+mark("start")
+run = S.PreparedSolve(prob, opts)
+run.engine.step_async()
+mark("first step (graph capture + 1 iteration)")
+run.run(spec.max_iter - 1)
+mark(f"{spec.max_iter - 1} iterations")
+res = run.collect()
+mark("collect (histories, factors download)")
+run.close()
+prev = marks[0][1]
+for label, t in marks[1:]:
+    print(f"{t - prev:8.3f} s  {label}")
+    prev = t
+print(f"{marks[-1][1] - marks[0][1]:8.3f} s  total; als sweeps mean {np.mean(res.compression_iters):.1f}")
