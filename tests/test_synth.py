@@ -93,9 +93,11 @@ def test_device_noise_power_and_determinism(P):
     y = noisy.cpu().numpy()
     assert (y >= 0).all()
     d = y - x
-    keep = x > 6 * sig                     # entries the clip cannot reach
+    keep = x > 4 * sig                     # entries the clip (almost) never reaches
     z = d[keep] / sig
-    assert abs(z.mean()) < 0.02 and abs(z.std() - 1.0) < 0.02
+    tol = 5.0 / np.sqrt(z.size)            # 5 standard errors
+    assert z.size > 2000
+    assert abs(z.mean()) < tol and abs(z.std() - 1.0) < 2 * tol
     again, _ = synth.device_block(facs, None, dtype="fp64", noise="gauss", snr_db=snr, key=99, block=3)
     np.testing.assert_array_equal(again.cpu().numpy(), y)
     other, _ = synth.device_block(facs, None, dtype="fp64", noise="gauss", snr_db=snr, key=99, block=4)

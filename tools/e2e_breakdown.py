@@ -68,3 +68,10 @@ for label, t in marks[1:]:
     print(f"{t - prev:8.3f} s  {label}")
     prev = t
 print(f"{marks[-1][1] - marks[0][1]:8.3f} s  total; als sweeps mean {np.mean(res.compression_iters):.1f}")
+# per-iteration device time (trace timestamps of the accepted iterations)
+t = np.array([r.elapsed_s for r in res.trace])
+d = np.diff(t) * 1e3
+for k in (1, 2, 5, 10, 20, 50, 100, 150, len(d) - 1):
+    if k < len(d):
+        print(f"iteration {k:4d}: {d[k]:8.3f} ms")
+print(f"n_restarts {res.n_restarts}")
