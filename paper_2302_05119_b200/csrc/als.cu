@@ -8,6 +8,14 @@
 // 3-way blocks use the fiber / contract / slab kernels (two tensor passes per
 // sweep: the residual rides on the next sweep's fiber pass); other orders use
 // the generic MTTKRP and residual kernels.
+//
+// fp32-storage throughput mode with ranks > 16 (c5): both tensor passes of a
+// sweep are register-tiled fp64 GEMMs over TMA boxes (xslab5.cu: mode-2
+// D = X_r A0, and T = X x3 A2), and the residual is the gram expansion
+// ||M||^2 - 2 <A2, MTT2> + 1^T (G0 * G1 * G2) 1 (mathematically the explicit
+// residual; its rounding, ~1e-16 ||M||^2 / res relative, is far below the
+// fp32 storage rounding these blocks already carry).  The fp64 parity mode
+// keeps the explicit residual.
 #include <math.h>
 #include <string.h>
 
@@ -44,7 +52,9 @@ struct AlsCtx {
   double* rel;             // S current rel err
   double* norm;            // S ||M||
   double* hist;            // S * max_iter
-  double* res;             // S (generic residuals)
+  double* res;             // S (generic residuals, or the gram expansion)
+  const double* nsq;       // S ||M||^2
+  int res_expand;          // residual from the gram expansion (k_als_solve, last mode)
   const double* rpart;     // fiber residual partials
   const int* fib_first;
   const double* slab_part;
@@ -168,6 +178,22 @@ __global__ void __launch_bounds__(256) k_als_solve(AlsCtx c, int n, int src) {
   }
   bad = block_max(bad, red);
   if (threadIdx.x == 0 && bad > 0.0) c.converged[s] = -1;   // diverged marker
+  if (c.res_expand && n == N - 1) {
+    // ||M - [[U]]||^2 = ||M||^2 - 2 sum_ir U[i,r] MTT[i,r] + 1^T (had_m G_m) 1
+    __syncthreads();
+    const double* M = c.MTT[s];
+    double in = 0.0;
+    for (long long e = threadIdx.x; e < In * R; e += blockDim.x) in = fma(U[e], M[e], in);
+    in = block_sum(in, red);
+    double ms = 0.0;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      double v = 1.0;
+      for (int m = 0; m < N; ++m) v *= c.G[s * N + m][e];
+      ms += v;
+    }
+    ms = block_sum(ms, red);
+    if (threadIdx.x == 0) c.res[s] = c.nsq[s] - 2.0 * in + ms;
+  }
 }
 
 // per-sweep bookkeeping: residual -> rel err, history, stop rule (cpd_als.py:107-117)
@@ -184,7 +210,7 @@ __global__ void k_als_control(AlsCtx c, int init) {
         continue;
       }
       double res = 0.0;
-      if (c.fast3) {
+      if (c.fast3 && !c.res_expand) {
         res = c.rpart[s];   // per-block total folded by the fiber kernel
       } else {
         res = c.res[s];
@@ -290,7 +316,12 @@ static int als_sweep(cb_als* h) {
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
-  if (h->fast3) {
+  if (h->fast3 && h->ctx.res_expand) {
+    // T for the next sweep (GEMM pass); the residual came from the expansion
+    int rc = sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st);
+    if (rc) return rc;
+    CB_CHECK_LAUNCH();
+  } else if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
     launch_fiber(h->pc, h->rb, h->tma, 1, 0, 1, a, h->d_fib, (int)h->tab.fib.size(), h->tab, st);
@@ -414,6 +445,12 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       rel0[s] = norms[s] == 0.0 ? 0.0 : 1.0;
     }
     CB_CUDA(cudaMemcpyAsync(c.norm, norms.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    std::vector<double> sq(S);
+    for (int s = 0; s < S; ++s) sq[s] = hs[3 * s];
+    double* dnsq;
+    TRY(dalloc((void**)&dnsq, sizeof(double) * S, A));
+    CB_CUDA(cudaMemcpyAsync(dnsq, sq.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
+    c.nsq = dnsq;
     CB_CUDA(cudaMemcpyAsync(c.rel, rel0.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
     CB_CUDA(cudaMemcpyAsync(c.active, act.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
     CB_CUDA(cudaStreamSynchronize(st));
@@ -489,6 +526,8 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       if (sl5_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->sl5) != CB_OK)
         h->sl5 = nullptr;
     }
+    // both passes as GEMMs (unsplit T) with the gram-expansion residual
+    c.res_expand = (h->sl5 && sl5_tpass_ok(h->sl5) && h->tab.fib_unsplit) ? 1 : 0;
     {
       int* d_s3;
       TRY(upload(h->tab.s3_first, &d_s3, A, st));
@@ -514,7 +553,10 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   h->solve_smem = sizeof(double) * ((size_t)h->rmax * h->rmax + h->rmax + 48);
   CB_CUDA(cudaFuncSetAttribute(k_als_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->solve_smem));
   // initial T buffer (X x_3 U_2 of the starting factors)
-  if (h->fast3) {
+  if (h->fast3 && c.res_expand) {
+    TRY(sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st));
+    CB_CHECK_LAUNCH();
+  } else if (h->fast3) {
     XArgs a = h->xa;
     a.t_other = 1;
     launch_fiber(h->pc, h->rb, h->tma, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), h->tab, st);

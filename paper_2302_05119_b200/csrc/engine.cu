@@ -70,7 +70,9 @@ struct cb_solver {
   std::vector<int> n_rows;
   State* d_state = nullptr;
   State* h_state = nullptr;     // pinned mirror
-  size_t blk_smem = 0, mu_smem = 0, qr_smem = 0;
+  size_t blk_smem = 0, mu_smem = 0, qr_smem = 0, qrc_smem = 0;
+  int qr_ch = 32;             // TSQR chunk rows (k_qr_factor)
+  bool qr_core3 = false;      // 3-way GEMM-form ||core||^2 (k_qr_core3)
   std::vector<double*> h_U;     // device pointer tables mirrored on host
   std::vector<double*> h_MTT;
   std::vector<double*> h_LAM;
@@ -325,9 +327,14 @@ static int enqueue_sweep(cb_solver* h, int redo) {
 
 static int enqueue_qr(cb_solver* h, int redo) {
   if (!emit(h)) return CB_OK;
-  launch_k(k_qr_factor, dim3(h->S * h->N), dim3(256), h->qr_smem, h->st, h->ctx, redo);
+  launch_k(k_qr_factor, dim3(h->S * h->N), dim3(QR_THREADS), h->qr_smem, h->st, h->ctx, redo,
+           h->qr_ch);
   prof(h, redo ? "redo:qr_factor" : "qr_factor");
-  launch_k(k_qr_core, dim3(h->S * h->ctx.qr_nchunks), dim3(256), 0, h->st, h->ctx, redo);
+  if (h->qr_core3)
+    launch_k(k_qr_core3, dim3(h->S * h->ctx.qr_nchunks), dim3(256), h->qrc_smem, h->st, h->ctx,
+             redo);
+  else
+    launch_k(k_qr_core, dim3(h->S * h->ctx.qr_nchunks), dim3(256), 0, h->st, h->ctx, redo);
   prof(h, redo ? "redo:qr_core" : "qr_core");
   count_launch(2);
   CB_CHECK_LAUNCH();
@@ -825,7 +832,24 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   TRY(dalloc((void**)&c.tile_cnt, sizeof(int) * (maxIn / MU_ROWS + 2), A));
   if (h->lra) {
     TRY(dalloc((void**)&c.qr_buf, sizeof(double) * (size_t)S * N * QR_MAXC * QR_MAXC, A));
-    c.qr_nchunks = 8;
+    // ||core||^2: the GEMM form for 3-way blocks whose R1 / R2 images fit in
+    // shared memory, else the generic per-entry kernel
+    long long pairs = 1, na = 1;
+    size_t qrc = 0;
+    for (int s = 0; s < S; ++s) {
+      const long long Cc = h->R[s] + h->Rt[s];
+      if (N != 3) break;
+      const long long K0 = std::min(h->dims[3 * s], Cc), K1 = std::min(h->dims[3 * s + 1], Cc);
+      const long long K2 = std::min(h->dims[3 * s + 2], Cc);
+      const long long nas = std::min(K0, QRC_PAIRS / K1 + 2);
+      pairs = std::max(pairs, K0 * K1);
+      na = std::max(na, nas);
+      qrc = std::max(qrc, sizeof(double) * (size_t)(Cc + Cc * K1 + Cc * K2 + Cc * nas));
+      if (K2 > 16 * QRC_CT) qrc = SIZE_MAX;
+    }
+    h->qr_core3 = N == 3 && qrc <= 200 * 1024;
+    h->qrc_smem = h->qr_core3 ? qrc : 0;
+    c.qr_nchunks = h->qr_core3 ? (int)((pairs + QRC_PAIRS - 1) / QRC_PAIRS) : 8;
     TRY(dalloc((void**)&c.qr_part, sizeof(double) * S * c.qr_nchunks, A));
   }
   TRY(dalloc((void**)&c.h_obj, sizeof(double) * (h->max_iter + 1), A));
@@ -985,7 +1009,9 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   if (h->lra) {
     int cmax = 0;
     for (int s = 0; s < S; ++s) cmax = std::max(cmax, h->R[s] + h->Rt[s]);
-    h->qr_smem = sizeof(double) * ((size_t)(cmax + QR_CHUNK_ROWS) * (cmax + 1) + (cmax + QR_CHUNK_ROWS) + 40 + cmax + 8);
+    const size_t cap = 227 * 1024;
+    h->qr_ch = qr_chunk_rows(cmax, cap);
+    h->qr_smem = sizeof(double) * ((size_t)cmax * (cmax + 1) + (size_t)h->qr_ch * (cmax + 1) + cmax + 64);
   }
   CB_CUDA(cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
@@ -999,7 +1025,12 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_restore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_mode_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->mu_smem));
   if (h->lra)
+  {
     CB_CUDA(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qr_smem));
+    if (h->qr_core3)
+      CB_CUDA(cudaFuncSetAttribute(k_qr_core3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)h->qrc_smem));
+  }
   // ---- iteration 0 (an emulated group runs it through cb_group_step)
   if (!shard || h->comm) {
     TRY(init_evaluation(h));

@@ -9,7 +9,6 @@ namespace cb {
 
 constexpr int MU_ROWS = 32;        // rows per mode-update CTA
 constexpr int QR_MAXC = 128;       // R~ + R limit of the QR route
-constexpr int QR_CHUNK_ROWS = 32;  // rows streamed per TSQR step
 
 // Iteration state living in device memory; only the control kernel writes it.
 struct State {

@@ -709,7 +709,26 @@ __device__ __forceinline__ bool qr_route_needed(const Ctx& c, int s) {
   return c.res_t[s] < 1e-3 * c.tsq[s];
 }
 
-__global__ void __launch_bounds__(256) k_qr_factor(Ctx c, int redo) {
+// TSQR with the running triangle on top: the rows of [Ut_n, U_n] stream in
+// chunks of `ch` rows (as many as shared memory holds: 256 at Rt + R = 80);
+// every chunk is annihilated against the current R by Cc Householder
+// reflectors on the stacked [R; chunk] matrix.  Because R is upper
+// triangular, reflector k touches only row k of R and the chunk rows, so a
+// step costs O(ch (Cc - k)) — the dot products run one warp per column
+// (lanes over the chunk rows, shuffle fold).  Result: R (Cc x Cc, upper
+// triangular) of the QR of [Ut_n, U_n] up to row signs, which ||core||^2
+// does not see.  Grid: S * N CTAs of QR_THREADS.
+constexpr int QR_THREADS = 512;
+
+__host__ __device__ inline int qr_chunk_rows(int Cc, size_t smem_cap) {
+  // R (Cc x (Cc+1)) + chunk (ch x (Cc+1)) + w (Cc) + red (64) doubles
+  const long long avail = (long long)(smem_cap / sizeof(double)) - Cc - 64 - (long long)Cc * (Cc + 1);
+  long long ch = avail / (Cc + 1);
+  ch = ch / 32 * 32;
+  return (int)(ch > 256 ? 256 : (ch < 32 ? 32 : ch));
+}
+
+__global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int ch) {
   griddep_wait();
   if (stopped(c, redo)) return;
   const int s = blockIdx.x / c.N;
@@ -719,68 +738,159 @@ __global__ void __launch_bounds__(256) k_qr_factor(Ctx c, int redo) {
   const int R = c.R[s], Rt = c.Rt[s];
   const int Cc = Rt + R;
   const long long In = c.dims[s * c.N + n];
-  const int ldm = Cc + 1;
-  const int MR = Cc + QR_CHUNK_ROWS;      // stacked rows: current R (Cc) + chunk
-  double* M = smd;                        // MR x ldm
-  double* vv = M + MR * ldm;              // MR Householder vector
-  double* red = vv + MR;                  // 40
-  double* wv = red + 40;                  // Cc  (v^T M)
-  for (int e = threadIdx.x; e < MR * ldm; e += blockDim.x) M[e] = 0.0;
-  __syncthreads();
+  const int ld = Cc + 1;
+  double* Rm = smd;                      // Cc x ld, upper triangular
+  double* X = Rm + Cc * ld;              // ch x ld chunk
+  double* w = X + (long long)ch * ld;    // Cc
+  double* red = w + Cc;                  // 64
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = QR_THREADS / 32;
+  for (int e = threadIdx.x; e < Cc * ld; e += QR_THREADS) Rm[e] = 0.0;
   const double* A = c.Ut[s * c.N + n];
   const double* B = c.U[s * c.N + n];
-  for (long long c0 = 0; c0 < In; c0 += QR_CHUNK_ROWS) {
-    const int nr = (int)(In - c0 < QR_CHUNK_ROWS ? In - c0 : QR_CHUNK_ROWS);
-    // rows Cc.. of M <- next chunk of [Ut, U]; zero the rest
-    for (int e = threadIdx.x; e < QR_CHUNK_ROWS * Cc; e += blockDim.x) {
-      const int il = e / Cc, j = e - il * Cc;
-      double v = 0.0;
-      if (il < nr) v = j < Rt ? A[(c0 + il) * Rt + j] : B[(c0 + il) * R + (j - Rt)];
-      M[(Cc + il) * ldm + j] = v;
+  for (long long c0 = 0; c0 < In; c0 += ch) {
+    const int nr = (int)(In - c0 < ch ? In - c0 : ch);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * Cc; e += QR_THREADS) {
+      const int i = e / Cc, j = e - i * Cc;
+      X[i * ld + j] = j < Rt ? A[(c0 + i) * Rt + j] : B[(c0 + i) * R + (j - Rt)];
     }
     __syncthreads();
-    // Householder on the stacked (Cc + nr) x Cc matrix
-    const int mrows = Cc + nr;
     for (int k = 0; k < Cc; ++k) {
-      // norm of column k below the diagonal
+      // ||[R_kk; X[:, k]]||^2
       double ss = 0.0;
-      for (int i = k + threadIdx.x; i < mrows; i += blockDim.x) ss = fma(M[i * ldm + k], M[i * ldm + k], ss);
-      ss = block_sum(ss, red);
-      const double x0 = M[k * ldm + k];
+      for (int i = threadIdx.x; i < nr; i += QR_THREADS) ss = fma(X[i * ld + k], X[i * ld + k], ss);
+      ss = warp_sum(ss);
+      if (lane == 0) red[wid] = ss;
+      __syncthreads();
+      ss = 0.0;
+      for (int q = 0; q < nw; ++q) ss += red[q];
+      const double x0 = Rm[k * ld + k];
+      ss = fma(x0, x0, ss);
       const double nrm = sqrt(ss);
-      if (nrm == 0.0) continue;
       const double alpha = x0 >= 0.0 ? -nrm : nrm;
-      // v = x - alpha e_k ; v^T v = 2 (nrm^2 - alpha x0)
-      for (int i = k + threadIdx.x; i < mrows; i += blockDim.x)
-        vv[i] = (i == k) ? x0 - alpha : M[i * ldm + k];
-      __syncthreads();
+      const double v0 = x0 - alpha;
       const double vtv = 2.0 * (ss - alpha * x0);
-      if (vtv == 0.0) continue;
-      // w_j = v^T M[:, j] for j > k
-      for (int j = k + 1 + threadIdx.x; j < Cc; j += blockDim.x) {
-        double a = 0.0;
-        for (int i = k; i < mrows; ++i) a = fma(vv[i], M[i * ldm + j], a);
-        wv[j] = a;
+      if (!(vtv > 0.0)) {
+        // the column is already zero below R_kk: no reflection
+        __syncthreads();
+        continue;
       }
-      __syncthreads();
       const double beta = 2.0 / vtv;
-      for (int e = threadIdx.x; e < (mrows - k) * (Cc - k - 1); e += blockDim.x) {
-        const int i = k + e / (Cc - k - 1);
-        const int j = k + 1 + e % (Cc - k - 1);
-        M[i * ldm + j] -= beta * vv[i] * wv[j];
+      // w_j = v0 R_kj + sum_i X_ik X_ij, one warp per column
+      for (int j = k + 1 + wid; j < Cc; j += nw) {
+        double a = 0.0;
+        for (int i = lane; i < nr; i += 32) a = fma(X[i * ld + k], X[i * ld + j], a);
+        a = warp_sum(a);
+        if (lane == 0) w[j] = fma(v0, Rm[k * ld + j], a);
       }
       __syncthreads();
-      if (threadIdx.x == 0) M[k * ldm + k] = alpha;
-      for (int i = k + 1 + threadIdx.x; i < mrows; i += blockDim.x) M[i * ldm + k] = 0.0;
+      const int ncol = Cc - k - 1;
+      for (int e = threadIdx.x; e < (nr + 1) * ncol; e += QR_THREADS) {
+        const int i = e / ncol, j = k + 1 + (e - i * ncol);
+        const double bw = beta * w[j];
+        if (i == 0) Rm[k * ld + j] -= v0 * bw;
+        else X[(i - 1) * ld + j] -= X[(i - 1) * ld + k] * bw;
+      }
       __syncthreads();
+      if (threadIdx.x == 0) Rm[k * ld + k] = alpha;
     }
-    // rows >= Cc are now zero; the top Cc x Cc block is the running R
   }
+  __syncthreads();
   double* out = c.qr_buf + ((long long)s * c.N + n) * QR_MAXC * QR_MAXC;
-  for (int e = threadIdx.x; e < Cc * Cc; e += blockDim.x) {
+  for (int e = threadIdx.x; e < Cc * Cc; e += QR_THREADS) {
     const int i = e / Cc, j = e - i * Cc;
-    out[e] = j >= i ? M[i * ldm + j] : 0.0;
+    out[e] = j >= i ? Rm[i * ld + j] : 0.0;
   }
+}
+
+// 3-way ||core||^2 as a GEMM: core[(a, b), c] = sum_q P[(a, b), q] R2[c, q]
+// with P[(a, b), q] = wts[q] R0[a, q] R1[b, q].  A CTA owns QRC_PAIRS (a, b)
+// rows and every c; thread tile 4 pairs x ceil(K2 / 16) columns, R1 / R2
+// transposed in shared memory (broadcast-friendly), the squares summed in
+// registers; per-CTA partials folded in order by k_control.  Grid:
+// S * qr_nchunks, qr_nchunks = ceil(max K0 K1 / QRC_PAIRS).
+constexpr int QRC_PAIRS = 64;
+constexpr int QRC_CT = 8;     // max columns per thread (K2 <= 128)
+
+__global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
+  griddep_wait();
+  if (stopped(c, redo)) return;
+  const int s = blockIdx.x / c.qr_nchunks;
+  const int ch = blockIdx.x - s * c.qr_nchunks;
+  if (!qr_route_needed(c, s)) return;
+  extern __shared__ double smd[];
+  const int R = c.R[s], Rt = c.Rt[s];
+  const int Cc = Rt + R;
+  const int K0 = (int)(c.dims[s * 3] < Cc ? c.dims[s * 3] : Cc);
+  const int K1 = (int)(c.dims[s * 3 + 1] < Cc ? c.dims[s * 3 + 1] : Cc);
+  const int K2 = (int)(c.dims[s * 3 + 2] < Cc ? c.dims[s * 3 + 2] : Cc);
+  const int p0 = ch * QRC_PAIRS;
+  const int npair = K0 * K1 - p0 < QRC_PAIRS ? K0 * K1 - p0 : QRC_PAIRS;
+  __shared__ double red[40];
+  if (npair <= 0) {
+    if (threadIdx.x == 0) c.qr_part[(long long)s * c.qr_nchunks + ch] = 0.0;
+    return;
+  }
+  const int a_lo = p0 / K1, a_hi = (p0 + npair - 1) / K1;
+  const int na = a_hi - a_lo + 1;
+  double* wq = smd;                      // Cc
+  double* R1T = wq + Cc;                 // Cc x K1
+  double* R2T = R1T + Cc * K1;           // Cc x K2
+  double* R0T = R2T + Cc * K2;           // Cc x na
+  const double* Rb = c.qr_buf + (long long)s * 3 * QR_MAXC * QR_MAXC;
+  const long long MS = (long long)QR_MAXC * QR_MAXC;
+  for (int q = threadIdx.x; q < Cc; q += blockDim.x)
+    wq[q] = q < Rt ? c.TW[s][q] : -c.LAM[s][q - Rt];
+  for (int e = threadIdx.x; e < Cc * K1; e += blockDim.x) {
+    const int b = e / Cc, q = e - b * Cc;
+    R1T[q * K1 + b] = Rb[MS + b * Cc + q];
+  }
+  for (int e = threadIdx.x; e < Cc * K2; e += blockDim.x) {
+    const int cc = e / Cc, q = e - cc * Cc;
+    R2T[q * K2 + cc] = Rb[2 * MS + cc * Cc + q];
+  }
+  for (int e = threadIdx.x; e < Cc * na; e += blockDim.x) {
+    const int a = e / Cc, q = e - a * Cc;
+    R0T[q * na + a] = Rb[(long long)(a_lo + a) * Cc + q];
+  }
+  __syncthreads();
+  const int grp = threadIdx.x >> 4, col = threadIdx.x & 15;   // 16 pair groups x 16 columns
+  int pa[4], pb[4];
+  bool pv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int pl = grp * 4 + u;
+    pv[u] = pl < npair;
+    const int p = p0 + (pv[u] ? pl : 0);
+    pa[u] = p / K1 - a_lo;
+    pb[u] = p - (p / K1) * K1;
+  }
+  double acc[4][QRC_CT];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < QRC_CT; ++v) acc[u][v] = 0.0;
+  for (int q = 0; q < Cc; ++q) {
+    const double wv = wq[q];
+    double P[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) P[u] = wv * R0T[q * na + pa[u]] * R1T[q * K1 + pb[u]];
+#pragma unroll
+    for (int v = 0; v < QRC_CT; ++v) {
+      const int cc = col + 16 * v;
+      const double r2 = cc < K2 ? R2T[q * K2 + cc] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u][v] = fma(P[u], r2, acc[u][v]);
+    }
+  }
+  double ssq = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < QRC_CT; ++v)
+      if (pv[u]) ssq = fma(acc[u][v], acc[u][v], ssq);
+  ssq = block_sum(ssq, red);
+  if (threadIdx.x == 0) c.qr_part[(long long)s * c.qr_nchunks + ch] = ssq;
 }
 
 // ||core||^2 with core[a_0..a_{N-1}] = sum_q wts[q] prod_m Rm[a_m, q],

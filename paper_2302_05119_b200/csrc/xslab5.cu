@@ -71,14 +71,155 @@ struct Sl5Plan {
   CUtensorMap* tmaps = nullptr;
   Sl5Block* blk = nullptr;
   Sl5Tile* tiles = nullptr;
+  // T pass (T = X x3 A2) as a GEMM over (J x I2) boxes; off when it does
+  // not fit (tg_ok false)
+  bool tg_ok = false;
+  int tg_rb = 0, tg_grid = 0, tg_ntiles = 0;
+  size_t tg_smem = 0;
+  CUtensorMap* tg_maps = nullptr;
+  Sl5Tile* tg_tiles = nullptr;
 };
 
+// ----------------------------------------------------------------------------
+// T pass as a register-tiled fp64 GEMM (the ALS sweep's second X stream):
+//   T[r][j] = sum_{i2} X[j + J i2] A2[i2, r],   j = i0 + I0 i1,  J = I0 I1
+// X viewed as I2 rows of J contiguous fp32 values; a producer lane streams
+// TG_M x TG_KC boxes (j fastest, no swizzle) through a 4-stage mbarrier
+// ring; 256 consumers own 4 consecutive j (one float4 per i2 row) x RB/8
+// columns; A2 (fp64, zero-padded) is staged per block; T is written once,
+// fp64, into the buffer the contract kernels read ([R][J], unsplit).
+// ----------------------------------------------------------------------------
 __device__ __forceinline__ void sl5_tma(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+constexpr int TG_M = 128;                      // j per tile
+constexpr int TG_KC = 32;                      // i2 rows per box
+constexpr int TG_BOX = TG_M * TG_KC * 4;       // 16 KB
+constexpr int TG_NST = 4;
+
+struct TgArgs {
+  const CUtensorMap* tmaps;
+  const Sl5Block* blk;
+  const Sl5Tile* tiles;
+  int ntiles;
+  const double* const* U;    // S*3 factors (A2 = U[3 s + 2])
+  const int* active;
+  void* const* T0;           // T buffers, index (*tsel) ^ t_other
+  void* const* T1;
+  const int* tsel;
+  int t_other;
+};
+
+template <int RB>
+__global__ void __launch_bounds__(SL5_THREADS, 1) k_tg_pass(TgArgs a) {
+  griddep_wait();
+  constexpr int CG = RB / 8;                   // columns per thread
+  extern __shared__ unsigned char tg_raw[];
+  const uint32_t raw_u32 = smem_u32(tg_raw);
+  unsigned char* sm = tg_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  unsigned char* ring = sm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + TG_NST * TG_BOX);
+  uint64_t* empty = full + TG_NST;
+  double* a2s = reinterpret_cast<double*>(empty + TG_NST + 2);   // [I2pad][RB]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int t_begin = (int)((long long)blockIdx.x * a.ntiles / G);
+  const int t_end = (int)((long long)(blockIdx.x + 1) * a.ntiles / G);
+  const int sel = (a.tsel ? *a.tsel : 0) ^ a.t_other;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TG_NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], SL5_CONS / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == SL5_CONS / 32) {
+    if (lane == 0) {
+      int st = 0, ph = 0;
+      for (int q = t_begin; q < t_end; ++q) {
+        const Sl5Tile tt = a.tiles[q];
+        if (a.active && !a.active[tt.s]) continue;
+        const int nch = (int)((a.blk[tt.s].I2 + TG_KC - 1) / TG_KC);
+        const CUtensorMap* tm = a.tmaps + tt.s;
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&full[st], TG_BOX);
+          sl5_tma(ring + (size_t)st * TG_BOX, tm, tt.t * TG_M, c * TG_KC, &full[st]);
+          if (++st == TG_NST) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+  const int jg = lane;                         // j = 4 jg .. 4 jg + 3 of the tile
+  const int cg = warp;                         // columns [cg CG, (cg + 1) CG)
+  int st = 0, ph = 0, cur = -1;
+  for (int q = t_begin; q < t_end; ++q) {
+    const Sl5Tile tt = a.tiles[q];
+    if (a.active && !a.active[tt.s]) continue;
+    const Sl5Block& b = a.blk[tt.s];
+    const int nch = (int)((b.I2 + TG_KC - 1) / TG_KC);
+    const int R = b.R;
+    const long long J = b.I0 * b.I1;
+    if (tt.s != cur) {
+      asm volatile("bar.sync 1, %0;" ::"r"(SL5_CONS) : "memory");
+      cur = tt.s;
+      const double* A2 = a.U[3 * tt.s + 2];
+      const int kpad = nch * TG_KC;
+      for (int e = threadIdx.x; e < kpad * RB; e += SL5_CONS) {
+        const int k = e / RB, r = e - (e / RB) * RB;
+        a2s[e] = (k < b.I2 && r < R) ? A2[(long long)k * R + r] : 0.0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(SL5_CONS) : "memory");
+    }
+    double acc[4][CG];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < CG; ++v) acc[u][v] = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(&full[st], ph);
+      const float* tile = reinterpret_cast<const float*>(ring + (size_t)st * TG_BOX);
+      const double* ar = a2s + (size_t)c * TG_KC * RB + cg * CG;
+#pragma unroll 4
+      for (int k = 0; k < TG_KC; ++k) {
+        const float4 x4 = *reinterpret_cast<const float4*>(tile + k * TG_M + 4 * jg);
+        const double xv[4] = {x4.x, x4.y, x4.z, x4.w};
+        double av[CG];
+#pragma unroll
+        for (int v = 0; v < CG; ++v) av[v] = ar[k * RB + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < CG; ++v) acc[u][v] = fma(xv[u], av[v], acc[u][v]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == TG_NST) { st = 0; ph ^= 1; }
+    }
+    double* T = reinterpret_cast<double*>(sel ? a.T1[tt.s] : a.T0[tt.s]);
+    const long long j0 = (long long)tt.t * TG_M + 4 * jg;
+#pragma unroll
+    for (int v = 0; v < CG; ++v) {
+      const int r = cg * CG + v;
+      if (r >= R) continue;
+      double* dst = T + (long long)r * J + j0;
+      if (j0 + 3 < J) {
+        reinterpret_cast<double2*>(dst)[0] = make_double2(acc[0][v], acc[1][v]);
+        reinterpret_cast<double2*>(dst)[1] = make_double2(acc[2][v], acc[3][v]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u < J) dst[u] = acc[u][v];
+      }
+    }
+  }
 }
 
 template <int RB>
@@ -332,7 +473,96 @@ int sl5_plan_create(int S, const void* const* X, const long long* dims, const in
     default: SL5_ATTR(64); break;
   }
 #undef SL5_ATTR
+  // ---- T pass GEMM: J % 4 == 0 (16-byte rows of the (J x I2) view), R > 8,
+  // staging within shared memory
+  {
+    long long i2pad = 1;
+    bool ok = true;
+    for (int s = 0; s < S; ++s) {
+      const long long J = dims[3 * s] * dims[3 * s + 1];
+      ok = ok && J % 4 == 0 && R[s] > 8;
+      i2pad = std::max(i2pad, (dims[3 * s + 2] + TG_KC - 1) / TG_KC * TG_KC);
+    }
+    const int trb = p->rb < 16 ? 16 : (p->rb == 12 ? 16 : p->rb);
+    const size_t tsm = 1024 + (size_t)TG_NST * TG_BOX + 8 * (2 * TG_NST + 2) + (size_t)i2pad * trb * 8;
+    if (ok && tsm <= (size_t)SL5_SMEM_MAX) {
+      std::vector<CUtensorMap> tm(S);
+      std::vector<Sl5Tile> tt;
+      for (int s = 0; s < S && ok; ++s) {
+        const long long J = dims[3 * s] * dims[3 * s + 1];
+        for (long long t = 0; t < (J + TG_M - 1) / TG_M; ++t) tt.push_back({s, (int)t});
+        cuuint64_t gdim[2] = {(cuuint64_t)J, (cuuint64_t)dims[3 * s + 2]};
+        cuuint64_t gstride[1] = {(cuuint64_t)J * 4};
+        cuuint32_t box[2] = {TG_M, TG_KC};
+        cuuint32_t estr[2] = {1, 1};
+        ok = enc(&tm[s], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(X[s]), gdim,
+                 gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
+      if (ok) {
+        p->tg_rb = trb;
+        p->tg_smem = tsm;
+        p->tg_ntiles = (int)tt.size();
+        p->tg_grid = std::max(1, std::min(nsm, p->tg_ntiles));
+        if ((rc = dalloc((void**)&p->tg_maps, sizeof(CUtensorMap) * S, A)) ||
+            (rc = dalloc((void**)&p->tg_tiles, sizeof(Sl5Tile) * tt.size(), A))) {
+          sl5_plan_destroy(p);
+          return rc;
+        }
+        CB_CUDA(cudaMemcpyAsync(p->tg_maps, tm.data(), sizeof(CUtensorMap) * S,
+                                cudaMemcpyHostToDevice, st));
+        CB_CUDA(cudaMemcpyAsync(p->tg_tiles, tt.data(), sizeof(Sl5Tile) * tt.size(),
+                                cudaMemcpyHostToDevice, st));
+#define TG_ATTR(RBV)                                                                      \
+  CB_CUDA(cudaFuncSetAttribute(k_tg_pass<RBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               (int)p->tg_smem))
+        switch (p->tg_rb) {
+          case 16: TG_ATTR(16); break;
+          case 24: TG_ATTR(24); break;
+          case 32: TG_ATTR(32); break;
+          case 40: TG_ATTR(40); break;
+          case 48: TG_ATTR(48); break;
+          default: TG_ATTR(64); break;
+        }
+#undef TG_ATTR
+        p->tg_ok = true;
+      }
+    }
+  }
   *out = p;
+  return CB_OK;
+}
+
+bool sl5_tpass_ok(const Sl5Plan* p) { return p && p->tg_ok; }
+
+int sl5_tpass(Sl5Plan* p, const double* const* U_dev, const int* active, void* const* T0,
+              void* const* T1, const int* tsel, int t_other, cudaStream_t st) {
+  if (!p->tg_ok) {
+    set_error("T-pass GEMM not available for these blocks");
+    return CB_ERR_UNSUPPORTED;
+  }
+  TgArgs a;
+  memset(&a, 0, sizeof(a));
+  a.tmaps = p->tg_maps;
+  a.blk = p->blk;
+  a.tiles = p->tg_tiles;
+  a.ntiles = p->tg_ntiles;
+  a.U = U_dev;
+  a.active = active;
+  a.T0 = T0;
+  a.T1 = T1;
+  a.tsel = tsel;
+  a.t_other = t_other;
+  switch (p->tg_rb) {
+    case 16: CB_CUDA(launch_k(k_tg_pass<16>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
+    case 24: CB_CUDA(launch_k(k_tg_pass<24>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
+    case 32: CB_CUDA(launch_k(k_tg_pass<32>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
+    case 40: CB_CUDA(launch_k(k_tg_pass<40>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
+    case 48: CB_CUDA(launch_k(k_tg_pass<48>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
+    default: CB_CUDA(launch_k(k_tg_pass<64>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
+  }
+  count_launch(1);
   return CB_OK;
 }
 

@@ -16,4 +16,11 @@ void sl5_plan_destroy(Sl5Plan* p);
 int sl5_mode2(Sl5Plan* p, const double* const* U_dev, const int* active, double* const* mtt,
               cudaStream_t st, const int* gate = nullptr);
 
+// T = X x3 A2 of every active block as an fp64 GEMM (the ALS sweep's T pass),
+// written unsplit into T buffer (*tsel) ^ t_other; available when
+// sl5_tpass_ok (J % 4 == 0, rank > 8, A2 staging fits)
+bool sl5_tpass_ok(const Sl5Plan* p);
+int sl5_tpass(Sl5Plan* p, const double* const* U_dev, const int* active, void* const* T0,
+              void* const* T1, const int* tsel, int t_other, cudaStream_t st);
+
 }  // namespace cb

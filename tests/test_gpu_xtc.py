@@ -176,3 +176,35 @@ def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, tol, max_iter):
         np.testing.assert_array_equal(ba.weights, bb.weights)
         for fa, fb in zip(ba.factors, bb.factors):
             np.testing.assert_array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("name,blocks", [("c5", [0, 1]), ("c3", [0, 1, 2])])
+def test_gemm_pass_als_matches_explicit_fp64_als(P, name, blocks):
+    """The fp32-storage ALS of ranks > 16 (both tensor passes as fp64 GEMMs
+    over TMA boxes, residual by the gram expansion; csrc/xslab5.cu k_tg_pass /
+    k_sl5_dpass, csrc/als.cu) against the fp64-storage ALS on the same values
+    (explicit residual, the reference's formula cpd_als.py:107-110): the
+    relative-error histories within 1e-10 absolute per sweep, same number of
+    sweeps, factors within 1e-8 relative."""
+    import torch
+    from paper_2302_05119_b200 import _lib as L
+    from paper_2302_05119_b200.cpd_als import als_compress_blocks
+    from paper_2302_05119_b200.synth import generate_config_device
+    dev, spec = generate_config_device(name, blocks=blocks)
+    flat32 = [t.permute(2, 1, 0).contiguous().reshape(-1) for t in dev]
+    flat64 = [f.to(torch.float64) for f in flat32]
+    dims = [tuple(spec.dims)] * len(blocks)
+    st = L.c_vp(torch.cuda.current_stream().cuda_stream)
+    out = {}
+    for code, data in ((L.CB_F32, flat32), (L.CB_F64, flat64)):
+        h = als_compress_blocks(data, dims, [spec.rank] * len(blocks), 1e-4, 200,
+                                [0 + b for b in blocks], code, st, 0, total_blocks=spec.n_blocks)
+        out[code] = [h.block(s) for s in range(len(blocks))]
+        h.close()
+    for s in range(len(blocks)):
+        fa, _, ha, na, ca = out[L.CB_F32][s]
+        fb, _, hb, nb, cb = out[L.CB_F64][s]
+        assert na == nb and ca == cb
+        np.testing.assert_allclose(ha, hb, rtol=0, atol=1e-10)
+        for a, b in zip(fa, fb):
+            assert np.abs(a - b).max() <= 1e-8 * np.abs(b).max()
