@@ -834,22 +834,20 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     TRY(dalloc((void**)&c.qr_buf, sizeof(double) * (size_t)S * N * QR_MAXC * QR_MAXC, A));
     // ||core||^2: the GEMM form for 3-way blocks whose R1 / R2 images fit in
     // shared memory, else the generic per-entry kernel
-    long long pairs = 1, na = 1;
+    long long pairs = 1;
     size_t qrc = 0;
     for (int s = 0; s < S; ++s) {
       const long long Cc = h->R[s] + h->Rt[s];
       if (N != 3) break;
       const long long K0 = std::min(h->dims[3 * s], Cc), K1 = std::min(h->dims[3 * s + 1], Cc);
       const long long K2 = std::min(h->dims[3 * s + 2], Cc);
-      const long long nas = std::min(K0, QRC_PAIRS / K1 + 2);
-      pairs = std::max(pairs, K0 * K1);
-      na = std::max(na, nas);
-      qrc = std::max(qrc, sizeof(double) * (size_t)(Cc + Cc * K1 + Cc * K2 + Cc * nas));
+      pairs = std::max(pairs, K0);
+      qrc = std::max(qrc, sizeof(double) * (size_t)(Cc + Cc * K1 + Cc * K2 + Cc * QRC_A));
       if (K2 > 16 * QRC_CT) qrc = SIZE_MAX;
     }
     h->qr_core3 = N == 3 && qrc <= 200 * 1024;
     h->qrc_smem = h->qr_core3 ? qrc : 0;
-    c.qr_nchunks = h->qr_core3 ? (int)((pairs + QRC_PAIRS - 1) / QRC_PAIRS) : 8;
+    c.qr_nchunks = h->qr_core3 ? (int)((pairs + QRC_A - 1) / QRC_A) : 8;
     TRY(dalloc((void**)&c.qr_part, sizeof(double) * S * c.qr_nchunks, A));
   }
   TRY(dalloc((void**)&c.h_obj, sizeof(double) * (h->max_iter + 1), A));

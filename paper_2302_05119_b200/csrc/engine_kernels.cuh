@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
   double* Rm = smd;                      // Cc x ld, upper triangular
   double* X = Rm + Cc * ld;              // ch x ld chunk
   double* w = X + (long long)ch * ld;    // Cc
-  double* red = w + Cc;                  // 64
+  double* red = w + Cc;                  // 2 x 32 (double-buffered column norms)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = QR_THREADS / 32;
   for (int e = threadIdx.x; e < Cc * ld; e += QR_THREADS) Rm[e] = 0.0;
   const double* A = c.Ut[s * c.N + n];
@@ -750,49 +750,54 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
   for (long long c0 = 0; c0 < In; c0 += ch) {
     const int nr = (int)(In - c0 < ch ? In - c0 : ch);
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * Cc; e += QR_THREADS) {
-      const int i = e / Cc, j = e - i * Cc;
-      X[i * ld + j] = j < Rt ? A[(c0 + i) * Rt + j] : B[(c0 + i) * R + (j - Rt)];
+    for (int i = wid; i < nr; i += nw)
+      for (int j = lane; j < Cc; j += 32)
+        X[i * ld + j] = j < Rt ? A[(c0 + i) * Rt + j] : B[(c0 + i) * R + (j - Rt)];
+    __syncthreads();
+    // squared norm of column 0 of the chunk (per-warp partials)
+    {
+      double ss = 0.0;
+      for (int i = threadIdx.x; i < nr; i += QR_THREADS) ss = fma(X[i * ld], X[i * ld], ss);
+      ss = warp_sum(ss);
+      if (lane == 0) red[wid] = ss;
     }
     __syncthreads();
     for (int k = 0; k < Cc; ++k) {
-      // ||[R_kk; X[:, k]]||^2
+      const double* rk = red + (k & 1) * 32;
       double ss = 0.0;
-      for (int i = threadIdx.x; i < nr; i += QR_THREADS) ss = fma(X[i * ld + k], X[i * ld + k], ss);
-      ss = warp_sum(ss);
-      if (lane == 0) red[wid] = ss;
-      __syncthreads();
-      ss = 0.0;
-      for (int q = 0; q < nw; ++q) ss += red[q];
+      for (int q = 0; q < nw; ++q) ss += rk[q];
       const double x0 = Rm[k * ld + k];
       ss = fma(x0, x0, ss);
       const double nrm = sqrt(ss);
       const double alpha = x0 >= 0.0 ? -nrm : nrm;
       const double v0 = x0 - alpha;
       const double vtv = 2.0 * (ss - alpha * x0);
-      if (!(vtv > 0.0)) {
-        // the column is already zero below R_kk: no reflection
-        __syncthreads();
-        continue;
-      }
-      const double beta = 2.0 / vtv;
+      const bool refl = vtv > 0.0;
+      const double beta = refl ? 2.0 / vtv : 0.0;
       // w_j = v0 R_kj + sum_i X_ik X_ij, one warp per column
-      for (int j = k + 1 + wid; j < Cc; j += nw) {
-        double a = 0.0;
-        for (int i = lane; i < nr; i += 32) a = fma(X[i * ld + k], X[i * ld + j], a);
-        a = warp_sum(a);
-        if (lane == 0) w[j] = fma(v0, Rm[k * ld + j], a);
-      }
+      if (refl)
+        for (int j = k + 1 + wid; j < Cc; j += nw) {
+          double a = 0.0;
+          for (int i = lane; i < nr; i += 32) a = fma(X[i * ld + k], X[i * ld + j], a);
+          a = warp_sum(a);
+          if (lane == 0) w[j] = fma(v0, Rm[k * ld + j], a) * beta;
+        }
       __syncthreads();
-      const int ncol = Cc - k - 1;
-      for (int e = threadIdx.x; e < (nr + 1) * ncol; e += QR_THREADS) {
-        const int i = e / ncol, j = k + 1 + (e - i * ncol);
-        const double bw = beta * w[j];
-        if (i == 0) Rm[k * ld + j] -= v0 * bw;
-        else X[(i - 1) * ld + j] -= X[(i - 1) * ld + k] * bw;
+      // rank-1 update (warp per row, lanes over columns); lane 0 of every warp
+      // also sums the squares of the updated column k + 1 (next step's norm)
+      double nss = 0.0;
+      for (int i = wid; i <= nr; i += nw) {
+        double* row = i == 0 ? Rm + k * ld : X + (i - 1) * ld;
+        const double vi = i == 0 ? v0 : X[(i - 1) * ld + k];
+        for (int j = k + 1 + lane; j < Cc; j += 32) {
+          const double x = refl ? row[j] - vi * w[j] : row[j];
+          if (refl) row[j] = x;
+          if (j == k + 1 && i > 0) nss = fma(x, x, nss);
+        }
       }
+      if (lane == 0) red[((k + 1) & 1) * 32 + wid] = nss;
+      if (threadIdx.x == 0) Rm[k * ld + k] = refl ? alpha : x0;
       __syncthreads();
-      if (threadIdx.x == 0) Rm[k * ld + k] = alpha;
     }
   }
   __syncthreads();
@@ -810,6 +815,7 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
 // registers; per-CTA partials folded in order by k_control.  Grid:
 // S * qr_nchunks, qr_nchunks = ceil(max K0 K1 / QRC_PAIRS).
 constexpr int QRC_PAIRS = 64;
+constexpr int QRC_A = 8;      // core rows a per CTA
 constexpr int QRC_CT = 8;     // max columns per thread (K2 <= 128)
 
 __global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
@@ -824,19 +830,19 @@ __global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
   const int K0 = (int)(c.dims[s * 3] < Cc ? c.dims[s * 3] : Cc);
   const int K1 = (int)(c.dims[s * 3 + 1] < Cc ? c.dims[s * 3 + 1] : Cc);
   const int K2 = (int)(c.dims[s * 3 + 2] < Cc ? c.dims[s * 3 + 2] : Cc);
-  const int p0 = ch * QRC_PAIRS;
-  const int npair = K0 * K1 - p0 < QRC_PAIRS ? K0 * K1 - p0 : QRC_PAIRS;
   __shared__ double red[40];
-  if (npair <= 0) {
+  // this CTA: rows a in [a_lo, a_hi) of the core, every (b, c)
+  const int a_lo = ch * QRC_A;
+  const int a_hi = a_lo + QRC_A < K0 ? a_lo + QRC_A : K0;
+  if (a_lo >= a_hi) {
     if (threadIdx.x == 0) c.qr_part[(long long)s * c.qr_nchunks + ch] = 0.0;
     return;
   }
-  const int a_lo = p0 / K1, a_hi = (p0 + npair - 1) / K1;
-  const int na = a_hi - a_lo + 1;
+  const int na = a_hi - a_lo;
   double* wq = smd;                      // Cc
   double* R1T = wq + Cc;                 // Cc x K1
   double* R2T = R1T + Cc * K1;           // Cc x K2
-  double* R0T = R2T + Cc * K2;           // Cc x na
+  double* R0T = R2T + Cc * K2;           // Cc x QRC_A
   const double* Rb = c.qr_buf + (long long)s * 3 * QR_MAXC * QR_MAXC;
   const long long MS = (long long)QR_MAXC * QR_MAXC;
   for (int q = threadIdx.x; q < Cc; q += blockDim.x)
@@ -851,44 +857,47 @@ __global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
   }
   for (int e = threadIdx.x; e < Cc * na; e += blockDim.x) {
     const int a = e / Cc, q = e - a * Cc;
-    R0T[q * na + a] = Rb[(long long)(a_lo + a) * Cc + q];
+    R0T[q * QRC_A + a] = Rb[(long long)(a_lo + a) * Cc + q];
   }
   __syncthreads();
   const int grp = threadIdx.x >> 4, col = threadIdx.x & 15;   // 16 pair groups x 16 columns
-  int pa[4], pb[4];
-  bool pv[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int pl = grp * 4 + u;
-    pv[u] = pl < npair;
-    const int p = p0 + (pv[u] ? pl : 0);
-    pa[u] = p / K1 - a_lo;
-    pb[u] = p - (p / K1) * K1;
-  }
-  double acc[4][QRC_CT];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < QRC_CT; ++v) acc[u][v] = 0.0;
-  for (int q = 0; q < Cc; ++q) {
-    const double wv = wq[q];
-    double P[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) P[u] = wv * R0T[q * na + pa[u]] * R1T[q * K1 + pb[u]];
-#pragma unroll
-    for (int v = 0; v < QRC_CT; ++v) {
-      const int cc = col + 16 * v;
-      const double r2 = cc < K2 ? R2T[q * K2 + cc] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u][v] = fma(P[u], r2, acc[u][v]);
-    }
-  }
+  const int npairs = na * K1;
   double ssq = 0.0;
+  for (int p0 = 0; p0 < npairs; p0 += QRC_PAIRS) {
+    int pa[4], pb[4];
+    bool pv[4];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + grp * 4 + u;
+      pv[u] = p < npairs;
+      const int pp = pv[u] ? p : 0;
+      pa[u] = pp / K1;
+      pb[u] = pp - pa[u] * K1;
+    }
+    double acc[4][QRC_CT];
 #pragma unroll
-    for (int v = 0; v < QRC_CT; ++v)
-      if (pv[u]) ssq = fma(acc[u][v], acc[u][v], ssq);
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < QRC_CT; ++v) acc[u][v] = 0.0;
+    for (int q = 0; q < Cc; ++q) {
+      const double wv = wq[q];
+      double P[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) P[u] = wv * R0T[q * QRC_A + pa[u]] * R1T[q * K1 + pb[u]];
+#pragma unroll
+      for (int v = 0; v < QRC_CT; ++v) {
+        const int cc = col + 16 * v;
+        const double r2 = cc < K2 ? R2T[q * K2 + cc] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u][v] = fma(P[u], r2, acc[u][v]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < QRC_CT; ++v)
+        if (pv[u]) ssq = fma(acc[u][v], acc[u][v], ssq);
+  }
   ssq = block_sum(ssq, red);
   if (threadIdx.x == 0) c.qr_part[(long long)s * c.qr_nchunks + ch] = ssq;
 }

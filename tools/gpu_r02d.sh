@@ -1,0 +1,12 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02d
+mkdir -p $O
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 600 python tools/e2e_breakdown.py c5 > $O/e2e_c5.txt 2>&1
+timeout 600 python tools/profile_late.py c5 150 5 > $O/prof_c5_late.txt 2>&1
+timeout 600 python tools/als_probe.py 8 10 > $O/als_probe.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/als_launches.csv python tools/als_probe.py 8 4 > $O/als_ncu.log 2>&1
+timeout 900 python bench.py > $O/bench_c5.jsonl 2> $O/bench_c5.err
+echo done
