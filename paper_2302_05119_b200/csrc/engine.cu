@@ -50,6 +50,7 @@ struct cb_solver {
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t st3 = nullptr;     // capture stream of the conditional restart body
+  cudaStream_t st_main = nullptr; // the iteration's stream while a body is captured
   bool cond_capture = false;
   bool in_body = false;
   int S = 0, N = 0, lra = 0, update_core = 1, dtype = CB_F64, objective = 0, fast3 = 0, pc = 0;
@@ -126,16 +127,27 @@ static inline bool emit(const cb_solver* h) {
   return h->seg_want == -1 || h->seg_cur == h->seg_want;
 }
 
+static int begin_cond_body(cb_solver* h);
+static int end_cond_body(cb_solver* h);
+
 // exchange point: recv <- sum over ranks of send (count doubles); closes the
-// current segment
+// current segment.  Inside a captured conditional restart body the NCCL call
+// is issued in the parent graph between two bodies (collectives stay out of
+// conditional nodes; every rank runs the same graph).  There it also runs
+// when no restart happens: the send buffers are then unchanged since their
+// last exchange, so the all-reduce rewrites recv with the values it holds.
 static int xchg(cb_solver* h, double* send, double* recv, long long count) {
   if (!h->shard) return CB_OK;
   if (h->comm) {
     if (emit(h)) {
+      const bool split = h->in_body && h->cond_capture;
+      int rc;
+      if (split && (rc = end_cond_body(h))) return rc;
       NcclApi& api = nccl_api();
       ncclResult_t r = api.ncclAllReduce(send, recv, (size_t)count, ncclFloat64, ncclSum,
                                          (ncclComm_t)h->comm, h->st);
       if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+      if (split && (rc = begin_cond_body(h))) return rc;
     }
   } else if (h->seg_cur == h->seg_want) {
     h->pending.push_back(cb_solver::Xchg{send, recv, count});
@@ -353,14 +365,14 @@ static int enqueue_control(cb_solver* h, int mode, int extra = 0) {
     return CB_OK;
   }
   if (emit(h)) {
-    launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 1);
+    launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 1 | extra);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
   int rc = xchg(h, h->ctx.ctl_w, h->ctx.ctl, 3LL * h->S_tot);
   if (rc) return rc;
   if (emit(h)) {
-    launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 2);
+    launch_k(k_control, dim3(1), dim3(256), 0, h->st, h->ctx, mode, bsrc, 2 | extra);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -446,15 +458,15 @@ static int enqueue_redo_branch(cb_solver* h) {
 }
 
 // Under graph capture (h->cond_capture) the restart branch becomes the body of
-// a conditional IF node, so an iteration without restart launches none of its
-// ~15 kernels; otherwise it is enqueued inline as gated no-ops.
-static int enqueue_redo(cb_solver* h) {
-  if (!h->cond_capture) return enqueue_redo_branch(h);
+// a conditional IF node (sharded: one node per stretch between exchanges), so
+// an iteration without restart launches none of its ~15 kernels; otherwise it
+// is enqueued inline as gated no-ops.
+static int begin_cond_body(cb_solver* h) {
   cudaStreamCaptureStatus cs;
   cudaGraph_t g;
   const cudaGraphNode_t* deps = nullptr;
   size_t nd = 0;
-  CB_CUDA(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &g, &deps, &nd));
+  CB_CUDA(cudaStreamGetCaptureInfo(h->st_main, &cs, nullptr, &g, &deps, &nd));
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h->ctx.cond;
@@ -463,20 +475,32 @@ static int enqueue_redo(cb_solver* h) {
   cudaGraphNode_t node;
   CB_CUDA(cudaGraphAddNode(&node, g, deps, nd, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CB_CUDA(cudaStreamUpdateCaptureDependencies(h->st, &node, 1, cudaStreamSetCaptureDependencies));
-  cudaStream_t main = h->st;
+  CB_CUDA(cudaStreamUpdateCaptureDependencies(h->st_main, &node, 1,
+                                              cudaStreamSetCaptureDependencies));
   h->st = h->st3;
   CB_CUDA(cudaStreamBeginCaptureToGraph(h->st3, body, nullptr, nullptr, 0,
                                         cudaStreamCaptureModeThreadLocal));
-  h->in_body = true;
-  int rc = enqueue_redo_branch(h);
-  h->in_body = false;
+  return CB_OK;
+}
+
+static int end_cond_body(cb_solver* h) {
   cudaGraph_t done_body;
   cudaError_t e = cudaStreamEndCapture(h->st3, &done_body);
-  h->st = main;
-  if (rc) return rc;
+  h->st = h->st_main;
   CB_CUDA(e);
   return CB_OK;
+}
+
+static int enqueue_redo(cb_solver* h) {
+  if (!h->cond_capture) return enqueue_redo_branch(h);
+  h->st_main = h->st;
+  int rc = begin_cond_body(h);
+  if (rc) return rc;
+  h->in_body = true;
+  rc = enqueue_redo_branch(h);
+  h->in_body = false;
+  const int rc2 = end_cond_body(h);
+  return rc ? rc : rc2;
 }
 
 // one full APG iteration (solver.py:586-610), device-gated
@@ -970,7 +994,9 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       // pipelined only when the trace pass is large enough to hide the sweep
       // behind (c3, c5); on small blocks (c4: 35 MB) the extra snapshot /
       // rollback work costs more than it hides (measured)
-      h->pipe = h->xtc != nullptr && !shard && d->pipeline != 2 &&
+      // sharded: with an NCCL communicator (the emulated group runs the
+      // classic order segment by segment)
+      h->pipe = h->xtc != nullptr && (!shard || d->nccl_comm) && d->pipeline != 2 &&
                 (xtc_bytes(h->xtc) >= 64e6 || d->pipeline == 1);
       if (h->pipe) {
         // leave SMs for the sweep that runs beside the trace: its per-block
@@ -1108,8 +1134,8 @@ int cb_solver_step_async(cb_solver* h) {
     cudaGraph_t g;
     cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
-      // conditional restart branch (not with NCCL exchanges inside it)
-      if (!h->shard) {
+      // conditional restart branch (sharded: NCCL exchanges between the bodies)
+      if (!h->shard || h->comm) {
         cudaGraph_t cg;
         cudaStreamCaptureStatus cs;
         if (cudaStreamGetCaptureInfo(h->st, &cs, nullptr, &cg, nullptr, nullptr) == cudaSuccess &&

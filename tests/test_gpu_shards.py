@@ -112,5 +112,32 @@ def test_nccl_path_single_rank_equals_single_gpu(P, tmp_path):
             want = P.solve(prob, opts)
             got = P.solver.solve_distributed(prob, opts)
             _same(got, want)
+        # restarts through the conditional restart bodies split at the NCCL
+        # exchanges (fp32 storage, c2-shaped blocks)
+        from paper_2302_05119_b200.configs import generate_config
+        tensors, spec = generate_config("c2", blocks=range(3))
+        prob = P.CoupledProblem(list(tensors), spec.rank, list(spec.coupled))
+        opts = P.SolverOptions(max_iter=200, seed=0, precision="fp32")
+        want = P.solve(prob, opts)
+        got = P.solver.solve_distributed(prob, opts)
+        _same(got, want)
+        assert want.n_restarts > 0
+        # the pipelined lra iteration under sharding (trace pass beside the
+        # next sweep, exchanges on the sweep stream), max_iter and tol stops
+        rng = np.random.default_rng(33)
+        facs = lambda d: [rng.random((n, 20)) for n in d]  # noqa: E731
+        blocks = []
+        for _ in range(3):
+            f = facs((64, 40, 30))
+            t = np.einsum("ir,jr,kr->ijk", *f)
+            blocks.append(np.maximum(t + 0.05 * rng.standard_normal(t.shape), 0.0).astype(np.float32))
+        for tol, mi in ((1e-30, 40), (1e-5, 400)):
+            prob = P.CoupledProblem(blocks, 20, [5, 5, 0], mode="lra")
+            kw = dict(max_iter=mi, tol=tol, seed=5, precision="fp32", compute="tc", pipeline="on")
+            want = P.solve(prob, P.SolverOptions(**kw))
+            got = P.solver.solve_distributed(prob, P.SolverOptions(**kw))
+            _same(got, want)
+            off = P.solve(prob, P.SolverOptions(**{**kw, "pipeline": "off"}))
+            _same(off, want)
     finally:
         dist.destroy_process_group()
