@@ -497,24 +497,33 @@ class PreparedSolve:
             self.dev = []
             self.dims = []
             first_bad, bad_msg = None, None     # (block, 0 order / 1 values)
+            limit = len(problem.tensors)
             for g, t in enumerate(problem.tensors):
                 try:
                     problem._validate_block(g, t)
                 except ValueError as exc:
-                    first_bad, bad_msg = (g, 0), exc
+                    first_bad, bad_msg, limit = (g, 0), exc, g
                     break
-                if g not in self.local:
-                    continue
+            # uploads and element scans of the blocks before the first order
+            # error, all enqueued, one synchronisation (stats slot per block)
+            scan = [g for g in self.local if g < limit]
+            stats = torch.empty((max(len(scan), 1), 3), dtype=torch.float64, device=D.device())
+            for k, g in enumerate(scan):
+                t = problem.tensors[g]
                 src, dims = D.tensor_to_dev(t, D.source_dtype(t))
-                try:
-                    _raise_values(g, src)
-                except ValueError as exc:
-                    first_bad, bad_msg = (g, 1), exc
-                    break
+                code = L.CB_F32 if D.source_dtype(t) == "fp32" else L.CB_F64
+                L.check(L.lib.cb_tensor_stats(code, D.ptr(src), src.numel(), D.ptr(stats[k]),
+                                              D.stream()))
                 flat = src if D.source_dtype(t) == prec else D.cast_flat(src, prec)
                 del src
                 self.dev.append(flat)
                 self.dims.append(dims)
+            host = stats.cpu().numpy() if scan else np.zeros((0, 3))
+            for k, g in enumerate(scan):
+                if host[k, 2] != 0.0 or host[k, 1] < 0.0:
+                    which = "non-finite values" if host[k, 2] != 0.0 else "negative entries"
+                    first_bad, bad_msg = (g, 1), ValueError(f"block {g} contains {which}")
+                    break
             if agree is not None:
                 first_bad, bad_msg = agree(first_bad, bad_msg, problem)
             if bad_msg is not None:
