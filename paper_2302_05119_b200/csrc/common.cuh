@@ -36,6 +36,21 @@ __device__ __forceinline__ void griddep_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Asynchronous global -> shared staging (LDGSTS): every thread issues its
+// 8-byte copies without waiting, so a staging loop costs one memory latency
+// instead of one per iteration.  Complete with cp_async8_wait() and a barrier.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8_wait() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+// dst[e] = src[e], e < n, all threads of the block (no wait)
+__device__ __forceinline__ void stage_async(double* dst, const double* src, long long n) {
+  for (long long e = threadIdx.x; e < n; e += blockDim.x) cp_async8(dst + e, src + e);
+}
+
 // Phase timestamps (profiling builds of a run: Ctx.dbg non-null): block 0
 // accumulates the time between consecutive PH() marks into dbg[slot].
 struct PhaseClock {

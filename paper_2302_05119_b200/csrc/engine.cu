@@ -1029,6 +1029,11 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   int maxRt = std::max(h->rtmax, 1);
   h->mu_smem = sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)MU_ROWS * h->rmax +
                                  (h->lra ? (size_t)maxRt * h->rmax : 0) + 16);
+  // lra 3-way staging: two cross grams, the tile's Ut rows, the weights
+  if (h->lra && N == 3)
+    h->mu_smem += sizeof(double) * (2 * (size_t)maxRt * h->rmax + (size_t)MU_ROWS * maxRt + maxRt);
+  // staged rows: current, previous, block 0's current / previous
+  h->mu_smem += sizeof(double) * 4 * (size_t)MU_ROWS * h->rmax;
   h->qr_smem = 0;
   if (h->lra) {
     int cmax = 0;

@@ -80,9 +80,9 @@ static __device__ __noinline__ void block_gram(const double* __restrict__ A, int
   for (long long c0 = 0; c0 < rows; c0 += CH) {
     const int nr = (int)(rows - c0 < CH ? rows - c0 : CH);
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * P; e += blockDim.x) As[e] = A[c0 * P + e];
-    if (!same)
-      for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) Bs[e] = B[c0 * Q + e];
+    stage_async(As, A + c0 * P, (long long)nr * P);
+    if (!same) stage_async(Bs, B + c0 * Q, (long long)nr * Q);
+    cp_async8_wait();
     __syncthreads();
     if (owner && t1) {
       double sacc = acc[0][0];
@@ -432,8 +432,34 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     sc[2] = extrap_weight(w_hat, c.lip_w[lup_idx(c, n, g)], c.lip_w[lu_idx(c, n, g)], c.delta_w);
     sc[3] = c.lip_w[lu_idx(c, n, g)];
   }
-  const double* stp = c.STEP[s];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) step[e] = stp[e];
+  stage_async(step, c.STEP[s], (long long)R * R);
+  // lra, 3-way: the two other modes' cross grams, this tile's Ut rows and the
+  // compression weights, staged with the step matrix in one round trip
+  const bool lra3 = src == 2 && N == 3;
+  double* Cs = sc + 8;                       // 2 x Rt*R (lra3)
+  double* Uts = Cs + (lra3 ? 2 * c.Rt[s] * R : 0);   // rows x Rt
+  double* tws = Uts + (lra3 ? MU_ROWS * c.Rt[s] : 0); // Rt
+  // this tile's current / previous rows (and block 0's common columns)
+  double* Ucs = tws + (lra3 ? c.Rt[s] : 0);            // rows x R
+  double* Ups = Ucs + MU_ROWS * R;                      // rows x R
+  double* U0s = Ups + MU_ROWS * R;                      // rows x R0 (L > 0)
+  double* U0ps = U0s + MU_ROWS * c.R[0];                // rows x R0 (L > 0)
+  stage_async(Ucs, c.U[s * N + n] + (long long)r0 * R, (long long)rows * R);
+  stage_async(Ups, c.Up[s * N + n] + (long long)r0 * R, (long long)rows * R);
+  if (L > 0) {
+    stage_async(U0s, c.U[n] + (long long)r0 * c.R[0], (long long)rows * c.R[0]);
+    stage_async(U0ps, c.Up[n] + (long long)r0 * c.R[0], (long long)rows * c.R[0]);
+  }
+  if (src == 0) stage_async(mt, c.MTT[s] + (long long)r0 * R, (long long)rows * R);
+  if (lra3) {
+    const int Rt = c.Rt[s];
+    int k = 0;
+    for (int m = 0; m < N; ++m)
+      if (m != n) stage_async(Cs + (k++) * Rt * R, c.C[s * N + m], (long long)Rt * R);
+    stage_async(Uts, c.Ut[s * N + n] + (long long)r0 * Rt, (long long)rows * Rt);
+    stage_async(tws, c.TW[s], Rt);
+  }
+  cp_async8_wait();
   __syncthreads();
   const double sumL = sc[0], wc = sc[1], ws = sc[2], lu = sc[3];
   PhaseClock pc;
@@ -443,21 +469,20 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   const int R0 = c.R[0];
   const double* U0c = c.U[n];
   const double* U0p = c.Up[n];
+  (void)U0c; (void)U0p; (void)Upr;
   for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
     const int il = e / R, r = e - il * R;
     const long long i = r0 + il;
     double v;
     if (r < L) {
-      const double cc = U0c[i * R0 + r], cp = U0p[i * R0 + r];
+      const double cc = U0s[il * R0 + r], cp = U0ps[il * R0 + r];
       v = cc + wc * (cc - cp);
     } else {
-      const double cur = Uc[i * R + r], prv = Upr[i * R + r];
+      const double cur = Ucs[e], prv = Ups[e];
       v = cur + ws * (cur - prv);
     }
     uh[e] = v;
-    if (src == 0) {
-      mt[e] = c.MTT[s][i * R + r];
-    } else if (src == 1) {
+    if (src == 1) {
       const int sb = c.slab_sb;
       const long long g = i / sb;
       const int m = (int)(i - g * sb);
@@ -468,7 +493,20 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
       mt[e] = a;
     }
   }
-  if (src == 2) {
+  if (lra3) {
+    // P = C_a o C_b (mode order), then mt = (Ut o tw) P from shared memory
+    const int Rt = c.Rt[s];
+    for (int e = threadIdx.x; e < Rt * R; e += blockDim.x) P[e] = Cs[e] * Cs[Rt * R + e];
+    for (int e = threadIdx.x; e < rows * Rt; e += blockDim.x) Uts[e] *= tws[e % Rt];
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+      const int il = e / R, r = e - il * R;
+      const double* ur = Uts + il * Rt;
+      double a = 0.0;
+      for (int q = 0; q < Rt; ++q) a = fma(ur[q], P[q * R + r], a);
+      mt[e] = a;
+    }
+  } else if (src == 2) {
     const int Rt = c.Rt[s];
     for (int e = threadIdx.x; e < Rt * R; e += blockDim.x) {
       double v = 0.0;
@@ -500,7 +538,7 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     const int il = e / R, r = e - il * R;
     const long long i = r0 + il;
     if (lu == 0.0) {
-      if (r >= L) Un[i * R + r] = Uc[i * R + r];
+      if (r >= L) Un[i * R + r] = Ucs[e];
       continue;
     }
     double g = 0.0;
