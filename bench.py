@@ -403,6 +403,12 @@ def run_ours(args):
                "solve_seconds": res.solve_seconds,
                "als_sweeps_mean": (float(np.mean(res.compression_iters))
                                    if res.compression_iters else None),
+               # the config's whole run length (late iterations included:
+               # QR route, clustered spectra), device timestamps of the
+               # accepted iterations, compression and setup excluded
+               "iterations_per_s_full_run": (
+                   res.n_iter / max(res.trace[-1].elapsed_s - res.trace[0].elapsed_s, 1e-12)
+                   if len(res.trace) > 1 else None),
                "step": f"one solve() call of {res.n_iter} iterations on pinned host torch "
                        "buffers: upload, device value checks, ALS compression, engine setup, "
                        "graph capture, iterations, result download"}

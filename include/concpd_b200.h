@@ -247,6 +247,9 @@ typedef struct {
    * beside iteration k+1's sweep (results bitwise those of the serial order).
    * 0 = auto (on when the trace pass streams >= 64 MB), 1 = on, 2 = off. */
   int pipeline;
+  /* SMs the pipelined trace pass leaves to the sweep beside it (0 = auto,
+   * ceil(S / 3), at most a third of the SMs) */
+  int pipeline_reserve;
 } cb_solver_desc;
 
 typedef struct {

@@ -46,6 +46,7 @@ class SolverDesc(ctypes.Structure):
         ("objective", c_int), ("compute", c_int), ("delta_w", c_dbl), ("tol", c_dbl), ("max_iter", c_int),
         ("world_size", c_int), ("rank_id", c_int), ("nccl_comm", c_vp),
         ("total_blocks", c_int), ("block_offset", c_int), ("pipeline", c_int),
+        ("pipeline_reserve", c_int),
     ]
 
 

@@ -1004,7 +1004,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        int reserve = (S + 2) / 3;
+        int reserve = d->pipeline_reserve > 0 ? d->pipeline_reserve : (S + 2) / 3;
         reserve = std::max(0, std::min(reserve, nsm / 3));
         xtc_set_grid_cap(h->xtc, nsm - reserve);
       }

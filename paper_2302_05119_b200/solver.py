@@ -168,6 +168,7 @@ class SolverOptions:
     objective: str = "auto"        # "auto" | "explicit" | "expansion"
     compute: str = "auto"          # fp32 storage: "auto" | "fp64" | "fp32" | "tc" (lra trace)
     pipeline: str = "auto"         # lra tensor-core trace beside the next sweep: "auto" | "on" | "off"
+    pipeline_reserve: int = 0      # SMs the pipelined trace leaves to the sweep (0 = auto)
 
     def __post_init__(self):
         if self.max_iter < 0:
@@ -609,6 +610,7 @@ class PreparedSolve:
         desc.total_blocks = S_all
         desc.block_offset = sh.begin
         desc.pipeline = {"auto": 0, "on": 1, "off": 2}[opts.pipeline]
+        desc.pipeline_reserve = int(opts.pipeline_reserve)
         self.t0 = time.perf_counter()
         self.engine = _Engine(desc, st)
         self.tilde_ranks = tilde_ranks
