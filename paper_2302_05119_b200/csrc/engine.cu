@@ -73,7 +73,11 @@ struct cb_solver {
   State* h_state = nullptr;     // pinned mirror
   size_t blk_smem = 0, mu_smem = 0, qr_smem = 0, qrc_smem = 0;
   int qr_ch = 32;             // TSQR chunk rows (k_qr_factor)
+  bool cluster = false;       // mode update + finalize as one cluster launch
+  size_t cl_smem = 0;
+  int cl_off = 0;             // doubles of the common-gradient partial
   bool qr_core3 = false;      // 3-way GEMM-form ||core||^2 (k_qr_core3)
+  int qrc_ct = 8;             // its columns per thread
   std::vector<double*> h_U;     // device pointer tables mirrored on host
   std::vector<double*> h_MTT;
   std::vector<double*> h_LAM;
@@ -299,6 +303,16 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       prof(h, "generic_mttkrp");
     }
     const bool split = par && n + 1 < h->N;
+    if (h->cluster) {
+      // the whole mode update in one cluster launch (k_mode_cluster)
+      if (emit(h)) {
+        CB_CUDA(launch_cluster(k_mode_cluster, dim3(h->S), dim3(256), h->cl_smem, st,
+                               (unsigned)h->S, h->ctx, n, redo, src, split ? 0 : 1, h->cl_off));
+        count_launch(1);
+        CB_CHECK_LAUNCH();
+      }
+      prof(h, redo ? "redo:mode_cluster" : "mode_cluster");
+    } else {
     if (emit(h)) {
       launch_k(k_mode_update, dim3(h->n_rows[n]), dim3(256), h->mu_smem, st, h->ctx, n, redo, src, h->d_rows[n]);
       count_launch(1);
@@ -321,6 +335,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       CB_CHECK_LAUNCH();
     }
     prof(h, redo ? "redo:finalize" : "finalize");
+    }
     if (split) {
       if ((rc = fork_side(h))) return rc;
       if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
@@ -342,9 +357,14 @@ static int enqueue_qr(cb_solver* h, int redo) {
   launch_k(k_qr_factor, dim3(h->S * h->N), dim3(QR_THREADS), h->qr_smem, h->st, h->ctx, redo,
            h->qr_ch);
   prof(h, redo ? "redo:qr_factor" : "qr_factor");
-  if (h->qr_core3)
-    launch_k(k_qr_core3, dim3(h->S * h->ctx.qr_nchunks), dim3(256), h->qrc_smem, h->st, h->ctx,
-             redo);
+  if (h->qr_core3) {
+    // columns per thread: ceil(K2 / 16) rounded to the instantiated tiles
+    const dim3 g(h->S * h->ctx.qr_nchunks);
+    if (h->qrc_ct <= 2) launch_k(k_qr_core3<2>, g, dim3(256), h->qrc_smem, h->st, h->ctx, redo);
+    else if (h->qrc_ct <= 4) launch_k(k_qr_core3<4>, g, dim3(256), h->qrc_smem, h->st, h->ctx, redo);
+    else if (h->qrc_ct <= 5) launch_k(k_qr_core3<5>, g, dim3(256), h->qrc_smem, h->st, h->ctx, redo);
+    else launch_k(k_qr_core3<8>, g, dim3(256), h->qrc_smem, h->st, h->ctx, redo);
+  }
   else
     launch_k(k_qr_core, dim3(h->S * h->ctx.qr_nchunks), dim3(256), 0, h->st, h->ctx, redo);
   prof(h, redo ? "redo:qr_core" : "qr_core");
@@ -858,7 +878,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     TRY(dalloc((void**)&c.qr_buf, sizeof(double) * (size_t)S * N * QR_MAXC * QR_MAXC, A));
     // ||core||^2: the GEMM form for 3-way blocks whose R1 / R2 images fit in
     // shared memory, else the generic per-entry kernel
-    long long pairs = 1;
+    long long pairs = 1, k2max = 1;
     size_t qrc = 0;
     for (int s = 0; s < S; ++s) {
       const long long Cc = h->R[s] + h->Rt[s];
@@ -867,9 +887,11 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       const long long K2 = std::min(h->dims[3 * s + 2], Cc);
       pairs = std::max(pairs, K0);
       qrc = std::max(qrc, sizeof(double) * (size_t)(Cc + Cc * K1 + Cc * K2 + Cc * QRC_A));
+      k2max = std::max(k2max, K2);
       if (K2 > 16 * QRC_CT) qrc = SIZE_MAX;
     }
     h->qr_core3 = N == 3 && qrc <= 200 * 1024;
+    h->qrc_ct = (int)((k2max + 15) / 16);
     h->qrc_smem = h->qr_core3 ? qrc : 0;
     c.qr_nchunks = h->qr_core3 ? (int)((pairs + QRC_A - 1) / QRC_A) : 8;
     TRY(dalloc((void**)&c.qr_part, sizeof(double) * S * c.qr_nchunks, A));
@@ -1047,6 +1069,40 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  // one cluster per mode update: single GPU, S <= 16, the partial and the
+  // scratch within shared memory, and a cluster of S CTAs schedulable
+  if (!shard && S <= 16) {
+    long long part = 0;
+    for (int n = 0; n < N; ++n)
+      for (int s2 = 0; s2 < S; ++s2) part = std::max(part, h->dims[s2 * N + n] * h->counts[n]);
+    h->cl_off = (int)((part + 1) & ~1LL);
+    h->cl_smem = sizeof(double) * (size_t)h->cl_off + std::max(h->mu_smem, h->blk_smem);
+    bool ok = h->cl_smem <= 200 * 1024;
+    if (ok && S > 8)
+      ok = cudaFuncSetAttribute(k_mode_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+           cudaSuccess;
+    if (ok)
+      ok = cudaFuncSetAttribute(k_mode_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)h->cl_smem) == cudaSuccess;
+    if (ok) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(S);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = h->cl_smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = S;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      ok = cudaOccupancyMaxActiveClusters(&nclusters, k_mode_cluster, &cfg) == cudaSuccess &&
+           nclusters >= 1;
+    }
+    cudaGetLastError();
+    h->cluster = ok;
+  }
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
@@ -1056,9 +1112,12 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   if (h->lra)
   {
     CB_CUDA(cudaFuncSetAttribute(k_qr_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qr_smem));
-    if (h->qr_core3)
-      CB_CUDA(cudaFuncSetAttribute(k_qr_core3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)h->qrc_smem));
+    if (h->qr_core3) {
+      CB_CUDA(cudaFuncSetAttribute(k_qr_core3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qrc_smem));
+      CB_CUDA(cudaFuncSetAttribute(k_qr_core3<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qrc_smem));
+      CB_CUDA(cudaFuncSetAttribute(k_qr_core3<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qrc_smem));
+      CB_CUDA(cudaFuncSetAttribute(k_qr_core3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->qrc_smem));
+    }
   }
   // ---- iteration 0 (an emulated group runs it through cb_group_step)
   if (!shard || h->comm) {

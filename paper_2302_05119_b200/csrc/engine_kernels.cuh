@@ -7,6 +7,8 @@
 // whole iteration (including the restart branch) can be enqueued or captured
 // in a CUDA graph without a host round trip.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "engine.h"
 #include "../../include/concpd_b200.h"
 
@@ -400,19 +402,18 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
 // common gradient; the last CTA of each row tile forms the new common columns
 // (solver.py:397-451).  src: 0 = MTT buffer, 1 = slab partials, 2 = lra.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int src,
-                                                      const RowUnit* __restrict__ units) {
-  griddep_wait();
-  if (stopped(c, redo)) return;
-  tl_begin(c.tl, TL_MU + n);
-  extern __shared__ double smd[];
-  const RowUnit u = units[blockIdx.x];
-  const int s = u.s;
+// One row tile [r0, r0 + MU_ROWS) of block s: extrapolate, gradient, project
+// the individual columns into Un, and the common-gradient partial into gcp
+// (row-major I_n x L; global slots or a cluster CTA's shared memory).
+// `smd` is the tile's shared scratch; returns the tile's (sumL, w_common)
+// through sc_out (valid on every thread).
+static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int redo, int src, int s,
+                                                     int r0, double* smd, double* gcp,
+                                                     double* sc_out) {
   const int R = c.R[s];
   const int N = c.N;
   const int L = c.counts[n];
   const long long In = c.dims[s * N + n];
-  const int r0 = u.r0;
   const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
   const double w_hat = redo ? 0.0 : c.st->w_hat;
   double* step = smd;                       // R*R
@@ -533,7 +534,6 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
   __syncthreads();
   pc.mark(c.dbg, 6);
   double* Un = c.Un[s * N + n];
-  double* gcp = c.gc_w + (long long)(c.off + s) * c.gc_stride;
   for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
     const int il = e / R, r = e - il * R;
     const long long i = r0 + il;
@@ -547,6 +547,30 @@ __global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int
     if (r < L) gcp[i * L + r] = g;
     else Un[i * R + r] = pos(uh[e] - g / lu);
   }
+  sc_out[0] = sumL;
+  sc_out[1] = wc;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int src,
+                                                      const RowUnit* __restrict__ units) {
+  griddep_wait();
+  if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_MU + n);
+  extern __shared__ double smd[];
+  const RowUnit u = units[blockIdx.x];
+  const int s = u.s;
+  const int L = c.counts[n];
+  const long long In = c.dims[s * c.N + n];
+  const int r0 = u.r0;
+  const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
+  double sl2[2];
+  mode_update_tile(c, n, redo, src, s, r0, smd, c.gc_w + (long long)(c.off + s) * c.gc_stride,
+                   sl2);
+  const double sumL = sl2[0], wc = sl2[1];
+  PhaseClock pc;
+  pc.start(c.dbg);
+  double* sc = smd;   // scratch reused (the tile is done)
   // sharded: the partials are all-reduced first; k_common folds them
   pc.mark(c.dbg, 7);
   tl_end(c.tl, TL_MU + n);
@@ -600,13 +624,8 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
 // ---------------------------------------------------------------------------
 // with_step = 0: the next mode's step matrix is left to k_step, which the 3-way
 // path runs concurrently with the next MTTKRP (they share no inputs)
-__global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int with_step) {
-  griddep_wait();
-  if (stopped(c, redo)) return;
-  tl_begin(c.tl, TL_FIN + n);
-  extern __shared__ double smd[];
-  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
-  const int s = blockIdx.x;
+static __device__ __noinline__ void finalize_block(const Ctx& c, int n, int s, int with_step,
+                                                   const BlockSmem& sm) {
   const int N = c.N;
   const int R = c.R[s];
   const int L = c.counts[n];
@@ -666,7 +685,79 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
     final_quantities(c, s, sm);
     pc.mark(c.dbg, 3);
   }
+}
+
+__global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int with_step) {
+  griddep_wait();
+  if (stopped(c, redo)) return;
+  tl_begin(c.tl, TL_FIN + n);
+  extern __shared__ double smd[];
+  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  finalize_block(c, n, blockIdx.x, with_step, sm);
   tl_end(c.tl, TL_FIN + n);
+}
+
+// ---------------------------------------------------------------------------
+// The whole mode-n update of a single-GPU solve with S <= 16 blocks as ONE
+// thread-block cluster (one CTA per block, cluster rank = block):
+//   phase A: every row tile of the block (mode_update_tile), the
+//            common-gradient partial kept in this CTA's shared memory;
+//   cluster barrier;
+//   phase B: CTA s folds rows [s I_n / S, (s+1) I_n / S) of the common
+//            columns, reading every block's partial through distributed
+//            shared memory in block order (solver.py:444-451, the same fma
+//            order as common_fold) into cnew;
+//   cluster barrier (release / acquire at cluster scope orders cnew);
+//   phase C: the block's finalize (prev <- curr, curr <- [cnew | new],
+//            gram / cross-gram refresh, next step matrix + lambda_max or the
+//            evaluation quantities).
+// Replaces k_mode_update + k_finalize (two launches, the atomic last-CTA
+// fold and a launch gap per mode).  Dynamic shared memory: the partial
+// (I_n x L doubles) then the larger of the tile scratch and BlockSmem.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mode_cluster(Ctx c, int n, int redo, int src,
+                                                       int with_step, int scratch_off) {
+  griddep_wait();
+  if (stopped(c, redo)) return;   // uniform over the cluster (device flag)
+  tl_begin(c.tl, TL_MU + n);
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double smd[];
+  const int s = (int)cl.block_rank();
+  const int N = c.N;
+  const int L = c.counts[n];
+  const long long In = c.dims[s * N + n];
+  double* gpart = smd;                       // In x L
+  double* scratch = smd + scratch_off;
+  double sl2[2] = {0.0, 0.0};
+  for (long long r0 = 0; r0 < In; r0 += MU_ROWS)
+    mode_update_tile(c, n, redo, src, s, (int)r0, scratch, gpart, sl2);
+  const double sumL = sl2[0], wc = sl2[1];
+  cl.sync();
+  if (L > 0) {
+    const int S = c.S;
+    const long long lo = (long long)s * In / S, hi = (long long)(s + 1) * In / S;
+    const int R0 = c.R[0];
+    const double* U0c = c.U[n];
+    const double* U0p = c.Up[n];
+    for (long long e = lo * L + threadIdx.x; e < hi * L; e += blockDim.x) {
+      const long long i = e / L;
+      const int l = (int)(e - i * L);
+      double acc = 0.0;
+      for (int q = 0; q < S; ++q) {
+        if (!(c.lip[lu_idx(c, n, q)] > 0.0)) continue;
+        const double* rp = cl.map_shared_rank(gpart, q);
+        acc += rp[e];
+      }
+      const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
+      const double chat = cc + wc * (cc - cp);
+      c.cnew[e] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
+    }
+  }
+  cl.sync();
+  tl_end(c.tl, TL_MU + n);
+  const BlockSmem sm = carve(scratch, c.rmax, c.rmax);
+  finalize_block(c, n, s, with_step, sm);
 }
 
 // evaluation algebra of the 3-way full path, run beside the fiber pass:
@@ -856,6 +947,7 @@ constexpr int QRC_PAIRS = 64;
 constexpr int QRC_A = 8;      // core rows a per CTA
 constexpr int QRC_CT = 8;     // max columns per thread (K2 <= 128)
 
+template <int CT>
 __global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
   griddep_wait();
   if (stopped(c, redo)) return;
@@ -912,18 +1004,18 @@ __global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
       pa[u] = pp / K1;
       pb[u] = pp - pa[u] * K1;
     }
-    double acc[4][QRC_CT];
+    double acc[4][CT];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < QRC_CT; ++v) acc[u][v] = 0.0;
+      for (int v = 0; v < CT; ++v) acc[u][v] = 0.0;
     for (int q = 0; q < Cc; ++q) {
       const double wv = wq[q];
       double P[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) P[u] = wv * R0T[q * QRC_A + pa[u]] * R1T[q * K1 + pb[u]];
 #pragma unroll
-      for (int v = 0; v < QRC_CT; ++v) {
+      for (int v = 0; v < CT; ++v) {
         const int cc = col + 16 * v;
         const double r2 = cc < K2 ? R2T[q * K2 + cc] : 0.0;
 #pragma unroll
@@ -933,7 +1025,7 @@ __global__ void __launch_bounds__(256) k_qr_core3(Ctx c, int redo) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < QRC_CT; ++v)
+      for (int v = 0; v < CT; ++v)
         if (pv[u]) ssq = fma(acc[u][v], acc[u][v], ssq);
   }
   ssq = block_sum(ssq, red);
