@@ -76,6 +76,7 @@ struct cb_solver {
   bool cluster = false;       // mode update + finalize as one cluster launch
   size_t cl_smem = 0;
   int cl_off = 0;             // doubles of the common-gradient partial
+  int cl_rows = MU_ROWS;      // rows per phase-A tile of the cluster kernel
   bool qr_core3 = false;      // 3-way GEMM-form ||core||^2 (k_qr_core3)
   int qrc_ct = 8;             // its columns per thread
   std::vector<double*> h_U;     // device pointer tables mirrored on host
@@ -307,7 +308,8 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       // the whole mode update in one cluster launch (k_mode_cluster)
       if (emit(h)) {
         CB_CUDA(launch_cluster(k_mode_cluster, dim3(h->S), dim3(256), h->cl_smem, st,
-                               (unsigned)h->S, h->ctx, n, redo, src, split ? 0 : 1, h->cl_off));
+                               (unsigned)h->S, h->ctx, n, redo, src, split ? 0 : 1, h->cl_off,
+                               h->cl_rows));
         count_launch(1);
         CB_CHECK_LAUNCH();
       }
@@ -1076,7 +1078,22 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     for (int n = 0; n < N; ++n)
       for (int s2 = 0; s2 < S; ++s2) part = std::max(part, h->dims[s2 * N + n] * h->counts[n]);
     h->cl_off = (int)((part + 1) & ~1LL);
-    h->cl_smem = sizeof(double) * (size_t)h->cl_off + std::max(h->mu_smem, h->blk_smem);
+    // phase-A tile: every row of a block at once where shared memory allows
+    long long imax = 1;
+    for (long long d : h->dims) imax = std::max(imax, d);
+    const int rtm = std::max(h->rtmax, 1);
+    auto tile_smem = [&](long long tr) {
+      return sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)tr * h->rmax +
+                               (h->lra ? (size_t)rtm * h->rmax : 0) + 16 +
+                               (h->lra && N == 3 ? 2 * (size_t)rtm * h->rmax + (size_t)tr * rtm + rtm : 0) +
+                               4 * (size_t)tr * h->rmax);
+    };
+    long long tr = std::min<long long>(imax, 512);
+    while (tr > MU_ROWS && sizeof(double) * (size_t)h->cl_off +
+                               std::max(tile_smem(tr), h->blk_smem) > 200 * 1024)
+      tr = (tr + 1) / 2;
+    h->cl_rows = (int)std::max<long long>(tr, MU_ROWS);
+    h->cl_smem = sizeof(double) * (size_t)h->cl_off + std::max(tile_smem(h->cl_rows), h->blk_smem);
     bool ok = h->cl_smem <= 200 * 1024;
     if (ok && S > 8)
       ok = cudaFuncSetAttribute(k_mode_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==

@@ -409,17 +409,17 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
 // through sc_out (valid on every thread).
 static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int redo, int src, int s,
                                                      int r0, double* smd, double* gcp,
-                                                     double* sc_out) {
+                                                     double* sc_out, int TR = MU_ROWS) {
   const int R = c.R[s];
   const int N = c.N;
   const int L = c.counts[n];
   const long long In = c.dims[s * N + n];
-  const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
+  const int rows = (int)(In - r0 < TR ? In - r0 : TR);
   const double w_hat = redo ? 0.0 : c.st->w_hat;
   double* step = smd;                       // R*R
   double* uh = step + R * R;                // MU_ROWS*R
-  double* mt = uh + MU_ROWS * R;            // MU_ROWS*R
-  double* P = mt + MU_ROWS * R;             // Rt*R (lra)
+  double* mt = uh + TR * R;            // MU_ROWS*R
+  double* P = mt + TR * R;             // Rt*R (lra)
   double* sc = P + (c.lra ? c.Rt[s] * R : 0);  // scalars
   const double* lam = c.LAM[s];
   if (threadIdx.x == 0) {
@@ -439,12 +439,12 @@ static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int re
   const bool lra3 = src == 2 && N == 3;
   double* Cs = sc + 8;                       // 2 x Rt*R (lra3)
   double* Uts = Cs + (lra3 ? 2 * c.Rt[s] * R : 0);   // rows x Rt
-  double* tws = Uts + (lra3 ? MU_ROWS * c.Rt[s] : 0); // Rt
+  double* tws = Uts + (lra3 ? TR * c.Rt[s] : 0); // Rt
   // this tile's current / previous rows (and block 0's common columns)
   double* Ucs = tws + (lra3 ? c.Rt[s] : 0);            // rows x R
-  double* Ups = Ucs + MU_ROWS * R;                      // rows x R
-  double* U0s = Ups + MU_ROWS * R;                      // rows x R0 (L > 0)
-  double* U0ps = U0s + MU_ROWS * c.R[0];                // rows x R0 (L > 0)
+  double* Ups = Ucs + TR * R;                      // rows x R
+  double* U0s = Ups + TR * R;                      // rows x R0 (L > 0)
+  double* U0ps = U0s + TR * c.R[0];                // rows x R0 (L > 0)
   stage_async(Ucs, c.U[s * N + n] + (long long)r0 * R, (long long)rows * R);
   stage_async(Ups, c.Up[s * N + n] + (long long)r0 * R, (long long)rows * R);
   if (L > 0) {
@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
 // (I_n x L doubles) then the larger of the tile scratch and BlockSmem.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_mode_cluster(Ctx c, int n, int redo, int src,
-                                                       int with_step, int scratch_off) {
+                                                       int with_step, int scratch_off, int TR) {
   griddep_wait();
   if (stopped(c, redo)) return;   // uniform over the cluster (device flag)
   tl_begin(c.tl, TL_MU + n);
@@ -730,8 +730,8 @@ __global__ void __launch_bounds__(256) k_mode_cluster(Ctx c, int n, int redo, in
   double* gpart = smd;                       // In x L
   double* scratch = smd + scratch_off;
   double sl2[2] = {0.0, 0.0};
-  for (long long r0 = 0; r0 < In; r0 += MU_ROWS)
-    mode_update_tile(c, n, redo, src, s, (int)r0, scratch, gpart, sl2);
+  for (long long r0 = 0; r0 < In; r0 += TR)
+    mode_update_tile(c, n, redo, src, s, (int)r0, scratch, gpart, sl2, TR);
   const double sumL = sl2[0], wc = sl2[1];
   cl.sync();
   if (L > 0) {
