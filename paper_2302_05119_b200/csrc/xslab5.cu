@@ -97,6 +97,44 @@ __device__ __forceinline__ void sl5_tma(void* dst, const void* tmap, int c0, int
       : "memory");
 }
 
+// The CTA's share of the tiles of the ACTIVE blocks (ALS: converged blocks
+// drop out): tiles are numbered over active blocks only and split evenly
+// over the grid, so the last sweeps (few blocks left) still use every SM.
+// Every role of a CTA walks the same sequence.
+struct ActTiles {
+  int s;            // current block
+  long long t;      // tile within the block
+  long long left;   // tiles left for this CTA
+};
+
+template <typename NT>
+__device__ __forceinline__ ActTiles act_tiles_begin(const int* active, int S, NT ntiles) {
+  long long A = 0;
+  for (int s = 0; s < S; ++s)
+    if (!active || active[s]) A += ntiles(s);
+  const long long G = gridDim.x;
+  const long long q0 = (long long)blockIdx.x * A / G, q1 = (long long)(blockIdx.x + 1) * A / G;
+  ActTiles it{0, 0, q1 - q0};
+  long long off = 0;
+  for (; it.s < S; ++it.s) {
+    if (active && !active[it.s]) continue;
+    const long long n = ntiles(it.s);
+    if (q0 < off + n) break;
+    off += n;
+  }
+  it.t = q0 - off;
+  return it;
+}
+
+template <typename NT>
+__device__ __forceinline__ void act_tiles_next(ActTiles& it, const int* active, int S, NT ntiles) {
+  --it.left;
+  if (++it.t >= ntiles(it.s)) {
+    it.t = 0;
+    do { ++it.s; } while (it.s < S && active && !active[it.s]);
+  }
+}
+
 constexpr int TG_M = 128;                      // j per tile
 constexpr int TG_KC = 32;                      // i2 rows per box
 constexpr int TG_BOX = TG_M * TG_KC * 4;       // 16 KB
@@ -113,6 +151,7 @@ struct TgArgs {
   void* const* T1;
   const int* tsel;
   int t_other;
+  int S;
 };
 
 template <int RB>
@@ -127,10 +166,10 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_tg_pass(TgArgs a) {
   uint64_t* empty = full + TG_NST;
   double* a2s = reinterpret_cast<double*>(empty + TG_NST + 2);   // [I2pad][RB]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
-  const int t_begin = (int)((long long)blockIdx.x * a.ntiles / G);
-  const int t_end = (int)((long long)(blockIdx.x + 1) * a.ntiles / G);
   const int sel = (a.tsel ? *a.tsel : 0) ^ a.t_other;
+  auto ntl = [&](int s) -> long long {
+    return (a.blk[s].I0 * a.blk[s].I1 + TG_M - 1) / TG_M;
+  };
   if (threadIdx.x == 0) {
     for (int i = 0; i < TG_NST; ++i) {
       mbar_init(&full[i], 1);
@@ -142,9 +181,9 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_tg_pass(TgArgs a) {
   if (warp == SL5_CONS / 32) {
     if (lane == 0) {
       int st = 0, ph = 0;
-      for (int q = t_begin; q < t_end; ++q) {
-        const Sl5Tile tt = a.tiles[q];
-        if (a.active && !a.active[tt.s]) continue;
+      for (ActTiles it = act_tiles_begin(a.active, a.S, ntl); it.left > 0;
+           act_tiles_next(it, a.active, a.S, ntl)) {
+        const Sl5Tile tt{it.s, (int)it.t};
         const int nch = (int)((a.blk[tt.s].I2 + TG_KC - 1) / TG_KC);
         const CUtensorMap* tm = a.tmaps + tt.s;
         for (int c = 0; c < nch; ++c) {
@@ -160,9 +199,9 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_tg_pass(TgArgs a) {
   const int jg = lane;                         // j = 4 jg .. 4 jg + 3 of the tile
   const int cg = warp;                         // columns [cg CG, (cg + 1) CG)
   int st = 0, ph = 0, cur = -1;
-  for (int q = t_begin; q < t_end; ++q) {
-    const Sl5Tile tt = a.tiles[q];
-    if (a.active && !a.active[tt.s]) continue;
+  for (ActTiles it = act_tiles_begin(a.active, a.S, ntl); it.left > 0;
+       act_tiles_next(it, a.active, a.S, ntl)) {
+    const Sl5Tile tt{it.s, (int)it.t};
     const Sl5Block& b = a.blk[tt.s];
     const int nch = (int)((b.I2 + TG_KC - 1) / TG_KC);
     const int R = b.R;
@@ -235,9 +274,7 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_sl5_dpass(Sl5Args a) {
   uint64_t* empty = full + SL5_NST;
   double* a0s = reinterpret_cast<double*>(empty + SL5_NST + 2);   // [I0 + pad][RB]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
-  const int t_begin = (int)((long long)blockIdx.x * a.ntiles / G);
-  const int t_end = (int)((long long)(blockIdx.x + 1) * a.ntiles / G);
+  auto ntl = [&](int s) -> long long { return a.blk[s].ntiles; };
   if (threadIdx.x == 0) {
     for (int i = 0; i < SL5_NST; ++i) {
       mbar_init(&full[i], 1);
@@ -250,9 +287,9 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_sl5_dpass(Sl5Args a) {
     // ------------------------------------------------------- producer lane
     if (lane == 0) {
       int st = 0, ph = 0;
-      for (int q = t_begin; q < t_end; ++q) {
-        const Sl5Tile tt = a.tiles[q];
-        if (a.active && !a.active[tt.s]) continue;
+      for (ActTiles it = act_tiles_begin(a.active, a.S, ntl); it.left > 0;
+           act_tiles_next(it, a.active, a.S, ntl)) {
+        const Sl5Tile tt{it.s, (int)it.t};
         const int nch = a.blk[tt.s].nch;
         const CUtensorMap* tm = a.tmaps + tt.s;
         for (int c = 0; c < nch; ++c) {
@@ -269,9 +306,9 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_sl5_dpass(Sl5Args a) {
   const int rg = threadIdx.x & 63;             // rows rg, rg + 64 of the tile
   const int cg = threadIdx.x >> 6;             // columns [cg CG, (cg + 1) CG)
   int st = 0, ph = 0, cur = -1;
-  for (int q = t_begin; q < t_end; ++q) {
-    const Sl5Tile tt = a.tiles[q];
-    if (a.active && !a.active[tt.s]) continue;
+  for (ActTiles it = act_tiles_begin(a.active, a.S, ntl); it.left > 0;
+       act_tiles_next(it, a.active, a.S, ntl)) {
+    const Sl5Tile tt{it.s, (int)it.t};
     const Sl5Block& b = a.blk[tt.s];
     const int nch = b.nch;
     const int R = b.R;
@@ -554,6 +591,7 @@ int sl5_tpass(Sl5Plan* p, const double* const* U_dev, const int* active, void* c
   a.T1 = T1;
   a.tsel = tsel;
   a.t_other = t_other;
+  a.S = p->S;
   switch (p->tg_rb) {
     case 16: CB_CUDA(launch_k(k_tg_pass<16>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
     case 24: CB_CUDA(launch_k(k_tg_pass<24>, dim3(p->tg_grid), dim3(SL5_THREADS), p->tg_smem, st, a)); break;
