@@ -73,10 +73,6 @@ struct cb_solver {
   State* h_state = nullptr;     // pinned mirror
   size_t blk_smem = 0, mu_smem = 0, qr_smem = 0, qrc_smem = 0;
   int qr_ch = 32;             // TSQR chunk rows (k_qr_factor)
-  bool cluster = false;       // mode update + finalize as one cluster launch
-  size_t cl_smem = 0;
-  int cl_off = 0;             // doubles of the common-gradient partial
-  int cl_rows = MU_ROWS;      // rows per phase-A tile of the cluster kernel
   bool qr_core3 = false;      // 3-way GEMM-form ||core||^2 (k_qr_core3)
   int qrc_ct = 8;             // its columns per thread
   std::vector<double*> h_U;     // device pointer tables mirrored on host
@@ -304,17 +300,6 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       prof(h, "generic_mttkrp");
     }
     const bool split = par && n + 1 < h->N;
-    if (h->cluster) {
-      // the whole mode update in one cluster launch (k_mode_cluster)
-      if (emit(h)) {
-        CB_CUDA(launch_cluster(k_mode_cluster, dim3(h->S), dim3(256), h->cl_smem, st,
-                               (unsigned)h->S, h->ctx, n, redo, src, split ? 0 : 1, h->cl_off,
-                               h->cl_rows));
-        count_launch(1);
-        CB_CHECK_LAUNCH();
-      }
-      prof(h, redo ? "redo:mode_cluster" : "mode_cluster");
-    } else {
     if (emit(h)) {
       launch_k(k_mode_update, dim3(h->n_rows[n]), dim3(256), h->mu_smem, st, h->ctx, n, redo, src, h->d_rows[n]);
       count_launch(1);
@@ -337,7 +322,6 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       CB_CHECK_LAUNCH();
     }
     prof(h, redo ? "redo:finalize" : "finalize");
-    }
     if (split) {
       if ((rc = fork_side(h))) return rc;
       if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
@@ -1071,55 +1055,6 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
-  // one cluster per mode update: single GPU, S <= 16, the partial and the
-  // scratch within shared memory, and a cluster of S CTAs schedulable
-  if (!shard && S <= 16) {
-    long long part = 0;
-    for (int n = 0; n < N; ++n)
-      for (int s2 = 0; s2 < S; ++s2) part = std::max(part, h->dims[s2 * N + n] * h->counts[n]);
-    h->cl_off = (int)((part + 1) & ~1LL);
-    // phase-A tile: every row of a block at once where shared memory allows
-    long long imax = 1;
-    for (long long d : h->dims) imax = std::max(imax, d);
-    const int rtm = std::max(h->rtmax, 1);
-    auto tile_smem = [&](long long tr) {
-      return sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)tr * h->rmax +
-                               (h->lra ? (size_t)rtm * h->rmax : 0) + 16 +
-                               (h->lra && N == 3 ? 2 * (size_t)rtm * h->rmax + (size_t)tr * rtm + rtm : 0) +
-                               4 * (size_t)tr * h->rmax);
-    };
-    long long tr = std::min<long long>(imax, 512);
-    while (tr > MU_ROWS && sizeof(double) * (size_t)h->cl_off +
-                               std::max(tile_smem(tr), h->blk_smem) > 200 * 1024)
-      tr = (tr + 1) / 2;
-    h->cl_rows = (int)std::max<long long>(tr, MU_ROWS);
-    h->cl_smem = sizeof(double) * (size_t)h->cl_off + std::max(tile_smem(h->cl_rows), h->blk_smem);
-    bool ok = h->cl_smem <= 200 * 1024;
-    if (ok && S > 8)
-      ok = cudaFuncSetAttribute(k_mode_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-           cudaSuccess;
-    if (ok)
-      ok = cudaFuncSetAttribute(k_mode_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)h->cl_smem) == cudaSuccess;
-    if (ok) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(S);
-      cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = h->cl_smem;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = S;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int nclusters = 0;
-      ok = cudaOccupancyMaxActiveClusters(&nclusters, k_mode_cluster, &cfg) == cudaSuccess &&
-           nclusters >= 1;
-    }
-    cudaGetLastError();
-    h->cluster = ok;
-  }
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));

@@ -7,8 +7,6 @@
 // whole iteration (including the restart branch) can be enqueued or captured
 // in a CUDA graph without a host round trip.
 #pragma once
-#include <cooperative_groups.h>
-
 #include "engine.h"
 #include "../../include/concpd_b200.h"
 
@@ -404,7 +402,7 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
 // ---------------------------------------------------------------------------
 // One row tile [r0, r0 + MU_ROWS) of block s: extrapolate, gradient, project
 // the individual columns into Un, and the common-gradient partial into gcp
-// (row-major I_n x L; global slots or a cluster CTA's shared memory).
+// (row-major I_n x L, this block's global slot).
 // `smd` is the tile's shared scratch; returns the tile's (sumL, w_common)
 // through sc_out (valid on every thread).
 static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int redo, int src, int s,
@@ -695,69 +693,6 @@ __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int wi
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
   finalize_block(c, n, blockIdx.x, with_step, sm);
   tl_end(c.tl, TL_FIN + n);
-}
-
-// ---------------------------------------------------------------------------
-// The whole mode-n update of a single-GPU solve with S <= 16 blocks as ONE
-// thread-block cluster (one CTA per block, cluster rank = block):
-//   phase A: every row tile of the block (mode_update_tile), the
-//            common-gradient partial kept in this CTA's shared memory;
-//   cluster barrier;
-//   phase B: CTA s folds rows [s I_n / S, (s+1) I_n / S) of the common
-//            columns, reading every block's partial through distributed
-//            shared memory in block order (solver.py:444-451, the same fma
-//            order as common_fold) into cnew;
-//   cluster barrier (release / acquire at cluster scope orders cnew);
-//   phase C: the block's finalize (prev <- curr, curr <- [cnew | new],
-//            gram / cross-gram refresh, next step matrix + lambda_max or the
-//            evaluation quantities).
-// Replaces k_mode_update + k_finalize (two launches, the atomic last-CTA
-// fold and a launch gap per mode).  Dynamic shared memory: the partial
-// (I_n x L doubles) then the larger of the tile scratch and BlockSmem.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_mode_cluster(Ctx c, int n, int redo, int src,
-                                                       int with_step, int scratch_off, int TR) {
-  griddep_wait();
-  if (stopped(c, redo)) return;   // uniform over the cluster (device flag)
-  tl_begin(c.tl, TL_MU + n);
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ double smd[];
-  const int s = (int)cl.block_rank();
-  const int N = c.N;
-  const int L = c.counts[n];
-  const long long In = c.dims[s * N + n];
-  double* gpart = smd;                       // In x L
-  double* scratch = smd + scratch_off;
-  double sl2[2] = {0.0, 0.0};
-  for (long long r0 = 0; r0 < In; r0 += TR)
-    mode_update_tile(c, n, redo, src, s, (int)r0, scratch, gpart, sl2, TR);
-  const double sumL = sl2[0], wc = sl2[1];
-  cl.sync();
-  if (L > 0) {
-    const int S = c.S;
-    const long long lo = (long long)s * In / S, hi = (long long)(s + 1) * In / S;
-    const int R0 = c.R[0];
-    const double* U0c = c.U[n];
-    const double* U0p = c.Up[n];
-    for (long long e = lo * L + threadIdx.x; e < hi * L; e += blockDim.x) {
-      const long long i = e / L;
-      const int l = (int)(e - i * L);
-      double acc = 0.0;
-      for (int q = 0; q < S; ++q) {
-        if (!(c.lip[lu_idx(c, n, q)] > 0.0)) continue;
-        const double* rp = cl.map_shared_rank(gpart, q);
-        acc += rp[e];
-      }
-      const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
-      const double chat = cc + wc * (cc - cp);
-      c.cnew[e] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
-    }
-  }
-  cl.sync();
-  tl_end(c.tl, TL_MU + n);
-  const BlockSmem sm = carve(scratch, c.rmax, c.rmax);
-  finalize_block(c, n, s, with_step, sm);
 }
 
 // evaluation algebra of the 3-way full path, run beside the fiber pass:
