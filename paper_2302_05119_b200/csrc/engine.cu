@@ -1321,6 +1321,7 @@ int cb_solver_timeline(cb_solver* h, int op, unsigned long long* out, int cap) {
     h->allocs.push_back(h->ctx.tl);
     h->xa_main.tl = h->ctx.tl;
     h->xa_redo.tl = h->ctx.tl;
+    xtc_set_timeline(h->xtc, h->ctx.tl);
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }   // recapture
     if (h->gexec_pipe) { cudaGraphExecDestroy(h->gexec_pipe); h->gexec_pipe = nullptr; }
   }
@@ -1328,6 +1329,7 @@ int cb_solver_timeline(cb_solver* h, int op, unsigned long long* out, int cap) {
     h->ctx.tl = nullptr;
     h->xa_main.tl = nullptr;
     h->xa_redo.tl = nullptr;
+    xtc_set_timeline(h->xtc, nullptr);
     // both iteration graphs captured the timeline pointer: recapture them
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
     if (h->gexec_pipe) { cudaGraphExecDestroy(h->gexec_pipe); h->gexec_pipe = nullptr; }

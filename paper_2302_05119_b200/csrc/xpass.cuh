@@ -102,7 +102,8 @@ __device__ __forceinline__ void tl_end(unsigned long long* tl, int slot) {
 }
 enum TlSlot {
   TL_SWEEP = 0, TL_C0 = 1, TL_C1 = 2, TL_SLAB = 3, TL_FIBER = 4, TL_MU = 5, TL_FIN = 8,
-  TL_STEP = 11, TL_CONTROL = 14, TL_COMMON = 15, TL_QR = 18, TL_RESTORE = 20, TL_NSLOT = 24
+  TL_STEP = 11, TL_CONTROL = 14, TL_COMMON = 15, TL_QR = 18, TL_RESTORE = 20, TL_TRACE = 21,
+  TL_PREP = 22, TL_NSLOT = 24
 };
 
 __device__ __forceinline__ bool gated(const XArgs& a) {

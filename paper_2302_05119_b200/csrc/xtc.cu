@@ -117,6 +117,7 @@ struct XtcArgs {
   const int* active;      // per-block activity (ALS) or null
   double* bsum;           // [s][RSTRIDE]
   const int* gate;
+  unsigned long long* tl; // iteration timeline (profiling) or null
 };
 
 struct XtcPlan {
@@ -133,6 +134,7 @@ struct XtcPlan {
   double* part = nullptr;
   int* cnt = nullptr;
   unsigned int* maxbits = nullptr;
+  unsigned long long* tl = nullptr;   // iteration timeline (profiling)
 };
 
 // --------------------------------------------------------------------------
@@ -164,6 +166,7 @@ template <int N>
 __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const* U) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
+  tl_begin(a.tl, TL_PREP);
   const int s = blockIdx.x;
   const XtcBlock b = a.blk[s];
   const double* A0 = U[3 * s];
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     const long long r = e / I2, i = e - r * I2;
     b.ut2[e] = (float)A2[i * R + r];
   }
+  tl_end(a.tl, TL_PREP);
 }
 
 // --------------------------------------------------------------------------
@@ -299,6 +303,7 @@ template <int N>
 __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
+  tl_begin(a.tl, TL_TRACE);
   constexpr int EG = xtc_eg<N>();    // epilogue groups
   constexpr int NH = N / EG;         // columns per epilogue group
   constexpr int NE = 128 * EG;       // epilogue threads
@@ -711,6 +716,7 @@ done:
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  tl_end(a.tl, TL_TRACE);
 }
 
 // --------------------------------------------------------------------------
@@ -908,6 +914,10 @@ void xtc_set_grid_cap(XtcPlan* p, int cap) {
   if (p) p->grid_cap = cap;
 }
 
+void xtc_set_timeline(XtcPlan* p, unsigned long long* tl) {
+  if (p) p->tl = tl;
+}
+
 template <int N>
 static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStream_t st,
                   int parts = 3) {
@@ -930,7 +940,7 @@ static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStre
 // pass only (reads only the prepared operands), 3 = both
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
               cudaStream_t st, int parts) {
-  XtcArgs a;
+  XtcArgs a{};
   a.tmaps = p->tmaps;
   a.blk = p->blk;
   a.units = p->units;
@@ -943,6 +953,7 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.cnt = p->cnt;
   a.bsum = bsum;
   a.gate = gate;
+  a.tl = p->tl;
   a.mode2 = 0;
   a.m2part = nullptr;
   a.active = nullptr;
@@ -960,7 +971,7 @@ int xtc_mode2(XtcPlan* p, const double* const* U_dev, const int* active, double*
     set_error("xtc plan was not created for the mode-2 MTTKRP");
     return CB_ERR_STATE;
   }
-  XtcArgs a;
+  XtcArgs a{};
   memset(&a, 0, sizeof(a));
   a.tmaps = p->tmaps;
   a.blk = p->blk;

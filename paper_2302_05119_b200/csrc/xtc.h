@@ -42,6 +42,8 @@ int xtc_mode2(XtcPlan* p, const double* const* U_dev, const int* active, double*
 // cap the streaming kernel's persistent grid (0: one CTA per SM), leaving
 // SMs to work that runs beside it (the pipelined lra sweep)
 void xtc_set_grid_cap(XtcPlan* p, int cap);
+// per-launch timeline slots (TL_TRACE, TL_PREP) of the solver's profiling mode
+void xtc_set_timeline(XtcPlan* p, unsigned long long* tl);
 
 // algorithmic bytes streamed per xtc_trace call (sum_s |X_s| * 4)
 double xtc_bytes(const XtcPlan* p);

@@ -18,12 +18,14 @@ import torch
 import paper_2302_05119_b200 as P
 from paper_2302_05119_b200 import _lib as L
 from paper_2302_05119_b200.configs import CONFIGS, generate_config
+from paper_2302_05119_b200.synth import generate_config_device
 from paper_2302_05119_b200.solver import PreparedSolve
 
 NAMES = {0: "sweep_begin", 1: "contract0", 2: "contract1", 3: "slab", 4: "fiber",
          5: "mode_update0", 6: "mode_update1", 7: "mode_update2", 8: "finalize0",
          9: "finalize1", 10: "finalize2", 11: "step1", 12: "step2", 14: "control",
-         15: "common0", 16: "common1", 17: "common2", 18: "qr", 20: "restore"}
+         15: "common0", 16: "common1", 17: "common2", 18: "qr", 20: "restore", 21: "trace",
+         22: "trace_prep"}
 NSLOT = 24
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
@@ -31,9 +33,8 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 flush_on = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 spec = CONFIGS[name]
 nblk = int(os.environ.get("TL_BLOCKS", "0"))
-tensors, _ = generate_config(name, blocks=range(nblk) if nblk else None)
-prob = P.CoupledProblem([np.asarray(t, dtype=float) for t in tensors], spec.rank,
-                        list(spec.coupled), mode=spec.mode)
+tensors, _ = generate_config_device(name, blocks=range(nblk) if nblk else None)
+prob = P.CoupledProblem(tensors, spec.rank, list(spec.coupled), mode=spec.mode)
 run = PreparedSolve(prob, P.SolverOptions(max_iter=iters + 20, tol=float(np.nextafter(0, 1)),
                                           precision=spec.dtype))
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
