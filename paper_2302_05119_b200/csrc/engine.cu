@@ -72,6 +72,7 @@ struct cb_solver {
   State* d_state = nullptr;
   State* h_state = nullptr;     // pinned mirror
   size_t blk_smem = 0, mu_smem = 0, qr_smem = 0, qrc_smem = 0;
+  size_t blk_smem_ng = 0;      // per-block kernels without gram staging
   int qr_ch = 32;             // TSQR chunk rows (k_qr_factor)
   bool qr_core3 = false;      // 3-way GEMM-form ||core||^2 (k_qr_core3)
   int qrc_ct = 8;             // its columns per thread
@@ -166,6 +167,25 @@ static int xchg_lip(cb_solver* h, int n) {
 }
 static int xchg_gc(cb_solver* h, int n) {
   if (!h->shard || h->counts[n] == 0) return CB_OK;
+  // equal shards over NCCL: an all-gather of each rank's own contiguous
+  // slot range (half the traffic of the all-reduce with zero foreign slots,
+  // same result); otherwise the all-reduce
+  if (h->comm && h->S_tot == h->S * h->world) {
+    if (emit(h)) {
+      const bool split = h->in_body && h->cond_capture;
+      int rc;
+      if (split && (rc = end_cond_body(h))) return rc;
+      const long long cnt = (long long)h->S * h->ctx.gc_stride;
+      NcclApi& api = nccl_api();
+      ncclResult_t r = api.ncclAllGather(h->ctx.gc_w + (long long)h->off * h->ctx.gc_stride,
+                                         h->ctx.gc_part, (size_t)cnt, ncclFloat64,
+                                         (ncclComm_t)h->comm, h->st);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+      if (split && (rc = begin_cond_body(h))) return rc;
+    }
+    h->seg_cur += 1;
+    return CB_OK;
+  }
   return xchg(h, h->ctx.gc_w, h->ctx.gc_part, (long long)h->S_tot * h->ctx.gc_stride);
 }
 
@@ -278,7 +298,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
     if ((rc = enqueue_mttkrp3(h, 0, xa, redo, h->st2))) return rc;
   }
   if (emit(h)) {
-    launch_k(k_sweep_begin, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, redo);
+    launch_k(k_sweep_begin, dim3(h->S), dim3(256), h->blk_smem_ng, st, h->ctx, redo);
     count_launch(1);
     CB_CHECK_LAUNCH();
   }
@@ -326,7 +346,7 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       if ((rc = fork_side(h))) return rc;
       if ((rc = enqueue_mttkrp3(h, n + 1, xa, redo, h->st2))) return rc;
       if (emit(h)) {
-        launch_k(k_step, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, n + 1, redo);
+        launch_k(k_step, dim3(h->S), dim3(256), h->blk_smem_ng, st, h->ctx, n + 1, redo);
         count_launch(1);
         CB_CHECK_LAUNCH();
       }
@@ -408,7 +428,7 @@ static int enqueue_eval_full(cb_solver* h, int redo) {
     const bool par = !h->in_body;
     if (par && (rc = fork_side(h))) return rc;
     if (emit(h)) {
-      launch_k(k_eval_side, dim3(h->S), dim3(256), h->blk_smem, par ? h->st2 : h->st, h->ctx, redo);
+      launch_k(k_eval_side, dim3(h->S), dim3(256), h->blk_smem_ng, par ? h->st2 : h->st, h->ctx, redo);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
@@ -1034,6 +1054,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   }
   // ---- shared memory sizes
   h->blk_smem = block_smem_bytes(c.rmax, c.rmax);
+  h->blk_smem_ng = block_smem_bytes(c.rmax, 0);
   int maxRt = std::max(h->rtmax, 1);
   h->mu_smem = sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)MU_ROWS * h->rmax +
                                  (h->lra ? (size_t)maxRt * h->rmax : 0) + 16);
@@ -1051,10 +1072,10 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     h->qr_smem = sizeof(double) * ((size_t)cmax * (cmax + 1) + (size_t)h->qr_ch * (cmax + 1) + cmax + 64);
   }
   CB_CUDA(cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
-  CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem_ng));
   CB_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
-  CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
-  CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
+  CB_CUDA(cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem_ng));
+  CB_CUDA(cudaFuncSetAttribute(k_eval_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem_ng));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
   CB_CUDA(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
   CB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));

@@ -44,12 +44,13 @@ __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
   b.red = b.vec + 128;
   b.gr = b.red + 40;
   b.gw = gw;
-  b.misc = b.gr + 2 * gram_rows(gw) * gw;
+  b.misc = b.gr + 4 * gram_rows(gw) * gw;
   return b;
 }
 
+// gram staging: two buffers (double buffering) of A and B chunks
 __host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
-  return sizeof(double) * ((size_t)lm_smem_doubles(rmax) + 2 * (size_t)gram_rows(gw) * gw + 4 * 64 + 8);
+  return sizeof(double) * ((size_t)lm_smem_doubles(rmax) + 4 * (size_t)gram_rows(gw) * gw + 4 * 64 + 8);
 }
 
 // out[P x Q] = A^T B with A rows x P, B rows x Q (row-major), whole block,
@@ -60,10 +61,11 @@ __host__ __device__ inline size_t block_smem_bytes(int rmax, int gw) {
 static __device__ __noinline__ void block_gram(const double* __restrict__ A, int P, const double* __restrict__ B,
                            int Q, long long rows, double* __restrict__ out, const BlockSmem& sm) {
   const int CH = gram_rows(sm.gw);
-  double* As = sm.gr;
-  // a gram of one matrix with itself reads one staged copy
+  // a gram of one matrix with itself reads one staged copy; chunk k + 1 is
+  // in flight while chunk k is multiplied (two buffers per operand)
   const bool same = (A == B) && (P == Q);
-  double* Bs = same ? As : sm.gr + CH * sm.gw;
+  auto bufA = [&](int b) { return sm.gr + (size_t)b * 2 * CH * sm.gw; };
+  auto bufB = [&](int b) { return same ? bufA(b) : sm.gr + ((size_t)b * 2 + 1) * CH * sm.gw; };
   // small grams (P Q <= 256): one output per thread (more parallel rows
   // chains); larger: 4 x 4 tiles
   const bool t1 = P * Q <= 256;
@@ -77,13 +79,24 @@ static __device__ __noinline__ void block_gram(const double* __restrict__ A, int
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-  for (long long c0 = 0; c0 < rows; c0 += CH) {
+  auto issue = [&](long long c0, int b) {
     const int nr = (int)(rows - c0 < CH ? rows - c0 : CH);
+    stage_async(bufA(b), A + c0 * P, (long long)nr * P);
+    if (!same) stage_async(bufB(b), B + c0 * Q, (long long)nr * Q);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  __syncthreads();                 // the buffers may still be read by a previous call
+  if (rows > 0) issue(0, 0);
+  int buf = 0;
+  for (long long c0 = 0; c0 < rows; c0 += CH, buf ^= 1) {
+    const int nr = (int)(rows - c0 < CH ? rows - c0 : CH);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // chunk c0 visible to all; every thread is done with the previous chunk,
+    // so its buffer takes the next one (in flight during this chunk's FMAs)
     __syncthreads();
-    stage_async(As, A + c0 * P, (long long)nr * P);
-    if (!same) stage_async(Bs, B + c0 * Q, (long long)nr * Q);
-    cp_async8_wait();
-    __syncthreads();
+    if (c0 + CH < rows) issue(c0 + CH, buf ^ 1);
+    const double* As = bufA(buf);
+    const double* Bs = bufB(buf);
     if (owner && t1) {
       double sacc = acc[0][0];
       for (int i = 0; i < nr; ++i) sacc = fma(As[i * P + p0], Bs[i * Q + q0], sacc);
@@ -275,7 +288,7 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_SWEEP);
   extern __shared__ double smd[];
-  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const BlockSmem sm = carve(smd, c.rmax, 0);   // no gram staging
   const int s = blockIdx.x;
   const int R = c.R[s];
   const int ld = lm_ld(R);
@@ -345,20 +358,23 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
 
 // sum over all blocks (global order) of the mode-n Lipschitz constants and of
 // their "previous" values (solver.py:422-425)
+// Called by a whole warp; lane 0 gets the sums.  The loads are issued by
+// all lanes at once, the adds stay sequential in block order on lane 0.
 __device__ inline void common_lip_sums(const Ctx& c, int n, double& sl, double& slp) {
+  const int lane = threadIdx.x & 31;
   sl = 0.0;
   slp = 0.0;
-  for (int q0 = 0; q0 < c.S_tot; q0 += 8) {
-    double a8[8], b8[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int q = q0 + k;
-      a8[k] = q < c.S_tot ? c.lip[lu_idx(c, n, q)] : 0.0;
-      b8[k] = q < c.S_tot ? c.lip[lup_idx(c, n, q)] : 0.0;
+  for (int q0 = 0; q0 < c.S_tot; q0 += 32) {
+    const int q = q0 + lane;
+    const double a = q < c.S_tot ? c.lip[lu_idx(c, n, q)] : 0.0;
+    const double b = q < c.S_tot ? c.lip[lup_idx(c, n, q)] : 0.0;
+    const int m = c.S_tot - q0 < 32 ? c.S_tot - q0 : 32;
+    for (int k = 0; k < m; ++k) {
+      const double ak = __shfl_sync(0xffffffffu, a, k);
+      const double bk = __shfl_sync(0xffffffffu, b, k);
+      sl += ak;
+      slp += bk;
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (q0 + k < c.S_tot) { sl += a8[k]; slp += b8[k]; }
   }
 }
 
@@ -373,22 +389,22 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
   for (int e = threadIdx.x; e < rows * L; e += blockDim.x) {
     const int il = e / L, l = e - il * L;
     const long long i = r0 + il;
-    // partials of the blocks with L_u > 0, added in block order; loads in
-    // batches of 8 issued before their adds (latency, not bandwidth, bound)
+    // partials of the blocks with L_u > 0, added in block order; 32 loads
+    // in flight before their adds (latency, not bandwidth, bound)
     double acc = 0.0;
     const double cc = U0c[i * R0 + l], cp = U0p[i * R0 + l];
-    for (int q0 = 0; q0 < c.S_tot; q0 += 8) {
-      double g8[8];
-      bool on[8];
+    for (int q0 = 0; q0 < c.S_tot; q0 += 32) {
+      double g32[32];
+      bool on[32];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < 32; ++k) {
         const int q = q0 + k;
         on[k] = q < c.S_tot && c.lip[lu_idx(c, n, q)] > 0.0;
-        g8[k] = q < c.S_tot ? __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]) : 0.0;
+        g32[k] = q < c.S_tot ? __ldcg(&c.gc_part[(long long)q * c.gc_stride + i * L + l]) : 0.0;
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (on[k]) acc += g8[k];
+      for (int k = 0; k < 32; ++k)
+        if (on[k]) acc += g32[k];
     }
     const double chat = cc + wc * (cc - cp);
     c.cnew[i * L + l] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
@@ -420,16 +436,18 @@ static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int re
   double* P = mt + TR * R;             // Rt*R (lra)
   double* sc = P + (c.lra ? c.Rt[s] * R : 0);  // scalars
   const double* lam = c.LAM[s];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double sl, slp;
     common_lip_sums(c, n, sl, slp);
-    sc[0] = sl;
-    sc[1] = extrap_weight(w_hat, slp, sl, c.delta_w);
-    // own block: the written copy (current even where mode n is uncoupled
-    // and nothing is exchanged)
-    const int g = c.off + s;
-    sc[2] = extrap_weight(w_hat, c.lip_w[lup_idx(c, n, g)], c.lip_w[lu_idx(c, n, g)], c.delta_w);
-    sc[3] = c.lip_w[lu_idx(c, n, g)];
+    if (threadIdx.x == 0) {
+      sc[0] = sl;
+      sc[1] = extrap_weight(w_hat, slp, sl, c.delta_w);
+      // own block: the written copy (current even where mode n is uncoupled
+      // and nothing is exchanged)
+      const int g = c.off + s;
+      sc[2] = extrap_weight(w_hat, c.lip_w[lup_idx(c, n, g)], c.lip_w[lu_idx(c, n, g)], c.delta_w);
+      sc[3] = c.lip_w[lu_idx(c, n, g)];
+    }
   }
   stage_async(step, c.STEP[s], (long long)R * R);
   // lra, 3-way: the two other modes' cross grams, this tile's Ut rows and the
@@ -604,11 +622,13 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
   if (r0 >= In) return;
   const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
   __shared__ double sc[2];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double sl, slp;
     common_lip_sums(c, n, sl, slp);
-    sc[0] = sl;
-    sc[1] = extrap_weight(redo ? 0.0 : c.st->w_hat, slp, sl, c.delta_w);
+    if (threadIdx.x == 0) {
+      sc[0] = sl;
+      sc[1] = extrap_weight(redo ? 0.0 : c.st->w_hat, slp, sl, c.delta_w);
+    }
   }
   __syncthreads();
   common_fold(c, n, r0, rows, sc[0], sc[1]);
@@ -723,7 +743,7 @@ __global__ void __launch_bounds__(256) k_eval_side(Ctx c, int redo) {
   griddep_wait();
   if (stopped(c, redo)) return;
   extern __shared__ double smd[];
-  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const BlockSmem sm = carve(smd, c.rmax, 0);   // no gram staging
   eval_side_block(c, blockIdx.x, sm);
 }
 
@@ -733,7 +753,7 @@ __global__ void __launch_bounds__(256) k_step(Ctx c, int n, int redo) {
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_STEP + n - 1);
   extern __shared__ double smd[];
-  const BlockSmem sm = carve(smd, c.rmax, c.rmax);
+  const BlockSmem sm = carve(smd, c.rmax, 0);   // no gram staging
   step_and_lipschitz(c, blockIdx.x, n, sm);
   tl_end(c.tl, TL_STEP + n - 1);
 }
