@@ -398,6 +398,81 @@ static __device__ __noinline__ double block_lam_max(const double* A, int R, doub
   return lm > 0.0 ? lm : 0.0;
 }
 
+// lambda_max of the same matrix slot as the previous call (a step matrix of
+// one block and mode, or its core gram): power steps from the slot's last
+// eigenvector `warm` (64 doubles, global; zero = none yet), accepted with
+// block_lam_max's test (rho >= 0, ||A v - rho v|| / ||v|| <= 1e-10 max|A| R),
+// at most 6 steps; otherwise the squaring solve.  The accepted eigenvector is
+// stored back.  The APG's matrices move little between iterations, so one
+// or two steps usually pass the test (c5: top-two ratio ~0.03).
+static __device__ __noinline__ double block_lam_max_warm(const double* A, int R, double* B, double* B2,
+                                                        double* vec, double* red, double* warm) {
+  const int ld = lm_ld(R);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
+  double* v = vec;
+  double* w = vec + 64;
+  unsigned* ured = reinterpret_cast<unsigned*>(red);
+  double m = 0.0;
+  for (int e = tid; e < R * R; e += nthr) {
+    const int i = e / R, j = e - i * R;
+    m = fmax(m, fabs(A[i * ld + j]));
+  }
+  m = block_max_approx(m, ured);
+  if (m == 0.0) return 0.0;
+  for (int i = tid; i < R; i += nthr) v[i] = warm[i];
+  __syncthreads();
+  for (int it = 0; it < 6; ++it) {
+    for (int i = wid; i < R; i += nw) {
+      double a = 0.0;
+      for (int j = lane; j < R; j += 32) a = fma(A[i * ld + j], v[j], a);
+      a = warp_sum(a);
+      if (lane == 0) w[i] = a;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double num = 0.0, den = 0.0, wm = 0.0;
+      for (int i = lane; i < R; i += 32) {
+        num = fma(v[i], w[i], num);
+        den = fma(v[i], v[i], den);
+        wm = fmax(wm, fabs(w[i]));
+      }
+      num = warp_sum(num);
+      den = warp_sum(den);
+      wm = warp_max(wm);
+      const double rho = den > 0.0 ? num / den : 0.0;
+      double r2 = 0.0;
+      for (int i = lane; i < R; i += 32) {
+        const double d = w[i] - rho * v[i];
+        r2 = fma(d, d, r2);
+      }
+      r2 = warp_sum(r2);
+      __syncwarp();
+      if (wm > 0.0)
+        for (int i = lane; i < R; i += 32) v[i] = w[i] / wm;
+      if (lane == 0) {
+        red[36] = rho;
+        red[37] = den > 0.0 ? sqrt(r2 / den) : INFINITY;
+        red[38] = (den > 0.0 && wm > 0.0) ? 1.0 : 0.0;
+      }
+    }
+    __syncthreads();
+    const double rho = red[36], resid = red[37];
+    const bool live = red[38] > 0.0;
+    __syncthreads();
+    if (!live) break;
+    if (rho >= 0.0 && resid <= 1e-10 * m * R) {
+      for (int i = tid; i < R; i += nthr) warm[i] = v[i];
+      return rho;
+    }
+  }
+  const double lam = block_lam_max(A, R, B, B2, vec, red);
+  // the squaring solve leaves its eigenvector in vec[0..R)
+  for (int i = tid; i < R; i += nthr) warm[i] = vec[i];
+  __syncthreads();
+  return lam;
+}
+
 // shared memory (doubles) of block_lam_max for rank R: A, B, B2, vec, red
 __host__ __device__ __forceinline__ int lm_smem_doubles(int R) {
   return ((R + 3) & ~3) * lm_ld(R) + 2 * lm_bsize(R) + 128 + 40;

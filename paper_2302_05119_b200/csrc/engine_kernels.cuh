@@ -29,9 +29,10 @@ struct BlockSmem {
   double* misc;   // 4 * 64
 };
 
-// rows staged per gram chunk: small ranks stage up to 128 rows at once, so
-// a whole factor (I_n <= 128) arrives in one round trip of loads
-__host__ __device__ __forceinline__ int gram_rows(int gw) { return gw <= 16 ? 128 : 64; }
+// rows staged per gram chunk, double-buffered (chunk k + 1 in flight while
+// chunk k is multiplied): the same shared memory as single 128 / 64-row
+// chunks, so the per-block kernels keep two CTAs per SM at R = 40
+__host__ __device__ __forceinline__ int gram_rows(int gw) { return gw <= 16 ? 64 : 32; }
 
 __device__ __forceinline__ BlockSmem carve(double* sm, int rmax, int gw) {
   BlockSmem b;
@@ -160,7 +161,8 @@ static __device__ __noinline__ void step_and_lipschitz(const Ctx& c, int s, int 
     step[e] = sm.lmA[i * ld + j];
   }
   pc.mark(c.dbg, 4);
-  const double lu = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.dbg);
+  const double lu = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red,
+                                      c.evec + ((long long)s * (c.N + 1) + n) * 64);
   if (threadIdx.x == 0) {
     const int idx = n * c.S + s;
     const double h = c.lipf_hist[idx];
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(256) k_init_block(Ctx c) {
   }
   final_quantities(c, s, sm);
   if (c.ld_pre && c.update_core) {
-    const double ld = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+    const double ld = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64);
     if (threadIdx.x == 0) c.ldcore[s] = ld;
   }
 }
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
     // evaluation's fiber pass (k_eval_side) from these same grams
     const double ldv = (!redo && c.ld_pre)
                            ? c.ldcore[s]
-                           : block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+                           : block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64);
     double* sc = sm.misc + 192;
     if (threadIdx.x == 0) {
       const double h = c.lipc_hist[s];
@@ -734,7 +736,7 @@ __device__ inline void eval_side_block(const Ctx& c, int s, const BlockSmem& sm)
   }
   final_quantities(c, s, sm);   // leaves hadamard_n G_n in sm.lmA
   if (c.update_core) {
-    const double ld = block_lam_max(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red);
+    const double ld = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64);
     if (threadIdx.x == 0) c.ldcore[s] = ld;
   }
 }
