@@ -402,11 +402,12 @@ static __device__ __noinline__ double block_lam_max(const double* A, int R, doub
 // one block and mode, or its core gram): power steps from the slot's last
 // eigenvector `warm` (64 doubles, global; zero = none yet), accepted with
 // block_lam_max's test (rho >= 0, ||A v - rho v|| / ||v|| <= 1e-10 max|A| R),
-// at most 6 steps; otherwise the squaring solve.  The accepted eigenvector is
+// at most 3 steps; otherwise the squaring solve.  The accepted eigenvector is
 // stored back.  The APG's matrices move little between iterations, so one
 // or two steps usually pass the test (c5: top-two ratio ~0.03).
 static __device__ __noinline__ double block_lam_max_warm(const double* A, int R, double* B, double* B2,
-                                                        double* vec, double* red, double* warm) {
+                                                        double* vec, double* red, double* warm,
+                                                        int* miss) {
   const int ld = lm_ld(R);
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
@@ -420,9 +421,20 @@ static __device__ __noinline__ double block_lam_max_warm(const double* A, int R,
   }
   m = block_max_approx(m, ured);
   if (m == 0.0) return 0.0;
+  // a slot whose spectrum defeated the warm steps recently (clustered top
+  // eigenvalues) goes straight to the squaring solve; retried every 8 calls
+  const int skip = *miss;
+  __syncthreads();
+  if (skip > 0) {
+    if (tid == 0) *miss = skip - 1;
+    const double lam = block_lam_max(A, R, B, B2, vec, red);
+    for (int i = tid; i < R; i += nthr) warm[i] = vec[i];
+    __syncthreads();
+    return lam;
+  }
   for (int i = tid; i < R; i += nthr) v[i] = warm[i];
   __syncthreads();
-  for (int it = 0; it < 6; ++it) {
+  for (int it = 0; it < 3; ++it) {
     for (int i = wid; i < R; i += nw) {
       double a = 0.0;
       for (int j = lane; j < R; j += 32) a = fma(A[i * ld + j], v[j], a);
@@ -466,6 +478,7 @@ static __device__ __noinline__ double block_lam_max_warm(const double* A, int R,
       return rho;
     }
   }
+  if (tid == 0) *miss = 8;
   const double lam = block_lam_max(A, R, B, B2, vec, red);
   // the squaring solve leaves its eigenvector in vec[0..R)
   for (int i = tid; i < R; i += nthr) warm[i] = vec[i];

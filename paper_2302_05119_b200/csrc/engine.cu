@@ -850,6 +850,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   }
   TRY(dalloc((void**)&c.lipc_hist, sizeof(double) * S, A));
   TRY(dalloc((void**)&c.evec, sizeof(double) * S * (N + 1) * 64, A));
+  TRY(dalloc((void**)&c.evec_miss, sizeof(int) * S * (N + 1), A));
   c.dbg = nullptr;
   TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
   TRY(dalloc((void**)&c.ldcore, sizeof(double) * S, A));

@@ -52,6 +52,7 @@ struct Ctx {
   double* dbg;                // phase-time accumulators (profiling only) or null
   double* lipf_hist;          // N*S
   double* evec;               // S*(N+1)*64 warm eigenvectors (step matrices, core)
+  int* evec_miss;             // S*(N+1) calls left before the warm path is retried
   // Block sharding (one process per GPU, blocks [off, off+S) of S_tot).  Every
   // quantity that couples blocks lives in a GLOBAL-slot array indexed by the
   // global block number; a rank writes only its own slots into the *_w copy,

@@ -162,7 +162,8 @@ static __device__ __noinline__ void step_and_lipschitz(const Ctx& c, int s, int 
   }
   pc.mark(c.dbg, 4);
   const double lu = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red,
-                                      c.evec + ((long long)s * (c.N + 1) + n) * 64);
+                                      c.evec + ((long long)s * (c.N + 1) + n) * 64,
+                                      c.evec_miss + (long long)s * (c.N + 1) + n);
   if (threadIdx.x == 0) {
     const int idx = n * c.S + s;
     const double h = c.lipf_hist[idx];
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(256) k_init_block(Ctx c) {
   }
   final_quantities(c, s, sm);
   if (c.ld_pre && c.update_core) {
-    const double ld = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64);
+    const double ld = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64, c.evec_miss + (long long)s * (c.N + 1) + c.N);
     if (threadIdx.x == 0) c.ldcore[s] = ld;
   }
 }
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(256) k_sweep_begin(Ctx c, int redo) {
     // evaluation's fiber pass (k_eval_side) from these same grams
     const double ldv = (!redo && c.ld_pre)
                            ? c.ldcore[s]
-                           : block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64);
+                           : block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64, c.evec_miss + (long long)s * (c.N + 1) + c.N);
     double* sc = sm.misc + 192;
     if (threadIdx.x == 0) {
       const double h = c.lipc_hist[s];
@@ -736,7 +737,7 @@ __device__ inline void eval_side_block(const Ctx& c, int s, const BlockSmem& sm)
   }
   final_quantities(c, s, sm);   // leaves hadamard_n G_n in sm.lmA
   if (c.update_core) {
-    const double ld = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64);
+    const double ld = block_lam_max_warm(sm.lmA, R, sm.lmB, sm.lmB2, sm.vec, sm.red, c.evec + ((long long)s * (c.N + 1) + c.N) * 64, c.evec_miss + (long long)s * (c.N + 1) + c.N);
     if (threadIdx.x == 0) c.ldcore[s] = ld;
   }
 }
