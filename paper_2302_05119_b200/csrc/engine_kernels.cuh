@@ -424,7 +424,7 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
 // (row-major I_n x L, this block's global slot).
 // `smd` is the tile's shared scratch; returns the tile's (sumL, w_common)
 // through sc_out (valid on every thread).
-static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int redo, int src, int s,
+static __device__ __forceinline__ void mode_update_tile(const Ctx& c, int n, int redo, int src, int s,
                                                      int r0, double* smd, double* gcp,
                                                      double* sc_out, int TR = MU_ROWS) {
   const int R = c.R[s];
@@ -519,12 +519,34 @@ static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int re
     for (int e = threadIdx.x; e < Rt * R; e += blockDim.x) P[e] = Cs[e] * Cs[Rt * R + e];
     for (int e = threadIdx.x; e < rows * Rt; e += blockDim.x) Uts[e] *= tws[e % Rt];
     __syncthreads();
-    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
-      const int il = e / R, r = e - il * R;
+    // 4-column register tiles: one broadcast load of Ut o tw feeds four FMA
+    // chains (each output keeps its q-ordered chain)
+    const int RG = (R + 3) >> 2;
+    for (int e = threadIdx.x; e < rows * RG; e += blockDim.x) {
+      const int il = e / RG, rb = (e - il * RG) << 2;
       const double* ur = Uts + il * Rt;
-      double a = 0.0;
-      for (int q = 0; q < Rt; ++q) a = fma(ur[q], P[q * R + r], a);
-      mt[e] = a;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (rb + 4 <= R) {
+        for (int q = 0; q < Rt; ++q) {
+          const double u = ur[q];
+          const double* pr = P + q * R + rb;
+          a0 = fma(u, pr[0], a0); a1 = fma(u, pr[1], a1);
+          a2 = fma(u, pr[2], a2); a3 = fma(u, pr[3], a3);
+        }
+      } else {
+        for (int q = 0; q < Rt; ++q) {
+          const double u = ur[q];
+          const double* pr = P + q * R + rb;
+          a0 = fma(u, pr[0], a0);
+          if (rb + 1 < R) a1 = fma(u, pr[1], a1);
+          if (rb + 2 < R) a2 = fma(u, pr[2], a2);
+        }
+      }
+      double* mo = mt + il * R + rb;
+      mo[0] = a0;
+      if (rb + 1 < R) mo[1] = a1;
+      if (rb + 2 < R) mo[2] = a2;
+      if (rb + 3 < R) mo[3] = a3;
     }
   } else if (src == 2) {
     const int Rt = c.Rt[s];
@@ -553,25 +575,52 @@ static __device__ __noinline__ void mode_update_tile(const Ctx& c, int n, int re
   __syncthreads();
   pc.mark(c.dbg, 6);
   double* Un = c.Un[s * N + n];
-  for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
-    const int il = e / R, r = e - il * R;
-    const long long i = r0 + il;
-    if (lu == 0.0) {
-      if (r >= L) Un[i * R + r] = Ucs[e];
-      continue;
+  if (lu == 0.0) {
+    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+      const int il = e / R, r = e - il * R;
+      if (r >= L) Un[(r0 + il) * (long long)R + r] = Ucs[e];
     }
-    double g = 0.0;
-    for (int q = 0; q < R; ++q) g = fma(uh[il * R + q], step[q * R + r], g);
-    g -= mt[e] * lam[r];
-    if (r < L) gcp[i * L + r] = g;
-    else Un[i * R + r] = pos(uh[e] - g / lu);
+  } else {
+    // gradient u_hat step - mt o lam in 4-column register tiles (each
+    // output's q-ordered FMA chain unchanged), then the projection
+    const int RG = (R + 3) >> 2;
+    for (int e = threadIdx.x; e < rows * RG; e += blockDim.x) {
+      const int il = e / RG, rb = (e - il * RG) << 2;
+      const double* ur = uh + il * R;
+      double g4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (rb + 4 <= R) {
+        for (int q = 0; q < R; ++q) {
+          const double u = ur[q];
+          const double* sr = step + q * R + rb;
+          g4[0] = fma(u, sr[0], g4[0]); g4[1] = fma(u, sr[1], g4[1]);
+          g4[2] = fma(u, sr[2], g4[2]); g4[3] = fma(u, sr[3], g4[3]);
+        }
+      } else {
+        for (int q = 0; q < R; ++q) {
+          const double u = ur[q];
+          const double* sr = step + q * R + rb;
+          g4[0] = fma(u, sr[0], g4[0]);
+          if (rb + 1 < R) g4[1] = fma(u, sr[1], g4[1]);
+          if (rb + 2 < R) g4[2] = fma(u, sr[2], g4[2]);
+        }
+      }
+      const long long i = r0 + il;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = rb + k;
+        if (r >= R) break;
+        const double g = g4[k] - mt[il * R + r] * lam[r];
+        if (r < L) gcp[i * L + r] = g;
+        else Un[i * R + r] = pos(ur[r] - g / lu);
+      }
+    }
   }
   sc_out[0] = sumL;
   sc_out[1] = wc;
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_mode_update(Ctx c, int n, int redo, int src,
+__global__ void __launch_bounds__(256, 1) k_mode_update(Ctx c, int n, int redo, int src,
                                                       const RowUnit* __restrict__ units) {
   griddep_wait();
   if (stopped(c, redo)) return;
