@@ -937,13 +937,29 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     CB_CUDA(cudaMemcpyAsync(c.nsq, ns.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st));
     CB_CUDA(cudaStreamSynchronize(st));
   }
+  // ---- mode-update tile: 64 rows for the lra 3-way path (the per-tile
+  // staging of the step matrix and two cross grams then serves twice the
+  // rows, half the CTAs) when its shared memory fits, else MU_ROWS
+  {
+    int maxL = 0;
+    for (int n = 0; n < N; ++n) maxL = std::max(maxL, h->counts[n]);
+    const int rtm = std::max(h->rtmax, 1);
+    auto mu_bytes = [&](long long tr) {
+      return sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)tr * h->rmax +
+                               (h->lra ? (size_t)rtm * h->rmax : 0) + 16 +
+                               (h->lra && N == 3 ? 2 * (size_t)rtm * h->rmax + (size_t)tr * rtm + rtm : 0) +
+                               2 * (size_t)tr * h->rmax + 2 * (size_t)tr * maxL);
+    };
+    c.mu_rows = (h->lra && N == 3 && mu_bytes(64) <= 200 * 1024) ? 64 : MU_ROWS;
+    h->mu_smem = mu_bytes(c.mu_rows);
+  }
   // ---- row-unit tables for the mode updates
   h->d_rows.assign(N, nullptr);
   h->n_rows.assign(N, 0);
   for (int n = 0; n < N; ++n) {
     std::vector<RowUnit> ru;
     for (int s = 0; s < S; ++s)
-      for (long long r0 = 0; r0 < h->dims[s * N + n]; r0 += MU_ROWS) ru.push_back(RowUnit{s, (int)r0});
+      for (long long r0 = 0; r0 < h->dims[s * N + n]; r0 += c.mu_rows) ru.push_back(RowUnit{s, (int)r0});
     h->n_rows[n] = (int)ru.size();
     TRY(upload(ru, &h->d_rows[n], A, st));
   }
@@ -1058,13 +1074,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   h->blk_smem = block_smem_bytes(c.rmax, c.rmax);
   h->blk_smem_ng = block_smem_bytes(c.rmax, 0);
   int maxRt = std::max(h->rtmax, 1);
-  h->mu_smem = sizeof(double) * ((size_t)h->rmax * h->rmax + 2 * (size_t)MU_ROWS * h->rmax +
-                                 (h->lra ? (size_t)maxRt * h->rmax : 0) + 16);
-  // lra 3-way staging: two cross grams, the tile's Ut rows, the weights
-  if (h->lra && N == 3)
-    h->mu_smem += sizeof(double) * (2 * (size_t)maxRt * h->rmax + (size_t)MU_ROWS * maxRt + maxRt);
-  // staged rows: current, previous, block 0's current / previous
-  h->mu_smem += sizeof(double) * 4 * (size_t)MU_ROWS * h->rmax;
+  // (mu_smem: set with the mode-update tile above)
   h->qr_smem = 0;
   if (h->lra) {
     int cmax = 0;

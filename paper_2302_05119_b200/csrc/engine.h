@@ -83,6 +83,7 @@ struct Ctx {
   double* qr_buf;             // S*N*QR_MAXC*QR_MAXC R factors
   double* qr_part;            // S*qr_nchunks partial core sums
   int qr_nchunks;
+  int mu_rows;                // rows per k_mode_update tile (MU_ROWS, or 64 for lra 3-way)
   int* qr_need;               // S flags: QR route taken this evaluation
   double* fib_bpart;          // per-block fiber totals: b (S x RSTRIDE)
   double* fib_rpart;          //   and explicit residual (S)

@@ -462,13 +462,20 @@ static __device__ __forceinline__ void mode_update_tile(const Ctx& c, int n, int
   // this tile's current / previous rows (and block 0's common columns)
   double* Ucs = tws + (lra3 ? c.Rt[s] : 0);            // rows x R
   double* Ups = Ucs + TR * R;                      // rows x R
-  double* U0s = Ups + TR * R;                      // rows x R0 (L > 0)
-  double* U0ps = U0s + TR * c.R[0];                // rows x R0 (L > 0)
+  double* U0s = Ups + TR * R;                      // rows x L (L > 0)
+  double* U0ps = U0s + TR * L;                     // rows x L (L > 0)
   stage_async(Ucs, c.U[s * N + n] + (long long)r0 * R, (long long)rows * R);
   stage_async(Ups, c.Up[s * N + n] + (long long)r0 * R, (long long)rows * R);
   if (L > 0) {
-    stage_async(U0s, c.U[n] + (long long)r0 * c.R[0], (long long)rows * c.R[0]);
-    stage_async(U0ps, c.Up[n] + (long long)r0 * c.R[0], (long long)rows * c.R[0]);
+    // block 0's common columns only (rows x L of its rows x R0)
+    const int R0s = c.R[0];
+    const double* g0 = c.U[n] + (long long)r0 * R0s;
+    const double* g1 = c.Up[n] + (long long)r0 * R0s;
+    for (int e = threadIdx.x; e < rows * L; e += blockDim.x) {
+      const int il = e / L, l = e - il * L;
+      cp_async8(U0s + e, g0 + (long long)il * R0s + l);
+      cp_async8(U0ps + e, g1 + (long long)il * R0s + l);
+    }
   }
   if (src == 0) stage_async(mt, c.MTT[s] + (long long)r0 * R, (long long)rows * R);
   if (lra3) {
@@ -495,7 +502,7 @@ static __device__ __forceinline__ void mode_update_tile(const Ctx& c, int n, int
     const long long i = r0 + il;
     double v;
     if (r < L) {
-      const double cc = U0s[il * R0 + r], cp = U0ps[il * R0 + r];
+      const double cc = U0s[il * L + r], cp = U0ps[il * L + r];
       v = cc + wc * (cc - cp);
     } else {
       const double cur = Ucs[e], prv = Ups[e];
@@ -631,10 +638,11 @@ __global__ void __launch_bounds__(256, 1) k_mode_update(Ctx c, int n, int redo, 
   const int L = c.counts[n];
   const long long In = c.dims[s * c.N + n];
   const int r0 = u.r0;
-  const int rows = (int)(In - r0 < MU_ROWS ? In - r0 : MU_ROWS);
+  const int TR = c.mu_rows;
+  const int rows = (int)(In - r0 < TR ? In - r0 : TR);
   double sl2[2];
   mode_update_tile(c, n, redo, src, s, r0, smd, c.gc_w + (long long)(c.off + s) * c.gc_stride,
-                   sl2);
+                   sl2, TR);
   const double sumL = sl2[0], wc = sl2[1];
   PhaseClock pc;
   pc.start(c.dbg);
@@ -647,7 +655,7 @@ __global__ void __launch_bounds__(256, 1) k_mode_update(Ctx c, int n, int redo, 
   __syncthreads();
   int* flag = reinterpret_cast<int*>(sc + 4);
   if (threadIdx.x == 0) {
-    const int t = r0 / MU_ROWS;
+    const int t = r0 / TR;
     const int old = atomicAdd(&c.tile_cnt[t], 1);
     flag[0] = (old == c.S - 1);
   }
@@ -658,7 +666,7 @@ __global__ void __launch_bounds__(256, 1) k_mode_update(Ctx c, int n, int redo, 
   common_fold(c, n, r0, rows, sumL, wc);
   pc.mark(c.dbg, 8);
   tl_end(c.tl, TL_MU + n);
-  if (threadIdx.x == 0) c.tile_cnt[r0 / MU_ROWS] = 0;
+  if (threadIdx.x == 0) c.tile_cnt[r0 / TR] = 0;
 }
 
 // sharded runs: new common columns of one row tile from the all-reduced

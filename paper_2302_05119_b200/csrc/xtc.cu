@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int st = 0, ph = 0, seg = 0, cur = -1;
+      const uint64_t pol = l2_evict_first_policy();
       // L2 prefetch runs XTC_PF tiles ahead of the ring: a tile (128 rows x
       // I0) is one contiguous span, one bulk prefetch
       int pu = u_begin, pt = a.units[u_begin].t0;
@@ -403,7 +404,8 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
           for (int c = 0; c < nch * XTC_SUB; ++c) {
             XTC_TW(0, mbar_wait(&empty[st], ph ^ 1));
             mbar_arrive_expect_tx(&full[st], XTC_STAGE);
-            tma_load_2d(ring + (size_t)st * XTC_STAGE, tm, c * XTC_KC, t * XTC_M, &full[st]);
+            tma_load_2d_stream(ring + (size_t)st * XTC_STAGE, tm, c * XTC_KC, t * XTC_M, &full[st],
+                               pol);
             if (++st == nst) { st = 0; ph ^= 1; }
           }
         }
