@@ -196,8 +196,12 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_tg_pass(TgArgs a) {
     }
     return;
   }
-  const int jg = lane;                         // j = 4 jg .. 4 jg + 3 of the tile
-  const int cg = warp;                         // columns [cg CG, (cg + 1) CG)
+  // 2 consecutive j (one float2 per i2 row) x RB/4 columns per thread: one
+  // fp32 -> fp64 conversion feeds RB/4 FMAs (the conversions share the
+  // fp64 pipe with the FMAs)
+  constexpr int CG2 = RB / 4;
+  const int jg = threadIdx.x & 63;             // j = 2 jg, 2 jg + 1 of the tile
+  const int cg = threadIdx.x >> 6;             // columns [cg CG2, (cg + 1) CG2)
   int st = 0, ph = 0, cur = -1;
   for (ActTiles it = act_tiles_begin(a.active, a.S, ntl); it.left > 0;
        act_tiles_next(it, a.active, a.S, ntl)) {
@@ -217,45 +221,43 @@ __global__ void __launch_bounds__(SL5_THREADS, 1) k_tg_pass(TgArgs a) {
       }
       asm volatile("bar.sync 1, %0;" ::"r"(SL5_CONS) : "memory");
     }
-    double acc[4][CG];
+    double acc[2][CG2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < CG; ++v) acc[u][v] = 0.0;
+      for (int v = 0; v < CG2; ++v) acc[u][v] = 0.0;
     for (int c = 0; c < nch; ++c) {
       mbar_wait(&full[st], ph);
       const float* tile = reinterpret_cast<const float*>(ring + (size_t)st * TG_BOX);
-      const double* ar = a2s + (size_t)c * TG_KC * RB + cg * CG;
+      const double* ar = a2s + (size_t)c * TG_KC * RB + cg * CG2;
 #pragma unroll 4
       for (int k = 0; k < TG_KC; ++k) {
-        const float4 x4 = *reinterpret_cast<const float4*>(tile + k * TG_M + 4 * jg);
-        const double xv[4] = {x4.x, x4.y, x4.z, x4.w};
-        double av[CG];
+        const float2 x2 = *reinterpret_cast<const float2*>(tile + k * TG_M + 2 * jg);
+        const double x0 = x2.x, x1 = x2.y;
+        double av[CG2];
 #pragma unroll
-        for (int v = 0; v < CG; ++v) av[v] = ar[k * RB + v];
+        for (int v = 0; v < CG2; ++v) av[v] = ar[k * RB + v];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < CG; ++v) acc[u][v] = fma(xv[u], av[v], acc[u][v]);
+        for (int v = 0; v < CG2; ++v) {
+          acc[0][v] = fma(x0, av[v], acc[0][v]);
+          acc[1][v] = fma(x1, av[v], acc[1][v]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (++st == TG_NST) { st = 0; ph ^= 1; }
     }
     double* T = reinterpret_cast<double*>(sel ? a.T1[tt.s] : a.T0[tt.s]);
-    const long long j0 = (long long)tt.t * TG_M + 4 * jg;
+    const long long j0 = (long long)tt.t * TG_M + 2 * jg;
 #pragma unroll
-    for (int v = 0; v < CG; ++v) {
-      const int r = cg * CG + v;
+    for (int v = 0; v < CG2; ++v) {
+      const int r = cg * CG2 + v;
       if (r >= R) continue;
       double* dst = T + (long long)r * J + j0;
-      if (j0 + 3 < J) {
+      if (j0 + 1 < J) {
         reinterpret_cast<double2*>(dst)[0] = make_double2(acc[0][v], acc[1][v]);
-        reinterpret_cast<double2*>(dst)[1] = make_double2(acc[2][v], acc[3][v]);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (j0 + u < J) dst[u] = acc[u][v];
+      } else if (j0 < J) {
+        dst[0] = acc[0][v];
       }
     }
   }
