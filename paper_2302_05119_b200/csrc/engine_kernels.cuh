@@ -930,13 +930,30 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
       // rank-1 update (warp per row, lanes over columns); lane 0 of every warp
       // also sums the squares of the updated column k + 1 (next step's norm)
       double nss = 0.0;
-      for (int i = wid; i <= nr; i += nw) {
-        double* row = i == 0 ? Rm + k * ld : X + (i - 1) * ld;
-        const double vi = i == 0 ? v0 : X[(i - 1) * ld + k];
+      // four rows per round: their v_i and row values are loaded before any
+      // store (independent chains instead of one load-fma-store per row)
+      for (int i0 = wid; i0 <= nr; i0 += 4 * nw) {
+        double vi[4];
+        double* row[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * nw;
+          row[u] = i == 0 ? Rm + k * ld : X + (i - 1) * ld;
+          vi[u] = i > nr ? 0.0 : (i == 0 ? v0 : X[(i - 1) * ld + k]);
+        }
         for (int j = k + 1 + lane; j < Cc; j += 32) {
-          const double x = refl ? row[j] - vi * w[j] : row[j];
-          if (refl) row[j] = x;
-          if (j == k + 1 && i > 0) nss = fma(x, x, nss);
+          const double wj = w[j];
+          double xv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xv[u] = i0 + u * nw <= nr ? row[u][j] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * nw;
+            if (i > nr) break;
+            const double x = refl ? xv[u] - vi[u] * wj : xv[u];
+            if (refl) row[u][j] = x;
+            if (j == k + 1 && i > 0) nss = fma(x, x, nss);
+          }
         }
       }
       if (lane == 0) red[((k + 1) & 1) * 32 + wid] = nss;
