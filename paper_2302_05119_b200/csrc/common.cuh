@@ -402,7 +402,8 @@ static __device__ __noinline__ double block_lam_max(const double* A, int R, doub
 // one block and mode, or its core gram): power steps from the slot's last
 // eigenvector `warm` (64 doubles, global; zero = none yet), accepted with
 // block_lam_max's test (rho >= 0, ||A v - rho v|| / ||v|| <= 1e-10 max|A| R),
-// at most 3 steps; otherwise the squaring solve.  The accepted eigenvector is
+// at most 10 steps while the residual keeps shrinking fast; otherwise the
+// squaring solve.  The accepted eigenvector is
 // stored back.  The APG's matrices move little between iterations, so one
 // or two steps usually pass the test (c5: top-two ratio ~0.03).
 static __device__ __noinline__ double block_lam_max_warm(const double* A, int R, double* B, double* B2,
@@ -434,7 +435,8 @@ static __device__ __noinline__ double block_lam_max_warm(const double* A, int R,
   }
   for (int i = tid; i < R; i += nthr) v[i] = warm[i];
   __syncthreads();
-  for (int it = 0; it < 3; ++it) {
+  double prev_resid = INFINITY;
+  for (int it = 0; it < 10; ++it) {
     for (int i = wid; i < R; i += nw) {
       double a = 0.0;
       for (int j = lane; j < R; j += 32) a = fma(A[i * ld + j], v[j], a);
@@ -477,6 +479,10 @@ static __device__ __noinline__ double block_lam_max_warm(const double* A, int R,
       for (int i = tid; i < R; i += nthr) warm[i] = v[i];
       return rho;
     }
+    // a slowly shrinking residual means clustered top eigenvalues: the
+    // squaring solve is cheaper than more steps
+    if (it >= 2 && resid > 0.5 * prev_resid) break;
+    prev_resid = resid;
   }
   if (tid == 0) *miss = 8;
   const double lam = block_lam_max(A, R, B, B2, vec, red);

@@ -602,7 +602,8 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
         cur = un.s;
         named_bar(1, NE);
         if (et < 128) auxs[et] = b.aux[et];
-        for (int e = et; e < R * I1; e += NE) u1s[e] = b.ut1[e];
+        if (a.u1_bytes)
+          for (int e = et; e < R * I1; e += NE) u1s[e] = b.ut1[e];
       }
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
         const int buf = tl & 1;
@@ -620,7 +621,9 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
         const int i2a = (int)(((long long)t * XTC_M) / I1);
         const long long r1 = std::min((long long)t * XTC_M + XTC_M, J) - 1;
         (void)r1;
-        const float* u1 = u1s + i1;                                   // shared
+        // shared when staged, else the L2-resident table (the ring took
+        // its shared memory: more bytes in flight per SM)
+        const float* u1 = (a.u1_bytes ? u1s : b.ut1) + i1;
         const float* u2 = u2s + buf * XTC_U2R * 64 + (i2 - i2a) * 64; // shared
         XTC_TW(5, mbar_wait(&d_full[buf], (tl >> 1) & 1));
         tc_fence_after();
@@ -836,10 +839,17 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   long long i1max = 1;
   for (int s = 0; s < S; ++s) i1max = std::max(i1max, hb[s].I1);
   int u1b = (int)(((long long)rmax * i1max * 4 + 127) / 128 * 128);
+  auto stages = [&](int u1) {
+    const size_t fixed = xtc_smem_for<16>(0, p->bimg_max, u1);
+    const int n = (int)((XTC_SMEM_MAX - fixed) / (XTC_STAGE + 16));
+    return std::min(n, 12) & ~1;   // even (chunks never wrap), >= 2 SUB
+  };
+  // the ring's depth bounds the bytes in flight per SM (Little's law: c5
+  // with the A1 table staged left 4 stages = 64 KB, ~38 GB/s per SM at the
+  // loaded DRAM latency); read A1 from L2 instead when that buys stages
+  if (stages(u1b) < 8 && stages(0) > stages(u1b)) u1b = 0;
   p->u1_bytes = u1b;
-  const size_t fixed = xtc_smem_for<16>(0, p->bimg_max, u1b);
-  int nst = (int)((XTC_SMEM_MAX - fixed) / (XTC_STAGE + 16));
-  nst = std::min(nst, 12) & ~1;   // even (chunks never wrap), >= 2 SUB
+  int nst = stages(u1b);
   if (nst < 2 * XTC_SUB) {
     delete p;
     set_error("xtc: operand image too large (%d bytes)", p->bimg_max);
