@@ -844,10 +844,9 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     const int n = (int)((XTC_SMEM_MAX - fixed) / (XTC_STAGE + 16));
     return std::min(n, 12) & ~1;   // even (chunks never wrap), >= 2 SUB
   };
-  // the ring's depth bounds the bytes in flight per SM (Little's law: c5
-  // with the A1 table staged left 4 stages = 64 KB, ~38 GB/s per SM at the
-  // loaded DRAM latency); read A1 from L2 instead when that buys stages
-  if (stages(u1b) < 8 && stages(0) > stages(u1b)) u1b = 0;
+  // (reading the A1 table from L2 to free its shared memory for 4 more ring
+  // stages measured slower on c5: the trace pass 3.63 -> 4.54 ms; the
+  // epilogue's row weights need the staged copy)
   p->u1_bytes = u1b;
   int nst = stages(u1b);
   if (nst < 2 * XTC_SUB) {
