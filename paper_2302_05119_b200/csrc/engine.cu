@@ -337,7 +337,8 @@ static int enqueue_sweep(cb_solver* h, int redo) {
       prof(h, redo ? "redo:common" : "common");
     }
     if (emit(h)) {
-      launch_k(k_finalize, dim3(h->S), dim3(256), h->blk_smem, st, h->ctx, n, redo, split ? 0 : 1);
+      launch_k(k_finalize, dim3(h->S, h->lra ? 3 : 2), dim3(256), h->blk_smem, st, h->ctx, n, redo,
+               split ? 0 : 1);
       count_launch(1);
       CB_CHECK_LAUNCH();
     }
@@ -851,6 +852,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
   TRY(dalloc((void**)&c.lipc_hist, sizeof(double) * S, A));
   TRY(dalloc((void**)&c.evec, sizeof(double) * S * (N + 1) * 64, A));
   TRY(dalloc((void**)&c.evec_miss, sizeof(int) * S * (N + 1), A));
+  TRY(dalloc((void**)&c.fin_cnt, sizeof(int) * S, A));
   c.dbg = nullptr;
   TRY(dalloc((void**)&c.lipf_hist, sizeof(double) * N * S, A));
   TRY(dalloc((void**)&c.ldcore, sizeof(double) * S, A));

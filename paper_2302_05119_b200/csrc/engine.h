@@ -53,6 +53,7 @@ struct Ctx {
   double* lipf_hist;          // N*S
   double* evec;               // S*(N+1)*64 warm eigenvectors (step matrices, core)
   int* evec_miss;             // S*(N+1) calls left before the warm path is retried
+  int* fin_cnt;               // S arrival counters of k_finalize's roles (self-resetting)
   // Block sharding (one process per GPU, blocks [off, off+S) of S_tot).  Every
   // quantity that couples blocks lives in a GLOBAL-slot array indexed by the
   // global block number; a rank writes only its own slots into the *_w copy,

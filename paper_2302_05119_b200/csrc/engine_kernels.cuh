@@ -410,7 +410,12 @@ __device__ inline void common_fold(const Ctx& c, int n, int r0, int rows, double
         if (on[k]) acc += g32[k];
     }
     const double chat = cc + wc * (cc - cp);
-    c.cnew[i * L + l] = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
+    const double cn = sumL > 0.0 ? pos(chat - acc / sumL) : cc;
+    c.cnew[i * L + l] = cn;
+    // every block's new factor is [c_new | new individual] (solver.py:452-456):
+    // the shared columns go straight into the blocks' Un, so finalize reads
+    // the new factor from one array
+    for (int s = 0; s < c.S; ++s) c.Un[s * c.N + n][i * c.R[s] + l] = cn;
   }
 }
 
@@ -702,76 +707,98 @@ __global__ void __launch_bounds__(256) k_common(Ctx c, int n, int redo) {
 // ---------------------------------------------------------------------------
 // with_step = 0: the next mode's step matrix is left to k_step, which the 3-way
 // path runs concurrently with the next MTTKRP (they share no inputs)
-static __device__ __noinline__ void finalize_block(const Ctx& c, int n, int s, int with_step,
-                                                   const BlockSmem& sm) {
+// The tail of a block's finalize (solver.py:402-406, :506-515): the next
+// mode's step matrix and Lipschitz constant, or after the last mode the
+// staged b and the evaluation quantities.  The grams of mode n are current.
+static __device__ __noinline__ void finalize_tail(const Ctx& c, int n, int s, int with_step,
+                                                  const BlockSmem& sm) {
   const int N = c.N;
   const int R = c.R[s];
-  const int L = c.counts[n];
   const long long In = c.dims[s * N + n];
-  double* Uc = c.U[s * N + n];
-  double* Upr = c.Up[s * N + n];
-  const double* Un = c.Un[s * N + n];
-  PhaseClock pc;
-  pc.start(c.dbg);
-  // prev <- curr, curr <- new: all loads of a batch in flight before its
-  // stores (the pointers may alias as far as the compiler knows)
-  for (long long base = 0; base < In * R; base += 8LL * blockDim.x) {
-    double cu[8], nv[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const long long e = base + threadIdx.x + (long long)k * blockDim.x;
-      if (e < In * R) {
-        const long long i = e / R;
-        const int r = (int)(e - i * R);
-        cu[k] = Uc[e];
-        nv[k] = r < L ? c.cnew[i * L + r] : Un[e];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const long long e = base + threadIdx.x + (long long)k * blockDim.x;
-      if (e < In * R) {
-        Upr[e] = cu[k];
-        Uc[e] = nv[k];
-      }
-    }
-  }
-  __syncthreads();
-  pc.mark(c.dbg, 0);
-  block_gram(Uc, R, Uc, R, In, c.G[s * N + n], sm);
-  if (c.lra) block_gram(c.Ut[s * N + n], c.Rt[s], Uc, R, In, c.C[s * N + n], sm);
-  __syncthreads();
-  pc.mark(c.dbg, 1);
   if (n + 1 < N) {
-    if (with_step) {
-      step_and_lipschitz(c, s, n + 1, sm);
-      pc.mark(c.dbg, 2);
-    }
+    if (with_step) step_and_lipschitz(c, s, n + 1, sm);
   } else if (!c.ld_pre) {
     if (c.b_mtt) {
       // staged core linear term b[r] = sum_i U_{N-1}[i, r] MTTKRP_{N-1}[i, r]
       // (solver.py:506-509); warp per r, lanes over rows, fixed order
+      const double* Un = c.Un[s * N + n];
       const double* M = c.MTT[s];
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
       for (int r = wid; r < R; r += blockDim.x >> 5) {
         double v = 0.0;
-        for (long long i = lane; i < In; i += 32) v = fma(Uc[i * R + r], M[i * R + r], v);
+        for (long long i = lane; i < In; i += 32) v = fma(Un[i * R + r], M[i * R + r], v);
         v = warp_sum(v);
         if (lane == 0) c.fib_bpart[(long long)s * RSTRIDE + r] = v;
       }
     }
     final_quantities(c, s, sm);
-    pc.mark(c.dbg, 3);
   }
 }
 
+static __device__ __forceinline__ bool finalize_has_tail(const Ctx& c, int n, int with_step) {
+  return (n + 1 < c.N) ? with_step != 0 : !c.ld_pre;
+}
+
+// finalize mode n (solver.py:452-457, :367-371): the new factor Un (shared
+// columns already written by the fold) becomes current, the current one
+// previous, the grams are refreshed, then the tail.  Grid (S, roles): role 0
+// the copies, role 1 the gram U_n^T U_n, role 2 (lra) the cross gram
+// Ut_n^T U_n, all from Un and independent of each other; the last role of
+// a block to finish runs the tail (step matrix + lambda_max, or the
+// evaluation quantities) once the grams are visible.
 __global__ void __launch_bounds__(256) k_finalize(Ctx c, int n, int redo, int with_step) {
   griddep_wait();
   if (stopped(c, redo)) return;
   tl_begin(c.tl, TL_FIN + n);
   extern __shared__ double smd[];
   const BlockSmem sm = carve(smd, c.rmax, c.rmax);
-  finalize_block(c, n, blockIdx.x, with_step, sm);
+  const int s = blockIdx.x;
+  const int role = blockIdx.y;
+  const int N = c.N;
+  const int R = c.R[s];
+  const long long In = c.dims[s * N + n];
+  double* Uc = c.U[s * N + n];
+  double* Upr = c.Up[s * N + n];
+  const double* Un = c.Un[s * N + n];
+  if (role == 0) {
+    // prev <- curr, curr <- new: all loads of a batch in flight before its
+    // stores (the pointers may alias as far as the compiler knows)
+    for (long long base = 0; base < In * R; base += 8LL * blockDim.x) {
+      double cu[8], nv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long e = base + threadIdx.x + (long long)k * blockDim.x;
+        if (e < In * R) { cu[k] = Uc[e]; nv[k] = Un[e]; }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long e = base + threadIdx.x + (long long)k * blockDim.x;
+        if (e < In * R) { Upr[e] = cu[k]; Uc[e] = nv[k]; }
+      }
+    }
+  } else if (role == 1) {
+    block_gram(Un, R, Un, R, In, c.G[s * N + n], sm);
+  } else {
+    block_gram(c.Ut[s * N + n], c.Rt[s], Un, R, In, c.C[s * N + n], sm);
+  }
+  if (!finalize_has_tail(c, n, with_step)) {
+    tl_end(c.tl, TL_FIN + n);
+    return;
+  }
+  __threadfence();
+  __syncthreads();
+  int* flag = reinterpret_cast<int*>(sm.misc);
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(&c.fin_cnt[s], 1);
+    const int last = old == (int)gridDim.y - 1;
+    if (last) c.fin_cnt[s] = 0;
+    flag[0] = last;
+  }
+  __syncthreads();
+  if (!flag[0]) return;
+  __threadfence();
+  __syncthreads();
+  finalize_tail(c, n, s, with_step, sm);
   tl_end(c.tl, TL_FIN + n);
 }
 
