@@ -409,6 +409,9 @@ static __device__ __noinline__ double block_lam_max(const double* A, int R, doub
 static __device__ __noinline__ double block_lam_max_warm(const double* A, int R, double* B, double* B2,
                                                         double* vec, double* red, double* warm,
                                                         int* miss) {
+  // small ranks: the squaring solve (R^3 per squaring) costs less than a few
+  // barrier-bound power steps (measured on c2, R = 10)
+  if (R <= 16) return block_lam_max(A, R, B, B2, vec, red);
   const int ld = lm_ld(R);
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
