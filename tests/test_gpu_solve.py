@@ -152,6 +152,18 @@ def test_config_c5_subset_matches_reference(P):
             _rel_close(a, b, 1e-4, f"compression block {s} mode {m}")
 
 
+def test_config_c5_subset_fp64_matches_reference(P):
+    """c5 blocks {0, 1} in the fp64 parity mode (fp64 storage and arithmetic
+    everywhere: ALS, sweep, the trace term by the CUDA-core fiber pass):
+    histories element-wise at 1e-9 (north_star), iteration / restart counts,
+    factors and the compression at 1e-8."""
+    res, want = _config(P, "c5", "fp64")
+    compare(res, want, rtol=1e-9, factor_rtol=1e-8)
+    for s, (blk, (wf, _)) in enumerate(zip(res.compression, want["compression"])):
+        for m, (a, b) in enumerate(zip(blk.factors, wf)):
+            _rel_close(a, b, 1e-8, f"compression block {s} mode {m}")
+
+
 def test_config_c5_subset_tensor_core_als(P):
     """compute="tc": the ALS mode-2 MTTKRP on the tensor cores as well."""
     res, want = _config(P, "c5", "fp32", compute="tc")
