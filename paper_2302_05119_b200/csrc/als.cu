@@ -25,8 +25,8 @@
 #include "engine_host.h"
 #include "ops_internal.h"
 #include "status.h"
+#include "xoz.h"
 #include "xslab5.h"
-#include "xtc.h"
 
 namespace cb {
 
@@ -239,8 +239,8 @@ using namespace cb;
 
 struct cb_als {
   cudaStream_t st = nullptr;
-  cb::XtcPlan* xtc = nullptr;   // mode-2 MTTKRP on the tensor cores (compute code 2)
   cb::Sl5Plan* sl5 = nullptr;   // fp64 mode-2 MTTKRP for ranks > 16 (xslab5.cu)
+  cb::OzPlan* oz = nullptr;     // both passes on the tensor cores over packed byte planes (xoz.cu)
   int S = 0, N = 0, dtype = CB_F64, max_iter = 0, rmax = 1, rb = 8, fast3 = 0, pc = 0;
   double tol = 1e-4;
   std::vector<long long> dims;
@@ -289,9 +289,9 @@ static int als_sweep(cb_als* h) {
         launch_contract(h->pc, n, h->xa, n == 0 ? h->d_c0 : h->d_c1,
                         (int)(n == 0 ? h->tab.c0.size() : h->tab.c1.size()), st);
       } else {
-        if (h->xtc) {
-          // tensor-core mode-2 MTTKRP (xtc.cu), written into MTT
-          int rc = xtc_mode2(h->xtc, h->xa.U, h->xa.active, h->xa.MTT, st);
+        if (h->oz) {
+          // exact int8 slice GEMM over the packed planes (xoz.cu), written into MTT
+          int rc = oz_mode2(h->oz, h->xa.U, h->xa.active, h->xa.MTT, st);
           if (rc) return rc;
         } else if (h->sl5) {
           // fp64 GEMM-tiled mode-2 MTTKRP (xslab5.cu), written into MTT
@@ -318,7 +318,8 @@ static int als_sweep(cb_als* h) {
   }
   if (h->fast3 && h->ctx.res_expand) {
     // T for the next sweep (GEMM pass); the residual came from the expansion
-    int rc = sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st);
+    int rc = h->oz ? oz_tpass(h->oz, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st)
+                   : sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st);
     if (rc) return rc;
     CB_CHECK_LAUNCH();
   } else if (h->fast3) {
@@ -344,8 +345,8 @@ int cb_als_destroy(cb_als* h) {
   if (!h) return CB_OK;
   if (h->st) cudaStreamSynchronize(h->st);
   for (void* p : h->allocs) cudaFree(p);
-  cb::xtc_plan_destroy(h->xtc);
   cb::sl5_plan_destroy(h->sl5);
+  cb::oz_plan_destroy(h->oz);
   if (h->h_state) cudaFreeHost(h->h_state);
   delete h;
   return CB_OK;
@@ -467,6 +468,18 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab,
                   d->total_blocks > S ? d->total_blocks : S);
     h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->dtype == CB_F32 ? 4 : 8);
+    // fp32 storage with fp64-grade arithmetic, ranks in (16, 48]: both tensor
+    // passes of a sweep as exact int8 slice GEMMs over byte planes packed once
+    // (xoz.cu).  T is then written unsplit whatever the fiber table chose.
+    if (h->pc == PC_F32_F64 && !h->tab.slab_direct &&
+        oz_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
+      if (oz_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->oz) != CB_OK)
+        h->oz = nullptr;
+      if (h->oz) {
+        h->tab.nsplit.assign(S, 1);
+        h->tab.fib_unsplit = 1;
+      }
+    }
     prepare_slab(h->pc, h->rb, h->tma, h->tab);
     prepare_fiber(h->pc, h->rb, h->tma, h->tab);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));
@@ -509,25 +522,14 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     xa.MTT = c.MTT; xa.gate = nullptr; xa.active = c.active;
     xa.ktime = nullptr;
     xa.slab_stage_rows = h->tab.slab_rows;
-    // compute code 2 (fp32 storage, ranks > 16 where the row-dot kernel does
-    // not apply): the mode-2 MTTKRP on the tensor cores; a plan that does not
-    // fit leaves the CUDA-core slab pass
-    if (d->compute == 2 && h->dtype == CB_F32 && !h->tab.slab_direct &&
-        xtc_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
-      bool i1_ok = true;
-      for (int s = 0; s < S; ++s) i1_ok = i1_ok && h->dims[3 * s + 1] >= 32;
-      if (i1_ok &&
-          xtc_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->xtc, 1) != CB_OK)
-        h->xtc = nullptr;
-    }
     // fp64 arithmetic with ranks > 16: the GEMM-tiled mode-2 pass
-    if (!h->xtc && h->pc == PC_F32_F64 && !h->tab.slab_direct &&
+    if (!h->oz && h->pc == PC_F32_F64 && !h->tab.slab_direct &&
         sl5_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
       if (sl5_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->sl5) != CB_OK)
         h->sl5 = nullptr;
     }
     // both passes as GEMMs (unsplit T) with the gram-expansion residual
-    c.res_expand = (h->sl5 && sl5_tpass_ok(h->sl5) && h->tab.fib_unsplit) ? 1 : 0;
+    c.res_expand = (h->oz || (h->sl5 && sl5_tpass_ok(h->sl5) && h->tab.fib_unsplit)) ? 1 : 0;
     {
       int* d_s3;
       TRY(upload(h->tab.s3_first, &d_s3, A, st));
@@ -554,7 +556,8 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   CB_CUDA(cudaFuncSetAttribute(k_als_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->solve_smem));
   // initial T buffer (X x_3 U_2 of the starting factors)
   if (h->fast3 && c.res_expand) {
-    TRY(sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st));
+    TRY(h->oz ? oz_tpass(h->oz, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st)
+              : sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st));
     CB_CHECK_LAUNCH();
   } else if (h->fast3) {
     XArgs a = h->xa;

@@ -111,10 +111,6 @@ struct XtcArgs {
   int u1_bytes;            // smem bytes of the staged A1^T table (0: read it from L2)
   double* part;           // [unit][64]
   int* cnt;               // per-block arrival counters (self-resetting)
-  // mode-2 MTTKRP instead of the trace (ALS): M2[i2, r] = sum_i1 A1[i1, r] D
-  int mode2;
-  double* m2part;         // [(tfirst + tile) * 4 + warp][2 segments][64]
-  const int* active;      // per-block activity (ALS) or null
   double* bsum;           // [s][RSTRIDE]
   const int* gate;
   unsigned long long* tl; // iteration timeline (profiling) or null
@@ -123,8 +119,6 @@ struct XtcArgs {
 struct XtcPlan {
   int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, u1_bytes = 0, ntiles = 0;
   int grid_cap = 0;          // > 0: at most this many CTAs (SMs left to concurrent work)
-  long long i2max = 1;
-  double* m2part = nullptr;
   size_t smem = 0;
   double bytes = 0.0;
   std::vector<void*> allocs;
@@ -229,32 +223,6 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     b.ut2[e] = (float)A2[i * R + r];
   }
   tl_end(a.tl, TL_PREP);
-}
-
-// --------------------------------------------------------------------------
-// mode-2 fold: M2[i2, r] = scale_r * sum over the warps covering rows
-// [i2 I1, (i2+1) I1) of their i2 segment, in warp order (deterministic)
-// --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_xtc_m2fold(XtcArgs a, double* const* mtt, int S,
-                                                    long long i2max) {
-  griddep_wait();
-  const long long total = (long long)S * i2max * 64;
-  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < total; e += (long long)gridDim.x * 256) {
-    const int s = (int)(e / (i2max * 64));
-    const long long rem = e - (long long)s * i2max * 64;
-    const long long i2 = rem >> 6;
-    const int r = (int)(rem & 63);
-    if (a.active && !a.active[s]) continue;
-    const XtcBlock& b = a.blk[s];
-    if (i2 >= b.I2 || r >= b.R) continue;
-    const long long ra = i2 * b.I1, rb = (i2 + 1) * b.I1 - 1;
-    double t = 0.0;
-    for (long long w = ra / 32; w <= rb / 32; ++w) {
-      const int seg = ((w * 32) / b.I1 == i2) ? 0 : 1;
-      t += a.m2part[(((long long)b.tfirst * 4 + w) * 2 + seg) * 64 + r];
-    }
-    mtt[s][i2 * b.R + r] = t * b.aux[r];
-  }
 }
 
 // --------------------------------------------------------------------------
@@ -386,7 +354,6 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
         for (int k = 0; k <= XTC_PF; ++k) prefetch_next();
       for (int u = u_begin; u < u_end; ++u) {
         const XtcUnit un = a.units[u];
-        if (a.active && !a.active[un.s]) continue;
         const XtcBlock& b = a.blk[un.s];
         const int nch = b.nch;
         if (un.s != cur && !(a.dbg & 4)) {
@@ -423,7 +390,6 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     const uint32_t bbase = smem_u32(bimg);
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
-      if (a.active && !a.active[un.s]) continue;
       const XtcBlock& b = a.blk[un.s];
       const int nch = b.nch;
       if (un.s != cur) {
@@ -478,7 +444,6 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     int rst = XTC_SUB * h, rph = 0;   // first ring stage of this group's next chunk
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
-      if (a.active && !a.active[un.s]) continue;
       const XtcBlock& b = a.blk[un.s];
       const int nch = b.nch;
       const float sx = ldexpf(1.0f, 20 - b.ex);
@@ -571,28 +536,22 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
       }
     };
     int tl = 0, cur = -1;
-    // the tile after the current one (active units only)
-    auto skip_idle = [&](int& uu) {
-      while (uu < u_end && a.active && !a.active[a.units[uu].s]) ++uu;
-    };
+    // the tile after the current one
     int nxt_u = u_begin;
-    skip_idle(nxt_u);
     int nxt_t = nxt_u < u_end ? a.units[nxt_u].t0 : 0;
     auto advance = [&](int& uu, int& tt) {
       if (++tt >= a.units[uu].t1) {
         ++uu;
-        skip_idle(uu);
         if (uu < u_end) tt = a.units[uu].t0;
       }
     };
     if (nxt_u < u_end) {
-      if (!a.mode2) stage_u2(a.units[nxt_u].s, nxt_t, 0);
+      stage_u2(a.units[nxt_u].s, nxt_t, 0);
       advance(nxt_u, nxt_t);
     }
     cp_async_commit();
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
-      if (a.active && !a.active[un.s]) continue;
       const XtcBlock& b = a.blk[un.s];
       const int I1 = (int)b.I1, I2 = (int)b.I2;
       const long long J = b.J;
@@ -610,7 +569,7 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
         cp_async_wait_all();          // this thread's copies for tile t
         named_bar(1, NE);             // everyone's; buf ^ 1 is free again
         if (nxt_u < u_end) {
-          if (!a.mode2) stage_u2(a.units[nxt_u].s, nxt_t, buf ^ 1);
+          stage_u2(a.units[nxt_u].s, nxt_t, buf ^ 1);
           advance(nxt_u, nxt_t);
         }
         cp_async_commit();
@@ -640,7 +599,7 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int r = col0 + j;
-            w[j] = (valid && r < R) ? (a.mode2 ? u1[r * I1] : u1[r * I1] * u2[r]) : 0.0f;
+            w[j] = (valid && r < R) ? u1[r * I1] * u2[r] : 0.0f;
           }
           tmem_wait_ld();
           if (a.dbg & 1) continue;
@@ -652,29 +611,11 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
                                      fma(i2d_exact(l2[j]), 65536.0, -corr[col0 + j])));
             c8[j] = v * (double)w[j];
           }
-          if (a.mode2) {
-            // mode-2 MTTKRP: per warp (32 rows, <= 2 values of i2 since
-            // I1 >= 32) one partial per i2 segment, folded per i2 later
-            const long long row0 = (long long)t * XTC_M + wq * 32;
-            const int i2w = row0 < J ? (int)(row0 / I1) : 0;
-            const bool s1 = valid && i2 != i2w;
-            double ca[8], cb[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { ca[j] = s1 ? 0.0 : c8[j]; cb[j] = s1 ? c8[j] : 0.0; }
-            const double fa = fold8(ca, lane);
-            const double fb = fold8(cb, lane);
-            if ((lane & 3) == 0) {
-              const long long pidx = ((long long)(b.tfirst + t) * 4 + wq) * 2;
-              a.m2part[pidx * 64 + col0 + (lane >> 2)] = fa;
-              a.m2part[(pidx + 1) * 64 + col0 + (lane >> 2)] = fb;
-            }
-          } else {
-            acc[cg] += fold8(c8, lane);
-          }
+          acc[cg] += fold8(c8, lane);
         }
         tc_fence_before();
         mbar_arrive(&d_empty[buf]);
-        if (t == un.t1 - 1 && !a.mode2) {
+        if (t == un.t1 - 1) {
           // unit done: fixed-order reduction over the 128 rows
 #pragma unroll
           for (int j = 0; j < NH / 8; ++j) {
@@ -773,7 +714,7 @@ static size_t xtc_smem_for(int nst, int bimg_max, int u1_bytes) {
 }
 
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
-                    cudaStream_t st, XtcPlan** out, int mode2) {
+                    cudaStream_t st, XtcPlan** out) {
   *out = nullptr;
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
@@ -867,7 +808,6 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   XTRY(dalloc((void**)&p->blk, sizeof(XtcBlock) * S, A));
   XTRY(dalloc((void**)&p->units, sizeof(XtcUnit) * hu.size(), A));
   XTRY(dalloc((void**)&p->part, sizeof(double) * 64 * hu.size(), A));
-  if (mode2) XTRY(dalloc((void**)&p->m2part, sizeof(double) * 64 * 8 * (size_t)p->ntiles, A));
   XTRY(dalloc((void**)&p->cnt, sizeof(int) * S, A));
   XTRY(dalloc((void**)&p->maxbits, sizeof(unsigned int) * S, A));
   XTRY(dalloc((void**)&aux, sizeof(double) * 128 * S, A));
@@ -882,7 +822,6 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     uo += 64 * (b.I1 + b.I2);
     b.bimg = bimg + bo;
     b.X = reinterpret_cast<const float*>(X[s]);
-    p->i2max = std::max(p->i2max, b.I2);
     bo += b.bimg_bytes;
   }
   CB_CUDA(cudaMemcpyAsync(p->tmaps, hm.data(), sizeof(CUtensorMap) * S, cudaMemcpyHostToDevice, st));
@@ -965,50 +904,12 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.bsum = bsum;
   a.gate = gate;
   a.tl = p->tl;
-  a.mode2 = 0;
-  a.m2part = nullptr;
-  a.active = nullptr;
   switch (p->N) {
     case 16: return xtc_go<16>(p, a, U_dev, st, parts);
     case 32: return xtc_go<32>(p, a, U_dev, st, parts);
     case 48: return xtc_go<48>(p, a, U_dev, st, parts);
     default: return xtc_go<64>(p, a, U_dev, st, parts);
   }
-}
-
-int xtc_mode2(XtcPlan* p, const double* const* U_dev, const int* active, double* const* mtt,
-              cudaStream_t st) {
-  if (!p->m2part) {
-    set_error("xtc plan was not created for the mode-2 MTTKRP");
-    return CB_ERR_STATE;
-  }
-  XtcArgs a{};
-  memset(&a, 0, sizeof(a));
-  a.tmaps = p->tmaps;
-  a.blk = p->blk;
-  a.units = p->units;
-  a.nunits = p->nunits;
-  a.nst = p->nst;
-  a.bimg_max = p->bimg_max;
-  a.u1_bytes = p->u1_bytes;
-  a.part = p->part;
-  a.cnt = p->cnt;
-  a.mode2 = 1;
-  a.m2part = p->m2part;
-  a.active = active;
-  int rc;
-  switch (p->N) {
-    case 16: rc = xtc_go<16>(p, a, U_dev, st); break;
-    case 32: rc = xtc_go<32>(p, a, U_dev, st); break;
-    case 48: rc = xtc_go<48>(p, a, U_dev, st); break;
-    default: rc = xtc_go<64>(p, a, U_dev, st); break;
-  }
-  if (rc) return rc;
-  const long long total = (long long)p->S * p->i2max * 64;
-  const int grid = (int)std::max(1LL, std::min((total + 255) / 256, 148LL * 8));
-  CB_CUDA(launch_k(k_xtc_m2fold, dim3(grid), dim3(256), 0, st, a, mtt, p->S, p->i2max));
-  count_launch(1);
-  return CB_OK;
 }
 
 }  // namespace cb
@@ -1029,7 +930,7 @@ extern "C" int cb_core_linear_term_tc(int n_blocks, const void* const* tensors,
   }
   cudaStream_t st = (cudaStream_t)stream;
   XtcPlan* p = nullptr;
-  int rc = xtc_plan_create(n_blocks, tensors, d.data(), ranks, st, &p, 0);
+  int rc = xtc_plan_create(n_blocks, tensors, d.data(), ranks, st, &p);
   if (rc) return rc;
   const double** dU = nullptr;
   cudaError_t e = cudaMalloc((void**)&dU, sizeof(double*) * 3 * n_blocks);

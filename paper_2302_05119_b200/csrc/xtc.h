@@ -23,7 +23,7 @@ bool xtc_supported(int S, const void* const* X, const long long* dims, const int
 // per-block tensor maps, unit tables, the per-block fixed-point exponent of X
 // (one max|X| pass, enqueued on `st`), operand images and partial buffers
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
-                    cudaStream_t st, XtcPlan** out, int mode2 = 0);
+                    cudaStream_t st, XtcPlan** out);
 void xtc_plan_destroy(XtcPlan* p);
 
 // b_s into bsum[s * RSTRIDE + r] (r < R[s]); factors from U (device array of
@@ -31,13 +31,6 @@ void xtc_plan_destroy(XtcPlan* p);
 // null).  Two launches: operand prep + the streaming MMA kernel.
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
               cudaStream_t st, int parts = 3);
-
-// mode-2 MTTKRP on the same pipeline (the ALS compression of rank > 16
-// blocks; plan created with mode2 = 1, I1 >= 32): mtt[s] (device array of S
-// pointers) gets M2[i2 * R + r] = sum_{i0,i1} X[i0,i1,i2] A0[i0,r] A1[i1,r];
-// blocks with active[s] == 0 are skipped.  Three launches (prep, stream, fold).
-int xtc_mode2(XtcPlan* p, const double* const* U_dev, const int* active, double* const* mtt,
-              cudaStream_t st);
 
 // cap the streaming kernel's persistent grid (0: one CTA per SM), leaving
 // SMs to work that runs beside it (the pipelined lra sweep)

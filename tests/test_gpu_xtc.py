@@ -120,35 +120,40 @@ def test_tc_trace_c5_block(P):
     assert rel.max() < 1e-7, rel.max()
 
 
-def test_tc_mode2_als_matches_fp64_als(P):
-    """ALS compression with the mode-2 MTTKRP on the tensor cores
-    (SolverOptions(compute="tc"), csrc/xtc.cu xtc_mode2) against the fp64
-    passes: the relative-error history within 1e-5 relative per sweep on these
-    small blocks (128K elements: the 2^-21 input rounding averages over few
-    products; 2e-11 measured on 400^3 c5 blocks, tools/als_probe.py)."""
+def test_plane_gemm_als_small_blocks_match_fp64_als(P):
+    """ALS compression with both tensor passes as exact int8 slice GEMMs over
+    the packed byte planes (csrc/xoz.cu: ragged tiles, K not a multiple of 32,
+    rank buckets 32 and 48) against the fp64-storage ALS on the same values:
+    relative-error histories within 1e-10 absolute per sweep, factors within
+    1e-8 relative after 12 sweeps."""
     import torch
     from paper_2302_05119_b200 import _lib as L
     from paper_2302_05119_b200 import _device as D
     from paper_2302_05119_b200.cpd_als import als_compress_blocks
     rng = np.random.default_rng(21)
-    shapes = [((64, 40, 50), 20), ((96, 36, 30), 20)]
-    devs, dims = [], []
+    shapes = [((64, 40, 50), 20), ((96, 36, 30), 24), ((70, 45, 33), 40), ((33, 70, 45), 17)]
+    dev32, dims = [], []
     for d, r in shapes:
         x, _ = _block(rng, d, r)
         flat, dd = D.tensor_to_dev(x, "fp32")
-        devs.append(flat)
+        dev32.append(flat)
         dims.append(dd)
+    dev64 = [f.to(torch.float64) for f in dev32]
+    ranks = [r for _, r in shapes]
     st = L.c_vp(torch.cuda.current_stream().cuda_stream)
     out = {}
-    for code in (0, 2):
-        h = als_compress_blocks(devs, dims, [20, 20], 1e-30, 12, [0, 1], L.CB_F32, st, code,
-                                total_blocks=2)
-        out[code] = [h.block(s)[2] for s in range(2)]
+    for code, data in ((L.CB_F32, dev32), (L.CB_F64, dev64)):
+        h = als_compress_blocks(data, dims, ranks, 1e-30, 12, list(range(len(shapes))), code, st, 0,
+                                total_blocks=len(shapes))
+        out[code] = [h.block(s) for s in range(len(shapes))]
         h.close()
-    for s in range(2):
-        a, b = np.asarray(out[0][s]), np.asarray(out[2][s])
-        assert len(a) == len(b) == 12
-        np.testing.assert_allclose(b, a, rtol=1e-5, atol=0)
+    for s in range(len(shapes)):
+        fa, _, ha, na, _ = out[L.CB_F32][s]
+        fb, _, hb, nb, _ = out[L.CB_F64][s]
+        assert na == nb == 12
+        np.testing.assert_allclose(ha, hb, rtol=0, atol=1e-10)
+        for a, b in zip(fa, fb):
+            assert np.abs(a - b).max() <= 1e-8 * np.abs(b).max()
 
 
 @pytest.mark.parametrize("tol,max_iter", [(1e-30, 40), (1e-5, 400)])
@@ -180,9 +185,9 @@ def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, tol, max_iter):
 
 @pytest.mark.parametrize("name,blocks", [("c5", [0, 1]), ("c3", [0, 1, 2])])
 def test_gemm_pass_als_matches_explicit_fp64_als(P, name, blocks):
-    """The fp32-storage ALS of ranks > 16 (both tensor passes as fp64 GEMMs
-    over TMA boxes, residual by the gram expansion; csrc/xslab5.cu k_tg_pass /
-    k_sl5_dpass, csrc/als.cu) against the fp64-storage ALS on the same values
+    """The fp32-storage ALS of ranks > 16 (both tensor passes as exact int8
+    slice GEMMs on the tensor cores over packed byte planes, residual by the
+    gram expansion; csrc/xoz.cu, csrc/als.cu) against the fp64-storage ALS on the same values
     (explicit residual, the reference's formula cpd_als.py:107-110): the
     relative-error histories within 1e-10 absolute per sweep, same number of
     sweeps, factors within 1e-8 relative."""
