@@ -4,55 +4,49 @@
 // cores with EXACT integer accumulation.
 //
 // Formulation.  View block s as the row-major matrix Xr (rows = (i1,i2),
-// J = I1*I2 rows; K = i0, I0 columns; the storage order of X, first index
-// fastest, makes every row contiguous).  Then
+// J = I1*I2 rows; K = i0, I0 columns).  Then
 //      D = Xr . A0          (J x R, a GEMM with K = I0)
 //      b[r] = sum_rows A1[i1,r] A2[i2,r] D[row,r]   (fp64 epilogue)
-// The reference computes in fp64; this pass reaches ~2^-20 relative per
+// The reference computes in fp64; this pass reaches ~2^-22 relative per
 // product with zero bias, via fixed-point byte slices and int8 MMAs:
-//   * X: one exponent per block (max|X| (1 + 2^-20) = m 2^eX), q =
-//     rint(x 2^(20-eX)), |q| < 2^20, offset q' = q + 0x208080 in [0, 2^22)
-//     as bytes q' = a0 2^16 + (a1 + 128) 2^8 + (a2 + 128): a0 in [16, 48]
-//     unsigned, a1, a2 in [-128, 127] signed, i.e. q + 2^21 = a0 2^16 +
-//     a1 2^8 + a2 with balanced low digits (all zero for x = 0).  One FFMA
-//     with a magic constant puts q' in the low mantissa bits; PRMT picks the
-//     bytes, one XOR recentres the low two.
+//   * X: one exponent per block (max|X| = m 2^eX, m in [0.5, 1)), q =
+//     rint(x 2^(22-eX)) = a0 2^16 + a1 2^8 + a2 with balanced signed bytes
+//     (a0 in [-64, 64]).  The three byte planes are written ONCE per solve
+//     (k_xtc_pack) in the MMA's shared-memory layout (K-major rows of 32
+//     bytes, 32-byte swizzle), tile by tile: an iteration then streams 3
+//     bytes per element instead of 4 and does no conversion work
+//     (the previous form of this pass converted fp32 tiles in 8 warps per
+//     SM and was bound by them at 38 GB/s per SM).
 //   * A0: one exponent per column, p = rint(u 2^(22-eU_r)) as balanced
-//     signed bytes p = b0 2^16 + b1 2^8 + b2 (b0 in [-64, 64]).
-//   * sum_k (q_k + 2^21) p_k = 2^32 L0 + 2^24 L1 + 2^16 L2 + (dropped
-//     levels 3-4), L0 = a0.b0, L1 = a0.b1 + a1.b0, L2 = a0.b2 + a1.b1 +
-//     a2.b0: six M=128 x N x K=32 kind::i8 MMAs per 32-column chunk into
-//     three int32 TMEM accumulators (exact; |L| < 2^31 for I0 <= 60000).
-//     The dropped terms are products of two balanced signed digits, ~2^-20
-//     of a product, zero-mean (and zero where x = 0); sum_k q_k p_k = that -
-//     2^21 sum_k p_k (exact correction).
-// Error: unbiased rounding of x (2^-21 of the block max) and u (2^-23 of the
-// column max); measured ~2e-8 relative on b (the A0 rounding is shared by
-// all rows, so it averages over K only).  The lra objective's cancellation
-// (res ~ 1% of |M|^2 at 20 dB) turns that into ~2e-6 on RelErr, inside the
-// fp32-mode 1e-4 (tests/test_gpu_xtc.py, tests/test_gpu_solve.py).
+//     signed bytes p = b0 2^16 + b1 2^8 + b2 (b0 in [-64, 64]), per call.
+//   * sum_k q_k p_k = 2^32 L0 + 2^24 L1 + 2^16 L2 + (dropped levels 3-4),
+//     L0 = a0.b0, L1 = a0.b1 + a1.b0, L2 = a0.b2 + a1.b1 + a2.b0: three
+//     M=128 x N x K=32 kind::i8 MMAs per K step (a_i x [b_0 | .. | b_{2-i}])
+//     into three int32 TMEM accumulators (exact; |L| < 2^31 for I0 <= 32768).
+//     The dropped terms are products of two balanced signed digits, ~2^-21
+//     of a product, zero-mean (and zero where x = 0).
+// Error: unbiased rounding of x (2^-23 of the block max) and u (2^-23 of the
+// column max); measured ~1e-8 relative on b.  The lra objective's
+// cancellation (res ~ 1% of |M|^2 at 20 dB) turns that into ~1e-6 on RelErr,
+// inside the fp32-mode 1e-4 (tests/test_gpu_xtc.py, tests/test_gpu_solve.py).
 //
 // Kernel (persistent, one CTA per SM, 320 threads):
-//   warp 9  : TMA producer — 2-D tensor-map tiles of 128 rows x 32 fp32
-//             (128-B swizzle) into an NST-stage ring, plus the block's B
-//             image (prepared by k_xtc_prep) by 1-D bulk copy per segment;
-//   warp 8  : MMA issuer — one lane issues tcgen05.mma (A from TMEM, B from
-//             shared memory), tcgen05.commit frees A slots / publishes D;
-//   warps 0-7: two groups of 4 (one warp per TMEM lane quarter) alternate
-//             chunks: shared -> registers (conflict-free swizzled float4
-//             reads), byte slicing, tcgen05.st into a TMEM A slot; and the
-//             epilogue (tcgen05.ld of the int32 levels, fp64 combine, A1/A2
-//             weights, per-thread fp64 row sums), each group for half of the
-//             N columns.
-// TMEM: 6 A slots (4 for N = 64) x 32 columns, 2 D buffers x 3 levels x N
-// columns (<= 512).  Row weights A1[i1,r] A2[i2,r] are fp32 (transposed
-// tables, loaded while the next tile converts); column constants in smem.
+//   warp 9  : producer - 12 KB bulk copies (one K = 32 step of a tile, three
+//             planes) into an NST-stage ring, plus the block's B image
+//             (prepared by k_xtc_prep) per segment;
+//   warp 8  : MMA issuer - one lane issues tcgen05.mma (A and B from shared
+//             memory), tcgen05.commit frees ring stages / publishes D;
+//   warps 0-7: epilogue, two groups of 4 (one warp per TMEM lane quarter, half
+//             of the N columns each): tcgen05.ld of the int32 levels, fp64
+//             combine, A1/A2 weights, fixed-order folds.
+// TMEM: 2 D buffers x 3 levels x N columns.  Row weights A1[i1,r] A2[i2,r]
+// are fp32 (transposed tables: A1's read from L2 ahead of the wait on D, the
+// tile's few A2 rows staged); column constants in smem.
 // Units of 8 tiles (never straddling a block) are the partial granularity:
 // partials are reduced in fixed order and folded per block in unit order by
 // the last arriving CTA, so b is bitwise independent of the grid size and
 // of how blocks are sharded over GPUs.
 #include <cuda.h>
-#include <cudaTypedefs.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -70,45 +64,39 @@
 namespace cb {
 
 constexpr int XTC_M = 128;                        // rows per tile (MMA M)
-constexpr int XTC_KC = 32;                        // fp32 columns per TMA box (= MMA K of int8)
-constexpr int XTC_SUB = 2;                        // boxes per chunk (one sync round trip)
-constexpr int XTC_BOX = XTC_M * XTC_KC * 4;       // 16 KB
-constexpr int XTC_STAGE = XTC_BOX;                // 16 KB per ring stage (a chunk = SUB stages)
+constexpr int XTC_SX = 3;                         // byte planes of X
+constexpr int XTC_PIECE = XTC_M * 32;             // 4 KB: one plane of one K = 32 step
+constexpr int XTC_STAGE = XTC_SX * XTC_PIECE;     // 12 KB per ring stage
 constexpr int XTC_TPU = 8;                        // tiles per unit
 constexpr int XTC_MAX_I0 = 512;
-// warps: 8 converters, 4 EG epilogue (EG = 1 for N <= 48, else 2), MMA, TMA
-template <int N> __host__ __device__ constexpr int xtc_eg() { return 2; }
+constexpr int XTC_XBITS = 22;
+constexpr int XTC_UBITS = 22;
 constexpr int XTC_U2R = 8;        // A2 rows staged per tile
-constexpr int XTC_PF = 0;         // tiles bulk-prefetched into L2 ahead (0: off; 1 measured slower)
-template <int N> __host__ __device__ constexpr int xtc_threads() { return (10 + 4 * xtc_eg<N>()) * 32; }
+constexpr int XTC_THREADS = 320;  // 8 epilogue warps, MMA, producer
 constexpr int XTC_SMEM_MAX = 227 * 1024;
-constexpr float XTC_MAGIC = 14712960.0f;          // 1.5 * 2^23 + 0x208080
 
 struct XtcBlock {
   long long I0, I1, I2, J;
-  int R, ntiles, nch;
+  int R, ntiles, nk;
   int ex;                 // fixed-point exponent of X
   int ufirst, nunits;
-  int tfirst;             // first tile of the block in the solve's tile numbering
   int bimg_bytes;
-  double* aux;            // [0,64): scale_r; [64,128): 2^21 sum_k p_kr
+  double* aux;            // [0,64): scale_r
   float* ut1;             // [r][I1] = A1[i1, r] (fp32 row weights)
   float* ut2;             // [r][I2] = A2[i2, r]
-  const float* X;         // the block (for L2 prefetch of whole tiles)
-  unsigned char* bimg;    // 3 slices x (SUB nch) K=32 steps x N rows x 32 B (K-major, 32-B swizzle)
+  const float* X;         // the block (read by the pack kernel only)
+  unsigned char* planes;  // [ntiles][nk][3 planes][128 rows x 32 B]
+  unsigned char* bimg;    // [nk][3 N rows][32 B] (K-major, 32-B swizzle)
 };
 
 struct XtcUnit { int s, t0, t1, u; };
 
 struct XtcArgs {
-  const CUtensorMap* tmaps;
   const XtcBlock* blk;
   const XtcUnit* units;
   int nunits;
   int nst;
   int bimg_max;
-  int dbg;                 // experiments: 1 = no epilogue math, 2 = no conversion math
-  int u1_bytes;            // smem bytes of the staged A1^T table (0: read it from L2)
   double* part;           // [unit][64]
   int* cnt;               // per-block arrival counters (self-resetting)
   double* bsum;           // [s][RSTRIDE]
@@ -117,12 +105,12 @@ struct XtcArgs {
 };
 
 struct XtcPlan {
-  int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, u1_bytes = 0, ntiles = 0;
+  int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, ntiles = 0;
   int grid_cap = 0;          // > 0: at most this many CTAs (SMs left to concurrent work)
   size_t smem = 0;
-  double bytes = 0.0;
+  double bytes = 0.0;        // algorithmic: sum_s |X_s| x 4
+  double stream_bytes = 0.0; // plane bytes one launch streams
   std::vector<void*> allocs;
-  CUtensorMap* tmaps = nullptr;
   XtcBlock* blk = nullptr;
   XtcUnit* units = nullptr;
   double* part = nullptr;
@@ -132,7 +120,7 @@ struct XtcPlan {
 };
 
 // --------------------------------------------------------------------------
-// one-time: per-block max |X| (as float bits) and the exponent eX
+// one-time: per-block max |X| (as float bits), the exponent eX, the planes
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_xtc_maxabs(const float* __restrict__ X, long long n,
                                                     unsigned int* out) {
@@ -148,13 +136,61 @@ __global__ void k_xtc_set_ex(XtcBlock* blk, const unsigned int* maxbits, int S) 
   if (s >= S) return;
   const float m = __uint_as_float(maxbits[s]);
   int e = 0;
-  if (m > 0.0f && isfinite(m)) frexpf(m * 1.00000095367431640625f, &e);
+  if (m > 0.0f && isfinite(m)) frexpf(m, &e);   // m = f 2^e, f in [0.5, 1)
   blk[s].ex = e;
+}
+
+// byte `byte` of four words as one word (k increasing with the address)
+__device__ __forceinline__ uint32_t pick4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                          int byte) {
+  const uint32_t sel = (uint32_t)byte | ((uint32_t)(byte + 4) << 4);
+  return __byte_perm(__byte_perm(t0, t1, sel), __byte_perm(t2, t3, sel), 0x5410);
+}
+
+// grid (max tiles, 1, S), 128 threads: each warp transposes its 32 rows of a
+// K = 32 step through shared memory (k is contiguous in X), thread m then
+// owns row m: q + 0x8080 = a0 2^16 + (a1 + 128) 2^8 + (a2 + 128)
+__global__ void __launch_bounds__(XTC_M) k_xtc_pack(const XtcBlock* blk) {
+  const XtcBlock& b = blk[blockIdx.z];
+  const int t = blockIdx.x;
+  if (t >= b.ntiles) return;
+  __shared__ float tile[XTC_M][33];
+  const int m = threadIdx.x;
+  const int warp = m >> 5, lane = m & 31;
+  const float sx = ldexpf(1.0f, XTC_XBITS - b.ex);
+  const float* __restrict__ X = b.X;
+  const int sw = (m >> 2) & 1;
+  for (int c = 0; c < b.nk; ++c) {
+    const int kk = c * 32 + lane;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const long long rr = (long long)t * XTC_M + warp * 32 + r;
+      tile[warp * 32 + r][lane] = (rr < b.J && kk < b.I0) ? __ldcs(X + rr * b.I0 + kk) : 0.0f;
+    }
+    __syncwarp();
+    uint32_t q[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) q[k] = (uint32_t)(__float2int_rn(tile[m][k] * sx) + 0x8080);
+    __syncwarp();
+    unsigned char* dst = b.planes + ((long long)t * b.nk + c) * XTC_STAGE + m * 32;
+#pragma unroll
+    for (int i = 0; i < XTC_SX; ++i) {
+      uint32_t w[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        w[g] = pick4(q[4 * g], q[4 * g + 1], q[4 * g + 2], q[4 * g + 3], 2 - i);
+        if (i > 0) w[g] ^= 0x80808080u;
+      }
+      uint4* d = reinterpret_cast<uint4*>(dst + i * XTC_PIECE);
+      d[sw] = make_uint4(w[0], w[1], w[2], w[3]);
+      d[sw ^ 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
 }
 
 // --------------------------------------------------------------------------
 // per call: A0 -> signed byte-slice image (the MMA B operand, exactly the
-// shared-memory layout), column scales and digit sums, A1/A2 transposed
+// shared-memory layout), column scales, A1/A2 transposed
 // --------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const* U) {
@@ -182,19 +218,17 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     }
   }
   __syncthreads();
-  const int kmax = b.nch * XTC_SUB * 32;
+  const int kmax = b.nk * 32;
   for (int e = threadIdx.x; e < kmax * N; e += 256) {
     const int k = e / N, n = e - (e / N) * N;
     long long p = 0;
-    if (k < I0 && n < R) p = llrint(ldexp(A0[(long long)k * R + n], 22 - eu[n]));
+    if (k < I0 && n < R) p = llrint(ldexp(A0[(long long)k * R + n], XTC_UBITS - eu[n]));
     const long long d2 = ((p + 128) & 255) - 128;
     const long long p1 = (p - d2) >> 8;
     const long long d1 = ((p1 + 128) & 255) - 128;
     const long long d0 = (p1 - d1) >> 8;
-    // chunk c = k / 32: N rows of 32 bytes, 16-byte halves swapped on rows
-    // with bit 2 set (Swizzle<1,4,3> of a 256-byte atom)
     // K step c = k / 32 holds the three slices as one operand of 3N rows
-    // ([b0 | b1 | b2], so one MMA covers a digit of A times all three), rows
+    // ([b0 | b1 | b2], so one MMA covers a digit of X times all three), rows
     // of 32 bytes, 16-byte halves swapped on rows with bit 2 set
     // (Swizzle<1,4,3> of a 256-byte atom; N % 16 == 0 keeps it per slice)
     const int c = k >> 5, kk = k & 31;
@@ -203,15 +237,10 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     b.bimg[off + N * 32] = (unsigned char)(signed char)d1;
     b.bimg[off + 2 * N * 32] = (unsigned char)(signed char)d2;
   }
-  for (int r = warp; r < N; r += 8) {
-    double t = 0.0;   // integers < 2^30: exact in any order
-    if (r < R)
-      for (int i = lane; i < I0; i += 32) t += (double)llrint(ldexp(A0[(long long)i * R + r], 22 - eu[r]));
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) {
-      b.aux[r] = r < R ? ldexp(1.0, b.ex - 20 + eu[r] - 22) : 0.0;
-      b.aux[64 + r] = ldexp(t, 21);
-    }
+  if (threadIdx.x < 64) {
+    const int r = threadIdx.x;
+    // q p = 2^16 (2^16 L0 + 2^8 L1 + L2)
+    b.aux[r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS) : 0.0;
   }
   const long long I1 = b.I1, I2 = b.I2;
   for (long long e = threadIdx.x; e < (long long)R * I1; e += 256) {
@@ -228,17 +257,6 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
 // --------------------------------------------------------------------------
 // the streaming MMA kernel
 // --------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t pick3(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
-                                          int byte) {
-  const uint32_t sel = (uint32_t)byte | ((uint32_t)(byte + 4) << 4);
-  const uint32_t lo = __byte_perm(t0, t1, sel);
-  const uint32_t hi = __byte_perm(t2, t3, sel);
-  return __byte_perm(lo, hi, 0x5410);
-}
-
-template <int N>
-__host__ __device__ constexpr int xtc_nsl() { return N <= 48 ? 4 : 2; }   // TMEM A slots
-
 // sum over the 32 lanes of v[0..8) by recursive halving (9 fp64 shuffles
 // instead of 40); lane l ends with the total of value l / 4.  Fixed order:
 // bitwise deterministic.
@@ -268,60 +286,40 @@ __device__ __forceinline__ double i2d_exact(uint32_t x) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
+__global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
   tl_begin(a.tl, TL_TRACE);
-  constexpr int EG = xtc_eg<N>();    // epilogue groups
-  constexpr int NH = N / EG;         // columns per epilogue group
-  constexpr int NE = 128 * EG;       // epilogue threads
-  constexpr int WMMA = 8 + 4 * EG, WTMA = WMMA + 1;
-  constexpr int NSL = xtc_nsl<N>();  // TMEM A slots (even: slot parity = group)
-  constexpr uint32_t SLOTW = 24u * XTC_SUB;   // 3 slices x SUB x 8 columns
-  constexpr uint32_t DBASE = SLOTW * NSL;
+  constexpr int NH = N / 2;          // columns per epilogue group
+  constexpr int NE = 256;            // epilogue threads
+  constexpr int WMMA = 8, WTMA = 9;
+  constexpr int DW = 3 * N;          // accumulator columns per buffer
   extern __shared__ unsigned char xtc_raw[];
   const uint32_t raw_u32 = smem_u32(xtc_raw);
   unsigned char* sm = xtc_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
-  const int nst = a.nst;             // power of two
+  const int nst = a.nst;
   unsigned char* ring = sm;
   unsigned char* bimg = sm + (size_t)nst * XTC_STAGE;
-  float* u1s = reinterpret_cast<float*>(bimg + a.bimg_max);       // [r][I1] of the segment
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bimg + a.bimg_max + a.u1_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bimg + a.bimg_max);
   uint64_t* full = bars;
   uint64_t* empty = bars + nst;
-  uint64_t* a_full = bars + 2 * nst;
-  uint64_t* a_empty = a_full + 8;
-  uint64_t* d_full = a_empty + 8;
+  uint64_t* d_full = empty + nst;
   uint64_t* d_empty = d_full + 2;
   uint64_t* b_full = d_empty + 2;
   uint64_t* b_empty = b_full + 1;
-  double* red = reinterpret_cast<double*>(b_empty + 1);      // [EG groups][4 warps][64]
-  double* auxs = red + 512;                                  // [128] of the segment
-  float* u2s = reinterpret_cast<float*>(auxs + 128);         // [2][XTC_U2R][64]
+  double* red = reinterpret_cast<double*>(b_empty + 1);      // [2 groups][4 warps][64]
+  double* auxs = red + 512;                                  // [64] of the segment
+  float* u2s = reinterpret_cast<float*>(auxs + 64);          // [2][XTC_U2R][64]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u2s + 2 * XTC_U2R * 64);
   int* shflag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
-  // experiments (CB_XTC_DBG & 8): cycles each role spends in its waits
-  long long twait[6] = {0, 0, 0, 0, 0, 0};
-  const long long t_start = clock64();
-#define XTC_TW(k, call)                                  \
-  do {                                                   \
-    if (a.dbg & 8) {                                     \
-      const long long t0_ = clock64();                   \
-      call;                                              \
-      twait[k] += clock64() - t0_;                       \
-    } else {                                             \
-      call;                                              \
-    }                                                    \
-  } while (0)
   const int u_begin = (int)((long long)blockIdx.x * a.nunits / G);
   const int u_end = (int)((long long)(blockIdx.x + 1) * a.nunits / G);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < nst; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 128); }
-    for (int i = 0; i < NSL; ++i) { mbar_init(&a_full[i], 128); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < nst; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], NE); }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
@@ -338,25 +336,11 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     if (lane == 0) {
       int st = 0, ph = 0, seg = 0, cur = -1;
       const uint64_t pol = l2_evict_first_policy();
-      // L2 prefetch runs XTC_PF tiles ahead of the ring: a tile (128 rows x
-      // I0) is one contiguous span, one bulk prefetch
-      int pu = u_begin, pt = a.units[u_begin].t0;
-      auto prefetch_next = [&]() {
-        if (pu >= u_end) return;
-        const XtcUnit pn = a.units[pu];
-        const XtcBlock& pb = a.blk[pn.s];
-        const long long r0 = (long long)pt * XTC_M;
-        const long long nr = min((long long)XTC_M, pb.J - r0);
-        bulk_prefetch_l2(pb.X + r0 * pb.I0, (uint32_t)(nr * pb.I0 * 4));
-        if (++pt >= pn.t1) { ++pu; if (pu < u_end) pt = a.units[pu].t0; }
-      };
-      if (XTC_PF > 0)
-        for (int k = 0; k <= XTC_PF; ++k) prefetch_next();
       for (int u = u_begin; u < u_end; ++u) {
         const XtcUnit un = a.units[u];
         const XtcBlock& b = a.blk[un.s];
-        const int nch = b.nch;
-        if (un.s != cur && !(a.dbg & 4)) {
+        const int nk = b.nk;
+        if (un.s != cur) {
           mbar_wait(b_empty, (seg & 1) ^ 1);
           const int bytes = b.bimg_bytes;
           mbar_arrive_expect_tx(b_full, (uint32_t)bytes);
@@ -365,14 +349,13 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
           cur = un.s;
           ++seg;
         }
-        const CUtensorMap* tm = a.tmaps + un.s;
         for (int t = un.t0; t < un.t1; ++t) {
-          if (XTC_PF > 0) prefetch_next();
-          for (int c = 0; c < nch * XTC_SUB; ++c) {
-            XTC_TW(0, mbar_wait(&empty[st], ph ^ 1));
+          const unsigned char* src = b.planes + (long long)t * nk * XTC_STAGE;
+          for (int c = 0; c < nk; ++c) {
+            mbar_wait(&empty[st], ph ^ 1);
             mbar_arrive_expect_tx(&full[st], XTC_STAGE);
-            tma_load_2d_stream(ring + (size_t)st * XTC_STAGE, tm, c * XTC_KC, t * XTC_M, &full[st],
-                               pol);
+            bulk_g2s_hint(ring + (size_t)st * XTC_STAGE, src + (size_t)c * XTC_STAGE, XTC_STAGE,
+                          &full[st], pol);
             if (++st == nst) { st = 0; ph ^= 1; }
           }
         }
@@ -380,18 +363,17 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     }
   } else if (warp == WMMA) {
     // --------------------------------------------------------- MMA issuer
-    if (a.dbg & 4) goto done;
     // D[L0 | L1 | L2] += a0 [b0|b1|b2]; D[L1 | L2] += a1 [b0|b1]; D[L2] += a2 b0
-    constexpr uint32_t id0 = idesc_i8(3 * N, 0, 1);   // a0 unsigned x b signed
-    constexpr uint32_t id1 = idesc_i8(2 * N, 1, 1);   // a1 signed
-    constexpr uint32_t id2 = idesc_i8(N, 1, 1);       // a2 signed
-    int g = 0, seg = 0, cur = -1, tl = 0;
-    int slot = 0, sphase = 0;
+    constexpr uint32_t id0 = idesc_i8(3 * N, 1, 1);
+    constexpr uint32_t id1 = idesc_i8(2 * N, 1, 1);
+    constexpr uint32_t id2 = idesc_i8(N, 1, 1);
+    int st = 0, ph = 0, seg = 0, cur = -1, tl = 0;
     const uint32_t bbase = smem_u32(bimg);
+    const uint32_t rbase = smem_u32(ring);
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
       const XtcBlock& b = a.blk[un.s];
-      const int nch = b.nch;
+      const int nk = b.nk;
       if (un.s != cur) {
         mbar_wait(b_full, seg & 1);
         tc_fence_after();
@@ -401,118 +383,38 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
       const bool last_seg = (u + 1 == u_end) || a.units[u + 1].s != un.s;
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
         const int buf = tl & 1;
-        XTC_TW(1, mbar_wait(&d_empty[buf], ((tl >> 1) & 1) ^ 1));
+        mbar_wait(&d_empty[buf], ((tl >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t dc = tmem + DBASE + (uint32_t)(buf * 3 * N);
-        for (int c = 0; c < nch; ++c, ++g) {
-          XTC_TW(2, mbar_wait(&a_full[slot], sphase));
+        const uint32_t dc = tmem + (uint32_t)(buf * DW);
+        for (int c = 0; c < nk; ++c) {
+          mbar_wait(&full[st], ph);
           tc_fence_after();
           if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < XTC_SUB; ++k) {
-              // slot layout: slice j of K step k at column 8 (SUB j + k)
-              const uint32_t ac = tmem + SLOTW * slot + 8u * k;
-              const uint64_t B = sdesc_k_sw32(bbase + (uint32_t)(c * XTC_SUB + k) * 3 * N * 32);
-              const uint32_t acc = (c > 0 || k > 0) ? 1u : 0u;
-              mma_i8_ts(dc, ac, B, id0, acc);
-              mma_i8_ts(dc + N, ac + 8 * XTC_SUB, B, id1, 1u);
-              mma_i8_ts(dc + 2 * N, ac + 16 * XTC_SUB, B, id2, 1u);
-            }
-            tc_commit(&a_empty[slot]);
-            if (c == nch - 1) {
+            const uint32_t ab = rbase + (uint32_t)st * XTC_STAGE;
+            const uint64_t B = sdesc_k_sw32(bbase + (uint32_t)c * 3 * N * 32);
+            mma_i8_ss(dc, sdesc_k_sw32(ab), B, id0, c > 0 ? 1u : 0u);
+            mma_i8_ss(dc + N, sdesc_k_sw32(ab + XTC_PIECE), B, id1, 1u);
+            mma_i8_ss(dc + 2 * N, sdesc_k_sw32(ab + 2 * XTC_PIECE), B, id2, 1u);
+            tc_commit(&empty[st]);
+            if (c == nk - 1) {
               tc_commit(&d_full[buf]);
               if (t == un.t1 - 1 && last_seg) tc_commit(b_empty);
             }
           }
           __syncwarp();
-          if (++slot == NSL) { slot = 0; sphase ^= 1; }
+          if (++st == nst) { st = 0; ph ^= 1; }
         }
       }
     }
-  } else if (warp < 8) {
-    // ------------------------------------------------ converters (warps 0-7)
-    // two groups of 4 (one warp per TMEM lane quarter) alternate chunks
-    const int h = warp >> 2;
-    const int wq = warp & 3;
-    const int m = wq * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    int g = 0;
-    // slot / phase of this group's next chunk: chunks alternate between the
-    // groups, slots cycle through NSL (even), so group h owns the slots of
-    // parity h and advances by 2; ring stages likewise (any nst >= 2)
-    int slot = h, sphase = 0;
-    int rst = XTC_SUB * h, rph = 0;   // first ring stage of this group's next chunk
-    for (int u = u_begin; u < u_end; ++u) {
-      const XtcUnit un = a.units[u];
-      const XtcBlock& b = a.blk[un.s];
-      const int nch = b.nch;
-      const float sx = ldexpf(1.0f, 20 - b.ex);
-      for (int t = un.t0; t < un.t1; ++t) {
-        for (int c = (h - g) & 1; c < nch; c += 2) {
-          // the chunk's SUB stages (consecutive; nst is even and the
-          // group's stages start at multiples of SUB, so no wrap inside)
-          const int st0 = rst, ph0 = rph;
-          rst += 2 * XTC_SUB;
-          if (rst >= nst) { rst -= nst; rph ^= 1; }
-          if (a.dbg & 4) {
-            for (int k = 0; k < XTC_SUB; ++k) {
-              XTC_TW(3, mbar_wait(&full[st0 + k], ph0));
-              mbar_arrive(&empty[st0 + k]);
-            }
-            continue;
-          }
-          XTC_TW(4, mbar_wait(&a_empty[slot], sphase ^ 1));
-          tc_fence_after();
-          const uint32_t ac = trow + SLOTW * slot;
-#pragma unroll
-          for (int k = 0; k < XTC_SUB; ++k) {
-            // a stage into registers, released before its conversion (the
-            // ring stays in flight)
-            XTC_TW(3, mbar_wait(&full[st0 + k], ph0));
-            const float4* rowp =
-                reinterpret_cast<const float4*>(ring + (size_t)(st0 + k) * XTC_STAGE + m * 128);
-            float4 vv[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) vv[q] = rowp[q ^ (m & 7)];
-            mbar_arrive(&empty[st0 + k]);
-            uint32_t w0[8], w1[8], w2[8];
-            if (a.dbg & 2) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) { w0[q] = 0x20202020u; w1[q] = 0; w2[q] = 0; }
-            } else {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const uint32_t t0 = __float_as_uint(fmaf(vv[q].x, sx, XTC_MAGIC));
-                const uint32_t t1 = __float_as_uint(fmaf(vv[q].y, sx, XTC_MAGIC));
-                const uint32_t t2 = __float_as_uint(fmaf(vv[q].z, sx, XTC_MAGIC));
-                const uint32_t t3 = __float_as_uint(fmaf(vv[q].w, sx, XTC_MAGIC));
-                w0[q] = pick3(t0, t1, t2, t3, 2) & 0x3F3F3F3Fu;
-                w1[q] = pick3(t0, t1, t2, t3, 1) ^ 0x80808080u;
-                w2[q] = pick3(t0, t1, t2, t3, 0) ^ 0x80808080u;
-              }
-            }
-            tmem_st8(ac + 8 * k, w0);
-            tmem_st8(ac + 8 * (XTC_SUB + k), w1);
-            tmem_st8(ac + 8 * (2 * XTC_SUB + k), w2);
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&a_full[slot]);
-          slot += 2;
-          if (slot >= NSL) { slot -= NSL; sphase ^= 1; }
-        }
-        g += nch;
-      }
-    }
-  } else if (!(a.dbg & 4)) {
-    // ------------------------------------------ epilogue (warps 8 .. 8+4EG-1)
-    // EG groups of 4 (one warp per lane quarter), each for N/EG of the
+  } else {
+    // ------------------------------------------------ epilogue (warps 0-7)
+    // two groups of 4 (one warp per lane quarter), each for half of the
     // columns: row weights A1[i1,r] (staged per segment) x A2[i2,r] (the
     // tile's few A2 rows, cp.async-staged one tile ahead), the int32 levels
     // of D from TMEM, fp64 row sums per thread; per unit a fixed-order
     // reduction into a partial, per block a fold in unit order
-    const int et = threadIdx.x - 256;
-    const int h = (warp - 8) >> 2;
+    const int et = threadIdx.x;
+    const int h = warp >> 2;
     const int wq = warp & 3;
     const int m = wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
@@ -522,7 +424,7 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
 #pragma unroll
     for (int j = 0; j < NH / 8; ++j) acc[j] = 0.0;
     // stage the A2 rows of tile (s, t) into u2s[buf]: rows i2 of its first
-    // .. last row (<= XTC_U2R of them, else the epilogue reads L2)
+    // .. last row (<= XTC_U2R of them)
     auto stage_u2 = [&](int s, int t, int buf) {
       const XtcBlock& b = a.blk[s];
       const long long r0 = (long long)t * XTC_M;
@@ -553,16 +455,14 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
       const XtcBlock& b = a.blk[un.s];
-      const int I1 = (int)b.I1, I2 = (int)b.I2;
+      const int I1 = (int)b.I1;
       const long long J = b.J;
       const int R = b.R;
       if (un.s != cur) {
         // a new segment: the block's column constants and A1^T table
         cur = un.s;
         named_bar(1, NE);
-        if (et < 128) auxs[et] = b.aux[et];
-        if (a.u1_bytes)
-          for (int e = et; e < R * I1; e += NE) u1s[e] = b.ut1[e];
+        if (et < 64) auxs[et] = b.aux[et];
       }
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
         const int buf = tl & 1;
@@ -578,16 +478,23 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
         const int i2 = valid ? (int)(row / I1) : 0;
         const int i1 = valid ? (int)(row - (long long)i2 * I1) : 0;
         const int i2a = (int)(((long long)t * XTC_M) / I1);
-        const long long r1 = std::min((long long)t * XTC_M + XTC_M, J) - 1;
-        (void)r1;
-        // shared when staged, else the L2-resident table (the ring took
-        // its shared memory: more bytes in flight per SM)
-        const float* u1 = (a.u1_bytes ? u1s : b.ut1) + i1;
-        const float* u2 = u2s + buf * XTC_U2R * 64 + (i2 - i2a) * 64; // shared
-        XTC_TW(5, mbar_wait(&d_full[buf], (tl >> 1) & 1));
+        const float* u2 = u2s + buf * XTC_U2R * 64 + (i2 - i2a) * 64;
+        // this row's A1 weights from the L2-resident transposed table (a
+        // warp reads 32 consecutive floats per column), issued before the
+        // wait on D so the latency hides behind it; shared memory is left to
+        // the ring (more bytes in flight per SM)
+        float w1[NH];
+        {
+          const float* u1 = b.ut1 + i1;
+#pragma unroll
+          for (int j = 0; j < NH; ++j) {
+            const int r = h * NH + j;
+            w1[j] = (valid && r < R) ? __ldg(u1 + (long long)r * I1) : 0.0f;
+          }
+        }
+        mbar_wait(&d_full[buf], (tl >> 1) & 1);
         tc_fence_after();
-        const uint32_t dc = trow + DBASE + (uint32_t)(buf * 3 * N);
-        const double* corr = auxs + 64;
+        const uint32_t dc = trow + (uint32_t)(buf * DW);
 #pragma unroll
         for (int cg = 0; cg < NH / 8; ++cg) {
           const int col0 = h * NH + cg * 8;
@@ -597,18 +504,14 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
           tmem_ld8(dc + 2 * N + col0, l2);
           float w[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int r = col0 + j;
-            w[j] = (valid && r < R) ? u1[r * I1] * u2[r] : 0.0f;
-          }
+          for (int j = 0; j < 8; ++j)   // (unstaged u2 entries of columns >= R are not read)
+            w[j] = (valid && col0 + j < R) ? w1[cg * 8 + j] * u2[col0 + j] : 0.0f;
           tmem_wait_ld();
-          if (a.dbg & 1) continue;
           double c8[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const double v = fma(i2d_exact(l0[j]), 4294967296.0,
-                                 fma(i2d_exact(l1[j]), 16777216.0,
-                                     fma(i2d_exact(l2[j]), 65536.0, -corr[col0 + j])));
+            const double v = fma(i2d_exact(l0[j]), 65536.0,
+                                 fma(i2d_exact(l1[j]), 256.0, i2d_exact(l2[j])));
             c8[j] = v * (double)w[j];
           }
           acc[cg] += fold8(c8, lane);
@@ -652,10 +555,6 @@ __global__ void __launch_bounds__(xtc_threads<N>(), 1) k_xtc_trace(XtcArgs a) {
     }
     cp_async_wait_all();
   }
-done:
-  if ((a.dbg & 8) && blockIdx.x == 0 && lane == 0)
-    printf("xtc cta0 warp %2d: total %lld  waits empty %lld d_empty %lld a_full %lld full %lld a_empty %lld d_full %lld\n",
-           warp, clock64() - t_start, twait[0], twait[1], twait[2], twait[3], twait[4], twait[5]);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -675,52 +574,27 @@ static int n_bucket(int rmax) {
   return 64;
 }
 
-
 bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R) {
   for (int s = 0; s < S; ++s) {
     const long long I0 = dims[3 * s], I1 = dims[3 * s + 1], I2 = dims[3 * s + 2];
     if (I0 < 1 || I1 < 1 || I2 < 1) return false;
-    if (I0 % 4 != 0 || I0 > XTC_MAX_I0) return false;
+    if (I0 > XTC_MAX_I0) return false;
     if (I1 * I2 >= (1LL << 31)) return false;
     if (R[s] < 1 || R[s] > 64) return false;
     if (I1 < 19) return false;            // a tile's rows span <= XTC_U2R values of i2
-    if ((reinterpret_cast<uintptr_t>(X[s]) & 15) != 0) return false;
+    if ((reinterpret_cast<uintptr_t>(X[s]) & 3) != 0) return false;
   }
   return true;
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
-                                         &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
-template <int N>
-static size_t xtc_smem_for(int nst, int bimg_max, int u1_bytes) {
-  return 1024 + (size_t)nst * XTC_STAGE + bimg_max + u1_bytes + 8 * (2 * nst + 22) + 640 * 8 +
+static size_t xtc_smem_for(int nst, int bimg_max) {
+  return 1024 + (size_t)nst * XTC_STAGE + bimg_max + 8 * (2 * nst + 6) + 576 * 8 +
          2 * XTC_U2R * 64 * 4 + 16;
 }
 
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
                     cudaStream_t st, XtcPlan** out) {
   *out = nullptr;
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return CB_ERR_CUDA;
-  }
   XtcPlan* p = new XtcPlan();
   p->S = S;
   int rmax = 1;
@@ -729,117 +603,102 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   const int N = p->N;
   std::vector<XtcBlock> hb(S);
   std::vector<XtcUnit> hu;
-  std::vector<CUtensorMap> hm(S);
   long long ut_elems = 0;
   long long bimg_total = 0;
+  size_t plane_bytes = 0;
+  int ntmax = 1;
   for (int s = 0; s < S; ++s) {
     XtcBlock& b = hb[s];
     b.I0 = dims[3 * s]; b.I1 = dims[3 * s + 1]; b.I2 = dims[3 * s + 2];
     b.J = b.I1 * b.I2;
     b.R = R[s];
     b.ntiles = (int)((b.J + XTC_M - 1) / XTC_M);
-    b.nch = (int)((b.I0 + XTC_SUB * XTC_KC - 1) / (XTC_SUB * XTC_KC));
+    b.nk = (int)((b.I0 + 31) / 32);
     b.ex = 0;
-    b.bimg_bytes = 3 * b.nch * XTC_SUB * N * 32;
+    b.bimg_bytes = 3 * b.nk * N * 32;
     p->bimg_max = std::max(p->bimg_max, b.bimg_bytes);
     b.ufirst = (int)hu.size();
-    b.tfirst = p->ntiles;
     p->ntiles += b.ntiles;
+    ntmax = std::max(ntmax, b.ntiles);
     for (int t = 0; t < b.ntiles; t += XTC_TPU)
       hu.push_back({s, t, std::min(b.ntiles, t + XTC_TPU), (int)hu.size()});
     b.nunits = (int)hu.size() - b.ufirst;
     ut_elems += 64 * (b.I1 + b.I2);
     bimg_total += b.bimg_bytes;
+    plane_bytes += (size_t)b.ntiles * b.nk * XTC_STAGE;
     p->bytes += (double)b.I0 * (double)b.J * 4.0;
-    // tensor map: 2-D {I0 (inner), J}, row pitch I0*4 bytes, 32 x 128 boxes,
-    // 128-byte swizzle (matches the conflict-free float4 reads), OOB -> 0
-    cuuint64_t gdim[2] = {(cuuint64_t)b.I0, (cuuint64_t)b.J};
-    cuuint64_t gstride[1] = {(cuuint64_t)b.I0 * 4};
-    cuuint32_t box[2] = {XTC_KC, XTC_M};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult cr = enc(&hm[s], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(X[s]), gdim,
-                      gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) {
-      delete p;
-      set_error("cuTensorMapEncodeTiled failed (%d) for block %d", (int)cr, s);
-      return CB_ERR_CUDA;
-    }
   }
+  p->stream_bytes = (double)plane_bytes;
   p->nunits = (int)hu.size();
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   p->grid = std::max(1, std::min(nsm, p->nunits));
-  // ring stages: what fits beside the B image, even (each stage then always
-  // serves the same converter group), at least 2
-  // shared memory: the B image, the segment's A1^T table (fp32, N x I1) when
-  // it fits beside a 4-stage ring, then as many ring stages (power of two,
-  // <= 8) as fit
-  long long i1max = 1;
-  for (int s = 0; s < S; ++s) i1max = std::max(i1max, hb[s].I1);
-  int u1b = (int)(((long long)rmax * i1max * 4 + 127) / 128 * 128);
-  auto stages = [&](int u1) {
-    const size_t fixed = xtc_smem_for<16>(0, p->bimg_max, u1);
-    const int n = (int)((XTC_SMEM_MAX - fixed) / (XTC_STAGE + 16));
-    return std::min(n, 12) & ~1;   // even (chunks never wrap), >= 2 SUB
-  };
-  // (reading the A1 table from L2 to free its shared memory for 4 more ring
-  // stages measured slower on c5: the trace pass 3.63 -> 4.54 ms; the
-  // epilogue's row weights need the staged copy)
-  p->u1_bytes = u1b;
-  int nst = stages(u1b);
-  if (nst < 2 * XTC_SUB) {
+  // shared memory: the B image, then as many ring stages (<= 14) as fit
+  const long long room = (long long)XTC_SMEM_MAX - (long long)xtc_smem_for(0, p->bimg_max);
+  const int nst = (int)std::min<long long>(14, room / (XTC_STAGE + 16));
+  if (nst < 3) {
     delete p;
     set_error("xtc: operand image too large (%d bytes)", p->bimg_max);
     return CB_ERR_UNSUPPORTED;
   }
   p->nst = nst;
-  p->smem = xtc_smem_for<16>(nst, p->bimg_max, u1b);
+  p->smem = xtc_smem_for(nst, p->bimg_max);
   // device buffers
   std::vector<void*>& A = p->allocs;
   int rc = CB_OK;
 #define XTRY(x) do { rc = (x); if (rc) { xtc_plan_destroy(p); return rc; } } while (0)
+#define XCUDA(x)                                                       \
+  do {                                                                 \
+    cudaError_t e_ = (x);                                              \
+    if (e_ != cudaSuccess) {                                           \
+      xtc_plan_destroy(p);                                             \
+      return cuda_fail(e_, #x, __FILE__, __LINE__);                    \
+    }                                                                  \
+  } while (0)
   double* aux = nullptr;
   float* ut = nullptr;
   unsigned char* bimg = nullptr;
-  XTRY(dalloc((void**)&p->tmaps, sizeof(CUtensorMap) * S, A));
+  unsigned char* planes = nullptr;
+  // every plane byte is written by the pack kernel: no memset
+  XCUDA(cudaMalloc((void**)&planes, plane_bytes));
+  A.push_back(planes);
   XTRY(dalloc((void**)&p->blk, sizeof(XtcBlock) * S, A));
   XTRY(dalloc((void**)&p->units, sizeof(XtcUnit) * hu.size(), A));
   XTRY(dalloc((void**)&p->part, sizeof(double) * 64 * hu.size(), A));
   XTRY(dalloc((void**)&p->cnt, sizeof(int) * S, A));
   XTRY(dalloc((void**)&p->maxbits, sizeof(unsigned int) * S, A));
-  XTRY(dalloc((void**)&aux, sizeof(double) * 128 * S, A));
+  XTRY(dalloc((void**)&aux, sizeof(double) * 64 * S, A));
   XTRY(dalloc((void**)&ut, sizeof(float) * ut_elems, A));
   XTRY(dalloc((void**)&bimg, (size_t)bimg_total, A));
   long long uo = 0, bo = 0;
+  size_t po = 0;
   for (int s = 0; s < S; ++s) {
     XtcBlock& b = hb[s];
-    b.aux = aux + 128LL * s;
+    b.aux = aux + 64LL * s;
     b.ut1 = ut + uo;
     b.ut2 = ut + uo + 64 * b.I1;
     uo += 64 * (b.I1 + b.I2);
     b.bimg = bimg + bo;
     b.X = reinterpret_cast<const float*>(X[s]);
+    b.planes = planes + po;
+    po += (size_t)b.ntiles * b.nk * XTC_STAGE;
     bo += b.bimg_bytes;
   }
-  CB_CUDA(cudaMemcpyAsync(p->tmaps, hm.data(), sizeof(CUtensorMap) * S, cudaMemcpyHostToDevice, st));
-  CB_CUDA(cudaMemcpyAsync(p->blk, hb.data(), sizeof(XtcBlock) * S, cudaMemcpyHostToDevice, st));
-  CB_CUDA(cudaMemcpyAsync(p->units, hu.data(), sizeof(XtcUnit) * hu.size(), cudaMemcpyHostToDevice, st));
-  CB_CUDA(cudaMemsetAsync(p->cnt, 0, sizeof(int) * S, st));
-  CB_CUDA(cudaMemsetAsync(p->maxbits, 0, sizeof(unsigned int) * S, st));
+  XCUDA(cudaMemcpyAsync(p->blk, hb.data(), sizeof(XtcBlock) * S, cudaMemcpyHostToDevice, st));
+  XCUDA(cudaMemcpyAsync(p->units, hu.data(), sizeof(XtcUnit) * hu.size(), cudaMemcpyHostToDevice, st));
   for (int s = 0; s < S; ++s) {
     const long long n = hb[s].I0 * hb[s].J;
     const int grid = (int)std::max(1LL, std::min((n + 255) / 256, (long long)nsm * 8));
     k_xtc_maxabs<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(X[s]), n, p->maxbits + s);
   }
   k_xtc_set_ex<<<(S + 127) / 128, 128, 0, st>>>(p->blk, p->maxbits, S);
-  CB_CHECK_LAUNCH();
-  count_launch(S + 1);
+  k_xtc_pack<<<dim3((unsigned)ntmax, 1, S), XTC_M, 0, st>>>(p->blk);
+  XCUDA(cudaGetLastError());
+  count_launch(S + 2);
 #define XTC_ATTR(NN)                                                                       \
-  CB_CUDA(cudaFuncSetAttribute(k_xtc_trace<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                               (int)p->smem))
+  XCUDA(cudaFuncSetAttribute(k_xtc_trace<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)p->smem))
   switch (N) {
     case 16: XTC_ATTR(16); break;
     case 32: XTC_ATTR(32); break;
@@ -848,6 +707,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   }
 #undef XTC_ATTR
 #undef XTRY
+#undef XCUDA
   *out = p;
   return CB_OK;
 }
@@ -859,6 +719,8 @@ void xtc_plan_destroy(XtcPlan* p) {
 }
 
 double xtc_bytes(const XtcPlan* p) { return p ? p->bytes : 0.0; }
+
+double xtc_stream_bytes(const XtcPlan* p) { return p ? p->stream_bytes : 0.0; }
 
 void xtc_set_grid_cap(XtcPlan* p, int cap) {
   if (p) p->grid_cap = cap;
@@ -878,9 +740,8 @@ static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStre
   if (parts & 2) {
     const int grid = p->grid_cap > 0 ? std::min(p->grid, p->grid_cap) : p->grid;
     // (launching it at the highest scheduling priority, so that its static
-    // partition is placed before the sweep's CTAs, measured slower on c5:
-    // 3.85 -> 4.0 ms per pipelined iteration)
-    CB_CUDA(launch_k(k_xtc_trace<N>, dim3(grid), dim3(xtc_threads<N>()), p->smem, st, a));
+    // partition is placed before the sweep's CTAs, measured slower on c5)
+    CB_CUDA(launch_k(k_xtc_trace<N>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a));
     count_launch(1);
   }
   return CB_OK;
@@ -891,14 +752,11 @@ static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStre
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
               cudaStream_t st, int parts) {
   XtcArgs a{};
-  a.tmaps = p->tmaps;
   a.blk = p->blk;
   a.units = p->units;
   a.nunits = p->nunits;
   a.nst = p->nst;
   a.bimg_max = p->bimg_max;
-  a.u1_bytes = p->u1_bytes;
-  a.dbg = 0;
   a.part = p->part;
   a.cnt = p->cnt;
   a.bsum = bsum;

@@ -15,13 +15,14 @@ namespace cb {
 
 struct XtcPlan;
 
-// usable for these blocks?  fp32 storage, I0 % 4 == 0 (TMA row pitch),
-// I0 <= XTC_MAX_I0, rank <= 64, 16-byte aligned tensors
+// usable for these blocks?  fp32 storage, I0 <= XTC_MAX_I0, I1 >= 19,
+// rank <= 64
 bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R);
 
 // plan for S blocks (device fp32 tensors X[s], dims S x 3, ranks R[s]):
-// per-block tensor maps, unit tables, the per-block fixed-point exponent of X
-// (one max|X| pass, enqueued on `st`), operand images and partial buffers
+// unit tables, the per-block fixed-point exponent of X (one max|X| pass) and
+// the three byte planes of every block (one pack pass), enqueued on `st`;
+// operand images and partial buffers
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
                     cudaStream_t st, XtcPlan** out);
 void xtc_plan_destroy(XtcPlan* p);
@@ -38,7 +39,10 @@ void xtc_set_grid_cap(XtcPlan* p, int cap);
 // per-launch timeline slots (TL_TRACE, TL_PREP) of the solver's profiling mode
 void xtc_set_timeline(XtcPlan* p, unsigned long long* tl);
 
-// algorithmic bytes streamed per xtc_trace call (sum_s |X_s| * 4)
+// algorithmic bytes of one xtc_trace call (sum_s |X_s| * 4: every element of
+// the fp32 blocks once) and the bytes it actually streams (three byte planes
+// per element plus tile padding)
 double xtc_bytes(const XtcPlan* p);
+double xtc_stream_bytes(const XtcPlan* p);
 
 }  // namespace cb

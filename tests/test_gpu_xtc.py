@@ -90,10 +90,20 @@ def test_tc_trace_batched_ragged_and_deterministic(P):
 
 def test_tc_trace_rejects_unsupported_shapes(P):
     rng = np.random.default_rng(1)
-    for dims in ((6, 5, 4), (30, 20, 4)):      # I1 < 19; I0 % 4 != 0
+    for dims in ((6, 5, 4), (516, 20, 4)):      # I1 < 19; I0 > 512
         x, g = _block(rng, dims, 3)
         with pytest.raises(Exception):
             P.core_linear_terms_tc([x], [g])
+
+
+def test_tc_trace_odd_leading_size(P):
+    """I0 not a multiple of 4 or 32 (the pack pads K with zeros)."""
+    rng = np.random.default_rng(2)
+    for dims, rank in (((30, 20, 4), 3), ((45, 37, 11), 12), ((33, 64, 9), 20)):
+        x, g = _block(rng, dims, rank)
+        got = P.core_linear_terms_tc([x], [g])[0]
+        want, scale = _want(x, g)
+        assert (np.abs(got - want) / scale).max() < 4e-6, dims
 
 
 def test_tc_trace_zero_and_scaled(P):
