@@ -1053,7 +1053,7 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         int reserve = d->pipeline_reserve > 0 ? d->pipeline_reserve : (S + 2) / 3;
-        reserve = std::max(0, std::min(reserve, nsm / 3));
+        reserve = std::max(0, std::min(reserve, nsm / 2));
         xtc_set_grid_cap(h->xtc, nsm - reserve);
       }
     }

@@ -5,8 +5,8 @@
 //
 // Formulation.  View block s as the row-major matrix Xr (rows = (i1,i2),
 // J = I1*I2 rows; K = i0, I0 columns).  Then
-//      D = Xr . A0          (J x R, a GEMM with K = I0)
-//      b[r] = sum_rows A1[i1,r] A2[i2,r] D[row,r]   (fp64 epilogue)
+//      D = A0^T . Xr^T      (R x J, a GEMM with K = I0)
+//      b[r] = sum_rows A1[i1,r] A2[i2,r] D[r,row]   (fp64 epilogue)
 // The reference computes in fp64; this pass reaches ~2^-22 relative per
 // product with zero bias, via fixed-point byte slices and int8 MMAs:
 //   * X: one exponent per block (max|X| = m 2^eX, m in [0.5, 1)), q =
@@ -14,35 +14,41 @@
 //     (a0 in [-64, 64]).  The three byte planes are written ONCE per solve
 //     (k_xtc_pack) in the MMA's shared-memory layout (K-major rows of 32
 //     bytes, 32-byte swizzle), tile by tile: an iteration then streams 3
-//     bytes per element instead of 4 and does no conversion work
-//     (the previous form of this pass converted fp32 tiles in 8 warps per
-//     SM and was bound by them at 38 GB/s per SM).
+//     bytes per element instead of 4 and does no conversion work.
 //   * A0: one exponent per column, p = rint(u 2^(22-eU_r)) as balanced
 //     signed bytes p = b0 2^16 + b1 2^8 + b2 (b0 in [-64, 64]), per call.
 //   * sum_k q_k p_k = 2^32 L0 + 2^24 L1 + 2^16 L2 + (dropped levels 3-4),
-//     L0 = a0.b0, L1 = a0.b1 + a1.b0, L2 = a0.b2 + a1.b1 + a2.b0: three
-//     M=128 x N x K=32 kind::i8 MMAs per K step (a_i x [b_0 | .. | b_{2-i}])
-//     into three int32 TMEM accumulators (exact; |L| < 2^31 for I0 <= 32768).
-//     The dropped terms are products of two balanced signed digits, ~2^-21
-//     of a product, zero-mean (and zero where x = 0).
+//     L0 = a0.b0, L1 = a0.b1 + a1.b0, L2 = a0.b2 + a1.b1 + a2.b0 (exact
+//     int32; |L| < 2^31 for I0 <= 32768).  The dropped terms are products of
+//     two balanced signed digits, ~2^-21 of a product, zero-mean.
+//   * operand roles.  A kind::i8 MMA of M = 128, K = 32 costs ~220 cycles
+//     whatever its N (tools/micro/imma_probe.cu), so the X rows go on N
+//     (256 per instruction) and the factor on M: the three slices of a column
+//     are stacked along M with a level's rows together, image rows
+//     [0 (Rp); 0 (Rp); b0; b1; b2; 0], Rp = R rounded up to 8, 3 Rp <= 128.
+//     The M = 128 window starting at row (2 - i) Rp is the operand for plane
+//     a_i: window 2 Rp = [b0; b1; b2], window Rp = [0; b0; b1], window 0 =
+//     [0; 0; b0], so three MMAs per K step accumulate D lanes [l Rp, (l+1) Rp)
+//     = level l for 256 rows of X (the lanes past 3 Rp collect dropped-level
+//     products and are not read).
 // Error: unbiased rounding of x (2^-23 of the block max) and u (2^-23 of the
 // column max); measured ~1e-8 relative on b.  The lra objective's
 // cancellation (res ~ 1% of |M|^2 at 20 dB) turns that into ~1e-6 on RelErr,
 // inside the fp32-mode 1e-4 (tests/test_gpu_xtc.py, tests/test_gpu_solve.py).
 //
 // Kernel (persistent, one CTA per SM, 320 threads):
-//   warp 9  : producer - 12 KB bulk copies (one K = 32 step of a tile, three
-//             planes) into an NST-stage ring, plus the block's B image
-//             (prepared by k_xtc_prep) per segment;
-//   warp 8  : MMA issuer - one lane issues tcgen05.mma (A and B from shared
-//             memory), tcgen05.commit frees ring stages / publishes D;
-//   warps 0-7: epilogue, two groups of 4 (one warp per TMEM lane quarter, half
-//             of the N columns each): tcgen05.ld of the int32 levels, fp64
-//             combine, A1/A2 weights, fixed-order folds.
-// TMEM: 2 D buffers x 3 levels x N columns.  Row weights A1[i1,r] A2[i2,r]
-// are fp32 (transposed tables: A1's read from L2 ahead of the wait on D, the
-// tile's few A2 rows staged); column constants in smem.
-// Units of 8 tiles (never straddling a block) are the partial granularity:
+//   warp 9  : producer - 24 KB bulk copies (one K = 32 step of a 256-row
+//             tile, three planes) into an NST-stage ring, plus the block's
+//             factor image (prepared by k_xtc_prep) per segment;
+//   warp 8  : MMA issuer - one lane issues tcgen05.mma (both operands from
+//             shared memory), tcgen05.commit frees ring stages / publishes D;
+//   warps 0-7: epilogue, one TMEM lane quarter x one half of the 256 columns
+//             each: a thread owns (level, r), walks its 128 rows with the
+//             weights A1[i1,r] (fp32, L2-resident, prefetched a batch ahead)
+//             and A2[i2,r], and keeps sum_rows w L in fp64 (int32 -> fp64
+//             exactly through the fp64 adder).
+// TMEM: 2 D buffers x 256 columns.
+// Units of 4 tiles (never straddling a block) are the partial granularity:
 // partials are reduced in fixed order and folded per block in unit order by
 // the last arriving CTA, so b is bitwise independent of the grid size and
 // of how blocks are sharded over GPUs.
@@ -63,15 +69,16 @@
 
 namespace cb {
 
-constexpr int XTC_M = 128;                        // rows per tile (MMA M)
+constexpr int XTC_NT = 256;                       // X rows per tile (MMA N)
 constexpr int XTC_SX = 3;                         // byte planes of X
-constexpr int XTC_PIECE = XTC_M * 32;             // 4 KB: one plane of one K = 32 step
-constexpr int XTC_STAGE = XTC_SX * XTC_PIECE;     // 12 KB per ring stage
-constexpr int XTC_TPU = 8;                        // tiles per unit
+constexpr int XTC_PIECE = XTC_NT * 32;            // 8 KB: one plane of one K = 32 step
+constexpr int XTC_STAGE = XTC_SX * XTC_PIECE;     // 24 KB per ring stage
+constexpr int XTC_TPU = 4;                        // tiles per unit
 constexpr int XTC_MAX_I0 = 512;
+constexpr int XTC_MAX_R = 40;                     // 3 levels x Rp lanes <= 128
 constexpr int XTC_XBITS = 22;
 constexpr int XTC_UBITS = 22;
-constexpr int XTC_U2R = 8;        // A2 rows staged per tile
+constexpr int XTC_WB = 16;        // columns per epilogue batch
 constexpr int XTC_THREADS = 320;  // 8 epilogue warps, MMA, producer
 constexpr int XTC_SMEM_MAX = 227 * 1024;
 
@@ -81,12 +88,12 @@ struct XtcBlock {
   int ex;                 // fixed-point exponent of X
   int ufirst, nunits;
   int bimg_bytes;
-  double* aux;            // [0,64): scale_r
-  float* ut1;             // [r][I1] = A1[i1, r] (fp32 row weights)
-  float* ut2;             // [r][I2] = A2[i2, r]
+  double* aux;            // [64] scale_r
+  float* w1;              // [I1][Rp] = A1[i1, r] (fp32 row weights, zero-padded columns)
+  float* w2;              // [I2][Rp] = A2[i2, r]
   const float* X;         // the block (read by the pack kernel only)
-  unsigned char* planes;  // [ntiles][nk][3 planes][128 rows x 32 B]
-  unsigned char* bimg;    // [nk][3 N rows][32 B] (K-major, 32-B swizzle)
+  unsigned char* planes;  // [ntiles][nk][3 planes][256 rows x 32 B]
+  unsigned char* bimg;    // [nk][2 Rp + 128 rows][32 B] (K-major, 32-B swizzle)
 };
 
 struct XtcUnit { int s, t0, t1, u; };
@@ -97,6 +104,7 @@ struct XtcArgs {
   int nunits;
   int nst;
   int bimg_max;
+  int Rp;                 // lanes per level (max rank rounded up to 8)
   double* part;           // [unit][64]
   int* cnt;               // per-block arrival counters (self-resetting)
   double* bsum;           // [s][RSTRIDE]
@@ -105,7 +113,7 @@ struct XtcArgs {
 };
 
 struct XtcPlan {
-  int S = 0, N = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, ntiles = 0;
+  int S = 0, Rp = 0, nst = 0, grid = 0, nunits = 0, bimg_max = 0, ntiles = 0;
   int grid_cap = 0;          // > 0: at most this many CTAs (SMs left to concurrent work)
   size_t smem = 0;
   double bytes = 0.0;        // algorithmic: sum_s |X_s| x 4
@@ -147,14 +155,14 @@ __device__ __forceinline__ uint32_t pick4(uint32_t t0, uint32_t t1, uint32_t t2,
   return __byte_perm(__byte_perm(t0, t1, sel), __byte_perm(t2, t3, sel), 0x5410);
 }
 
-// grid (max tiles, 1, S), 128 threads: each warp transposes its 32 rows of a
+// grid (max tiles, 1, S), 256 threads: each warp transposes its 32 rows of a
 // K = 32 step through shared memory (k is contiguous in X), thread m then
 // owns row m: q + 0x8080 = a0 2^16 + (a1 + 128) 2^8 + (a2 + 128)
-__global__ void __launch_bounds__(XTC_M) k_xtc_pack(const XtcBlock* blk) {
+__global__ void __launch_bounds__(XTC_NT) k_xtc_pack(const XtcBlock* blk) {
   const XtcBlock& b = blk[blockIdx.z];
   const int t = blockIdx.x;
   if (t >= b.ntiles) return;
-  __shared__ float tile[XTC_M][33];
+  __shared__ float tile[XTC_NT][33];
   const int m = threadIdx.x;
   const int warp = m >> 5, lane = m & 31;
   const float sx = ldexpf(1.0f, XTC_XBITS - b.ex);
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(XTC_M) k_xtc_pack(const XtcBlock* blk) {
     const int kk = c * 32 + lane;
 #pragma unroll 8
     for (int r = 0; r < 32; ++r) {
-      const long long rr = (long long)t * XTC_M + warp * 32 + r;
+      const long long rr = (long long)t * XTC_NT + warp * 32 + r;
       tile[warp * 32 + r][lane] = (rr < b.J && kk < b.I0) ? __ldcs(X + rr * b.I0 + kk) : 0.0f;
     }
     __syncwarp();
@@ -189,10 +197,9 @@ __global__ void __launch_bounds__(XTC_M) k_xtc_pack(const XtcBlock* blk) {
 }
 
 // --------------------------------------------------------------------------
-// per call: A0 -> signed byte-slice image (the MMA B operand, exactly the
-// shared-memory layout), column scales, A1/A2 transposed
+// per call: A0 -> the stacked signed byte-slice image (the MMA's M-side
+// operand, exactly the shared-memory layout), column scales, A1/A2 as fp32
 // --------------------------------------------------------------------------
-template <int N>
 __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const* U) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
@@ -202,11 +209,12 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
   const double* A0 = U[3 * s];
   const double* A1 = U[3 * s + 1];
   const double* A2 = U[3 * s + 2];
-  const int R = b.R;
+  const int R = b.R, Rp = a.Rp;
   const int I0 = (int)b.I0;
+  const int SR = 2 * Rp + 128;        // image rows per K step
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ int eu[64];
-  for (int r = warp; r < N; r += 8) {
+  for (int r = warp; r < Rp; r += 8) {
     double m = 0.0;
     if (r < R)
       for (int i = lane; i < I0; i += 32) m = fmax(m, fabs(A0[(long long)i * R + r]));
@@ -218,24 +226,29 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     }
   }
   __syncthreads();
+  // rows [2 Rp + l Rp + n] = slice l of column n; everything else stays zero
+  // (the image is zeroed at plan creation and only these bytes are rewritten)
   const int kmax = b.nk * 32;
-  for (int e = threadIdx.x; e < kmax * N; e += 256) {
-    const int k = e / N, n = e - (e / N) * N;
+  for (int e = threadIdx.x; e < kmax * Rp; e += 256) {
+    const int k = e / Rp, n = e - (e / Rp) * Rp;
     long long p = 0;
     if (k < I0 && n < R) p = llrint(ldexp(A0[(long long)k * R + n], XTC_UBITS - eu[n]));
     const long long d2 = ((p + 128) & 255) - 128;
     const long long p1 = (p - d2) >> 8;
     const long long d1 = ((p1 + 128) & 255) - 128;
     const long long d0 = (p1 - d1) >> 8;
-    // K step c = k / 32 holds the three slices as one operand of 3N rows
-    // ([b0 | b1 | b2], so one MMA covers a digit of X times all three), rows
-    // of 32 bytes, 16-byte halves swapped on rows with bit 2 set
-    // (Swizzle<1,4,3> of a 256-byte atom; N % 16 == 0 keeps it per slice)
     const int c = k >> 5, kk = k & 31;
-    const long long off = ((long long)c * 3 * N + n) * 32 + (((kk >> 4) ^ ((n >> 2) & 1)) << 4) + (kk & 15);
-    b.bimg[off] = (unsigned char)(signed char)d0;
-    b.bimg[off + N * 32] = (unsigned char)(signed char)d1;
-    b.bimg[off + 2 * N * 32] = (unsigned char)(signed char)d2;
+    // rows of 32 bytes, 16-byte halves swapped on rows with bit 2 set
+    // (Swizzle<1,4,3>; the K-step images start on multiples of 256 bytes)
+    auto put = [&](int l, long long d) {
+      const int row = (2 + l) * Rp + n;
+      const long long off =
+          ((long long)c * SR + row) * 32 + (((kk >> 4) ^ ((row >> 2) & 1)) << 4) + (kk & 15);
+      b.bimg[off] = (unsigned char)(signed char)d;
+    };
+    put(0, d0);
+    put(1, d1);
+    put(2, d2);
   }
   if (threadIdx.x < 64) {
     const int r = threadIdx.x;
@@ -243,13 +256,15 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     b.aux[r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS) : 0.0;
   }
   const long long I1 = b.I1, I2 = b.I2;
-  for (long long e = threadIdx.x; e < (long long)R * I1; e += 256) {
-    const long long r = e / I1, i = e - r * I1;
-    b.ut1[e] = (float)A1[i * R + r];
+  for (long long e = threadIdx.x; e < I1 * Rp; e += 256) {
+    const long long i = e / Rp;
+    const int r = (int)(e - i * Rp);
+    b.w1[e] = r < R ? (float)A1[i * R + r] : 0.0f;
   }
-  for (long long e = threadIdx.x; e < (long long)R * I2; e += 256) {
-    const long long r = e / I2, i = e - r * I2;
-    b.ut2[e] = (float)A2[i * R + r];
+  for (long long e = threadIdx.x; e < I2 * Rp; e += 256) {
+    const long long i = e / Rp;
+    const int r = (int)(e - i * Rp);
+    b.w2[e] = r < R ? (float)A2[i * R + r] : 0.0f;
   }
   tl_end(a.tl, TL_PREP);
 }
@@ -257,47 +272,24 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
 // --------------------------------------------------------------------------
 // the streaming MMA kernel
 // --------------------------------------------------------------------------
-// sum over the 32 lanes of v[0..8) by recursive halving (9 fp64 shuffles
-// instead of 40); lane l ends with the total of value l / 4.  Fixed order:
-// bitwise deterministic.
-__device__ __forceinline__ double fold8(double (&v)[8], int lane) {
-#pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int o = 16 >> st;
-    const int c = 8 >> st;
-    if (c > 1) {
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < c / 2; ++i) {
-        const double send = up ? v[i] : v[i + c / 2];
-        const double keep = up ? v[i + c / 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    } else {
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-    }
-  }
-  return v[0];
-}
-
 // int32 -> double through the fp64 adder (exact): 2^52 + 2^31 + x
 __device__ __forceinline__ double i2d_exact(uint32_t x) {
   return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
 }
 
-template <int N>
+template <int RP>
 __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
   tl_begin(a.tl, TL_TRACE);
-  constexpr int NH = N / 2;          // columns per epilogue group
   constexpr int NE = 256;            // epilogue threads
   constexpr int WMMA = 8, WTMA = 9;
-  constexpr int DW = 3 * N;          // accumulator columns per buffer
   extern __shared__ unsigned char xtc_raw[];
   const uint32_t raw_u32 = smem_u32(xtc_raw);
   unsigned char* sm = xtc_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
   const int nst = a.nst;
+  constexpr int Rp = RP;
+  constexpr int SR = 2 * Rp + 128;
   unsigned char* ring = sm;
   unsigned char* bimg = sm + (size_t)nst * XTC_STAGE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(bimg + a.bimg_max);
@@ -307,10 +299,8 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
   uint64_t* d_empty = d_full + 2;
   uint64_t* b_full = d_empty + 2;
   uint64_t* b_empty = b_full + 1;
-  double* red = reinterpret_cast<double*>(b_empty + 1);      // [2 groups][4 warps][64]
-  double* auxs = red + 512;                                  // [64] of the segment
-  float* u2s = reinterpret_cast<float*>(auxs + 64);          // [2][XTC_U2R][64]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u2s + 2 * XTC_U2R * 64);
+  double* red = reinterpret_cast<double*>(b_empty + 1);      // [2 column halves][128 lanes]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + 256);
   int* shflag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -363,10 +353,9 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
     }
   } else if (warp == WMMA) {
     // --------------------------------------------------------- MMA issuer
-    // D[L0 | L1 | L2] += a0 [b0|b1|b2]; D[L1 | L2] += a1 [b0|b1]; D[L2] += a2 b0
-    constexpr uint32_t id0 = idesc_i8(3 * N, 1, 1);
-    constexpr uint32_t id1 = idesc_i8(2 * N, 1, 1);
-    constexpr uint32_t id2 = idesc_i8(N, 1, 1);
+    // D lanes [l Rp, (l+1) Rp) += level l: plane a_i against the image window
+    // starting at row (2 - i) Rp
+    constexpr uint32_t idesc = idesc_i8(XTC_NT, 1, 1);
     int st = 0, ph = 0, seg = 0, cur = -1, tl = 0;
     const uint32_t bbase = smem_u32(bimg);
     const uint32_t rbase = smem_u32(ring);
@@ -385,16 +374,16 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
         const int buf = tl & 1;
         mbar_wait(&d_empty[buf], ((tl >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t dc = tmem + (uint32_t)(buf * DW);
+        const uint32_t dc = tmem + (uint32_t)(buf * XTC_NT);
         for (int c = 0; c < nk; ++c) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t ab = rbase + (uint32_t)st * XTC_STAGE;
-            const uint64_t B = sdesc_k_sw32(bbase + (uint32_t)c * 3 * N * 32);
-            mma_i8_ss(dc, sdesc_k_sw32(ab), B, id0, c > 0 ? 1u : 0u);
-            mma_i8_ss(dc + N, sdesc_k_sw32(ab + XTC_PIECE), B, id1, 1u);
-            mma_i8_ss(dc + 2 * N, sdesc_k_sw32(ab + 2 * XTC_PIECE), B, id2, 1u);
+            const uint32_t xb = rbase + (uint32_t)st * XTC_STAGE;
+            const uint32_t fb = bbase + (uint32_t)(c * SR * 32);
+            mma_i8_ss(dc, sdesc_k_sw32(fb + 2 * Rp * 32), sdesc_k_sw32(xb), idesc, c > 0 ? 1u : 0u);
+            mma_i8_ss(dc, sdesc_k_sw32(fb + Rp * 32), sdesc_k_sw32(xb + XTC_PIECE), idesc, 1u);
+            mma_i8_ss(dc, sdesc_k_sw32(fb), sdesc_k_sw32(xb + 2 * XTC_PIECE), idesc, 1u);
             tc_commit(&empty[st]);
             if (c == nk - 1) {
               tc_commit(&d_full[buf]);
@@ -408,128 +397,116 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
     }
   } else {
     // ------------------------------------------------ epilogue (warps 0-7)
-    // two groups of 4 (one warp per lane quarter), each for half of the
-    // columns: row weights A1[i1,r] (staged per segment) x A2[i2,r] (the
-    // tile's few A2 rows, cp.async-staged one tile ahead), the int32 levels
-    // of D from TMEM, fp64 row sums per thread; per unit a fixed-order
-    // reduction into a partial, per block a fold in unit order
+    // warp = (column half ch, lane quarter wq); the thread's TMEM lane is
+    // (level, r); it walks the 128 rows of its half in order, rows advancing
+    // i1 first: inner = sum_i1 A1[i1,r] L (per i2 stretch, four interleaved
+    // partial sums combined in a fixed order), acc += A2[i2,r] inner
     const int et = threadIdx.x;
-    const int h = warp >> 2;
+    const int ch = warp >> 2;
     const int wq = warp & 3;
-    const int m = wq * 32 + lane;
+    const int L = wq * 32 + lane;
+    const int lev = L / RP;
+    const int r = L - lev * RP;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    // per-lane unit sums: after each tile's 8-column warp fold, lane l holds
-    // column cg*8 + l/4 of this warp's 32 rows
-    double acc[NH / 8];
-#pragma unroll
-    for (int j = 0; j < NH / 8; ++j) acc[j] = 0.0;
-    // stage the A2 rows of tile (s, t) into u2s[buf]: rows i2 of its first
-    // .. last row (<= XTC_U2R of them)
-    auto stage_u2 = [&](int s, int t, int buf) {
-      const XtcBlock& b = a.blk[s];
-      const long long r0 = (long long)t * XTC_M;
-      const long long r1 = std::min(r0 + XTC_M, b.J) - 1;
-      const long long i2a = r0 / b.I1;
-      const int n2 = (int)(r1 / b.I1 - i2a + 1);   // <= XTC_U2R (I1 >= 19, host-checked)
-      for (int e = et; e < n2 * 64; e += NE) {
-        const int k = e >> 6, r = e & 63;
-        if (r < b.R)
-          cp_async4(u2s + buf * XTC_U2R * 64 + e, b.ut2 + (long long)r * b.I2 + i2a + k);
-      }
-    };
-    int tl = 0, cur = -1;
-    // the tile after the current one
-    int nxt_u = u_begin;
-    int nxt_t = nxt_u < u_end ? a.units[nxt_u].t0 : 0;
-    auto advance = [&](int& uu, int& tt) {
-      if (++tt >= a.units[uu].t1) {
-        ++uu;
-        if (uu < u_end) tt = a.units[uu].t0;
-      }
-    };
-    if (nxt_u < u_end) {
-      stage_u2(a.units[nxt_u].s, nxt_t, 0);
-      advance(nxt_u, nxt_t);
-    }
-    cp_async_commit();
+    double acc = 0.0;
+    int tl = 0;
     for (int u = u_begin; u < u_end; ++u) {
       const XtcUnit un = a.units[u];
       const XtcBlock& b = a.blk[un.s];
       const int I1 = (int)b.I1;
       const long long J = b.J;
-      const int R = b.R;
-      if (un.s != cur) {
-        // a new segment: the block's column constants and A1^T table
-        cur = un.s;
-        named_bar(1, NE);
-        if (et < 64) auxs[et] = b.aux[et];
-      }
+      // idle lanes (past the three levels, or columns >= R) read the zero
+      // padding columns of the weight tables / a valid address and weigh
+      // their products by zero
+      const bool act = lev < 3 && r < b.R;
+      const float* __restrict__ w1p = b.w1 + (act ? r : 0);
+      const float* __restrict__ w2p = b.w2 + (act ? r : 0);
+      const float wm = act ? 1.0f : 0.0f;
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
         const int buf = tl & 1;
-        cp_async_wait_all();          // this thread's copies for tile t
-        named_bar(1, NE);             // everyone's; buf ^ 1 is free again
-        if (nxt_u < u_end) {
-          stage_u2(a.units[nxt_u].s, nxt_t, buf ^ 1);
-          advance(nxt_u, nxt_t);
-        }
-        cp_async_commit();
-        const long long row = (long long)t * XTC_M + m;
-        const bool valid = row < J;
-        const int i2 = valid ? (int)(row / I1) : 0;
-        const int i1 = valid ? (int)(row - (long long)i2 * I1) : 0;
-        const int i2a = (int)(((long long)t * XTC_M) / I1);
-        const float* u2 = u2s + buf * XTC_U2R * 64 + (i2 - i2a) * 64;
-        // this row's A1 weights from the L2-resident transposed table (a
-        // warp reads 32 consecutive floats per column), issued before the
-        // wait on D so the latency hides behind it; shared memory is left to
-        // the ring (more bytes in flight per SM)
-        float w1[NH];
-        {
-          const float* u1 = b.ut1 + i1;
+        const long long row0 = (long long)t * XTC_NT + ch * 128;
+        int i2 = (int)(row0 / I1);
+        int i1 = (int)(row0 - (long long)i2 * I1);
+        const int nrow = (int)max(0LL, min(128LL, J - row0));   // rows of this half that exist
+        // a batch is plain when all its rows exist and share one i2
+        auto plain = [&](int j0, int i1s) { return j0 + XTC_WB <= nrow && i1s + XTC_WB <= I1; };
+        // weights of a batch of columns: A1[i1s + j (wrapping), r]
+        auto load_w1 = [&](int j0, int i1s, float (&w)[XTC_WB]) {
+          if (plain(j0, i1s)) {
+            const float* p = w1p + (long long)i1s * RP;
 #pragma unroll
-          for (int j = 0; j < NH; ++j) {
-            const int r = h * NH + j;
-            w1[j] = (valid && r < R) ? __ldg(u1 + (long long)r * I1) : 0.0f;
+            for (int j = 0; j < XTC_WB; ++j) w[j] = __ldg(p + j * RP);
+          } else {
+#pragma unroll
+            for (int j = 0; j < XTC_WB; ++j) {
+              int i = i1s + j;
+              if (i >= I1) i -= I1;   // one wrap at most (I1 >= XTC_WB)
+              w[j] = j0 + j < nrow ? __ldg(w1p + (long long)i * RP) : 0.0f;
+            }
           }
-        }
+        };
+        float wc[XTC_WB], wn[XTC_WB];
+        load_w1(0, i1, wc);
+        float w2 = nrow > 0 ? wm * __ldg(w2p + (long long)i2 * RP) : 0.0f;
+        double in0 = 0.0, in1 = 0.0, in2 = 0.0, in3 = 0.0;
         mbar_wait(&d_full[buf], (tl >> 1) & 1);
         tc_fence_after();
-        const uint32_t dc = trow + (uint32_t)(buf * DW);
-#pragma unroll
-        for (int cg = 0; cg < NH / 8; ++cg) {
-          const int col0 = h * NH + cg * 8;
-          uint32_t l0[8], l1[8], l2[8];
-          tmem_ld8(dc + col0, l0);
-          tmem_ld8(dc + N + col0, l1);
-          tmem_ld8(dc + 2 * N + col0, l2);
-          float w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)   // (unstaged u2 entries of columns >= R are not read)
-            w[j] = (valid && col0 + j < R) ? w1[cg * 8 + j] * u2[col0 + j] : 0.0f;
+        const uint32_t dc = trow + (uint32_t)(buf * XTC_NT + ch * 128);
+#pragma unroll 1
+        for (int j0 = 0; j0 < 128; j0 += XTC_WB) {
+          uint32_t v[XTC_WB];
+          tmem_ld16(dc + j0, v);
+          // next batch's weights while the TMEM load is in flight
+          int i1n = i1 + XTC_WB;
+          if (i1n >= I1) i1n -= I1;
+          if (j0 + XTC_WB < 128) load_w1(j0 + XTC_WB, i1n, wn);
           tmem_wait_ld();
-          double c8[8];
+          if (plain(j0, i1)) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const double v = fma(i2d_exact(l0[j]), 65536.0,
-                                 fma(i2d_exact(l1[j]), 256.0, i2d_exact(l2[j])));
-            c8[j] = v * (double)w[j];
+            for (int j = 0; j < XTC_WB; j += 4) {
+              in0 = fma((double)wc[j], i2d_exact(v[j]), in0);
+              in1 = fma((double)wc[j + 1], i2d_exact(v[j + 1]), in1);
+              in2 = fma((double)wc[j + 2], i2d_exact(v[j + 2]), in2);
+              in3 = fma((double)wc[j + 3], i2d_exact(v[j + 3]), in3);
+            }
+            i1 += XTC_WB;
+            if (i1 == I1) {
+              acc = fma((double)w2, (in0 + in1) + (in2 + in3), acc);
+              in0 = in1 = in2 = in3 = 0.0;
+              i1 = 0;
+              ++i2;
+              w2 = j0 + XTC_WB < nrow ? wm * __ldg(w2p + (long long)i2 * RP) : 0.0f;
+            }
+          } else {
+            // the batch crosses into the next i2 or past the block's rows
+#pragma unroll
+            for (int j = 0; j < XTC_WB; ++j) {
+              in0 = fma((double)wc[j], i2d_exact(v[j]), in0);
+              if (++i1 == I1) {
+                acc = fma((double)w2, (in0 + in1) + (in2 + in3), acc);
+                in0 = in1 = in2 = in3 = 0.0;
+                i1 = 0;
+                ++i2;
+                w2 = j0 + j + 1 < nrow ? wm * __ldg(w2p + (long long)i2 * RP) : 0.0f;
+              }
+            }
           }
-          acc[cg] += fold8(c8, lane);
+#pragma unroll
+          for (int j = 0; j < XTC_WB; ++j) wc[j] = wn[j];
         }
+        acc = fma((double)w2, (in0 + in1) + (in2 + in3), acc);
         tc_fence_before();
         mbar_arrive(&d_empty[buf]);
         if (t == un.t1 - 1) {
-          // unit done: fixed-order reduction over the 128 rows
-#pragma unroll
-          for (int j = 0; j < NH / 8; ++j) {
-            if ((lane & 3) == 0) red[(h * 4 + wq) * 64 + j * 8 + (lane >> 2)] = acc[j];
-            acc[j] = 0.0;
-          }
+          // unit done: levels and column halves combined in fixed order
+          red[ch * 128 + L] = acc;
+          acc = 0.0;
           named_bar(1, NE);
-          if (et < N) {
-            const int r = et, hh = r / NH, jj = r - hh * NH;
-            const double* q = red + hh * 4 * 64 + jj;
-            a.part[(long long)un.u * 64 + r] = (((q[0] + q[64]) + q[128]) + q[192]) * auxs[r];
+          if (et < b.R) {
+            const double s0 = red[et] + red[128 + et];
+            const double s1 = red[RP + et] + red[128 + RP + et];
+            const double s2 = red[2 * RP + et] + red[128 + 2 * RP + et];
+            a.part[(long long)un.u * 64 + et] = fma(s0, 65536.0, fma(s1, 256.0, s2)) * b.aux[et];
             __threadfence();
           }
           named_bar(1, NE);
@@ -542,18 +519,17 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
           named_bar(1, NE);
           if (*shflag) {
             __threadfence();
-            if (et < R) {
+            if (et < b.R) {
               double s = 0.0;
               for (int k = 0; k < b.nunits; ++k)
                 s += __ldcg(&a.part[(long long)(b.ufirst + k) * 64 + et]);
               a.bsum[(long long)un.s * RSTRIDE + et] = s;
             }
           }
-          // red / shflag / auxs are reused only after the next barrier
+          // red / shflag are reused only after the next unit's barriers
         }
       }
     }
-    cp_async_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -567,29 +543,21 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
 // --------------------------------------------------------------------------
 // host side
 // --------------------------------------------------------------------------
-static int n_bucket(int rmax) {
-  if (rmax <= 16) return 16;
-  if (rmax <= 32) return 32;
-  if (rmax <= 48) return 48;
-  return 64;
-}
-
 bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R) {
   for (int s = 0; s < S; ++s) {
     const long long I0 = dims[3 * s], I1 = dims[3 * s + 1], I2 = dims[3 * s + 2];
     if (I0 < 1 || I1 < 1 || I2 < 1) return false;
     if (I0 > XTC_MAX_I0) return false;
     if (I1 * I2 >= (1LL << 31)) return false;
-    if (R[s] < 1 || R[s] > 64) return false;
-    if (I1 < 19) return false;            // a tile's rows span <= XTC_U2R values of i2
+    if (R[s] < 1 || R[s] > XTC_MAX_R) return false;   // three levels of Rp lanes in M = 128
+    if (I1 < XTC_WB) return false;        // a weight batch wraps i1 at most once
     if ((reinterpret_cast<uintptr_t>(X[s]) & 3) != 0) return false;
   }
   return true;
 }
 
 static size_t xtc_smem_for(int nst, int bimg_max) {
-  return 1024 + (size_t)nst * XTC_STAGE + bimg_max + 8 * (2 * nst + 6) + 576 * 8 +
-         2 * XTC_U2R * 64 * 4 + 16;
+  return 1024 + (size_t)nst * XTC_STAGE + bimg_max + 8 * (2 * nst + 6) + 256 * 8 + 16;
 }
 
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
@@ -599,11 +567,12 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   p->S = S;
   int rmax = 1;
   for (int s = 0; s < S; ++s) rmax = std::max(rmax, R[s]);
-  p->N = n_bucket(rmax);
-  const int N = p->N;
+  p->Rp = (rmax + 7) / 8 * 8;
+  const int Rp = p->Rp;
+  const int SR = 2 * Rp + 128;
   std::vector<XtcBlock> hb(S);
   std::vector<XtcUnit> hu;
-  long long ut_elems = 0;
+  long long w_elems = 0;
   long long bimg_total = 0;
   size_t plane_bytes = 0;
   int ntmax = 1;
@@ -612,10 +581,10 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     b.I0 = dims[3 * s]; b.I1 = dims[3 * s + 1]; b.I2 = dims[3 * s + 2];
     b.J = b.I1 * b.I2;
     b.R = R[s];
-    b.ntiles = (int)((b.J + XTC_M - 1) / XTC_M);
+    b.ntiles = (int)((b.J + XTC_NT - 1) / XTC_NT);
     b.nk = (int)((b.I0 + 31) / 32);
     b.ex = 0;
-    b.bimg_bytes = 3 * b.nk * N * 32;
+    b.bimg_bytes = b.nk * SR * 32;
     p->bimg_max = std::max(p->bimg_max, b.bimg_bytes);
     b.ufirst = (int)hu.size();
     p->ntiles += b.ntiles;
@@ -623,7 +592,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     for (int t = 0; t < b.ntiles; t += XTC_TPU)
       hu.push_back({s, t, std::min(b.ntiles, t + XTC_TPU), (int)hu.size()});
     b.nunits = (int)hu.size() - b.ufirst;
-    ut_elems += 64 * (b.I1 + b.I2);
+    w_elems += (long long)Rp * (b.I1 + b.I2);
     bimg_total += b.bimg_bytes;
     plane_bytes += (size_t)b.ntiles * b.nk * XTC_STAGE;
     p->bytes += (double)b.I0 * (double)b.J * 4.0;
@@ -634,12 +603,13 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   p->grid = std::max(1, std::min(nsm, p->nunits));
-  // shared memory: the B image, then as many ring stages (<= 14) as fit
+  // shared memory: the factor image, then as many ring stages (<= 6) as fit
   const long long room = (long long)XTC_SMEM_MAX - (long long)xtc_smem_for(0, p->bimg_max);
-  const int nst = (int)std::min<long long>(14, room / (XTC_STAGE + 16));
-  if (nst < 3) {
+  const int nst = (int)std::min<long long>(6, room / (XTC_STAGE + 16));
+  if (nst < 2) {
+    const int bm = p->bimg_max;
     delete p;
-    set_error("xtc: operand image too large (%d bytes)", p->bimg_max);
+    set_error("xtc: operand image too large (%d bytes)", bm);
     return CB_ERR_UNSUPPORTED;
   }
   p->nst = nst;
@@ -657,7 +627,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     }                                                                  \
   } while (0)
   double* aux = nullptr;
-  float* ut = nullptr;
+  float* wts = nullptr;
   unsigned char* bimg = nullptr;
   unsigned char* planes = nullptr;
   // every plane byte is written by the pack kernel: no memset
@@ -669,16 +639,16 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   XTRY(dalloc((void**)&p->cnt, sizeof(int) * S, A));
   XTRY(dalloc((void**)&p->maxbits, sizeof(unsigned int) * S, A));
   XTRY(dalloc((void**)&aux, sizeof(double) * 64 * S, A));
-  XTRY(dalloc((void**)&ut, sizeof(float) * ut_elems, A));
-  XTRY(dalloc((void**)&bimg, (size_t)bimg_total, A));
-  long long uo = 0, bo = 0;
+  XTRY(dalloc((void**)&wts, sizeof(float) * w_elems, A));
+  XTRY(dalloc((void**)&bimg, (size_t)bimg_total, A));   // zeroed: the image's zero rows
+  long long wo = 0, bo = 0;
   size_t po = 0;
   for (int s = 0; s < S; ++s) {
     XtcBlock& b = hb[s];
     b.aux = aux + 64LL * s;
-    b.ut1 = ut + uo;
-    b.ut2 = ut + uo + 64 * b.I1;
-    uo += 64 * (b.I1 + b.I2);
+    b.w1 = wts + wo;
+    b.w2 = wts + wo + (long long)Rp * b.I1;
+    wo += (long long)Rp * (b.I1 + b.I2);
     b.bimg = bimg + bo;
     b.X = reinterpret_cast<const float*>(X[s]);
     b.planes = planes + po;
@@ -693,17 +663,18 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     k_xtc_maxabs<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(X[s]), n, p->maxbits + s);
   }
   k_xtc_set_ex<<<(S + 127) / 128, 128, 0, st>>>(p->blk, p->maxbits, S);
-  k_xtc_pack<<<dim3((unsigned)ntmax, 1, S), XTC_M, 0, st>>>(p->blk);
+  k_xtc_pack<<<dim3((unsigned)ntmax, 1, S), XTC_NT, 0, st>>>(p->blk);
   XCUDA(cudaGetLastError());
   count_launch(S + 2);
-#define XTC_ATTR(NN)                                                                       \
-  XCUDA(cudaFuncSetAttribute(k_xtc_trace<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+#define XTC_ATTR(RPV)                                                                       \
+  XCUDA(cudaFuncSetAttribute(k_xtc_trace<RPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)p->smem))
-  switch (N) {
+  switch (Rp) {
+    case 8: XTC_ATTR(8); break;
     case 16: XTC_ATTR(16); break;
+    case 24: XTC_ATTR(24); break;
     case 32: XTC_ATTR(32); break;
-    case 48: XTC_ATTR(48); break;
-    default: XTC_ATTR(64); break;
+    default: XTC_ATTR(40); break;
   }
 #undef XTC_ATTR
 #undef XTRY
@@ -730,23 +701,6 @@ void xtc_set_timeline(XtcPlan* p, unsigned long long* tl) {
   if (p) p->tl = tl;
 }
 
-template <int N>
-static int xtc_go(XtcPlan* p, const XtcArgs& a, const double* const* U, cudaStream_t st,
-                  int parts = 3) {
-  if (parts & 1) {
-    CB_CUDA(launch_k(k_xtc_prep<N>, dim3(p->S), dim3(256), 0, st, a, U));
-    count_launch(1);
-  }
-  if (parts & 2) {
-    const int grid = p->grid_cap > 0 ? std::min(p->grid, p->grid_cap) : p->grid;
-    // (launching it at the highest scheduling priority, so that its static
-    // partition is placed before the sweep's CTAs, measured slower on c5)
-    CB_CUDA(launch_k(k_xtc_trace<N>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a));
-    count_launch(1);
-  }
-  return CB_OK;
-}
-
 // parts: 1 = operand prep only (snapshots the factors), 2 = the streaming
 // pass only (reads only the prepared operands), 3 = both
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
@@ -757,17 +711,30 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.nunits = p->nunits;
   a.nst = p->nst;
   a.bimg_max = p->bimg_max;
+  a.Rp = p->Rp;
   a.part = p->part;
   a.cnt = p->cnt;
   a.bsum = bsum;
   a.gate = gate;
   a.tl = p->tl;
-  switch (p->N) {
-    case 16: return xtc_go<16>(p, a, U_dev, st, parts);
-    case 32: return xtc_go<32>(p, a, U_dev, st, parts);
-    case 48: return xtc_go<48>(p, a, U_dev, st, parts);
-    default: return xtc_go<64>(p, a, U_dev, st, parts);
+  if (parts & 1) {
+    CB_CUDA(launch_k(k_xtc_prep, dim3(p->S), dim3(256), 0, st, a, U_dev));
+    count_launch(1);
   }
+  if (parts & 2) {
+    const int grid = p->grid_cap > 0 ? std::min(p->grid, p->grid_cap) : p->grid;
+    // (launching it at the highest scheduling priority, so that its static
+    // partition is placed before the sweep's CTAs, measured slower on c5)
+    switch (p->Rp) {
+      case 8: CB_CUDA(launch_k(k_xtc_trace<8>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a)); break;
+      case 16: CB_CUDA(launch_k(k_xtc_trace<16>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a)); break;
+      case 24: CB_CUDA(launch_k(k_xtc_trace<24>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a)); break;
+      case 32: CB_CUDA(launch_k(k_xtc_trace<32>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a)); break;
+      default: CB_CUDA(launch_k(k_xtc_trace<40>, dim3(grid), dim3(XTC_THREADS), p->smem, st, a)); break;
+    }
+    count_launch(1);
+  }
+  return CB_OK;
 }
 
 }  // namespace cb

@@ -15,8 +15,8 @@ namespace cb {
 
 struct XtcPlan;
 
-// usable for these blocks?  fp32 storage, I0 <= XTC_MAX_I0, I1 >= 19,
-// rank <= 64
+// usable for these blocks?  fp32 storage, I0 <= 512, I1 >= 16, rank <= 40
+// (three byte levels of a column stacked along the MMA's M = 128)
 bool xtc_supported(int S, const void* const* X, const long long* dims, const int* R);
 
 // plan for S blocks (device fp32 tensors X[s], dims S x 3, ranks R[s]):

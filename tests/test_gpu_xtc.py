@@ -49,8 +49,9 @@ SHAPES = [
     ((112, 92, 40), 20),     # c3 mode sizes (shortened), J tail tile
     ((64, 71, 60), 30),      # c4 shape
     ((100, 100, 10), 10),    # c2 modes, N bucket 16
-    ((36, 20, 7), 64),       # rank 64 bucket, a single partial tile
-    ((4, 19, 2), 3),         # tiny (I1 = 19: the smallest staged mode-1 size)
+    ((36, 20, 7), 40),       # the largest rank (3 x 40 lanes), a single partial tile
+    ((50, 33, 21), 33),      # rank not a multiple of 8, ragged everything
+    ((4, 19, 2), 3),         # tiny
 ]
 
 
@@ -90,8 +91,8 @@ def test_tc_trace_batched_ragged_and_deterministic(P):
 
 def test_tc_trace_rejects_unsupported_shapes(P):
     rng = np.random.default_rng(1)
-    for dims in ((6, 5, 4), (516, 20, 4)):      # I1 < 19; I0 > 512
-        x, g = _block(rng, dims, 3)
+    for dims, rank in (((6, 5, 4), 3), ((516, 20, 4), 3), ((36, 20, 7), 41)):   # I1 < 16; I0 > 512; rank > 40
+        x, g = _block(rng, dims, rank)
         with pytest.raises(Exception):
             P.core_linear_terms_tc([x], [g])
 

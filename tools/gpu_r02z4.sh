@@ -2,9 +2,7 @@
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out/r02z4
 mkdir -p $O; rm -f $O/status.txt
-timeout 900 python -m pytest tests/test_gpu_xtc.py -m gpu -x -q > $O/pytest_xtc.log 2>&1; echo "pytest xtc rc=$?" >> $O/status.txt
-timeout 300 python tools/xtc_probe.py 64 3 > $O/xtc_probe.txt 2>&1; echo "probe rc=$?" >> $O/status.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_xtc_trace -c 1 -o $O/xtc_trace -f python tools/xtc_probe.py 64 1 > $O/ncu.log 2>&1; echo "ncu rc=$?" >> $O/status.txt
 python tools/ncu_summary.py $O/xtc_trace.ncu-rep 5 > $O/xtc_trace_summary.txt 2>&1
-python tools/ncu_lines.py $O/xtc_trace.ncu-rep 30 > $O/xtc_trace_lines.txt 2>&1
-cat $O/status.txt; tail -4 $O/pytest_xtc.log; cat $O/xtc_probe.txt; cat $O/xtc_trace_summary.txt; head -50 $O/xtc_trace_lines.txt
+python tools/ncu_lines.py $O/xtc_trace.ncu-rep 40 > $O/xtc_trace_lines.txt 2>&1
+cat $O/status.txt; cat $O/xtc_trace_summary.txt; head -45 $O/xtc_trace_lines.txt
