@@ -344,7 +344,7 @@ extern "C" {
 int cb_als_destroy(cb_als* h) {
   if (!h) return CB_OK;
   if (h->st) cudaStreamSynchronize(h->st);
-  for (void* p : h->allocs) cudaFree(p);
+  dfree_all(h->allocs);
   cb::sl5_plan_destroy(h->sl5);
   cb::oz_plan_destroy(h->oz);
   if (h->h_state) cudaFreeHost(h->h_state);
@@ -500,15 +500,36 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     TRY(dalloc((void**)&bsum, sizeof(double) * S * RSTRIDE, A));
     TRY(dalloc((void**)&rsum, sizeof(double) * S, A));
     TRY(dalloc((void**)&blk_cnt, sizeof(int) * S, A));
-    TRY(dalloc((void**)&spart, sizeof(double) * h->tab.slab.size() * h->tab.sb * RSTRIDE, A));
+    TRY(dalloc((void**)&spart,
+               h->oz ? 8 : sizeof(double) * h->tab.slab.size() * h->tab.sb * RSTRIDE, A));
     c.rpart = rsum;
     c.slab_part = spart;
     std::vector<void*> T0(S), T1(S);
     const int eb = pc_compute_bytes(h->pc);
-    for (int s = 0; s < S; ++s) {
-      const size_t tb = (size_t)h->tab.nsplit[s] * h->R[s] * h->dims[3 * s] * h->dims[3 * s + 1] * eb;
-      TRY(dalloc(&T0[s], tb, A));
-      TRY(dalloc(&T1[s], tb, A));
+    if (h->oz) {
+      // one unsplit T per block out of a single allocation: the T pass writes
+      // every element before the contractions read it (no memset), and the
+      // sweep is strictly sequential, so the two T selectors share a buffer
+      size_t tot = 0;
+      std::vector<size_t> ofs(S);
+      for (int s = 0; s < S; ++s) {
+        ofs[s] = tot;
+        tot += ((size_t)h->R[s] * h->dims[3 * s] * h->dims[3 * s + 1] * eb + 255) & ~(size_t)255;
+      }
+      char* tbuf = nullptr;
+      const cudaError_t te = cudaMalloc((void**)&tbuf, tot);
+      if (te != cudaSuccess) {
+        cb_als_destroy(h);
+        return cuda_fail(te, "cudaMalloc (T buffers)", __FILE__, __LINE__);
+      }
+      A.push_back(tbuf);
+      for (int s = 0; s < S; ++s) T0[s] = T1[s] = tbuf + ofs[s];
+    } else {
+      for (int s = 0; s < S; ++s) {
+        const size_t tb = (size_t)h->tab.nsplit[s] * h->R[s] * h->dims[3 * s] * h->dims[3 * s + 1] * eb;
+        TRY(dalloc(&T0[s], tb, A));
+        TRY(dalloc(&T1[s], tb, A));
+      }
     }
     void **pt0, **pt1;
     TRY(upload(T0, &pt0, A, st));

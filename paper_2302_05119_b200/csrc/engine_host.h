@@ -58,14 +58,15 @@ void launch_slab(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, in
 void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
                      cudaStream_t st);
 int dalloc(void** p, size_t bytes, std::vector<void*>& allocs);
+void dfree_all(std::vector<void*>& allocs);
 void set_alloc_stream(cudaStream_t st);
 
 template <typename T>
 int upload(const std::vector<T>& v, T** d, std::vector<void*>& allocs, cudaStream_t st) {
   *d = nullptr;
   if (v.empty()) return CB_OK;
-  CB_CUDA(cudaMalloc((void**)d, sizeof(T) * v.size()));
-  allocs.push_back(*d);
+  int rc = dalloc((void**)d, sizeof(T) * v.size(), allocs);
+  if (rc) return rc;
   CB_CUDA(cudaMemcpyAsync(*d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
   return CB_OK;
 }

@@ -585,7 +585,7 @@ int oz_plan_create(int S, const void* const* X, const long long* dims, const int
 
 void oz_plan_destroy(OzPlan* p) {
   if (!p) return;
-  for (void* q : p->allocs) cudaFree(q);
+  dfree_all(p->allocs);
   delete p;
 }
 

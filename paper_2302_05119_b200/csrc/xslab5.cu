@@ -571,7 +571,7 @@ int sl5_tpass(Sl5Plan* p, const double* const* U_dev, const int* active, void* c
 
 void sl5_plan_destroy(Sl5Plan* p) {
   if (!p) return;
-  for (void* q : p->allocs) cudaFree(q);
+  dfree_all(p->allocs);
   delete p;
 }
 

@@ -685,7 +685,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
 
 void xtc_plan_destroy(XtcPlan* p) {
   if (!p) return;
-  for (void* q : p->allocs) cudaFree(q);
+  dfree_all(p->allocs);
   delete p;
 }
 
