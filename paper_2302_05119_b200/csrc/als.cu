@@ -392,8 +392,6 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       mI = std::max(mI, In);
       TRY(dalloc((void**)&U[s * N + n], sizeof(double) * In * h->R[s], A));
       TRY(dalloc((void**)&G[s * N + n], sizeof(double) * h->R[s] * h->R[s], A));
-      CB_CUDA(cudaMemcpyAsync(U[s * N + n], d->init[s * N + n], sizeof(double) * In * h->R[s],
-                              cudaMemcpyHostToDevice, st));
     }
     TRY(dalloc((void**)&MTT[s], sizeof(double) * mI * h->R[s], A));
   }
@@ -419,6 +417,34 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   c.st = h->d_state;
   CB_CUDA(cudaMallocHost((void**)&h->h_state, sizeof(AlsState)));
   memset(h->h_state, 0, sizeof(AlsState));
+  // unit tables and the tensor-core plan first: its allocations (the byte
+  // planes: 34 GB on c5, ~0.1 s of host time) then run while the caller's
+  // host->device copies of the blocks are still in flight on `st`, ahead of
+  // the synchronisation below; its pack kernels queue behind those copies
+  if (h->fast3) {
+    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab,
+                  d->total_blocks > S ? d->total_blocks : S);
+    h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->dtype == CB_F32 ? 4 : 8);
+    // fp32 storage with fp64-grade arithmetic, ranks in (16, 48]: both tensor
+    // passes of a sweep as exact int8 slice GEMMs over byte planes packed once
+    // (xoz.cu).  T is then written unsplit whatever the fiber table chose.
+    if (h->pc == PC_F32_F64 && !h->tab.slab_direct &&
+        oz_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
+      if (oz_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->oz) != CB_OK)
+        h->oz = nullptr;
+      if (h->oz) {
+        h->tab.nsplit.assign(S, 1);
+        h->tab.fib_unsplit = 1;
+      }
+    }
+  }
+  // the starting factors (pageable host memory: these copies wait for the
+  // stream, so they come after every allocation above)
+  for (int s = 0; s < S; ++s)
+    for (int n = 0; n < N; ++n)
+      CB_CUDA(cudaMemcpyAsync(U[s * N + n], d->init[s * N + n],
+                              sizeof(double) * h->dims[s * N + n] * h->R[s],
+                              cudaMemcpyHostToDevice, st));
   // norms and the initial rel err (1, or 0 for a zero tensor: cpd_als.py:84-86)
   {
     double* stats;
@@ -465,21 +491,6 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       if (rc) { cb_als_destroy(h); return rc; }
     }
   if (h->fast3) {
-    build_xtables(S, h->dims.data(), h->R.data(), h->rb, h->pc, h->tab,
-                  d->total_blocks > S ? d->total_blocks : S);
-    h->tma = tma_rows_ok(S, h->dims.data(), h->X.data(), h->dtype == CB_F32 ? 4 : 8);
-    // fp32 storage with fp64-grade arithmetic, ranks in (16, 48]: both tensor
-    // passes of a sweep as exact int8 slice GEMMs over byte planes packed once
-    // (xoz.cu).  T is then written unsplit whatever the fiber table chose.
-    if (h->pc == PC_F32_F64 && !h->tab.slab_direct &&
-        oz_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
-      if (oz_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->oz) != CB_OK)
-        h->oz = nullptr;
-      if (h->oz) {
-        h->tab.nsplit.assign(S, 1);
-        h->tab.fib_unsplit = 1;
-      }
-    }
     prepare_slab(h->pc, h->rb, h->tma, h->tab);
     prepare_fiber(h->pc, h->rb, h->tma, h->tab);
     TRY(upload(h->tab.fib, &h->d_fib, A, st));

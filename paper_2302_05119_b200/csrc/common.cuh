@@ -36,6 +36,14 @@ __device__ __forceinline__ void griddep_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// The wait without the early trigger, for the persistent streaming kernels
+// (one CTA per SM for milliseconds): dependents launched early would sit
+// resident beside them for the whole stream and slow it (measured on the ALS
+// mode-2 pass: 9.0 -> 4.9 ms with its contraction kernel launched at exit).
+__device__ __forceinline__ void griddep_wait_no_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Asynchronous global -> shared staging (LDGSTS): every thread issues its
 // 8-byte copies without waiting, so a staging loop costs one memory latency
 // instead of one per iteration.  Complete with cp_async8_wait() and a barrier.

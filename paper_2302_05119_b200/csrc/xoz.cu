@@ -251,7 +251,7 @@ __device__ __forceinline__ double oz_i2d(uint32_t x) {
 // --------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_gemm(OzArgs a) {
-  griddep_wait();
+  griddep_wait_no_trigger();
   constexpr int NH = N / 2;          // columns per epilogue group
   constexpr int WMMA = 8, WTMA = 9;
   constexpr int DW = OZ_SB * N;      // accumulator columns per buffer

@@ -279,7 +279,7 @@ __device__ __forceinline__ double i2d_exact(uint32_t x) {
 
 template <int RP>
 __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
-  griddep_wait();
+  griddep_wait_no_trigger();
   if (a.gate && *a.gate == 0) return;
   tl_begin(a.tl, TL_TRACE);
   constexpr int NE = 256;            // epilogue threads

@@ -34,7 +34,7 @@ import numpy as np
 
 from . import _device as D
 from . import _lib as L
-from .cpd_als import AlsOptions, _check_feasible, als_compress_blocks
+from .cpd_als import AlsHandle, AlsOptions, _check_feasible, als_compress_blocks
 from .kruskal import CoupledFactorSet, KruskalTensor
 from .tensor_ops import hadamard_gram, spectral_norm
 
@@ -519,6 +519,41 @@ class PreparedSolve:
                 del src
                 self.dev.append(flat)
                 self.dims.append(dims)
+            # host-side checks that follow the value checks in the reference's
+            # order (ranks / counts, then the compression's feasibility)
+            ranks = None
+            late_exc = None
+            if bad_msg is None:
+                try:
+                    problem._validate_tail()
+                    if problem.mode == "lra":
+                        base = (problem.als_options if problem.als_options is not None
+                                else AlsOptions())
+                        ranks = [base.rank if base.rank is not None else problem.ranks[g]
+                                 for g in self.local]
+                        for s, (dims, r) in enumerate(zip(self.dims, ranks)):
+                            try:
+                                _check_feasible(dims, r)
+                            except ValueError as exc:
+                                raise ValueError(
+                                    f"compression of block {self.local[s]} failed: {exc}") from exc
+                except ValueError as exc:
+                    late_exc = exc
+            # lra stage 1 setup (solver.py:556-573) before the value checks'
+            # synchronisation: with pinned host tensors the uploads above are
+            # DMA in flight, and the ALS engine's allocations (byte planes,
+            # T buffers: ~0.1 s of host time on c5) run beside them
+            self.als = None
+            st = L.c_vp(self.stream.cuda_stream)
+            tic = time.perf_counter()
+            als_exc = None
+            if ranks is not None and late_exc is None:
+                try:
+                    self.als = AlsHandle(self.dev, self.dims, ranks, self.code, base.tol,
+                                         base.max_iter, [base.seed + g for g in self.local], st,
+                                         self.als_compute_code, S_all)
+                except ValueError as exc:
+                    als_exc = exc
             host = stats.cpu().numpy() if scan else np.zeros((0, 3))
             for k, g in enumerate(scan):
                 if host[k, 2] != 0.0 or host[k, 1] < 0.0:
@@ -527,38 +562,34 @@ class PreparedSolve:
                     break
             if agree is not None:
                 first_bad, bad_msg = agree(first_bad, bad_msg, problem)
+            if bad_msg is None:
+                bad_msg = late_exc
             if bad_msg is not None:
+                if self.als is not None:
+                    self.als.close()
+                    self.als = None
                 raise bad_msg
-            problem._validate_tail()
-        st = L.c_vp(self.stream.cuda_stream)
         # lra stage 1: batched device ALS (solver.py:556-573)
         self.compress_seconds = 0.0
-        self.als = None
         tilde_ranks = None
         if problem.mode == "lra":
-            base = problem.als_options if problem.als_options is not None else AlsOptions()
-            ranks = [base.rank if base.rank is not None else problem.ranks[g] for g in self.local]
-            for s, (dims, r) in enumerate(zip(self.dims, ranks)):
-                try:
-                    _check_feasible(dims, r)
-                except ValueError as exc:
-                    raise ValueError(f"compression of block {self.local[s]} failed: {exc}") from exc
-            tic = time.perf_counter()
             with torch.cuda.stream(self.stream):
                 try:
-                    self.als = als_compress_blocks(self.dev, self.dims, ranks, base.tol,
-                                                   base.max_iter,
-                                                   [base.seed + g for g in self.local],
-                                                   self.code, st, self.als_compute_code,
-                                                   total_blocks=S_all)
+                    if als_exc is not None:
+                        raise als_exc
+                    self.als.run()
                 except ValueError as exc:
                     msg = str(exc)
                     blk = 0
                     if msg.startswith("block "):
                         blk = self.local[int(msg.split()[1].rstrip(":"))]
                         msg = msg.split(": ", 1)[1]
+                    if self.als is not None:
+                        self.als.close()
+                        self.als = None
                     raise ValueError(f"compression of block {blk} failed: {msg}") from exc
             self.stream.synchronize()
+            # (includes the tail of the upload that the setup overlapped)
             self.compress_seconds = time.perf_counter() - tic
             tilde_ranks = ranks
         # the seeded start of ALL blocks (one PCG64 stream), then this shard's

@@ -40,17 +40,26 @@ def timed_create(self, desc, stream):
 
 
 S._Engine.__init__ = timed_create
-orig_als = S.als_compress_blocks
+# the ALS engine is created while the uploads are still in flight (its
+# allocations overlap the DMA), so the marks only bracket host time here
+orig_als_init = S.AlsHandle.__init__
+orig_als_run = S.AlsHandle.run
 
 
-def timed_als(*a, **k):
-    mark("upload + value checks")
-    h = orig_als(*a, **k)
-    mark("ALS compression")
-    return h
+def timed_als_init(self, *a, **k):
+    marks.append(("uploads enqueued (host)", time.perf_counter()))
+    orig_als_init(self, *a, **k)
+    marks.append(("ALS engine create (host; waits for the upload inside)", time.perf_counter()))
 
 
-S.als_compress_blocks = timed_als
+def timed_als_run(self):
+    mark("value checks (upload complete)")
+    orig_als_run(self)
+    mark("ALS sweeps")
+
+
+S.AlsHandle.__init__ = timed_als_init
+S.AlsHandle.run = timed_als_run
 prob = P.CoupledProblem(host, spec.rank, list(spec.coupled), mode=spec.mode)
 opts = P.SolverOptions(max_iter=spec.max_iter, tol=float(np.nextafter(0, 1)), seed=0,
                        precision=spec.dtype)
