@@ -309,3 +309,18 @@ def test_value_checks_in_input_dtype_and_reference_order(P):
     with pytest.raises(ValueError, match="block 1 has order 2"):
         P.solve(P.CoupledProblem([good, good[:, :, 0], -good], 2, [0, 0, 0]),
                 P.SolverOptions(max_iter=2))
+    # lra (the compression engine is set up beside the upload, before the
+    # value checks complete): a value error still comes before the
+    # compression's own feasibility error (solver.py:556-573)
+    als = P.AlsOptions(rank=50)
+    with pytest.raises(ValueError, match="block 1 contains negative entries"):
+        P.solve(P.CoupledProblem([good, -good], 2, [0, 0, 0], mode="lra", als_options=als),
+                P.SolverOptions(max_iter=2))
+    with pytest.raises(ValueError, match="compression of block 0 failed"):
+        P.solve(P.CoupledProblem([good, good], 2, [0, 0, 0], mode="lra", als_options=als),
+                P.SolverOptions(max_iter=2))
+    nan = good.copy()
+    nan[1, 1, 1] = np.inf
+    with pytest.raises(ValueError, match="block 1 contains non-finite values"):
+        P.solve(P.CoupledProblem([good, nan], 2, [0, 0, 0], mode="lra"),
+                P.SolverOptions(max_iter=2))
