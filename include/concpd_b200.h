@@ -180,10 +180,12 @@ typedef struct {
                                      I_n x R row-major initial factors      */
   double tol;                     /* AlsOptions.tol                         */
   int max_iter;                   /* AlsOptions.max_iter                    */
-  int compute;                    /* fp32 storage only: 0 = fp64 arithmetic in
-                                     the tensor passes, 1 = fp32 arithmetic,
-                                     2 = fp64 except the mode-2 MTTKRP of
-                                     ranks > 16, on the tensor cores (xtc)  */
+  int compute;                    /* fp32 storage only: 0 (and 2) = fp64-grade
+                                     arithmetic in the tensor passes (3-way
+                                     blocks of ranks in (16, 48]: exact int8
+                                     slice GEMMs on the tensor cores over
+                                     byte planes packed once, csrc/xoz.cu;
+                                     else fp64 FMAs), 1 = fp32 arithmetic   */
   int total_blocks;               /* blocks of the whole (sharded) problem;
                                      fixes each block's work decomposition so
                                      a shard reproduces the unsharded bits

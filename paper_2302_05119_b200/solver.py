@@ -486,12 +486,11 @@ class PreparedSolve:
         if compute == "auto":
             compute = "fp64" if (problem.mode == "full" or max(problem.ranks) <= 16) else "tc"
         self.compute_code = {"fp64": 0, "fp32": 1, "tc": 2}[compute] if prec == "fp32" else 0
-        # ALS compression: fp64 passes unless asked explicitly ("fp32", or
-        # "tc": the mode-2 MTTKRP of ranks > 16 on the tensor cores, ~2.7x
-        # faster per c5 sweep).  Not under "auto": the compressed model of
-        # an ill-conditioned fit moves by ~1e-5 relative under ~1e-9 MTTKRP
-        # changes, which the 1e-4 factor parity of c3 does not absorb.
-        self.als_compute_code = ({"fp32": 1, "tc": 2}.get(opts.compute, 0)
+        # ALS compression: fp64-grade passes (ranks in (16, 48]: exact int8
+        # slice GEMMs on the tensor cores, csrc/xoz.cu; the compressed model
+        # of an ill-conditioned fit moves by ~1e-5 relative under ~1e-9 MTTKRP
+        # changes, so the passes keep ~1e-13) unless "fp32" is asked for
+        self.als_compute_code = ({"fp32": 1}.get(opts.compute, 0)
                                  if prec == "fp32" else 0)
         S, N = len(self.local), problem.order
         with torch.cuda.stream(self.stream):

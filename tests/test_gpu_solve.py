@@ -164,8 +164,9 @@ def test_config_c5_subset_fp64_matches_reference(P):
             _rel_close(a, b, 1e-8, f"compression block {s} mode {m}")
 
 
-def test_config_c5_subset_tensor_core_als(P):
-    """compute="tc": the ALS mode-2 MTTKRP on the tensor cores as well."""
+def test_config_c5_subset_explicit_tc(P):
+    """compute="tc" asked for explicitly (the default for these ranks): the
+    tensor-core trace pass and the tensor-core ALS passes."""
     res, want = _config(P, "c5", "fp32", compute="tc")
     compare(res, want, rtol=1e-4, factor_rtol=1e-4)
 
