@@ -84,6 +84,7 @@ using namespace cb;
 
 struct cb_solver {
   cudaStream_t st = nullptr;
+  bool redo_reprep = false;   // pipelined lra: the restart branch re-prepares the trace operands
   // side stream of the 3-way full path: the MTTKRP of mode n runs on it
   // concurrently with mode n's step matrix / lambda_max on `st` (fork/join by
   // events, captured as parallel graph branches)
@@ -511,6 +512,8 @@ static int enqueue_trace_lra(cb_solver* h) {
 // one full APG iteration (solver.py:586-610), device-gated
 // restart branch (solver.py:594-599): restore, sweep with w_hat = 0,
 // re-evaluate, accept; every kernel is gated on go_redo
+static int enqueue_pipe_prep_redo(cb_solver* h);
+
 static int enqueue_redo_branch(cb_solver* h) {
   int rc;
   if ((rc = enqueue_restore(h))) return rc;
@@ -521,6 +524,7 @@ static int enqueue_redo_branch(cb_solver* h) {
   } else if ((rc = enqueue_qr(h, 1))) {
     return rc;
   }
+  if (h->redo_reprep && (rc = enqueue_pipe_prep_redo(h))) return rc;
   return enqueue_control(h, CTRL_REDO);
 }
 
@@ -603,15 +607,30 @@ static int enqueue_iteration(cb_solver* h) {
 //                      (k+1) -> redo -> prep(k+1) + snapshots
 //   drain:             trace(k), FINISH(k) (no speculative sweep to undo)
 // The arithmetic is that of the classic order, so results are identical.
-static int enqueue_pipe_prep(cb_solver* h) {
+// Operand prep of the next trace into the set the running trace does not
+// read, then (PREP_COMMIT) the lam / model_sq snapshots and the set flip.
+//   PREP_MAIN:   after DECIDE / redo on the main gate (the prologue);
+//   PREP_SPEC:   right after the sweep, beside the running trace: the
+//                factors are final unless the iteration restarts;
+//   PREP_REDO:   inside the restart branch (gate go_redo), after its sweep;
+//   PREP_COMMIT: snapshots + flip only.
+enum { PREP_MAIN = 0, PREP_SPEC = 1, PREP_REDO = 2, PREP_COMMIT = 3 };
+
+static int enqueue_pipe_prep(cb_solver* h, int mode) {
   if (!emit(h)) return CB_OK;
-  int rc = xtc_trace(h->xtc, h->xa_main.U, h->xa_main.gate, h->ctx.fib_bpart, h->st, 1);
-  if (rc) return rc;
+  if (mode != PREP_COMMIT) {
+    const int* gate = mode == PREP_REDO ? h->xa_redo.gate : h->xa_main.gate;
+    int rc = xtc_trace(h->xtc, h->xa_main.U, gate, h->ctx.fib_bpart, h->st, 1, 1);
+    if (rc) return rc;
+    if (mode != PREP_MAIN) return CB_OK;
+  }
   launch_k(k_pipe_snap, dim3(h->S), dim3(64), 0, h->st, h->ctx);
   count_launch(1);
   CB_CHECK_LAUNCH();
-  return CB_OK;
+  return xtc_flip(h->xtc, h->xa_main.gate, h->st);
 }
+
+static int enqueue_pipe_prep_redo(cb_solver* h) { return enqueue_pipe_prep(h, PREP_REDO); }
 
 static int enqueue_pipe_stream(cb_solver* h, cudaStream_t st) {
   if (!emit(h)) return CB_OK;
@@ -630,7 +649,7 @@ static int enqueue_pipe_prologue(cb_solver* h) {
   if ((rc = enqueue_qr(h, 0))) return rc;
   if ((rc = enqueue_control(h, CTRL_DECIDE, 16))) return rc;
   if ((rc = enqueue_redo(h))) return rc;
-  return enqueue_pipe_prep(h);
+  return enqueue_pipe_prep(h, PREP_MAIN);
 }
 
 static int enqueue_pipe_step(cb_solver* h) {
@@ -639,6 +658,7 @@ static int enqueue_pipe_step(cb_solver* h) {
   if ((rc = enqueue_pipe_stream(h, h->st2))) return rc;
   if ((rc = enqueue_sweep(h, 0))) return rc;
   if ((rc = enqueue_qr(h, 0))) return rc;
+  if ((rc = enqueue_pipe_prep(h, PREP_SPEC))) return rc;
   if ((rc = join_side(h))) return rc;
   if ((rc = enqueue_control(h, CTRL_FINISH, 16 | 32))) return rc;
   if (emit(h)) {
@@ -647,8 +667,11 @@ static int enqueue_pipe_step(cb_solver* h) {
     CB_CHECK_LAUNCH();
   }
   if ((rc = enqueue_control(h, CTRL_DECIDE, 16))) return rc;
-  if ((rc = enqueue_redo(h))) return rc;
-  return enqueue_pipe_prep(h);
+  h->redo_reprep = true;     // a restarted iteration re-prepares the operands
+  rc = enqueue_redo(h);
+  h->redo_reprep = false;
+  if (rc) return rc;
+  return enqueue_pipe_prep(h, PREP_COMMIT);
 }
 
 static int pipe_drain(cb_solver* h) {

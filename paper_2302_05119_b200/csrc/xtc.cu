@@ -88,12 +88,14 @@ struct XtcBlock {
   int ex;                 // fixed-point exponent of X
   int ufirst, nunits;
   int bimg_bytes;
-  double* aux;            // [64] scale_r
-  float* w1;              // [I1][Rp] = A1[i1, r] (fp32 row weights, zero-padded columns)
-  float* w2;              // [I2][Rp] = A2[i2, r]
+  // per-call operands, two sets: the pipelined iteration prepares the next
+  // trace's set while the current trace still reads the other
+  double* aux[2];         // [64] scale_r
+  float* w1[2];           // [I1][Rp] = A1[i1, r] (fp32 row weights, zero-padded columns)
+  float* w2[2];           // [I2][Rp] = A2[i2, r]
+  unsigned char* bimg[2]; // [nk][2 Rp + 128 rows][32 B] (K-major, 32-B swizzle)
   const float* X;         // the block (read by the pack kernel only)
   unsigned char* planes;  // [ntiles][nk][3 planes][256 rows x 32 B]
-  unsigned char* bimg;    // [nk][2 Rp + 128 rows][32 B] (K-major, 32-B swizzle)
 };
 
 struct XtcUnit { int s, t0, t1, u; };
@@ -105,6 +107,8 @@ struct XtcArgs {
   int nst;
   int bimg_max;
   int Rp;                 // lanes per level (max rank rounded up to 8)
+  const int* par;         // operand set the trace reads (device; flipped by k_xtc_flip)
+  int wr_other;           // prep: write the other set (pipelined), else the current one
   double* part;           // [unit][64]
   int* cnt;               // per-block arrival counters (self-resetting)
   double* bsum;           // [s][RSTRIDE]
@@ -123,6 +127,7 @@ struct XtcPlan {
   XtcUnit* units = nullptr;
   double* part = nullptr;
   int* cnt = nullptr;
+  int* par = nullptr;        // current operand set (device)
   unsigned int* maxbits = nullptr;
   unsigned long long* tl = nullptr;   // iteration timeline (profiling)
 };
@@ -206,6 +211,8 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
   tl_begin(a.tl, TL_PREP);
   const int s = blockIdx.x;
   const XtcBlock b = a.blk[s];
+  const int set = (*a.par) ^ a.wr_other;
+  unsigned char* bimg = b.bimg[set];
   const double* A0 = U[3 * s];
   const double* A1 = U[3 * s + 1];
   const double* A2 = U[3 * s + 2];
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
       const int row = (2 + l) * Rp + n;
       const long long off =
           ((long long)c * SR + row) * 32 + (((kk >> 4) ^ ((row >> 2) & 1)) << 4) + (kk & 15);
-      b.bimg[off] = (unsigned char)(signed char)d;
+      bimg[off] = (unsigned char)(signed char)d;
     };
     put(0, d0);
     put(1, d1);
@@ -253,20 +260,27 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
   if (threadIdx.x < 64) {
     const int r = threadIdx.x;
     // q p = 2^16 (2^16 L0 + 2^8 L1 + L2)
-    b.aux[r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS) : 0.0;
+    b.aux[set][r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS) : 0.0;
   }
   const long long I1 = b.I1, I2 = b.I2;
   for (long long e = threadIdx.x; e < I1 * Rp; e += 256) {
     const long long i = e / Rp;
     const int r = (int)(e - i * Rp);
-    b.w1[e] = r < R ? (float)A1[i * R + r] : 0.0f;
+    b.w1[set][e] = r < R ? (float)A1[i * R + r] : 0.0f;
   }
   for (long long e = threadIdx.x; e < I2 * Rp; e += 256) {
     const long long i = e / Rp;
     const int r = (int)(e - i * Rp);
-    b.w2[e] = r < R ? (float)A2[i * R + r] : 0.0f;
+    b.w2[set][e] = r < R ? (float)A2[i * R + r] : 0.0f;
   }
   tl_end(a.tl, TL_PREP);
+}
+
+// the set just prepared becomes the one the next trace reads
+__global__ void k_xtc_flip(int* par, const int* gate) {
+  griddep_wait();
+  if (gate && *gate == 0) return;
+  if (threadIdx.x == 0) *par ^= 1;
 }
 
 // --------------------------------------------------------------------------
@@ -304,6 +318,7 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
   int* shflag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int set = *a.par;
   const int G = gridDim.x;
   const int u_begin = (int)((long long)blockIdx.x * a.nunits / G);
   const int u_end = (int)((long long)(blockIdx.x + 1) * a.nunits / G);
@@ -335,7 +350,7 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
           const int bytes = b.bimg_bytes;
           mbar_arrive_expect_tx(b_full, (uint32_t)bytes);
           for (int off = 0; off < bytes; off += 32768)
-            bulk_g2s(bimg + off, b.bimg + off, (uint32_t)min(32768, bytes - off), b_full);
+            bulk_g2s(bimg + off, b.bimg[set] + off, (uint32_t)min(32768, bytes - off), b_full);
           cur = un.s;
           ++seg;
         }
@@ -419,8 +434,8 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
       // padding columns of the weight tables / a valid address and weigh
       // their products by zero
       const bool act = lev < 3 && r < b.R;
-      const float* __restrict__ w1p = b.w1 + (act ? r : 0);
-      const float* __restrict__ w2p = b.w2 + (act ? r : 0);
+      const float* __restrict__ w1p = b.w1[set] + (act ? r : 0);
+      const float* __restrict__ w2p = b.w2[set] + (act ? r : 0);
       const float wm = act ? 1.0f : 0.0f;
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
         const int buf = tl & 1;
@@ -506,7 +521,7 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
             const double s0 = red[et] + red[128 + et];
             const double s1 = red[RP + et] + red[128 + RP + et];
             const double s2 = red[2 * RP + et] + red[128 + 2 * RP + et];
-            a.part[(long long)un.u * 64 + et] = fma(s0, 65536.0, fma(s1, 256.0, s2)) * b.aux[et];
+            a.part[(long long)un.u * 64 + et] = fma(s0, 65536.0, fma(s1, 256.0, s2)) * b.aux[set][et];
             __threadfence();
           }
           named_bar(1, NE);
@@ -638,18 +653,21 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
   XTRY(dalloc((void**)&p->part, sizeof(double) * 64 * hu.size(), A));
   XTRY(dalloc((void**)&p->cnt, sizeof(int) * S, A));
   XTRY(dalloc((void**)&p->maxbits, sizeof(unsigned int) * S, A));
-  XTRY(dalloc((void**)&aux, sizeof(double) * 64 * S, A));
-  XTRY(dalloc((void**)&wts, sizeof(float) * w_elems, A));
-  XTRY(dalloc((void**)&bimg, (size_t)bimg_total, A));   // zeroed: the image's zero rows
+  XTRY(dalloc((void**)&p->par, sizeof(int), A));
+  XTRY(dalloc((void**)&aux, sizeof(double) * 2 * 64 * S, A));
+  XTRY(dalloc((void**)&wts, sizeof(float) * 2 * w_elems, A));
+  XTRY(dalloc((void**)&bimg, (size_t)2 * bimg_total, A));   // zeroed: the image's zero rows
   long long wo = 0, bo = 0;
   size_t po = 0;
   for (int s = 0; s < S; ++s) {
     XtcBlock& b = hb[s];
-    b.aux = aux + 64LL * s;
-    b.w1 = wts + wo;
-    b.w2 = wts + wo + (long long)Rp * b.I1;
+    for (int k = 0; k < 2; ++k) {
+      b.aux[k] = aux + 64LL * (2 * s + k);
+      b.w1[k] = wts + k * w_elems + wo;
+      b.w2[k] = wts + k * w_elems + wo + (long long)Rp * b.I1;
+      b.bimg[k] = bimg + (size_t)k * bimg_total + bo;
+    }
     wo += (long long)Rp * (b.I1 + b.I2);
-    b.bimg = bimg + bo;
     b.X = reinterpret_cast<const float*>(X[s]);
     b.planes = planes + po;
     po += (size_t)b.ntiles * b.nk * XTC_STAGE;
@@ -703,9 +721,17 @@ void xtc_set_timeline(XtcPlan* p, unsigned long long* tl) {
 
 // parts: 1 = operand prep only (snapshots the factors), 2 = the streaming
 // pass only (reads only the prepared operands), 3 = both
+int xtc_flip(XtcPlan* p, const int* gate, cudaStream_t st) {
+  CB_CUDA(launch_k(k_xtc_flip, dim3(1), dim3(32), 0, st, p->par, gate));
+  count_launch(1);
+  return CB_OK;
+}
+
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
-              cudaStream_t st, int parts) {
+              cudaStream_t st, int parts, int other) {
   XtcArgs a{};
+  a.par = p->par;
+  a.wr_other = other ? 1 : 0;
   a.blk = p->blk;
   a.units = p->units;
   a.nunits = p->nunits;

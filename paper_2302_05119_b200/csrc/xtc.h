@@ -30,8 +30,14 @@ void xtc_plan_destroy(XtcPlan* p);
 // b_s into bsum[s * RSTRIDE + r] (r < R[s]); factors from U (device array of
 // S*3 pointers, the engine's XArgs.U), skipped when *gate == 0 (gate may be
 // null).  Two launches: operand prep + the streaming MMA kernel.
+// parts: 1 = operand prep only (snapshots the factors), 2 = the streaming
+// pass only (reads only the prepared operands), 3 = both.  The operands
+// exist twice: with other = 1 the prep writes the set the trace is NOT
+// reading (the pipelined iteration prepares trace k+1 while trace k streams);
+// xtc_flip then makes that set current.
 int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* bsum,
-              cudaStream_t st, int parts = 3);
+              cudaStream_t st, int parts = 3, int other = 0);
+int xtc_flip(XtcPlan* p, const int* gate, cudaStream_t st);
 
 // cap the streaming kernel's persistent grid (0: one CTA per SM), leaving
 // SMs to work that runs beside it (the pipelined lra sweep)

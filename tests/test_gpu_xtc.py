@@ -194,6 +194,30 @@ def test_pipelined_lra_iteration_is_bitwise_unpipelined(P, tol, max_iter):
             np.testing.assert_array_equal(fa, fb)
 
 
+def test_pipelined_iteration_with_a_restart_is_bitwise_unpipelined(P):
+    """c3 (device-generated blocks) restarts once: the pipelined iteration
+    prepares the next trace's operands right after the sweep, beside the
+    running trace, and the restart branch re-prepares them from the redone
+    sweep (csrc/engine.cu PREP_SPEC / PREP_REDO); histories, counts and
+    factors equal the unpipelined solve's bitwise."""
+    from paper_2302_05119_b200.synth import generate_config_device
+    dev, spec = generate_config_device("c3")
+    out = {}
+    for pipe in ("on", "off"):
+        prob = P.CoupledProblem(dev, spec.rank, list(spec.coupled), mode=spec.mode)
+        out[pipe] = P.solve(prob, P.SolverOptions(max_iter=spec.max_iter, tol=float(np.nextafter(0, 1)),
+                                                  seed=0, precision="fp32", pipeline=pipe))
+    a, b = out["on"], out["off"]
+    assert a.n_restarts == b.n_restarts and a.n_restarts >= 1
+    assert a.n_iter == b.n_iter
+    assert a.objective_history == b.objective_history
+    assert a.rel_err_history == b.rel_err_history
+    for ba, bb in zip(a.factors.blocks, b.factors.blocks):
+        np.testing.assert_array_equal(ba.weights, bb.weights)
+        for fa, fb in zip(ba.factors, bb.factors):
+            np.testing.assert_array_equal(fa, fb)
+
+
 def test_tc_trace_stop_iteration_near_the_fp64_trace(P):
     """At the default tol = 1e-8 the stop rule |rel_k - rel_{k-1}| < tol sees the
     tensor-core trace's fixed-point rounding of A0 (2^-23 of a column maximum,

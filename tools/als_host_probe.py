@@ -11,14 +11,15 @@ from paper_2302_05119_b200.cpd_als import AlsHandle
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 mi = int(sys.argv[2]) if len(sys.argv) > 2 else 36
-I, R = 400, 40
+dims = tuple(int(x) for x in sys.argv[3].split("x")) if len(sys.argv) > 3 else (400, 400, 400)
+R = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 g = torch.Generator(device="cuda").manual_seed(0)
-dev = [torch.rand(I * I * I, device="cuda", generator=g) for _ in range(S)]
+dev = [torch.rand(dims[0] * dims[1] * dims[2], device="cuda", generator=g) for _ in range(S)]
 st = L.c_vp(torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
-for rep in range(2):
+for rep in range(3):
     t0 = time.perf_counter()
-    h = AlsHandle(dev, [(I, I, I)] * S, [R] * S, L.CB_F32, 1e-30, mi, list(range(S)), st, 0, S)
+    h = AlsHandle(dev, [dims] * S, [R] * S, L.CB_F32, 1e-30, mi, list(range(S)), st, 0, S)
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     t2 = time.perf_counter()
