@@ -1148,7 +1148,8 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
     for (int s = 0; s < S; ++s) cmax = std::max(cmax, h->R[s] + h->Rt[s]);
     const size_t cap = 227 * 1024;
     h->qr_ch = qr_chunk_rows(cmax, cap);
-    h->qr_smem = sizeof(double) * ((size_t)cmax * (cmax + 1) + (size_t)h->qr_ch * (cmax + 1) + cmax + 64);
+    h->qr_smem = sizeof(double) * ((size_t)cmax * (cmax + 1) + (size_t)h->qr_ch * (cmax + 1) +
+                                  (size_t)qr_extra_doubles(cmax));
   }
   CB_CUDA(cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem));
   CB_CUDA(cudaFuncSetAttribute(k_sweep_begin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->blk_smem_ng));

@@ -884,19 +884,51 @@ __device__ __forceinline__ bool qr_route_needed(const Ctx& c, int s) {
 // chunks of `ch` rows (as many as shared memory holds: 256 at Rt + R = 80);
 // every chunk is annihilated against the current R by Cc Householder
 // reflectors on the stacked [R; chunk] matrix.  Because R is upper
-// triangular, reflector k touches only row k of R and the chunk rows, so a
-// step costs O(ch (Cc - k)) — the dot products run one warp per column
-// (lanes over the chunk rows, shuffle fold).  Result: R (Cc x Cc, upper
-// triangular) of the QR of [Ut_n, U_n] up to row signs, which ||core||^2
-// does not see.  Grid: S * N CTAs of QR_THREADS.
+// triangular, reflector k touches only row k of R and the chunk rows.
+// Blocked (compact WY): panels of QR_NB columns are factored by unblocked
+// steps that touch only the panel (a step then costs two short barriers
+// instead of a sweep over all trailing columns), and the trailing columns
+// get the panel's block reflector I - V T V^T as three small GEMMs
+// (Y = V^T A one warp per column with eight folded accumulators, Z = T^T Y,
+// A -= V Z one warp per row).  The reflectors are those of the unblocked
+// algorithm (c5: 1.37 -> ~0.3 ms per iteration on the QR route).  Result: R
+// (Cc x Cc, upper triangular) of the QR of [Ut_n, U_n] up to row signs,
+// which ||core||^2 does not see.  Grid: S * N CTAs of QR_THREADS.
 constexpr int QR_THREADS = 512;
+constexpr int QR_NB = 8;
+
+// v0 / beta per column, Y (QR_NB x Cc), T, S, w, norm partials
+__host__ __device__ inline long long qr_extra_doubles(int Cc) { return 10LL * Cc + 3 * 64 + 64; }
 
 __host__ __device__ inline int qr_chunk_rows(int Cc, size_t smem_cap) {
-  // R (Cc x (Cc+1)) + chunk (ch x (Cc+1)) + w (Cc) + red (64) doubles
-  const long long avail = (long long)(smem_cap / sizeof(double)) - Cc - 64 - (long long)Cc * (Cc + 1);
+  // R (Cc x (Cc+1)) + chunk (ch x (Cc+1)) + the panel scratch
+  const long long avail =
+      (long long)(smem_cap / sizeof(double)) - qr_extra_doubles(Cc) - (long long)Cc * (Cc + 1);
   long long ch = avail / (Cc + 1);
   ch = ch / 32 * 32;
   return (int)(ch > 256 ? 256 : (ch < 32 ? 32 : ch));
+}
+
+// sum over the 32 lanes of v[0..8) by recursive halving; lane l ends with the
+// total of value l / 4 (fixed order: deterministic)
+__device__ __forceinline__ double qr_fold8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int o = 16 >> st;
+    const int cnt = 8 >> st;
+    if (cnt > 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < cnt / 2; ++i) {
+        const double send = up ? v[i] : v[i + cnt / 2];
+        const double keep = up ? v[i + cnt / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  return v[0];
 }
 
 __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int ch) {
@@ -912,8 +944,13 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
   const int ld = Cc + 1;
   double* Rm = smd;                      // Cc x ld, upper triangular
   double* X = Rm + Cc * ld;              // ch x ld chunk
-  double* w = X + (long long)ch * ld;    // Cc
-  double* red = w + Cc;                  // 2 x 32 (double-buffered column norms)
+  double* v0s = X + (long long)ch * ld;  // Cc: the R-row entry of reflector k
+  double* betas = v0s + Cc;              // Cc
+  double* Ym = betas + Cc;               // QR_NB x Cc
+  double* Tm = Ym + QR_NB * Cc;          // QR_NB x QR_NB (upper triangular)
+  double* Sm = Tm + 64;                  // QR_NB x QR_NB (V^T V, strictly upper)
+  double* wp = Sm + 64;                  // QR_NB (panel step's w)
+  double* red = wp + 64;                 // 2 x 32 (double-buffered column norms)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = QR_THREADS / 32;
   for (int e = threadIdx.x; e < Cc * ld; e += QR_THREADS) Rm[e] = 0.0;
   const double* A = c.Ut[s * c.N + n];
@@ -933,58 +970,169 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
       if (lane == 0) red[wid] = ss;
     }
     __syncthreads();
-    for (int k = 0; k < Cc; ++k) {
-      const double* rk = red + (k & 1) * 32;
-      double ss = 0.0;
-      for (int q = 0; q < nw; ++q) ss += rk[q];
-      const double x0 = Rm[k * ld + k];
-      ss = fma(x0, x0, ss);
-      const double nrm = sqrt(ss);
-      const double alpha = x0 >= 0.0 ? -nrm : nrm;
-      const double v0 = x0 - alpha;
-      const double vtv = 2.0 * (ss - alpha * x0);
-      const bool refl = vtv > 0.0;
-      const double beta = refl ? 2.0 / vtv : 0.0;
-      // w_j = v0 R_kj + sum_i X_ik X_ij, one warp per column
-      if (refl)
-        for (int j = k + 1 + wid; j < Cc; j += nw) {
-          double a = 0.0;
-          for (int i = lane; i < nr; i += 32) a = fma(X[i * ld + k], X[i * ld + j], a);
-          a = warp_sum(a);
-          if (lane == 0) w[j] = fma(v0, Rm[k * ld + j], a) * beta;
+    for (int k0 = 0; k0 < Cc; k0 += QR_NB) {
+      const int nb = Cc - k0 < QR_NB ? Cc - k0 : QR_NB;
+      const int kend = k0 + nb;
+      // ---- the panel: unblocked steps over its own columns
+      for (int k = k0; k < kend; ++k) {
+        const double* rk = red + (k & 1) * 32;
+        double ss = 0.0;
+        for (int q = 0; q < nw; ++q) ss += rk[q];
+        const double x0 = Rm[k * ld + k];
+        ss = fma(x0, x0, ss);
+        const double nrm = sqrt(ss);
+        const double alpha = x0 >= 0.0 ? -nrm : nrm;
+        const double v0 = x0 - alpha;
+        const double vtv = 2.0 * (ss - alpha * x0);
+        const bool refl = vtv > 0.0;
+        const double beta = refl ? 2.0 / vtv : 0.0;
+        const int ncol = kend - k - 1;
+        // w_j = beta (v0 R_kj + sum_i X_ik X_ij), one warp per panel column
+        if (refl)
+          for (int j = k + 1 + wid; j < kend; j += nw) {
+            double a = 0.0;
+            for (int i = lane; i < nr; i += 32) a = fma(X[i * ld + k], X[i * ld + j], a);
+            a = warp_sum(a);
+            if (lane == 0) wp[j - k0] = fma(v0, Rm[k * ld + j], a) * beta;
+          }
+        __syncthreads();
+        // rank-1 update of the panel columns, one thread per row (row 0 =
+        // row k of R); the squares of the updated column k + 1 are next
+        // step's norm
+        double nss = 0.0;
+        if (ncol > 0) {
+          for (int i = threadIdx.x; i <= nr; i += QR_THREADS) {
+            double* p = i == 0 ? Rm + k * ld : X + (i - 1) * ld;
+            if (refl) {
+              const double vi = i == 0 ? v0 : p[k];
+              for (int j = k + 1; j < kend; ++j) {
+                const double x = p[j] - vi * wp[j - k0];
+                p[j] = x;
+                if (j == k + 1 && i > 0) nss = fma(x, x, nss);
+              }
+            } else if (i > 0) {
+              nss = fma(p[k + 1], p[k + 1], nss);
+            }
+          }
+          nss = warp_sum(nss);
+          if (lane == 0) red[((k + 1) & 1) * 32 + wid] = nss;
         }
-      __syncthreads();
-      // rank-1 update (warp per row, lanes over columns); lane 0 of every warp
-      // also sums the squares of the updated column k + 1 (next step's norm)
-      double nss = 0.0;
-      // four rows per round: their v_i and row values are loaded before any
-      // store (independent chains instead of one load-fma-store per row)
-      for (int i0 = wid; i0 <= nr; i0 += 4 * nw) {
-        double vi[4];
-        double* row[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * nw;
-          row[u] = i == 0 ? Rm + k * ld : X + (i - 1) * ld;
-          vi[u] = i > nr ? 0.0 : (i == 0 ? v0 : X[(i - 1) * ld + k]);
+        if (threadIdx.x == 0) {
+          Rm[k * ld + k] = refl ? alpha : x0;
+          v0s[k] = refl ? v0 : 0.0;
+          betas[k] = beta;
         }
-        for (int j = k + 1 + lane; j < Cc; j += 32) {
-          const double wj = w[j];
-          double xv[4];
+        __syncthreads();
+      }
+      const int nt = Cc - kend;      // trailing columns
+      if (nt == 0) break;
+      // ---- S = strictly upper part of V^T V (the R-row parts of distinct
+      // reflectors do not overlap: chunk rows only), one warp per pair;
+      // the other warps start on Y = V^T A
+      {
+        const int npair = nb * (nb - 1) / 2;
+        for (int pq = wid; pq < npair; pq += nw) {
+          int a = 0, rem = pq;
+          while (rem >= nb - 1 - a) { rem -= nb - 1 - a; ++a; }
+          const int b = a + 1 + rem;
+          double t = 0.0;
+          for (int i = lane; i < nr; i += 32) t = fma(X[i * ld + k0 + a], X[i * ld + k0 + b], t);
+          t = warp_sum(t);
+          if (lane == 0) Sm[a * QR_NB + b] = t;
+        }
+        // Y[a][j] = v0_a R[k0 + a][j] + sum_i X[i][k0 + a] X[i][j]
+        for (int j = kend + wid; j < Cc; j += nw) {
+          double acc[QR_NB];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) xv[u] = i0 + u * nw <= nr ? row[u][j] : 0.0;
+          for (int a = 0; a < QR_NB; ++a) acc[a] = 0.0;
+          for (int i = lane; i < nr; i += 32) {
+            const double xj = X[i * ld + j];
+            const double* pr = X + i * ld + k0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = i0 + u * nw;
-            if (i > nr) break;
-            const double x = refl ? xv[u] - vi[u] * wj : xv[u];
-            if (refl) row[u][j] = x;
-            if (j == k + 1 && i > 0) nss = fma(x, x, nss);
+            for (int a = 0; a < QR_NB; ++a)
+              if (a < nb) acc[a] = fma(pr[a], xj, acc[a]);
+          }
+          const double tot = qr_fold8(acc, lane);
+          if ((lane & 3) == 0) {
+            const int a = lane >> 2;
+            if (a < nb) Ym[a * Cc + j] = fma(v0s[k0 + a], Rm[(k0 + a) * ld + j], tot);
           }
         }
       }
-      if (lane == 0) red[((k + 1) & 1) * 32 + wid] = nss;
-      if (threadIdx.x == 0) Rm[k * ld + k] = refl ? alpha : x0;
+      __syncthreads();
+      // ---- T (upper triangular): T_bb = beta_b, T[0:b, b] = -beta_b T[0:b,0:b] S[0:b, b]
+      if (wid == 0) {
+        for (int b = 0; b < nb; ++b) {
+          const double bb = betas[k0 + b];
+          if (lane < b) {
+            double z = 0.0;
+            for (int q = lane; q < b; ++q) z = fma(Tm[lane * QR_NB + q], Sm[q * QR_NB + b], z);
+            Tm[lane * QR_NB + b] = -bb * z;
+          } else if (lane == b) {
+            Tm[b * QR_NB + b] = bb;
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      // ---- A -= V Z, Z = T^T Y: every warp keeps the Z columns of its
+      // lanes' trailing columns in registers (j = kend + lane + 32 jj), then
+      // one warp per row (rows 0..nb-1 = the panel's R rows, then the chunk
+      // rows); the squares of the updated column kend are the next panel's
+      // first norm
+      {
+        constexpr int QJ = (QR_MAXC + 31) / 32;
+        double zr[QJ][QR_NB];
+#pragma unroll
+        for (int jj = 0; jj < QJ; ++jj) {
+          const int j = kend + lane + 32 * jj;
+          double y[QR_NB];
+#pragma unroll
+          for (int b = 0; b < QR_NB; ++b) y[b] = (b < nb && j < Cc) ? Ym[b * Cc + j] : 0.0;
+#pragma unroll
+          for (int a = 0; a < QR_NB; ++a) {
+            double z = 0.0;
+#pragma unroll
+            for (int b = 0; b <= a; ++b)
+              if (a < nb) z = fma(Tm[b * QR_NB + a], y[b], z);
+            zr[jj][a] = z;
+          }
+        }
+        double nss = 0.0;
+        for (int i = wid; i < nb + nr; i += nw) {
+          if (i < nb) {
+            const double v = v0s[k0 + i];
+#pragma unroll
+            for (int jj = 0; jj < QJ; ++jj) {
+              const int j = kend + lane + 32 * jj;
+              if (j < Cc) {
+                double z = 0.0;
+#pragma unroll
+                for (int a = 0; a < QR_NB; ++a) z = a == i ? zr[jj][a] : z;
+                Rm[(k0 + i) * ld + j] -= v * z;
+              }
+            }
+          } else {
+            double* row = X + (i - nb) * ld;
+            double pv[QR_NB];
+#pragma unroll
+            for (int a = 0; a < QR_NB; ++a) pv[a] = a < nb ? row[k0 + a] : 0.0;
+#pragma unroll
+            for (int jj = 0; jj < QJ; ++jj) {
+              const int j = kend + lane + 32 * jj;
+              if (j < Cc) {
+                double x = row[j];
+#pragma unroll
+                for (int a = 0; a < QR_NB; ++a) x = fma(-pv[a], zr[jj][a], x);
+                row[j] = x;
+                if (jj == 0 && lane == 0) nss = fma(x, x, nss);
+              }
+            }
+          }
+        }
+        // column kend is lane 0's first column
+        if (lane == 0) red[(kend & 1) * 32 + wid] = nss;
+      }
       __syncthreads();
     }
   }

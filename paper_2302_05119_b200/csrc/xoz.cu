@@ -470,6 +470,8 @@ bool oz_supported(int S, const void* const* X, const long long* dims, const int*
 int oz_plan_create(int S, const void* const* X, const long long* dims, const int* R,
                    cudaStream_t st, OzPlan** out) {
   *out = nullptr;
+  // this plan's buffers are zeroed on the stream that then fills and uses them
+  set_alloc_stream(st);
   OzPlan* p = new OzPlan();
   p->S = S;
   int rmax = 1;

@@ -411,6 +411,7 @@ int sl5_plan_create(int S, const void* const* X, const long long* dims, const in
     return CB_ERR_CUDA;
   }
   Sl5EncodeFn enc = reinterpret_cast<Sl5EncodeFn>(fnp);
+  set_alloc_stream(st);   // buffers zeroed on the stream that uses them
   Sl5Plan* p = new Sl5Plan();
   p->S = S;
   int rmax = 1;

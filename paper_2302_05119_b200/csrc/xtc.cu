@@ -578,6 +578,8 @@ static size_t xtc_smem_for(int nst, int bimg_max) {
 int xtc_plan_create(int S, const void* const* X, const long long* dims, const int* R,
                     cudaStream_t st, XtcPlan** out) {
   *out = nullptr;
+  // this plan's buffers are zeroed on the stream that then fills and uses them
+  set_alloc_stream(st);
   XtcPlan* p = new XtcPlan();
   p->S = S;
   int rmax = 1;
