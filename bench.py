@@ -398,11 +398,21 @@ def run_ours(args):
         e2e_opts = P.SolverOptions(max_iter=spec.max_iter, tol=TINY_TOL, seed=0, precision=prec)
         if world > 1:
             torch.distributed.barrier()
-        torch.cuda.synchronize()
-        tic = time.perf_counter()
-        res = (P.solve_distributed(e2e_problem, e2e_opts) if world > 1
-               else P.solve(e2e_problem, e2e_opts))
-        e2e_s = time.perf_counter() - tic
+        # one complete solve(); runs shorter than 0.5 s (c1-c4) are repeated
+        # and the median of 3 is reported (first-call effects are a large
+        # share of a 0.1 s solve)
+        runs = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            tic = time.perf_counter()
+            res = (P.solve_distributed(e2e_problem, e2e_opts) if world > 1
+                   else P.solve(e2e_problem, e2e_opts))
+            runs.append((time.perf_counter() - tic, res))
+            if world > 1 or runs[0][0] >= 0.5:   # (sharded: one solve, same on every rank)
+                break
+        runs.sort(key=lambda r: r[0])
+        e2e_s, res = runs[len(runs) // 2]
+        e2e_runs = len(runs)
         if world > 1:
             t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -414,7 +424,7 @@ def run_ours(args):
         e2e = {"value": res.n_iter / e2e_s, "unit": "it/s",
                "h2d_bytes_per_step": h2d / max(res.n_iter, 1),
                "d2h_bytes_per_step": d2h / max(res.n_iter, 1),
-               "seconds": e2e_s, "n_iter": res.n_iter,
+               "seconds": e2e_s, "n_iter": res.n_iter, "solves_timed": e2e_runs,
                "compress_seconds": res.compress_seconds,
                "solve_seconds": res.solve_seconds,
                "als_sweeps_mean": (float(np.mean(res.compression_iters))

@@ -1086,6 +1086,9 @@ __global__ void __launch_bounds__(QR_THREADS) k_qr_factor(Ctx c, int redo, int c
 #pragma unroll
         for (int jj = 0; jj < QJ; ++jj) {
           const int j = kend + lane + 32 * jj;
+#pragma unroll
+          for (int a = 0; a < QR_NB; ++a) zr[jj][a] = 0.0;
+          if (kend + 32 * jj >= Cc) continue;     // (warp-uniform) no such columns
           double y[QR_NB];
 #pragma unroll
           for (int b = 0; b < QR_NB; ++b) y[b] = (b < nb && j < Cc) ? Ym[b * Cc + j] : 0.0;
