@@ -44,6 +44,7 @@ struct AlsCtx {
   const long long* dims;
   const int* R;
   double* const* U;        // S*N
+  double* const* UT;       // S*N transposed factors [r][I_n], written by the solve (3-way)
   double* const* G;        // S*N
   double* const* MTT;      // S
   int* active;             // S
@@ -93,9 +94,12 @@ __global__ void __launch_bounds__(256) k_als_solve(AlsCtx c, int n, int src) {
   __syncthreads();
   const double ridge = s_ridge;
   double* U = c.U[s * N + n];
+  double* Ut = c.UT ? c.UT[s * N + n] : nullptr;
   if (!(ridge > 0.0)) {
     // the Khatri-Rao columns vanish: any factor fits, the reference takes 0
     for (long long e = threadIdx.x; e < In * R; e += blockDim.x) U[e] = 0.0;
+    if (Ut)
+      for (long long e = threadIdx.x; e < In * R; e += blockDim.x) Ut[e] = 0.0;
   } else {
     for (int i = threadIdx.x; i < R; i += blockDim.x) A[i * R + i] += ridge;
     __syncthreads();
@@ -163,6 +167,8 @@ __global__ void __launch_bounds__(256) k_als_solve(AlsCtx c, int n, int src) {
         y[r] = a / A[r * R + r];
       }
       for (int r = 0; r < R; ++r) U[i * R + r] = y[r];
+      if (Ut)
+        for (int r = 0; r < R; ++r) Ut[r * In + i] = y[r];
     }
   }
   __syncthreads();
@@ -291,7 +297,7 @@ static int als_sweep(cb_als* h) {
       } else {
         if (h->oz) {
           // exact int8 slice GEMM over the packed planes (xoz.cu), written into MTT
-          int rc = oz_mode2(h->oz, h->xa.U, h->xa.active, h->xa.MTT, st);
+          int rc = oz_mode2(h->oz, h->xa.U, h->xa.active, h->xa.MTT, st, h->xa.UT);
           if (rc) return rc;
         } else if (h->sl5) {
           // fp64 GEMM-tiled mode-2 MTTKRP (xslab5.cu), written into MTT
@@ -383,7 +389,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   std::vector<void*>& A = h->allocs;
   int rc;
 #define TRY(x) do { rc = (x); if (rc) { cb_als_destroy(h); return rc; } } while (0)
-  std::vector<double*> U(S * N), G(S * N), MTT(S);
+  std::vector<double*> U(S * N), G(S * N), MTT(S), UT(S * N, nullptr);
   std::vector<double> norms(S);
   for (int s = 0; s < S; ++s) {
     long long mI = 0;
@@ -392,6 +398,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       mI = std::max(mI, In);
       TRY(dalloc((void**)&U[s * N + n], sizeof(double) * In * h->R[s], A));
       TRY(dalloc((void**)&G[s * N + n], sizeof(double) * h->R[s] * h->R[s], A));
+      if (h->fast3) TRY(dalloc((void**)&UT[s * N + n], sizeof(double) * In * h->R[s], A));
     }
     TRY(dalloc((void**)&MTT[s], sizeof(double) * mI * h->R[s], A));
   }
@@ -404,6 +411,8 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   TRY(upload(h->R, &dr, A, st)); c.R = dr;
   double** p;
   TRY(upload(U, &p, A, st)); c.U = p;
+  c.UT = nullptr;
+  if (h->fast3) { TRY(upload(UT, &p, A, st)); c.UT = p; }
   TRY(upload(G, &p, A, st)); c.G = p;
   TRY(upload(MTT, &p, A, st)); c.MTT = p;
   TRY(dalloc((void**)&c.active, sizeof(int) * S, A));
@@ -549,6 +558,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     TRY(upload(h->X, &pX, A, st));
     XArgs& xa = h->xa;
     xa.X = pX; xa.dims = c.dims; xa.R = c.R; xa.U = (const double* const*)c.U; xa.LAM = nullptr;
+    xa.UT = (const double* const*)c.UT;
     xa.T0 = pt0; xa.T1 = pt1; xa.tsel = &h->d_state->tsel; xa.t_other = 0;
     xa.nsplit = d_ns; xa.bpart = bpart; xa.rpart = rpart; xa.slab_part = spart;
     xa.MTT = c.MTT; xa.gate = nullptr; xa.active = c.active;

@@ -90,6 +90,7 @@ struct OzArgs {
   const int* tsel;
   int t_other;
   const double* const* U;
+  const double* const* UT;   // transposed factors [r][I_n] (written by the ALS solve) or null
   double* const* mtt;
   long long i2max;
 };
@@ -424,10 +425,16 @@ __global__ void __launch_bounds__(256) k_oz_contract(OzArgs a) {
     if (a.active && !a.active[s]) continue;
     const OzBlock& b = a.blk[s];
     if (i2 >= b.I2 || r >= b.R) continue;
-    const double* A1 = a.U[3 * s + 1];
     const double* d = b.D + (long long)r * b.f[1].J + i2 * b.I1;
     double v = 0.0;
-    for (long long i1 = lane; i1 < b.I1; i1 += 32) v = fma(A1[i1 * b.R + r], d[i1], v);
+    if (a.UT) {
+      // column r of A1 from the transposed copy: both operands contiguous
+      const double* A1t = a.UT[3 * s + 1] + (long long)r * b.I1;
+      for (long long i1 = lane; i1 < b.I1; i1 += 32) v = fma(A1t[i1], d[i1], v);
+    } else {
+      const double* A1 = a.U[3 * s + 1];
+      for (long long i1 = lane; i1 < b.I1; i1 += 32) v = fma(A1[i1 * b.R + r], d[i1], v);
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) a.mtt[s][i2 * b.R + r] = v;
@@ -633,11 +640,12 @@ int oz_tpass(OzPlan* p, const double* const* U_dev, const int* active, void* con
 }
 
 int oz_mode2(OzPlan* p, const double* const* U_dev, const int* active, double* const* mtt,
-             cudaStream_t st) {
+             cudaStream_t st, const double* const* UT_dev) {
   OzArgs a;
   memset(&a, 0, sizeof(a));
   a.form = 1;
   a.U = U_dev;
+  a.UT = UT_dev;
   a.active = active;
   a.mtt = mtt;
   int rc = oz_go(p, a, st);

@@ -27,9 +27,10 @@ void oz_plan_destroy(OzPlan* p);
 // buffer (*tsel) ^ t_other
 int oz_tpass(OzPlan* p, const double* const* U_dev, const int* active, void* const* T0,
              void* const* T1, const int* tsel, int t_other, cudaStream_t st);
-// mtt[s] (device array of S pointers) <- M2 (I2 x R) of every active block
+// mtt[s] (device array of S pointers) <- M2 (I2 x R) of every active block;
+// UT_dev: optional transposed factors [r][I_n] (contiguous A1 columns)
 int oz_mode2(OzPlan* p, const double* const* U_dev, const int* active, double* const* mtt,
-             cudaStream_t st);
+             cudaStream_t st, const double* const* UT_dev = nullptr);
 // bytes one pass streams (all blocks active)
 double oz_pass_bytes(const OzPlan* p, int form);
 

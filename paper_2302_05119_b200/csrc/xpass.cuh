@@ -39,6 +39,7 @@ struct XArgs {
   const long long* dims;         // S*3
   const int* R;                  // per block rank
   const double* const* U;        // S*3 current factors
+  const double* const* UT;       // optional transposed factors [r][I_n] (ALS: written by its solve), or null
   const double* const* LAM;      // S weights (nullptr entries -> unit weights)
   void* const* T0;               // per block T buffers [nsplit][R][J], double-buffered:
   void* const* T1;               //   buffer index = (*tsel) ^ t_other
@@ -176,9 +177,18 @@ contract1_kernel(XArgs a, const RowUnit* __restrict__ units) {
   const TE* T = reinterpret_cast<const TE*>(tbuf(a, s));
   const int ns = a.nsplit[s];
   double acc = 0.0;
-  for (int sp = 0; sp < ns; ++sp) {
-    const TE* Tr = T + ((long long)sp * R + r) * J + I0 * i1;
-    for (long long i0 = lane; i0 < I0; i0 += 32) acc = fma((double)Tr[i0], A0[i0 * R + r], acc);
+  if (a.UT) {
+    // column r of A0 from the transposed copy: both operands contiguous
+    const double* A0t = a.UT[3 * s] + r * I0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const TE* Tr = T + ((long long)sp * R + r) * J + I0 * i1;
+      for (long long i0 = lane; i0 < I0; i0 += 32) acc = fma((double)Tr[i0], A0t[i0], acc);
+    }
+  } else {
+    for (int sp = 0; sp < ns; ++sp) {
+      const TE* Tr = T + ((long long)sp * R + r) * J + I0 * i1;
+      for (long long i0 = lane; i0 < I0; i0 += 32) acc = fma((double)Tr[i0], A0[i0 * R + r], acc);
+    }
   }
   acc = warp_sum(acc);
   if (lane == 0) a.MTT[s][i1 * R + r] = acc;
