@@ -202,6 +202,22 @@ __global__ void __launch_bounds__(256) k_als_solve(AlsCtx c, int n, int src) {
   }
 }
 
+// initial grams G_n = U_n^T U_n of every (block, mode) in one launch
+// (cpd_als.py:82), the same in-order row sums as the solve's gram refresh
+__global__ void __launch_bounds__(256) k_als_init_grams(AlsCtx c) {
+  const int s = blockIdx.x / c.N, n = blockIdx.x - (blockIdx.x / c.N) * c.N;
+  const int R = c.R[s];
+  const long long In = c.dims[s * c.N + n];
+  const double* U = c.U[s * c.N + n];
+  double* Gn = c.G[s * c.N + n];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int p = e / R, q = e - p * R;
+    double g = 0.0;
+    for (long long i = 0; i < In; ++i) g = fma(U[i * R + p], U[i * R + q], g);
+    Gn[e] = g;
+  }
+}
+
 // per-sweep bookkeeping: residual -> rel err, history, stop rule (cpd_als.py:107-117)
 __global__ void k_als_control(AlsCtx c, int init) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -491,14 +507,10 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     CB_CUDA(cudaMemcpyAsync(c.active, act.data(), sizeof(int) * S, cudaMemcpyHostToDevice, st));
     CB_CUDA(cudaStreamSynchronize(st));
   }
-  // initial grams (cpd_als.py:82)
-  for (int s = 0; s < S; ++s)
-    for (int n = 0; n < N; ++n) {
-      const double* mats[1] = {U[s * N + n]};
-      const int64_t rows[1] = {h->dims[s * N + n]};
-      rc = cb_hadamard_gram(mats, nullptr, rows, 1, -1, h->R[s], h->R[s], G[s * N + n], (void*)st);
-      if (rc) { cb_als_destroy(h); return rc; }
-    }
+  // initial grams (cpd_als.py:82): one launch for every (block, mode)
+  k_als_init_grams<<<S * N, 256, 0, st>>>(h->ctx);
+  count_launch(1);
+  CB_CHECK_LAUNCH();
   if (h->fast3) {
     prepare_slab(h->pc, h->rb, h->tma, h->tab);
     prepare_fiber(h->pc, h->rb, h->tma, h->tab);
