@@ -190,9 +190,23 @@ typedef struct {
                                      fixes each block's work decomposition so
                                      a shard reproduces the unsharded bits
                                      (0 = n_blocks)                          */
+  const void* const* ready_events; /* optional, host array of n_blocks
+                                     cudaEvent_t in block order: tensors[s] may
+                                     be read once ready_events[s] has completed
+                                     (its upload is still in flight on another
+                                     stream).  cb_als_run then starts each
+                                     block's compression as it arrives, beside
+                                     the remaining uploads (blocks are fitted
+                                     independently: same results).  NULL: the
+                                     tensors are ready in stream order        */
 } cb_als_desc;
 
 int cb_als_create(const cb_als_desc* desc, void* stream, cb_als** out);
+/* 1 if cb_als_create would start these blocks one by one at their
+ * ready_events (only then may the events be recorded after the create: the
+ * engine reads no tensor before cb_als_run); needs dims, ranks, dtype,
+ * compute, total_blocks only */
+int cb_als_staged_ok(const cb_als_desc* desc);
 /* runs every block to convergence or max_iter; synchronises the stream */
 int cb_als_run(cb_als* h);
 /* per block: rel_err, n_iter, converged flag, and the rel-err history

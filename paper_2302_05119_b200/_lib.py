@@ -59,7 +59,8 @@ class AlsDesc(ctypes.Structure):
     _fields_ = [("n_blocks", c_int), ("order", c_int), ("dims", c_i64p), ("ranks", c_ip),
                 ("dtype", c_int), ("tensors", ctypes.POINTER(c_vp)),
                 ("init", ctypes.POINTER(c_dp)), ("tol", c_dbl), ("max_iter", c_int),
-                ("compute", c_int), ("total_blocks", c_int)]
+                ("compute", c_int), ("total_blocks", c_int),
+                ("ready_events", ctypes.POINTER(c_vp))]
 
 
 def _sig(name, res, args):
@@ -98,6 +99,7 @@ _sig("cb_diff_sq", c_int, [c_int, c_vp, c_int, c_vp, c_i64, c_vp, c_vp])
 _sig("cb_performance_index", c_int, [c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64p,
                                      c_int, c_vp, c_vp, c_vp])
 _sig("cb_als_create", c_int, [ctypes.POINTER(AlsDesc), c_vp, ctypes.POINTER(c_vp)])
+_sig("cb_als_staged_ok", c_int, [ctypes.POINTER(AlsDesc)])
 _sig("cb_als_run", c_int, [c_vp])
 _sig("cb_als_block_result", c_int, [c_vp, c_int, c_dp, c_ip, c_ip, c_dp, ctypes.POINTER(c_dp)])
 _sig("cb_als_factor_device", c_vp, [c_vp, c_int, c_int])
@@ -126,7 +128,7 @@ EXPORTED = [
     "cb_tensor_stats", "cb_kruskal_residual", "cb_rowdot", "cb_gemm", "cb_factor_gradient",
     "cb_synth_stats", "cb_synth_fill", "cb_model_residual", "cb_diff_sq",
     "cb_performance_index",
-    "cb_als_create", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
+    "cb_als_create", "cb_als_staged_ok", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
     "cb_als_destroy", "cb_solver_create", "cb_solver_run", "cb_solver_step_async",
     "cb_solver_summary_get", "cb_solver_history", "cb_solver_block_factors",
     "cb_solver_set_timing", "cb_solver_timing", "cb_solver_profile", "cb_solver_timeline",

@@ -60,11 +60,28 @@ def _check_feasible(dims, rank):
             raise ValueError(f"rank {rank} infeasible: mode-{n} system has only {other} rows")
 
 
+def als_staged_ok(dims_list, ranks, dtype_code, compute_code=0, total_blocks=0):
+    """Would the batched ALS start these blocks one by one at their upload
+    events (`cb_als_staged_ok`)?  Only then may the uploads be enqueued after
+    the engine has been created."""
+    desc = L.AlsDesc()
+    desc.n_blocks = len(dims_list)
+    desc.order = len(dims_list[0])
+    dims_c = L.i64_array([d for dims in dims_list for d in dims])
+    ranks_c = L.int_array(ranks)
+    desc.dims = ctypes.cast(dims_c, L.c_i64p)
+    desc.ranks = ctypes.cast(ranks_c, L.c_ip)
+    desc.dtype = dtype_code
+    desc.compute = int(compute_code)
+    desc.total_blocks = int(total_blocks or 0)
+    return bool(L.lib.cb_als_staged_ok(ctypes.byref(desc)))
+
+
 class AlsHandle:
     """Owns a device ALS engine; factors stay resident for the solver."""
 
     def __init__(self, dev_tensors, dims_list, ranks, dtype_code, tol, max_iter, seeds, stream,
-                 compute_code=0, total_blocks=0):
+                 compute_code=0, total_blocks=0, ready_events=None):
         self.S = len(dev_tensors)
         self.N = len(dims_list[0])
         self.dims = dims_list
@@ -93,6 +110,13 @@ class AlsHandle:
         desc.max_iter = int(max_iter)
         desc.compute = int(compute_code)
         desc.total_blocks = int(total_blocks or 0)
+        # per-block upload events (torch.cuda.Event, recorded on the copy
+        # stream after each block's host->device copy): run() then starts
+        # every block as it arrives
+        self._events = list(ready_events) if ready_events is not None else None
+        if self._events is not None:
+            self._events_c = (L.c_vp * self.S)(*[L.c_vp(int(e.cuda_event)) for e in self._events])
+            desc.ready_events = ctypes.cast(self._events_c, ctypes.POINTER(L.c_vp))
         h = L.c_vp()
         L.check(L.lib.cb_als_create(ctypes.byref(desc), stream, ctypes.byref(h)))
         self.h = h

@@ -218,6 +218,36 @@ __global__ void __launch_bounds__(256) k_als_init_grams(AlsCtx c) {
   }
 }
 
+// deferred start (cb_als_desc.ready_events): blocks [lo, hi) have arrived:
+// their norms and initial rel err from the device stats (1, or 0 for a zero
+// tensor: cpd_als.py:84-86), the activity flags, and the mask of exactly
+// these blocks for their first T pass
+__global__ void k_als_activate(AlsCtx c, int lo, int hi, const double* stats, double* nsq,
+                               int* mask) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= c.S) return;
+  const bool in = s >= lo && s < hi;
+  mask[s] = in ? 1 : 0;
+  if (!in) return;
+  if (stats[3 * s + 2] > 0.0) {
+    // non-finite values: reported by cb_als_run
+    if (atomicCAS(&c.st->error, 0, CB_ERR_ARG) == 0) { c.st->err_block = s; c.st->err_sweep = 0; }
+    c.active[s] = 0;
+    mask[s] = 0;
+    return;
+  }
+  const double nr = sqrt(stats[3 * s]);
+  c.norm[s] = nr;
+  nsq[s] = stats[3 * s];
+  c.rel[s] = nr == 0.0 ? 0.0 : 1.0;
+  c.active[s] = c.max_iter > 0 ? 1 : 0;
+  if (c.active[s]) c.st->any_active = 1;
+}
+
+// the sweep state into the pinned host copy by a kernel store (not a D2H
+// copy: while uploads are in flight a copy-engine transfer queues behind them)
+__global__ void k_als_state_to_host(const AlsState* d, AlsState* h) { *h = *d; }
+
 // per-sweep bookkeeping: residual -> rel err, history, stop rule (cpd_als.py:107-117)
 __global__ void k_als_control(AlsCtx c, int init) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -263,6 +293,14 @@ struct cb_als {
   cudaStream_t st = nullptr;
   cb::Sl5Plan* sl5 = nullptr;   // fp64 mode-2 MTTKRP for ranks > 16 (xslab5.cu)
   cb::OzPlan* oz = nullptr;     // both passes on the tensor cores over packed byte planes (xoz.cu)
+  // deferred start: per-block upload events, blocks [0, started) are running
+  bool deferred = false;
+  std::vector<cudaEvent_t> ready;
+  int started = 0;
+  double* d_stats = nullptr;
+  double* d_stats_part = nullptr;
+  double* d_nsq = nullptr;
+  int* d_mask = nullptr;
   int S = 0, N = 0, dtype = CB_F64, max_iter = 0, rmax = 1, rb = 8, fast3 = 0, pc = 0;
   double tol = 1e-4;
   std::vector<long long> dims;
@@ -278,6 +316,7 @@ struct cb_als {
   RowUnit *d_c0 = nullptr, *d_c1 = nullptr;
   AlsState* d_state = nullptr;
   AlsState* h_state = nullptr;
+  AlsState* h_state_dev = nullptr;   // device address of the pinned host copy
   double* kr_scratch = nullptr;
   double* res_part = nullptr;
   int res_nparts = 0;
@@ -374,6 +413,27 @@ int cb_als_destroy(cb_als* h) {
   return CB_OK;
 }
 
+// would cb_als_create take the staged path (start each block at its
+// ready_event) for these blocks?  (3-way fp32 storage, fp64-grade arithmetic,
+// ranks and mode sizes the plane GEMMs support)
+int cb_als_staged_ok(const cb_als_desc* d) {
+  if (!d || d->n_blocks < 1 || d->order != 3 || d->dtype != CB_F32 || d->compute == 1) return 0;
+  const int S = d->n_blocks;
+  std::vector<long long> dims(d->dims, d->dims + 3 * S);
+  std::vector<int> R(d->ranks, d->ranks + S);
+  int rmax = 1;
+  for (int s = 0; s < S; ++s) {
+    if (R[s] < 1 || R[s] > CB_MAX_RANK) return 0;
+    rmax = std::max(rmax, R[s]);
+  }
+  std::vector<const void*> X(S, reinterpret_cast<const void*>(16));   // alignment only
+  if (!oz_supported(S, X.data(), dims.data(), R.data())) return 0;
+  XTables tab;
+  build_xtables(S, dims.data(), R.data(), rank_bucket(rmax), PC_F32_F64, tab,
+                d->total_blocks > S ? d->total_blocks : S);
+  return tab.slab_direct ? 0 : 1;
+}
+
 int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   CB_ARG(d && out, "null descriptor");
   *out = nullptr;
@@ -442,6 +502,7 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   c.st = h->d_state;
   CB_CUDA(cudaMallocHost((void**)&h->h_state, sizeof(AlsState)));
   memset(h->h_state, 0, sizeof(AlsState));
+  CB_CUDA(cudaHostGetDevicePointer((void**)&h->h_state_dev, h->h_state, 0));
   // unit tables and the tensor-core plan first: its allocations (the byte
   // planes: 34 GB on c5, ~0.1 s of host time) then run while the caller's
   // host->device copies of the blocks are still in flight on `st`, ahead of
@@ -455,12 +516,38 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     // (xoz.cu).  T is then written unsplit whatever the fiber table chose.
     if (h->pc == PC_F32_F64 && !h->tab.slab_direct &&
         oz_supported(S, h->X.data(), h->dims.data(), h->R.data())) {
-      if (oz_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->oz) != CB_OK)
+      if (oz_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->oz,
+                         d->ready_events != nullptr) != CB_OK)
         h->oz = nullptr;
       if (h->oz) {
         h->tab.nsplit.assign(S, 1);
         h->tab.fib_unsplit = 1;
       }
+    }
+  }
+  // blocks still uploading (ready_events): the plane-GEMM path starts each
+  // block as it arrives (cb_als_run); any other path waits for all of them here
+  if (d->ready_events) {
+    h->ready.resize(S);
+    for (int s = 0; s < S; ++s) h->ready[s] = (cudaEvent_t)d->ready_events[s];
+    h->deferred = h->oz != nullptr;
+    if (h->deferred) {
+      // every kernel of the staged run is loaded now, before the caller
+      // starts the uploads: with lazy module loading a kernel's first launch
+      // waits for all copies in flight
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, k_als_activate);
+      cudaFuncGetAttributes(&fa, k_als_state_to_host);
+      cudaFuncGetAttributes(&fa, k_als_solve);
+      cudaFuncGetAttributes(&fa, k_als_control);
+      tensor_stats_preload();
+      contract_preload();
+      oz_preload(h->oz);
+    }
+    if (!h->deferred) {
+      // (callers check cb_als_staged_ok first: the events must already have
+      // been recorded after the uploads for this path)
+      for (int s = 0; s < S; ++s) CB_CUDA(cudaStreamWaitEvent(st, h->ready[s], 0));
     }
   }
   // the starting factors (pageable host memory: these copies wait for the
@@ -471,7 +558,14 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
                               sizeof(double) * h->dims[s * N + n] * h->R[s],
                               cudaMemcpyHostToDevice, st));
   // norms and the initial rel err (1, or 0 for a zero tensor: cpd_als.py:84-86)
-  {
+  if (h->deferred) {
+    // per arriving range in cb_als_run (k_als_activate), from device stats
+    TRY(dalloc((void**)&h->d_stats, sizeof(double) * 3 * S, A));
+    TRY(dalloc((void**)&h->d_stats_part, sizeof(double) * 3 * 148 * 8, A));
+    TRY(dalloc((void**)&h->d_nsq, sizeof(double) * S, A));
+    TRY(dalloc((void**)&h->d_mask, sizeof(int) * S, A));
+    c.nsq = h->d_nsq;
+  } else {
     double* stats;
     TRY(dalloc((void**)&stats, sizeof(double) * 3 * S, A));
     double* part;
@@ -608,8 +702,10 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
   }
   h->solve_smem = sizeof(double) * ((size_t)h->rmax * h->rmax + h->rmax + 48);
   CB_CUDA(cudaFuncSetAttribute(k_als_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->solve_smem));
-  // initial T buffer (X x_3 U_2 of the starting factors)
-  if (h->fast3 && c.res_expand) {
+  // initial T buffer (X x_3 U_2 of the starting factors); deferred: per
+  // arriving range in cb_als_run
+  if (h->deferred) {
+  } else if (h->fast3 && c.res_expand) {
     TRY(h->oz ? oz_tpass(h->oz, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st)
               : sl5_tpass(h->sl5, h->xa.U, h->xa.active, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st));
     CB_CHECK_LAUNCH();
@@ -619,16 +715,86 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
     launch_fiber(h->pc, h->rb, h->tma, 1, 0, 0, a, h->d_fib, (int)h->tab.fib.size(), h->tab, st);
     CB_CHECK_LAUNCH();
   }
-  k_als_control<<<1, 32, 0, st>>>(h->ctx, 1);
-  count_launch(1);
-  CB_CHECK_LAUNCH();
+  if (!h->deferred) {
+    k_als_control<<<1, 32, 0, st>>>(h->ctx, 1);
+    count_launch(1);
+    CB_CHECK_LAUNCH();
+  }
 #undef TRY
   *out = h;
   return CB_OK;
 }
 
+// deferred start: activate the blocks [started, upto) that have arrived:
+// stats, exponents + byte planes, norms / flags, their first T pass
+static int als_activate(cb_als* h, int upto) {
+  cudaStream_t st = h->st;
+  const int lo = h->started;
+  for (int s = lo; s < upto; ++s) {
+    CB_CUDA(cudaStreamWaitEvent(st, h->ready[s], 0));
+    long long n = 1;
+    for (int m = 0; m < h->N; ++m) n *= h->dims[s * h->N + m];
+    const int np = (int)std::min<long long>(148 * 8, std::max<long long>(1, (n + 255) / 256));
+    int rc = tensor_stats(h->dtype, h->X[s], n, h->d_stats + 3 * s, h->d_stats_part, np, st);
+    if (rc) return rc;
+  }
+  int rc = oz_pack_range(h->oz, lo, upto, st);
+  if (rc) return rc;
+  k_als_activate<<<(h->S + 127) / 128, 128, 0, st>>>(h->ctx, lo, upto, h->d_stats, h->d_nsq,
+                                                    h->d_mask);
+  count_launch(1);
+  CB_CHECK_LAUNCH();
+  rc = oz_tpass(h->oz, h->xa.U, h->d_mask, h->xa.T0, h->xa.T1, h->xa.tsel, 1, st);
+  if (rc) return rc;
+  h->started = upto;
+  return CB_OK;
+}
+
+static int als_finish(cb_als* h) {
+  if (h->h_state->error == CB_ERR_ARG) {
+    set_error("tensor contains non-finite values");
+    return CB_ERR_ARG;
+  }
+  if (h->h_state->error) {
+    set_error("block %d: ALS diverged to non-finite values at sweep %d", h->h_state->err_block,
+              h->h_state->err_sweep);
+    return CB_ERR_DIVERGED;
+  }
+  return CB_OK;
+}
+
 int cb_als_run(cb_als* h) {
   CB_ARG(h, "null handle");
+  if (h->deferred) {
+    // start every block as its upload completes; between arrivals the
+    // blocks already here sweep in short chunks
+    const int S = h->S;
+    h->h_state->any_active = 0;
+    for (;;) {
+      int upto = h->started;
+      while (upto < S && cudaEventQuery(h->ready[upto]) == cudaSuccess) ++upto;
+      if (upto == h->started && upto < S && !h->h_state->any_active) {
+        // nothing to do until the next block is here
+        CB_CUDA(cudaEventSynchronize(h->ready[upto]));
+        continue;
+      }
+      if (upto > h->started) {
+        int rc = als_activate(h, upto);
+        if (rc) return rc;
+      }
+      const int chunk = h->started < S ? 2 : 8;
+      for (int i = 0; i < chunk; ++i) {
+        int rc = als_sweep(h);
+        if (rc) return rc;
+      }
+      k_als_state_to_host<<<1, 1, 0, h->st>>>(h->d_state, h->h_state_dev);
+      CB_CHECK_LAUNCH();
+      CB_CUDA(cudaStreamSynchronize(h->st));
+      if (h->h_state->error) break;
+      if (h->started == S && !h->h_state->any_active) break;
+    }
+    return als_finish(h);
+  }
   int sweeps = 0;
   CB_CUDA(cudaMemcpyAsync(h->h_state, h->d_state, sizeof(AlsState), cudaMemcpyDeviceToHost, h->st));
   CB_CUDA(cudaStreamSynchronize(h->st));
@@ -642,12 +808,7 @@ int cb_als_run(cb_als* h) {
     CB_CUDA(cudaMemcpyAsync(h->h_state, h->d_state, sizeof(AlsState), cudaMemcpyDeviceToHost, h->st));
     CB_CUDA(cudaStreamSynchronize(h->st));
   }
-  if (h->h_state->error) {
-    set_error("block %d: ALS diverged to non-finite values at sweep %d", h->h_state->err_block,
-              h->h_state->err_sweep);
-    return CB_ERR_DIVERGED;
-  }
-  return CB_OK;
+  return als_finish(h);
 }
 
 int cb_als_block_result(cb_als* h, int block, double* rel_err, int* n_iter, int* converged,

@@ -57,6 +57,7 @@ void launch_slab(int pc, int rb, bool tma, const XArgs& a, const SlabUnit* u, in
                  const XTables& t, cudaStream_t st);
 void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
                      cudaStream_t st);
+void contract_preload();   // load the contraction kernels now (lazy module loading)
 int dalloc(void** p, size_t bytes, std::vector<void*>& allocs);
 void dfree_all(std::vector<void*>& allocs);
 void set_alloc_stream(cudaStream_t st);

@@ -272,6 +272,16 @@ int tensor_stats(int dtype, const void* X, int64_t n, double* out3, double* part
   return CB_OK;
 }
 
+// Loads the stats kernels now (lazy module loading otherwise loads a kernel
+// at its first launch, which waits for every copy in flight: the staged ALS
+// start launches them beside the uploads)
+void tensor_stats_preload() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tensor_stats_kernel<float>);
+  cudaFuncGetAttributes(&fa, tensor_stats_kernel<double>);
+  cudaFuncGetAttributes(&fa, stats_final_kernel);
+}
+
 // ----------------------------------------------------------------------------
 // explicit Kruskal residual || X - [[w; U]] ||^2, generic order (two-stage)
 // ----------------------------------------------------------------------------

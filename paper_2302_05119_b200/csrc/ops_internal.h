@@ -46,6 +46,7 @@ int mttkrp_one(int dtype, const void* X, int order, const int64_t* dims,
                double* scratch, cudaStream_t st);
 int tensor_stats(int dtype, const void* X, int64_t n, double* out3, double* part, int nparts,
                  cudaStream_t st);
+void tensor_stats_preload();
 int kruskal_residual(int dtype, const ResidArgs& a, const void* X, double* out, double* part,
                      int nparts, cudaStream_t st);
 size_t lam_max_smem_bytes(int R);

@@ -104,6 +104,9 @@ struct OzPlan {
   std::vector<void*> allocs;
   OzBlock* blk = nullptr;
   unsigned int* maxbits = nullptr;
+  int nsm = 148, ntmax[2] = {1, 1};
+  std::vector<const float*> X;       // host copies for the pack launches
+  std::vector<long long> elems;
 };
 
 // --------------------------------------------------------------------------
@@ -475,7 +478,7 @@ bool oz_supported(int S, const void* const* X, const long long* dims, const int*
 }
 
 int oz_plan_create(int S, const void* const* X, const long long* dims, const int* R,
-                   cudaStream_t st, OzPlan** out) {
+                   cudaStream_t st, OzPlan** out, bool defer_pack) {
   *out = nullptr;
   // this plan's buffers are zeroed on the stream that then fills and uses them
   set_alloc_stream(st);
@@ -561,16 +564,19 @@ int oz_plan_create(int S, const void* const* X, const long long* dims, const int
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   p->grid = nsm;
+  p->nsm = nsm;
+  p->ntmax[0] = (int)ntmax[0];
+  p->ntmax[1] = (int)ntmax[1];
+  p->X.assign(S, nullptr);
+  p->elems.assign(S, 0);
   for (int s = 0; s < S; ++s) {
-    const long long n = hb[s].f[0].J * hb[s].f[0].K;
-    const int grid = (int)std::max(1LL, std::min((n + 255) / 256, (long long)nsm * 8));
-    k_oz_maxabs<<<grid, 256, 0, st>>>(hb[s].X, n, p->maxbits + s);
+    p->X[s] = hb[s].X;
+    p->elems[s] = hb[s].f[0].J * hb[s].f[0].K;
   }
-  k_oz_set_ex<<<(S + 127) / 128, 128, 0, st>>>(p->blk, p->maxbits, S);
-  k_oz_pack<0><<<dim3((unsigned)ntmax[0], 1, S), OZ_M, 0, st>>>(p->blk);
-  k_oz_pack<1><<<dim3((unsigned)ntmax[1], 1, S), OZ_M, 0, st>>>(p->blk);
-  OCUDA(cudaGetLastError());
-  count_launch(S + 3);
+  if (!defer_pack) {
+    rc = oz_pack_range(p, 0, S, st);
+    if (rc) { oz_plan_destroy(p); return rc; }
+  }
   for (int f = 0; f < 2; ++f) {
     p->nst[f] = oz_stages(p->bimg_max[f]);
     if (p->nst[f] < 3) {
@@ -590,6 +596,39 @@ int oz_plan_create(int S, const void* const* X, const long long* dims, const int
 #undef OCUDA
   *out = p;
   return CB_OK;
+}
+
+// block exponents and byte planes of blocks [lo, hi) (their tensors must be
+// readable in stream order on `st`)
+int oz_pack_range(OzPlan* p, int lo, int hi, cudaStream_t st) {
+  if (hi <= lo) return CB_OK;
+  for (int s = lo; s < hi; ++s) {
+    const long long n = p->elems[s];
+    const int grid = (int)std::max(1LL, std::min((n + 255) / 256, (long long)p->nsm * 8));
+    k_oz_maxabs<<<grid, 256, 0, st>>>(p->X[s], n, p->maxbits + s);
+  }
+  const int nb = hi - lo;
+  k_oz_set_ex<<<(nb + 127) / 128, 128, 0, st>>>(p->blk + lo, p->maxbits + lo, nb);
+  k_oz_pack<0><<<dim3((unsigned)p->ntmax[0], 1, nb), OZ_M, 0, st>>>(p->blk + lo);
+  k_oz_pack<1><<<dim3((unsigned)p->ntmax[1], 1, nb), OZ_M, 0, st>>>(p->blk + lo);
+  CB_CHECK_LAUNCH();
+  count_launch(nb + 3);
+  return CB_OK;
+}
+
+// loads every kernel of the passes now (see tensor_stats_preload)
+void oz_preload(const OzPlan* p) {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_oz_maxabs);
+  cudaFuncGetAttributes(&fa, k_oz_set_ex);
+  cudaFuncGetAttributes(&fa, k_oz_pack<0>);
+  cudaFuncGetAttributes(&fa, k_oz_pack<1>);
+  cudaFuncGetAttributes(&fa, k_oz_contract);
+  switch (p->N) {
+    case 16: cudaFuncGetAttributes(&fa, k_oz_prep<16>); cudaFuncGetAttributes(&fa, k_oz_gemm<16>); break;
+    case 32: cudaFuncGetAttributes(&fa, k_oz_prep<32>); cudaFuncGetAttributes(&fa, k_oz_gemm<32>); break;
+    default: cudaFuncGetAttributes(&fa, k_oz_prep<48>); cudaFuncGetAttributes(&fa, k_oz_gemm<48>); break;
+  }
 }
 
 void oz_plan_destroy(OzPlan* p) {

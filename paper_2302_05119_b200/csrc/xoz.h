@@ -19,9 +19,15 @@ struct OzPlan;
 // fp32 blocks of order 3, 16 < max rank <= 48, operand images within shared
 // memory (I0, I2 <= ~670 at rank 40), rows < 2^31
 bool oz_supported(int S, const void* const* X, const long long* dims, const int* R);
-// allocates and packs the byte planes of both forms (enqueued on `st`)
+// allocates and packs the byte planes of both forms (enqueued on `st`);
+// defer_pack: allocate only, the caller packs block ranges as their tensors
+// arrive (oz_pack_range)
 int oz_plan_create(int S, const void* const* X, const long long* dims, const int* R,
-                   cudaStream_t st, OzPlan** out);
+                   cudaStream_t st, OzPlan** out, bool defer_pack = false);
+int oz_pack_range(OzPlan* p, int lo, int hi, cudaStream_t st);
+// load the passes' kernels now (a first launch beside copies in flight would
+// wait for them: lazy module loading)
+void oz_preload(const OzPlan* p);
 void oz_plan_destroy(OzPlan* p);
 // T = X x3 A2 of every active block, written unsplit ([R][J] fp64) into T
 // buffer (*tsel) ^ t_other

@@ -291,6 +291,14 @@ void launch_contract(int pc, int mode, const XArgs& a, const RowUnit* u, int n,
   count_launch(1);
 }
 
+void contract_preload() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, contract0_kernel<float>);
+  cudaFuncGetAttributes(&fa, contract0_kernel<double>);
+  cudaFuncGetAttributes(&fa, contract1_kernel<float>);
+  cudaFuncGetAttributes(&fa, contract1_kernel<double>);
+}
+
 bool tma_rows_ok(int S, const long long* dims, const void* const* X, int elem_bytes) {
   for (int s = 0; s < S; ++s) {
     const long long J = dims[3 * s] * dims[3 * s + 1];

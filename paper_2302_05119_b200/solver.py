@@ -34,7 +34,7 @@ import numpy as np
 
 from . import _device as D
 from . import _lib as L
-from .cpd_als import AlsHandle, AlsOptions, _check_feasible, als_compress_blocks
+from .cpd_als import AlsHandle, AlsOptions, _check_feasible, als_compress_blocks, als_staged_ok
 from .kruskal import CoupledFactorSet, KruskalTensor
 from .tensor_ops import hadamard_gram, spectral_norm
 
@@ -504,22 +504,12 @@ class PreparedSolve:
                 except ValueError as exc:
                     first_bad, bad_msg, limit = (g, 0), exc, g
                     break
-            # uploads and element scans of the blocks before the first order
-            # error, all enqueued, one synchronisation (stats slot per block)
             scan = [g for g in self.local if g < limit]
             stats = torch.empty((max(len(scan), 1), 3), dtype=torch.float64, device=D.device())
-            for k, g in enumerate(scan):
-                t = problem.tensors[g]
-                src, dims = D.tensor_to_dev(t, D.source_dtype(t))
-                code = L.CB_F32 if D.source_dtype(t) == "fp32" else L.CB_F64
-                L.check(L.lib.cb_tensor_stats(code, D.ptr(src), src.numel(), D.ptr(stats[k]),
-                                              D.stream()))
-                flat = src if D.source_dtype(t) == prec else D.cast_flat(src, prec)
-                del src
-                self.dev.append(flat)
-                self.dims.append(dims)
+            shapes = [tuple(int(d) for d in problem.tensors[g].shape) for g in scan]
             # host-side checks that follow the value checks in the reference's
-            # order (ranks / counts, then the compression's feasibility)
+            # order (ranks / counts, then the compression's feasibility); they
+            # only need the shapes
             ranks = None
             late_exc = None
             if bad_msg is None:
@@ -530,7 +520,7 @@ class PreparedSolve:
                                 else AlsOptions())
                         ranks = [base.rank if base.rank is not None else problem.ranks[g]
                                  for g in self.local]
-                        for s, (dims, r) in enumerate(zip(self.dims, ranks)):
+                        for s, (dims, r) in enumerate(zip(shapes, ranks)):
                             try:
                                 _check_feasible(dims, r)
                             except ValueError as exc:
@@ -538,21 +528,92 @@ class PreparedSolve:
                                     f"compression of block {self.local[s]} failed: {exc}") from exc
                 except ValueError as exc:
                     late_exc = exc
-            # lra stage 1 setup (solver.py:556-573) before the value checks'
-            # synchronisation: with pinned host tensors the uploads above are
-            # DMA in flight, and the ALS engine's allocations (byte planes,
-            # T buffers: ~0.1 s of host time on c5) run beside them
             self.als = None
             st = L.c_vp(self.stream.cuda_stream)
-            tic = time.perf_counter()
             als_exc = None
-            if ranks is not None and late_exc is None:
+            als_ran = False
+            t_als = 0.0
+            want = torch.float32 if prec == "fp32" else torch.float64
+
+            def _stageable(t, dims):
+                return (isinstance(t, torch.Tensor) and not t.is_cuda and t.is_pinned()
+                        and t.dtype == want and tuple(t.stride()) == D.fortran_strides(dims))
+
+            # lra solves on pinned host tensors already in the solve's dtype and
+            # layout (single process): the uploads run on a copy stream with an
+            # event per block and the compression starts every block as it
+            # arrives, beside the remaining uploads (cb_als_desc.ready_events;
+            # blocks are fitted independently: same results).  Device
+            # allocations synchronise with copies in flight, so all of them (the
+            # blocks' buffers, then the compression engine's) come before the
+            # first copy.
+            staged = (ranks is not None and late_exc is None and agree is None and len(scan) > 1
+                      and all(_stageable(problem.tensors[g], shapes[k])
+                              for k, g in enumerate(scan))
+                      and als_staged_ok(shapes, ranks, self.code, self.als_compute_code, S_all))
+            copy_stream = self.stream
+            if staged:
+                code = L.CB_F32 if prec == "fp32" else L.CB_F64
+                self.dims = list(shapes)
+                self.dev = [torch.empty(int(np.prod(d)), dtype=want, device=D.device())
+                            for d in shapes]
+                arrived = [torch.cuda.Event() for _ in scan]
+                for ev in arrived:
+                    ev.record(self.stream)      # creates the event; re-recorded after its copy
+                tic = time.perf_counter()
                 try:
                     self.als = AlsHandle(self.dev, self.dims, ranks, self.code, base.tol,
                                          base.max_iter, [base.seed + g for g in self.local], st,
-                                         self.als_compute_code, S_all)
+                                         self.als_compute_code, S_all, ready_events=arrived)
                 except ValueError as exc:
                     als_exc = exc
+                t_als = time.perf_counter() - tic
+                copy_stream = torch.cuda.Stream()
+                copy_stream.wait_stream(self.stream)
+                with torch.cuda.stream(copy_stream):
+                    for k, g in enumerate(scan):
+                        t = problem.tensors[g]
+                        dst = self.dev[k]
+                        dst.record_stream(copy_stream)
+                        dst.copy_(t.as_strided((t.numel(),), (1,)), non_blocking=True)
+                        arrived[k].record(copy_stream)
+                        L.check(L.lib.cb_tensor_stats(code, D.ptr(dst), dst.numel(),
+                                                      D.ptr(stats[k]), D.stream()))
+                if self.als is not None:
+                    tic = time.perf_counter()
+                    try:
+                        # sweeps of the blocks that are here while the rest uploads
+                        self.als.run()
+                        als_ran = True
+                    except ValueError as exc:
+                        als_exc = exc
+                    t_als += time.perf_counter() - tic
+            else:
+                # uploads and element scans of the blocks before the first order
+                # error, all enqueued, one synchronisation (stats slot per block)
+                for k, g in enumerate(scan):
+                    t = problem.tensors[g]
+                    src, dims = D.tensor_to_dev(t, D.source_dtype(t))
+                    code = L.CB_F32 if D.source_dtype(t) == "fp32" else L.CB_F64
+                    L.check(L.lib.cb_tensor_stats(code, D.ptr(src), src.numel(), D.ptr(stats[k]),
+                                                  D.stream()))
+                    flat = src if D.source_dtype(t) == prec else D.cast_flat(src, prec)
+                    del src
+                    self.dev.append(flat)
+                    self.dims.append(dims)
+                # lra stage 1 setup (solver.py:556-573) before the value checks'
+                # synchronisation: the ALS engine's allocations run beside
+                # whatever part of the uploads is asynchronous
+                tic = time.perf_counter()
+                if ranks is not None and late_exc is None:
+                    try:
+                        self.als = AlsHandle(self.dev, self.dims, ranks, self.code, base.tol,
+                                             base.max_iter, [base.seed + g for g in self.local],
+                                             st, self.als_compute_code, S_all)
+                    except ValueError as exc:
+                        als_exc = exc
+            copy_stream.synchronize()
+            self.stream.wait_stream(copy_stream)
             host = stats.cpu().numpy() if scan else np.zeros((0, 3))
             for k, g in enumerate(scan):
                 if host[k, 2] != 0.0 or host[k, 1] < 0.0:
@@ -576,7 +637,8 @@ class PreparedSolve:
                 try:
                     if als_exc is not None:
                         raise als_exc
-                    self.als.run()
+                    if not als_ran:
+                        self.als.run()
                 except ValueError as exc:
                     msg = str(exc)
                     blk = 0
@@ -588,8 +650,9 @@ class PreparedSolve:
                         self.als = None
                     raise ValueError(f"compression of block {blk} failed: {msg}") from exc
             self.stream.synchronize()
-            # (includes the tail of the upload that the setup overlapped)
-            self.compress_seconds = time.perf_counter() - tic
+            # staged: the engine setup plus the run that overlapped the uploads;
+            # else from the setup (beside the upload's tail) to the last sweep
+            self.compress_seconds = t_als if als_ran else time.perf_counter() - tic
             tilde_ranks = ranks
         # the seeded start of ALL blocks (one PCG64 stream), then this shard's
         start = init_factors(problem, opts.seed)

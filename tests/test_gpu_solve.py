@@ -270,6 +270,45 @@ def test_device_resident_fp32_inputs(P):
     assert res_dev.objective_history == res_host.objective_history
 
 
+def test_staged_upload_compression_equals_resident_inputs(P):
+    """lra on pinned host tensors: the blocks upload on a copy stream and the
+    compression starts each block as it arrives (cb_als_desc.ready_events:
+    deferred stats / plane packing / first T pass per arriving range,
+    csrc/als.cu).  Blocks are fitted independently, so the compression and the
+    solve equal, bitwise, those of the same blocks already resident on the
+    device (all blocks started together)."""
+    import torch
+    from paper_2302_05119_b200._device import fortran_view
+    rng = np.random.default_rng(12)
+    shapes = [(96, 80, 72)] * 5
+    host, dev = [], []
+    for d in shapes:
+        f = [rng.random((n, 20)) for n in d]
+        x = np.einsum("ir,jr,kr->ijk", *f) + 0.3 * rng.standard_normal(d)
+        flat = torch.from_numpy(np.ravel(np.maximum(x, 0).astype(np.float32), order="F").copy())
+        pinned = torch.empty_strided(d, (1, d[0], d[0] * d[1]), dtype=torch.float32, pin_memory=True)
+        pinned.copy_(fortran_view(flat, d))
+        host.append(pinned)
+        dev.append(fortran_view(flat.cuda(), d))
+    out = {}
+    for name, ts in (("host", host), ("dev", dev)):
+        out[name] = P.solve(P.CoupledProblem(ts, 20, [5, 5, 0], mode="lra"),
+                            P.SolverOptions(max_iter=30, seed=2, precision="fp32"))
+    a, b = out["host"], out["dev"]
+    assert a.compression_iters == b.compression_iters
+    for ca, cb in zip(a.compression, b.compression):
+        for fa, fb in zip(ca.factors, cb.factors):
+            np.testing.assert_array_equal(fa, fb)
+    assert a.objective_history == b.objective_history
+    assert a.rel_err_history == b.rel_err_history
+    # a non-finite block is still reported as the reference reports it
+    bad = host[3].clone().pin_memory()
+    bad[1, 2, 3] = float("nan")
+    with pytest.raises(ValueError, match="block 3 contains non-finite values"):
+        P.solve(P.CoupledProblem(host[:3] + [bad] + host[4:], 20, [5, 5, 0], mode="lra"),
+                P.SolverOptions(max_iter=3, precision="fp32"))
+
+
 def test_device_value_checks_raise_reference_messages(P):
     """The single-process solve scans the uploaded blocks on the device; the
     errors are the reference's (solver.py:114-117), with the block index."""

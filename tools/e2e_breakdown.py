@@ -53,9 +53,11 @@ def timed_als_init(self, *a, **k):
 
 
 def timed_als_run(self):
-    mark("value checks (upload complete)")
+    # no device synchronisation before the run: with staged uploads it starts
+    # blocks as they arrive (the run itself ends synchronised)
+    marks.append(("(host) before ALS run", time.perf_counter()))
     orig_als_run(self)
-    mark("ALS sweeps")
+    marks.append(("ALS run: blocks start as they arrive; sweeps", time.perf_counter()))
 
 
 S.AlsHandle.__init__ = timed_als_init
