@@ -175,12 +175,32 @@ __global__ void __launch_bounds__(256) k_als_solve(AlsCtx c, int n, int src) {
   // gram refresh (cpd_als.py:106) and divergence flag
   double* Gn = c.G[s * N + n];
   double bad = 0.0;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int p = e / R, q = e - p * R;
-    double g = 0.0;
-    for (long long i = 0; i < In; ++i) g = fma(U[i * R + p], U[i * R + q], g);
-    Gn[e] = g;
-    if (!isfinite(g)) bad = 1.0;
+  if (Ut) {
+    // from the transposed copy: the two columns of an entry are contiguous
+    // (one warp per entry p <= q, lanes over the rows, mirrored)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int p = 0; p < R; ++p) {
+      const double* ap = Ut + (long long)p * In;
+      for (int q = p + wid; q < R; q += nw) {
+        const double* bq = Ut + (long long)q * In;
+        double g = 0.0;
+        for (long long i = lane; i < In; i += 32) g = fma(ap[i], bq[i], g);
+        g = warp_sum(g);
+        if (lane == 0) {
+          Gn[p * R + q] = g;
+          Gn[q * R + p] = g;
+          if (!isfinite(g)) bad = 1.0;
+        }
+      }
+    }
+  } else {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int p = e / R, q = e - p * R;
+      double g = 0.0;
+      for (long long i = 0; i < In; ++i) g = fma(U[i * R + p], U[i * R + q], g);
+      Gn[e] = g;
+      if (!isfinite(g)) bad = 1.0;
+    }
   }
   bad = block_max(bad, red);
   if (threadIdx.x == 0 && bad > 0.0) c.converged[s] = -1;   // diverged marker
