@@ -309,6 +309,41 @@ def test_staged_upload_compression_equals_resident_inputs(P):
                 P.SolverOptions(max_iter=3, precision="fp32"))
 
 
+def test_staged_upload_edge_cases(P):
+    """Staged start with heterogeneous blocks (shapes and ranks differ), an
+    all-zero block (rel err 0 from the start, cpd_als.py:84-86) and a
+    compression capped at zero sweeps: same results as resident inputs."""
+    import torch
+    from paper_2302_05119_b200._device import fortran_view
+    rng = np.random.default_rng(31)
+    specs = [((64, 48, 40), 18), ((80, 48, 40), 24), ((64, 48, 56), 20), ((72, 48, 40), 17)]
+    host, dev, ranks = [], [], []
+    for k, (d, r) in enumerate(specs):
+        f = [rng.random((n, r)) for n in d]
+        x = np.einsum("ir,jr,kr->ijk", *f) + 0.2 * rng.standard_normal(d)
+        x = np.maximum(x, 0).astype(np.float32)
+        if k == 2:
+            x[:] = 0.0
+        flat = torch.from_numpy(np.ravel(x, order="F").copy())
+        pinned = torch.empty_strided(d, (1, d[0], d[0] * d[1]), dtype=torch.float32, pin_memory=True)
+        pinned.copy_(fortran_view(flat, d))
+        host.append(pinned)
+        dev.append(fortran_view(flat.cuda(), d))
+        ranks.append(r)
+    for als in (None, P.AlsOptions(max_iter=0), P.AlsOptions(max_iter=5, tol=1e-30)):
+        out = {}
+        for name, ts in (("host", host), ("dev", dev)):
+            out[name] = P.solve(P.CoupledProblem(ts, ranks, [0, 6, 0], mode="lra", als_options=als),
+                                P.SolverOptions(max_iter=12, seed=4, precision="fp32"))
+        a, b = out["host"], out["dev"]
+        assert a.compression_iters == b.compression_iters
+        for ca, cb in zip(a.compression, b.compression):
+            for fa, fb in zip(ca.factors, cb.factors):
+                np.testing.assert_array_equal(fa, fb)
+        assert a.objective_history == b.objective_history
+        assert a.rel_err_history == b.rel_err_history
+
+
 def test_device_value_checks_raise_reference_messages(P):
     """The single-process solve scans the uploaded blocks on the device; the
     errors are the reference's (solver.py:114-117), with the block index."""
