@@ -202,6 +202,10 @@ typedef struct {
 } cb_als_desc;
 
 int cb_als_create(const cb_als_desc* desc, void* stream, cb_als** out);
+/* frees the sweep workspace (byte planes, GEMM scratch) once cb_als_run has
+ * finished; results and device factors stay valid, the handle cannot run
+ * again */
+int cb_als_release_scratch(cb_als* h);
 /* 1 if cb_als_create would start these blocks one by one at their
  * ready_events (only then may the events be recorded after the create: the
  * engine reads no tensor before cb_als_run); needs dims, ranks, dtype,

@@ -100,6 +100,7 @@ _sig("cb_performance_index", c_int, [c_int, ctypes.POINTER(c_vp), ctypes.POINTER
                                      c_int, c_vp, c_vp, c_vp])
 _sig("cb_als_create", c_int, [ctypes.POINTER(AlsDesc), c_vp, ctypes.POINTER(c_vp)])
 _sig("cb_als_staged_ok", c_int, [ctypes.POINTER(AlsDesc)])
+_sig("cb_als_release_scratch", c_int, [c_vp])
 _sig("cb_als_run", c_int, [c_vp])
 _sig("cb_als_block_result", c_int, [c_vp, c_int, c_dp, c_ip, c_ip, c_dp, ctypes.POINTER(c_dp)])
 _sig("cb_als_factor_device", c_vp, [c_vp, c_int, c_int])
@@ -128,7 +129,7 @@ EXPORTED = [
     "cb_tensor_stats", "cb_kruskal_residual", "cb_rowdot", "cb_gemm", "cb_factor_gradient",
     "cb_synth_stats", "cb_synth_fill", "cb_model_residual", "cb_diff_sq",
     "cb_performance_index",
-    "cb_als_create", "cb_als_staged_ok", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
+    "cb_als_create", "cb_als_staged_ok", "cb_als_release_scratch", "cb_als_run", "cb_als_block_result", "cb_als_factor_device",
     "cb_als_destroy", "cb_solver_create", "cb_solver_run", "cb_solver_step_async",
     "cb_solver_summary_get", "cb_solver_history", "cb_solver_block_factors",
     "cb_solver_set_timing", "cb_solver_timing", "cb_solver_profile", "cb_solver_timeline",

@@ -124,6 +124,11 @@ class AlsHandle:
     def run(self):
         L.check(L.lib.cb_als_run(self.h))
 
+    def release_scratch(self):
+        """Free the sweep workspace (byte planes, GEMM scratch); the fitted
+        factors stay on the device for the solver."""
+        L.check(L.lib.cb_als_release_scratch(self.h))
+
     def block(self, s):
         rel = ctypes.c_double()
         it = ctypes.c_int()

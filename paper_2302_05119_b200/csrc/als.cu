@@ -315,6 +315,7 @@ struct cb_als {
   cb::OzPlan* oz = nullptr;     // both passes on the tensor cores over packed byte planes (xoz.cu)
   // deferred start: per-block upload events, blocks [0, started) are running
   bool deferred = false;
+  bool released = false;        // cb_als_release_scratch was called
   std::vector<cudaEvent_t> ready;
   int started = 0;
   double* d_stats = nullptr;
@@ -785,6 +786,7 @@ static int als_finish(cb_als* h) {
 
 int cb_als_run(cb_als* h) {
   CB_ARG(h, "null handle");
+  CB_ARG(!h->released, "cb_als_run after cb_als_release_scratch");
   if (h->deferred) {
     // start every block as its upload completes; between arrivals the
     // blocks already here sweep in short chunks
@@ -829,6 +831,21 @@ int cb_als_run(cb_als* h) {
     CB_CUDA(cudaStreamSynchronize(h->st));
   }
   return als_finish(h);
+}
+
+// frees what only the sweeps need (byte planes, D, fp64 GEMM scratch): the
+// factors, histories and counters stay for cb_als_block_result /
+// cb_als_factor_device.  c5: ~37 GB returned before the solver engine packs
+// its own trace planes.  The handle cannot run again afterwards.
+int cb_als_release_scratch(cb_als* h) {
+  CB_ARG(h, "null handle");
+  if (h->st) CB_CUDA(cudaStreamSynchronize(h->st));
+  cb::oz_plan_destroy(h->oz);
+  h->oz = nullptr;
+  cb::sl5_plan_destroy(h->sl5);
+  h->sl5 = nullptr;
+  h->released = true;
+  return CB_OK;
 }
 
 int cb_als_block_result(cb_als* h, int block, double* rel_err, int* n_iter, int* converged,

@@ -650,6 +650,9 @@ class PreparedSolve:
                         self.als = None
                     raise ValueError(f"compression of block {blk} failed: {msg}") from exc
             self.stream.synchronize()
+            # the sweep workspace (c5: ~37 GB of byte planes and scratch) goes
+            # back before the solver engine allocates its own trace planes
+            self.als.release_scratch()
             # staged: the engine setup plus the run that overlapped the uploads;
             # else from the setup (beside the upload's tail) to the last sweep
             self.compress_seconds = t_als if als_ran else time.perf_counter() - tic
