@@ -78,6 +78,7 @@ constexpr int XTC_MAX_I0 = 512;
 constexpr int XTC_MAX_R = 40;                     // 3 levels x Rp lanes <= 128
 constexpr int XTC_XBITS = 22;
 constexpr int XTC_UBITS = 22;
+constexpr int XTC_WBITS = 26;                     // A1 row weights: |w| <= 2^26
 constexpr int XTC_WB = 16;        // columns per epilogue batch
 constexpr int XTC_THREADS = 320;  // 8 epilogue warps, MMA, producer
 constexpr int XTC_SMEM_MAX = 227 * 1024;
@@ -91,7 +92,8 @@ struct XtcBlock {
   // per-call operands, two sets: the pipelined iteration prepares the next
   // trace's set while the current trace still reads the other
   double* aux[2];         // [64] scale_r
-  float* w1[2];           // [I1][Rp] = A1[i1, r] (fp32 row weights, zero-padded columns)
+  int* w1[2];             // [I1][Rp] = rint(A1[i1, r] 2^(26 - e1_r)): 27-bit fixed-point row weights
+                          // (zero-padded columns); 2^(e1_r - 26) is folded into aux
   float* w2[2];           // [I2][Rp] = A2[i2, r]
   unsigned char* bimg[2]; // [nk][2 Rp + 128 rows][32 B] (K-major, 32-B swizzle)
   const float* X;         // the block (read by the pack kernel only)
@@ -257,16 +259,33 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
     put(1, d1);
     put(2, d2);
   }
+  const long long I1 = b.I1, I2 = b.I2;
+  // A1 as 27-bit fixed point per column: the epilogue multiplies the int32
+  // levels by it in integer arithmetic (one IMAD.WIDE per row instead of
+  // conversions and fp64 FMAs, which share their pipe with the MMAs)
+  __shared__ int e1[64];
+  for (int r = warp; r < Rp; r += 8) {
+    double m = 0.0;
+    if (r < R)
+      for (long long i = lane; i < I1; i += 32) m = fmax(m, fabs(A1[i * R + r]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      int e = 0;
+      if (m > 0.0) frexp(m, &e);
+      e1[r] = e;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x < 64) {
     const int r = threadIdx.x;
-    // q p = 2^16 (2^16 L0 + 2^8 L1 + L2)
-    b.aux[set][r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS) : 0.0;
+    // q p = 2^16 (2^16 L0 + 2^8 L1 + L2); weights carry 2^(26 - e1)
+    b.aux[set][r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS + e1[r] - XTC_WBITS)
+                          : 0.0;
   }
-  const long long I1 = b.I1, I2 = b.I2;
   for (long long e = threadIdx.x; e < I1 * Rp; e += 256) {
     const long long i = e / Rp;
     const int r = (int)(e - i * Rp);
-    b.w1[set][e] = r < R ? (float)A1[i * R + r] : 0.0f;
+    b.w1[set][e] = r < R ? (int)llrint(ldexp(A1[i * R + r], XTC_WBITS - e1[r])) : 0;
   }
   for (long long e = threadIdx.x; e < I2 * Rp; e += 256) {
     const long long i = e / Rp;
@@ -434,7 +453,7 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
       // padding columns of the weight tables / a valid address and weigh
       // their products by zero
       const bool act = lev < 3 && r < b.R;
-      const float* __restrict__ w1p = b.w1[set] + (act ? r : 0);
+      const int* __restrict__ w1p = b.w1[set] + (act ? r : 0);
       const float* __restrict__ w2p = b.w2[set] + (act ? r : 0);
       const float wm = act ? 1.0f : 0.0f;
       for (int t = un.t0; t < un.t1; ++t, ++tl) {
@@ -446,9 +465,9 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
         // a batch is plain when all its rows exist and share one i2
         auto plain = [&](int j0, int i1s) { return j0 + XTC_WB <= nrow && i1s + XTC_WB <= I1; };
         // weights of a batch of columns: A1[i1s + j (wrapping), r]
-        auto load_w1 = [&](int j0, int i1s, float (&w)[XTC_WB]) {
+        auto load_w1 = [&](int j0, int i1s, int (&w)[XTC_WB]) {
           if (plain(j0, i1s)) {
-            const float* p = w1p + (long long)i1s * RP;
+            const int* p = w1p + (long long)i1s * RP;
 #pragma unroll
             for (int j = 0; j < XTC_WB; ++j) w[j] = __ldg(p + j * RP);
           } else {
@@ -456,14 +475,16 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
             for (int j = 0; j < XTC_WB; ++j) {
               int i = i1s + j;
               if (i >= I1) i -= I1;   // one wrap at most (I1 >= XTC_WB)
-              w[j] = j0 + j < nrow ? __ldg(w1p + (long long)i * RP) : 0.0f;
+              w[j] = j0 + j < nrow ? __ldg(w1p + (long long)i * RP) : 0;
             }
           }
         };
-        float wc[XTC_WB], wn[XTC_WB];
+        int wc[XTC_WB], wn[XTC_WB];
         load_w1(0, i1, wc);
         float w2 = nrow > 0 ? wm * __ldg(w2p + (long long)i2 * RP) : 0.0f;
-        double in0 = 0.0, in1 = 0.0, in2 = 0.0, in3 = 0.0;
+        // sum_i1 w L exactly in int64 (|w L| < 2^51, <= 128 rows), four
+        // interleaved chains
+        long long in0 = 0, in1 = 0, in2 = 0, in3 = 0;
         mbar_wait(&d_full[buf], (tl >> 1) & 1);
         tc_fence_after();
         const uint32_t dc = trow + (uint32_t)(buf * XTC_NT + ch * 128);
@@ -479,15 +500,15 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
           if (plain(j0, i1)) {
 #pragma unroll
             for (int j = 0; j < XTC_WB; j += 4) {
-              in0 = fma((double)wc[j], i2d_exact(v[j]), in0);
-              in1 = fma((double)wc[j + 1], i2d_exact(v[j + 1]), in1);
-              in2 = fma((double)wc[j + 2], i2d_exact(v[j + 2]), in2);
-              in3 = fma((double)wc[j + 3], i2d_exact(v[j + 3]), in3);
+              in0 += (long long)wc[j] * (int)v[j];
+              in1 += (long long)wc[j + 1] * (int)v[j + 1];
+              in2 += (long long)wc[j + 2] * (int)v[j + 2];
+              in3 += (long long)wc[j + 3] * (int)v[j + 3];
             }
             i1 += XTC_WB;
             if (i1 == I1) {
-              acc = fma((double)w2, (in0 + in1) + (in2 + in3), acc);
-              in0 = in1 = in2 = in3 = 0.0;
+              acc = fma((double)w2, (double)((in0 + in1) + (in2 + in3)), acc);
+              in0 = in1 = in2 = in3 = 0;
               i1 = 0;
               ++i2;
               w2 = j0 + XTC_WB < nrow ? wm * __ldg(w2p + (long long)i2 * RP) : 0.0f;
@@ -496,10 +517,10 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
             // the batch crosses into the next i2 or past the block's rows
 #pragma unroll
             for (int j = 0; j < XTC_WB; ++j) {
-              in0 = fma((double)wc[j], i2d_exact(v[j]), in0);
+              in0 += (long long)wc[j] * (int)v[j];
               if (++i1 == I1) {
-                acc = fma((double)w2, (in0 + in1) + (in2 + in3), acc);
-                in0 = in1 = in2 = in3 = 0.0;
+                acc = fma((double)w2, (double)((in0 + in1) + (in2 + in3)), acc);
+                in0 = in1 = in2 = in3 = 0;
                 i1 = 0;
                 ++i2;
                 w2 = j0 + j + 1 < nrow ? wm * __ldg(w2p + (long long)i2 * RP) : 0.0f;
@@ -509,7 +530,7 @@ __global__ void __launch_bounds__(XTC_THREADS, 1) k_xtc_trace(XtcArgs a) {
 #pragma unroll
           for (int j = 0; j < XTC_WB; ++j) wc[j] = wn[j];
         }
-        acc = fma((double)w2, (in0 + in1) + (in2 + in3), acc);
+        acc = fma((double)w2, (double)((in0 + in1) + (in2 + in3)), acc);
         tc_fence_before();
         mbar_arrive(&d_empty[buf]);
         if (t == un.t1 - 1) {
@@ -665,7 +686,7 @@ int xtc_plan_create(int S, const void* const* X, const long long* dims, const in
     XtcBlock& b = hb[s];
     for (int k = 0; k < 2; ++k) {
       b.aux[k] = aux + 64LL * (2 * s + k);
-      b.w1[k] = wts + k * w_elems + wo;
+      b.w1[k] = reinterpret_cast<int*>(wts + k * w_elems + wo);
       b.w2[k] = wts + k * w_elems + wo + (long long)Rp * b.I1;
       b.bimg[k] = bimg + (size_t)k * bimg_total + bo;
     }
