@@ -207,11 +207,14 @@ __global__ void __launch_bounds__(XTC_NT) k_xtc_pack(const XtcBlock* blk) {
 // per call: A0 -> the stacked signed byte-slice image (the MMA's M-side
 // operand, exactly the shared-memory layout), column scales, A1/A2 as fp32
 // --------------------------------------------------------------------------
+// grid (S, 4): parts 0 / 1 write the two halves of the factor image (part 0
+// also the column scales), part 2 the A1 weights, part 3 the A2 weights
 __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const* U) {
   griddep_wait();
   if (a.gate && *a.gate == 0) return;
   tl_begin(a.tl, TL_PREP);
   const int s = blockIdx.x;
+  const int part = blockIdx.y;
   const XtcBlock b = a.blk[s];
   const int set = (*a.par) ^ a.wr_other;
   unsigned char* bimg = b.bimg[set];
@@ -220,77 +223,78 @@ __global__ void __launch_bounds__(256) k_xtc_prep(XtcArgs a, const double* const
   const double* A2 = U[3 * s + 2];
   const int R = b.R, Rp = a.Rp;
   const int I0 = (int)b.I0;
+  const long long I1 = b.I1, I2 = b.I2;
   const int SR = 2 * Rp + 128;        // image rows per K step
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ int eu[64];
-  for (int r = warp; r < Rp; r += 8) {
-    double m = 0.0;
-    if (r < R)
-      for (int i = lane; i < I0; i += 32) m = fmax(m, fabs(A0[(long long)i * R + r]));
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) {
-      int e = 0;
-      if (m > 0.0) frexp(m, &e);
-      eu[r] = e;
+  __shared__ int eu[64];              // column exponents of A0
+  __shared__ int e1[64];              // column exponents of A1
+  // column exponent of an I x R factor: max |.| = m 2^e, m in [0.5, 1)
+  auto col_exps = [&](const double* A, long long I, int* out) {
+    for (int r = warp; r < Rp; r += 8) {
+      double m = 0.0;
+      if (r < R)
+        for (long long i = lane; i < I; i += 32) m = fmax(m, fabs(A[i * R + r]));
+      for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) {
+        int e = 0;
+        if (m > 0.0) frexp(m, &e);
+        out[r] = e;
+      }
     }
-  }
-  __syncthreads();
-  // rows [2 Rp + l Rp + n] = slice l of column n; everything else stays zero
-  // (the image is zeroed at plan creation and only these bytes are rewritten)
-  const int kmax = b.nk * 32;
-  for (int e = threadIdx.x; e < kmax * Rp; e += 256) {
-    const int k = e / Rp, n = e - (e / Rp) * Rp;
-    long long p = 0;
-    if (k < I0 && n < R) p = llrint(ldexp(A0[(long long)k * R + n], XTC_UBITS - eu[n]));
-    const long long d2 = ((p + 128) & 255) - 128;
-    const long long p1 = (p - d2) >> 8;
-    const long long d1 = ((p1 + 128) & 255) - 128;
-    const long long d0 = (p1 - d1) >> 8;
-    const int c = k >> 5, kk = k & 31;
-    // rows of 32 bytes, 16-byte halves swapped on rows with bit 2 set
-    // (Swizzle<1,4,3>; the K-step images start on multiples of 256 bytes)
-    auto put = [&](int l, long long d) {
-      const int row = (2 + l) * Rp + n;
-      const long long off =
-          ((long long)c * SR + row) * 32 + (((kk >> 4) ^ ((row >> 2) & 1)) << 4) + (kk & 15);
-      bimg[off] = (unsigned char)(signed char)d;
-    };
-    put(0, d0);
-    put(1, d1);
-    put(2, d2);
-  }
-  const long long I1 = b.I1, I2 = b.I2;
-  // A1 as 27-bit fixed point per column: the epilogue multiplies the int32
-  // levels by it in integer arithmetic (one IMAD.WIDE per row instead of
-  // conversions and fp64 FMAs, which share their pipe with the MMAs)
-  __shared__ int e1[64];
-  for (int r = warp; r < Rp; r += 8) {
-    double m = 0.0;
-    if (r < R)
-      for (long long i = lane; i < I1; i += 32) m = fmax(m, fabs(A1[i * R + r]));
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) {
-      int e = 0;
-      if (m > 0.0) frexp(m, &e);
-      e1[r] = e;
+  };
+  if (part <= 1) {
+    col_exps(A0, I0, eu);
+    if (part == 0) col_exps(A1, I1, e1);
+    __syncthreads();
+    // rows [2 Rp + l Rp + n] = slice l of column n; everything else stays zero
+    // (the image is zeroed at plan creation and only these bytes are rewritten)
+    const int kmax = b.nk * 32;
+    const int khalf = (b.nk + 1) / 2 * 32;
+    const int k_lo = part == 0 ? 0 : khalf, k_hi = part == 0 ? min(khalf, kmax) : kmax;
+    for (int e = k_lo * Rp + threadIdx.x; e < k_hi * Rp; e += 256) {
+      const int k = e / Rp, n = e - (e / Rp) * Rp;
+      long long p = 0;
+      if (k < I0 && n < R) p = llrint(ldexp(A0[(long long)k * R + n], XTC_UBITS - eu[n]));
+      const long long d2 = ((p + 128) & 255) - 128;
+      const long long p1 = (p - d2) >> 8;
+      const long long d1 = ((p1 + 128) & 255) - 128;
+      const long long d0 = (p1 - d1) >> 8;
+      const int c = k >> 5, kk = k & 31;
+      // rows of 32 bytes, 16-byte halves swapped on rows with bit 2 set
+      // (Swizzle<1,4,3>; the K-step images start on multiples of 256 bytes)
+      auto put = [&](int l, long long d) {
+        const int row = (2 + l) * Rp + n;
+        const long long off =
+            ((long long)c * SR + row) * 32 + (((kk >> 4) ^ ((row >> 2) & 1)) << 4) + (kk & 15);
+        bimg[off] = (unsigned char)(signed char)d;
+      };
+      put(0, d0);
+      put(1, d1);
+      put(2, d2);
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < 64) {
-    const int r = threadIdx.x;
-    // q p = 2^16 (2^16 L0 + 2^8 L1 + L2); weights carry 2^(26 - e1)
-    b.aux[set][r] = r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS + e1[r] - XTC_WBITS)
-                          : 0.0;
-  }
-  for (long long e = threadIdx.x; e < I1 * Rp; e += 256) {
-    const long long i = e / Rp;
-    const int r = (int)(e - i * Rp);
-    b.w1[set][e] = r < R ? (int)llrint(ldexp(A1[i * R + r], XTC_WBITS - e1[r])) : 0;
-  }
-  for (long long e = threadIdx.x; e < I2 * Rp; e += 256) {
-    const long long i = e / Rp;
-    const int r = (int)(e - i * Rp);
-    b.w2[set][e] = r < R ? (float)A2[i * R + r] : 0.0f;
+    if (part == 0 && threadIdx.x < 64) {
+      const int r = threadIdx.x;
+      // q p = 2^16 (2^16 L0 + 2^8 L1 + L2); the A1 weights carry 2^(26 - e1)
+      b.aux[set][r] =
+          r < R ? ldexp(1.0, 16 + b.ex - XTC_XBITS + eu[r] - XTC_UBITS + e1[r] - XTC_WBITS) : 0.0;
+    }
+  } else if (part == 2) {
+    // A1 as 27-bit fixed point per column: the epilogue multiplies the int32
+    // levels by it in integer arithmetic (one IMAD.WIDE per row instead of
+    // conversions and fp64 FMAs, which share their pipe with the MMAs)
+    col_exps(A1, I1, e1);
+    __syncthreads();
+    for (long long e = threadIdx.x; e < I1 * Rp; e += 256) {
+      const long long i = e / Rp;
+      const int r = (int)(e - i * Rp);
+      b.w1[set][e] = r < R ? (int)llrint(ldexp(A1[i * R + r], XTC_WBITS - e1[r])) : 0;
+    }
+  } else {
+    for (long long e = threadIdx.x; e < I2 * Rp; e += 256) {
+      const long long i = e / Rp;
+      const int r = (int)(e - i * Rp);
+      b.w2[set][e] = r < R ? (float)A2[i * R + r] : 0.0f;
+    }
   }
   tl_end(a.tl, TL_PREP);
 }
@@ -767,7 +771,7 @@ int xtc_trace(XtcPlan* p, const double* const* U_dev, const int* gate, double* b
   a.gate = gate;
   a.tl = p->tl;
   if (parts & 1) {
-    CB_CUDA(launch_k(k_xtc_prep, dim3(p->S), dim3(256), 0, st, a, U_dev));
+    CB_CUDA(launch_k(k_xtc_prep, dim3(p->S, 4), dim3(256), 0, st, a, U_dev));
     count_launch(1);
   }
   if (parts & 2) {
