@@ -197,8 +197,13 @@ typedef struct {
                                      stream).  cb_als_run then starts each
                                      block's compression as it arrives, beside
                                      the remaining uploads (blocks are fitted
-                                     independently: same results).  NULL: the
-                                     tensors are ready in stream order        */
+                                     independently: same results).  Only for
+                                     blocks cb_als_staged_ok accepts
+                                     (CB_ERR_UNSUPPORTED otherwise, also when
+                                     the plan's memory cannot be allocated:
+                                     create again without events once the
+                                     uploads are done).  NULL: the tensors
+                                     are ready in stream order               */
 } cb_als_desc;
 
 int cb_als_create(const cb_als_desc* desc, void* stream, cb_als** out);

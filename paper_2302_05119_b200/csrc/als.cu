@@ -566,9 +566,12 @@ int cb_als_create(const cb_als_desc* d, void* stream, cb_als** out) {
       oz_preload(h->oz);
     }
     if (!h->deferred) {
-      // (callers check cb_als_staged_ok first: the events must already have
-      // been recorded after the uploads for this path)
-      for (int s = 0; s < S; ++s) CB_CUDA(cudaStreamWaitEvent(st, h->ready[s], 0));
+      // cb_als_staged_ok said yes but the plan could not be built (device
+      // memory): the caller falls back to uploading first (the events may
+      // not have been recorded yet, so nothing can be read here)
+      cb_als_destroy(h);
+      set_error("staged start unavailable (the plane-GEMM plan could not be created)");
+      return CB_ERR_UNSUPPORTED;
     }
   }
   // the starting factors (pageable host memory: these copies wait for the

@@ -561,12 +561,16 @@ class PreparedSolve:
                 for ev in arrived:
                     ev.record(self.stream)      # creates the event; re-recorded after its copy
                 tic = time.perf_counter()
+                staged_fallback = False
                 try:
                     self.als = AlsHandle(self.dev, self.dims, ranks, self.code, base.tol,
                                          base.max_iter, [base.seed + g for g in self.local], st,
                                          self.als_compute_code, S_all, ready_events=arrived)
                 except ValueError as exc:
                     als_exc = exc
+                except NotImplementedError:
+                    # the staged plan did not fit: upload first, then a plain handle
+                    staged_fallback = True
                 t_als = time.perf_counter() - tic
                 copy_stream = torch.cuda.Stream()
                 copy_stream.wait_stream(self.stream)
@@ -579,7 +583,17 @@ class PreparedSolve:
                         arrived[k].record(copy_stream)
                         L.check(L.lib.cb_tensor_stats(code, D.ptr(dst), dst.numel(),
                                                       D.ptr(stats[k]), D.stream()))
-                if self.als is not None:
+                if staged_fallback:
+                    copy_stream.synchronize()
+                    tic = time.perf_counter()
+                    try:
+                        self.als = AlsHandle(self.dev, self.dims, ranks, self.code, base.tol,
+                                             base.max_iter, [base.seed + g for g in self.local],
+                                             st, self.als_compute_code, S_all)
+                    except ValueError as exc:
+                        als_exc = exc
+                    t_als = 0.0
+                elif self.als is not None:
                     tic = time.perf_counter()
                     try:
                         # sweeps of the blocks that are here while the rest uploads

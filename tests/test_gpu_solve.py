@@ -344,6 +344,34 @@ def test_staged_upload_edge_cases(P):
         assert a.rel_err_history == b.rel_err_history
 
 
+def test_staged_upload_falls_back_when_the_plan_is_unavailable(P, monkeypatch):
+    """cb_als_create with upload events refuses blocks it cannot start one by
+    one (CB_ERR_UNSUPPORTED: here small ranks, in production a plan that does
+    not fit in device memory); solve() then finishes the uploads and runs the
+    plain compression: same results as resident inputs."""
+    import torch
+    from paper_2302_05119_b200 import solver as S
+    from paper_2302_05119_b200._device import fortran_view
+    rng = np.random.default_rng(8)
+    d = (24, 20, 16)
+    host, dev = [], []
+    for _ in range(3):
+        x = np.maximum(rng.random(d) + 0.1 * rng.standard_normal(d), 0).astype(np.float32)
+        flat = torch.from_numpy(np.ravel(x, order="F").copy())
+        pinned = torch.empty_strided(d, (1, d[0], d[0] * d[1]), dtype=torch.float32, pin_memory=True)
+        pinned.copy_(fortran_view(flat, d))
+        host.append(pinned)
+        dev.append(fortran_view(flat.cuda(), d))
+    want = P.solve(P.CoupledProblem(dev, 4, [2, 2, 0], mode="lra"),
+                   P.SolverOptions(max_iter=15, seed=3, precision="fp32"))
+    monkeypatch.setattr(S, "als_staged_ok", lambda *a, **k: True)
+    got = P.solve(P.CoupledProblem(host, 4, [2, 2, 0], mode="lra"),
+                  P.SolverOptions(max_iter=15, seed=3, precision="fp32"))
+    assert got.compression_iters == want.compression_iters
+    assert got.objective_history == want.objective_history
+    assert got.rel_err_history == want.rel_err_history
+
+
 def test_device_value_checks_raise_reference_messages(P):
     """The single-process solve scans the uploaded blocks on the device; the
     errors are the reference's (solver.py:114-117), with the block index."""
