@@ -531,34 +531,49 @@ static __device__ __forceinline__ void mode_update_tile(const Ctx& c, int n, int
     for (int e = threadIdx.x; e < Rt * R; e += blockDim.x) P[e] = Cs[e] * Cs[Rt * R + e];
     for (int e = threadIdx.x; e < rows * Rt; e += blockDim.x) Uts[e] *= tws[e % Rt];
     __syncthreads();
-    // 4-column register tiles: one broadcast load of Ut o tw feeds four FMA
+    // 2 rows x 4 columns register tiles: six shared loads feed eight FMA
     // chains (each output keeps its q-ordered chain)
     const int RG = (R + 3) >> 2;
-    for (int e = threadIdx.x; e < rows * RG; e += blockDim.x) {
-      const int il = e / RG, rb = (e - il * RG) << 2;
-      const double* ur = Uts + il * Rt;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int H = (rows + 1) >> 1;
+    for (int e = threadIdx.x; e < H * RG; e += blockDim.x) {
+      const int i0 = e / RG, rb = (e - i0 * RG) << 2;
+      const int i1 = i0 + H;
+      const bool two = i1 < rows;
+      const double* u0 = Uts + i0 * Rt;
+      const double* u1 = Uts + (two ? i1 : i0) * Rt;
+      double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
       if (rb + 4 <= R) {
         for (int q = 0; q < Rt; ++q) {
-          const double u = ur[q];
+          const double x0 = u0[q], x1 = u1[q];
           const double* pr = P + q * R + rb;
-          a0 = fma(u, pr[0], a0); a1 = fma(u, pr[1], a1);
-          a2 = fma(u, pr[2], a2); a3 = fma(u, pr[3], a3);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double pk = pr[k];
+            a[0][k] = fma(x0, pk, a[0][k]);
+            a[1][k] = fma(x1, pk, a[1][k]);
+          }
         }
       } else {
         for (int q = 0; q < Rt; ++q) {
-          const double u = ur[q];
+          const double x0 = u0[q], x1 = u1[q];
           const double* pr = P + q * R + rb;
-          a0 = fma(u, pr[0], a0);
-          if (rb + 1 < R) a1 = fma(u, pr[1], a1);
-          if (rb + 2 < R) a2 = fma(u, pr[2], a2);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (rb + k < R) {
+              const double pk = pr[k];
+              a[0][k] = fma(x0, pk, a[0][k]);
+              a[1][k] = fma(x1, pk, a[1][k]);
+            }
         }
       }
-      double* mo = mt + il * R + rb;
-      mo[0] = a0;
-      if (rb + 1 < R) mo[1] = a1;
-      if (rb + 2 < R) mo[2] = a2;
-      if (rb + 3 < R) mo[3] = a3;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        if (h2 == 1 && !two) break;
+        double* mo = mt + (h2 ? i1 : i0) * R + rb;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (rb + k < R) mo[k] = a[h2][k];
+      }
     }
   } else if (src == 2) {
     const int Rt = c.Rt[s];
@@ -593,37 +608,55 @@ static __device__ __forceinline__ void mode_update_tile(const Ctx& c, int n, int
       if (r >= L) Un[(r0 + il) * (long long)R + r] = Ucs[e];
     }
   } else {
-    // gradient u_hat step - mt o lam in 4-column register tiles (each
-    // output's q-ordered FMA chain unchanged), then the projection
+    // gradient u_hat step - mt o lam in 2 rows x 4 columns register tiles
+    // (each output's q-ordered FMA chain unchanged), then the projection
     const int RG = (R + 3) >> 2;
-    for (int e = threadIdx.x; e < rows * RG; e += blockDim.x) {
-      const int il = e / RG, rb = (e - il * RG) << 2;
-      const double* ur = uh + il * R;
-      double g4[4] = {0.0, 0.0, 0.0, 0.0};
+    const int H = (rows + 1) >> 1;
+    for (int e = threadIdx.x; e < H * RG; e += blockDim.x) {
+      const int l0 = e / RG, rb = (e - l0 * RG) << 2;
+      const int l1 = l0 + H;
+      const bool two = l1 < rows;
+      const double* ur0 = uh + l0 * R;
+      const double* ur1 = uh + (two ? l1 : l0) * R;
+      double g4[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
       if (rb + 4 <= R) {
         for (int q = 0; q < R; ++q) {
-          const double u = ur[q];
+          const double x0 = ur0[q], x1 = ur1[q];
           const double* sr = step + q * R + rb;
-          g4[0] = fma(u, sr[0], g4[0]); g4[1] = fma(u, sr[1], g4[1]);
-          g4[2] = fma(u, sr[2], g4[2]); g4[3] = fma(u, sr[3], g4[3]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double sk = sr[k];
+            g4[0][k] = fma(x0, sk, g4[0][k]);
+            g4[1][k] = fma(x1, sk, g4[1][k]);
+          }
         }
       } else {
         for (int q = 0; q < R; ++q) {
-          const double u = ur[q];
+          const double x0 = ur0[q], x1 = ur1[q];
           const double* sr = step + q * R + rb;
-          g4[0] = fma(u, sr[0], g4[0]);
-          if (rb + 1 < R) g4[1] = fma(u, sr[1], g4[1]);
-          if (rb + 2 < R) g4[2] = fma(u, sr[2], g4[2]);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (rb + k < R) {
+              const double sk = sr[k];
+              g4[0][k] = fma(x0, sk, g4[0][k]);
+              g4[1][k] = fma(x1, sk, g4[1][k]);
+            }
         }
       }
-      const long long i = r0 + il;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int r = rb + k;
-        if (r >= R) break;
-        const double g = g4[k] - mt[il * R + r] * lam[r];
-        if (r < L) gcp[i * L + r] = g;
-        else Un[i * R + r] = pos(ur[r] - g / lu);
+      for (int h2 = 0; h2 < 2; ++h2) {
+        if (h2 == 1 && !two) break;
+        const int il = h2 ? l1 : l0;
+        const double* ur = h2 ? ur1 : ur0;
+        const long long i = r0 + il;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = rb + k;
+          if (r >= R) break;
+          const double g = g4[h2][k] - mt[il * R + r] * lam[r];
+          if (r < L) gcp[i * L + r] = g;
+          else Un[i * R + r] = pos(ur[r] - g / lu);
+        }
       }
     }
   }
