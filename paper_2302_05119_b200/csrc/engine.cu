@@ -1113,12 +1113,12 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
         // leave SMs for the sweep that runs beside the trace (its per-block
         // CTAs).  The trace pass stays HBM bound down to ~100 SMs (its MMA time
         // per SM is half its HBM share, its epilogue is integer), so the sweep
-        // gets up to 48: c5 (S = 64) measured 2.39 ms per iteration at 32, 2.33
-        // at 40, 2.30 at 48, 2.37 at 52
+        // gets up to 40: c5 (S = 64) measured 2.32 ms per iteration at 32, 2.28
+        // at 36, 2.29 at 40, 2.33 at 44, 2.37 at 48
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        int reserve = d->pipeline_reserve > 0 ? d->pipeline_reserve : std::min(S, 48);
+        int reserve = d->pipeline_reserve > 0 ? d->pipeline_reserve : std::min(S, 40);
         reserve = std::max(0, std::min(reserve, nsm / 2));
         xtc_set_grid_cap(h->xtc, nsm - reserve);
       }
