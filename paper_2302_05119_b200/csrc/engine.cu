@@ -1102,13 +1102,14 @@ int cb_solver_create(const cb_solver_desc* d, void* stream, cb_solver** out) {
       // a plan that does not fit (shared memory) leaves the CUDA-core pass
       if (xtc_plan_create(S, h->X.data(), h->dims.data(), h->R.data(), st, &h->xtc) != CB_OK)
         h->xtc = nullptr;
-      // pipelined only when the trace pass is large enough to hide the sweep
-      // behind (c3, c5); on small blocks (c4: 35 MB) the extra snapshot /
-      // rollback work costs more than it hides (measured)
+      // pipelined when the trace pass streams >= 32 MB (c3, c4, c5; c4, 35 MB:
+      // 1710 -> 1780 it/s over its 500 iterations since the operand prep left
+      // the critical path); below that the snapshot / rollback work costs
+      // more than the hidden trace
       // sharded: with an NCCL communicator (the emulated group runs the
       // classic order segment by segment)
       h->pipe = h->xtc != nullptr && (!shard || d->nccl_comm) && d->pipeline != 2 &&
-                (xtc_bytes(h->xtc) >= 64e6 || d->pipeline == 1);
+                (xtc_bytes(h->xtc) >= 32e6 || d->pipeline == 1);
       if (h->pipe) {
         // leave SMs for the sweep that runs beside the trace (its per-block
         // CTAs).  The trace pass stays HBM bound down to ~100 SMs (its MMA time
