@@ -501,7 +501,6 @@ int oz_plan_create(int S, const void* const* X, const long long* dims, const int
     }                                                                   \
   } while (0)
   long long ntmax[2] = {1, 1};
-  long long tiles = 0;
   size_t plane_bytes = 0, bimg_bytes = 0;
   for (int s = 0; s < S; ++s) {
     OzBlock& b = hb[s];
@@ -525,7 +524,6 @@ int oz_plan_create(int S, const void* const* X, const long long* dims, const int
       plane_bytes += (size_t)F.nt * F.nk * OZ_STAGE;
       bimg_bytes += (size_t)F.nk * OZ_SB * N * 32;
     }
-    tiles = std::max(tiles, (long long)0);
     p->i2max = std::max(p->i2max, I2);
   }
   // planes (every byte is written by the pack kernels: no memset), factor
