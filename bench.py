@@ -344,7 +344,7 @@ def run_ours(args):
     traffic_tab = {
         ("c2", "slab"): (40.186624e6, "profiles/r01f_c2_streaming_ncu_summary.txt"),
         ("c2", "fiber4"): (40.100096e6 + 18.944e3, "profiles/r01f_c2_streaming_ncu_summary.txt"),
-        ("c5", "xtc"): (12.794423e9 + 4.118272e6, "profiles/r02_xtc_c5_ncu_summary.txt"),
+        ("c5", "xtc"): (12.794673e9 + 4.373504e6, "profiles/r02_xtc_c5_ncu_summary.txt"),
     }
     traffic, traffic_src = traffic_tab.get((spec.name, kname), (None, None))
     iter_bytes = (1 if spec.mode == "lra" else 3) * spec.tensor_bytes
