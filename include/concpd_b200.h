@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CB_ABI_VERSION 1
+#define CB_ABI_VERSION 2   /* 2: cb_als_desc.ready_events, cb_als_staged_ok, cb_als_release_scratch */
 
 typedef enum {
   CB_OK = 0,

@@ -20,7 +20,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     missing = [name for name in sorted(declared) if not hasattr(L.lib, name)]
     assert not missing, f"library is missing {missing}"
     assert set(L.EXPORTED) == declared
-    assert L.lib.cb_abi_version() == 1
+    assert L.lib.cb_abi_version() == 2
 
 
 def test_library_is_sm100a():
